@@ -1,0 +1,173 @@
+/*
+ * tinyserve.h — C ABI of libtinyserve.so, the B200 (sm_100a) decode-time hot path of
+ * TinyServe (arXiv 2509.12211, §3.5 "Query-Aware Page Selection", Alg. 1).
+ *
+ * One decode step of one attention layer, for a batch of sequences held in a paged KV
+ * cache (vLLM-style block table):
+ *
+ *   ts_meta_append        metadata maintenance on KV append      Eq. 1
+ *   ts_score_pages        bounding-box relevance of every page   Eq. 2; Alg. 1 Step 1
+ *   ts_select_topk        top-K pages per (sequence, kv head)    PAPER.md:162-167; Alg. 1 Step 2
+ *   ts_sparse_decode_attn softmax attention over selected pages  PAPER.md:169-172; Alg. 1 Steps 3-4
+ *   ts_decode_step        score -> select -> attend in one call  Alg. 1, PAPER.md:209-249 ("single pass")
+ *   ts_lse_merge          merge of partial attentions (split-K / multi-GPU)
+ *
+ * Conventions (apply to every entry point):
+ *  - POINTERS: every tensor argument is a DEVICE pointer (cudaMalloc'd or torch CUDA
+ *    storage) owned by the caller, except `ts_layout*`, which is a HOST pointer read
+ *    during the call only.  The library never allocates, frees, synchronises or keeps a
+ *    pointer after returning.  `stream` is a cudaStream_t passed as void* (NULL = the
+ *    legacy default stream); all work is enqueued asynchronously on it.
+ *  - LAYOUT, all row-major, contiguous:
+ *      q          [batch][num_q_heads][head_dim]             kv_dtype
+ *      k_pool     [num_blocks][num_kv_heads][page_size][head_dim]   kv_dtype
+ *      v_pool     [num_blocks][num_kv_heads][page_size][head_dim]   kv_dtype
+ *      meta       [num_blocks][num_kv_heads][2][head_dim]    kv_dtype; [..][0][:] = m (min),
+ *                 [..][1][:] = M (max) of the valid keys of the block (Eq. 1)
+ *      page_table [batch][max_pages] int32: LOCAL page index -> physical block
+ *      seq_lens   [batch] int32: GLOBAL number of tokens in the cache (before the append
+ *                 for ts_meta_append, after it for everything else)
+ *      scores     [batch][num_kv_heads][max_pages] fp32, indexed by LOCAL page
+ *      o          [batch][num_q_heads][head_dim] fp32;  lse [batch][num_q_heads] fp32
+ *    q head h belongs to kv head h / (num_q_heads / num_kv_heads) (GQA, reading R16).
+ *  - SEQUENCE SHARDING: a rank owns global pages j with
+ *    j % shard_stride == shard_offset and stores global page j at local index
+ *    j / shard_stride.  Unsharded: shard_stride = 1, shard_offset = 0.  Page ids that
+ *    cross the boundary (sel_ids) are always GLOBAL.
+ *  - PRECISION: q, K, V and meta share kv_dtype (bf16 or fp32); scores, o and lse are
+ *    fp32 (reading R10).  K_b = min(P_b, max(1, floor(budget_tokens / page_size))).
+ *  - ERRORS: host-side validation only (no device synchronisation):
+ *      TS_ERR_CONFIG       non-positive size, budget < 1, unknown dtype
+ *      TS_ERR_SHAPE        num_q_heads % num_kv_heads != 0, k < 1, bad shard
+ *      TS_ERR_ALIGN        a tensor pointer not 16-byte aligned (128-bit loads / TMA)
+ *      TS_ERR_UNSUPPORTED  head_dim / page_size / group size outside the compiled set
+ *      TS_ERR_WORKSPACE    ws NULL or smaller than ts_workspace_bytes()
+ *      TS_ERR_CUDA         a CUDA launch failed (cudaGetLastError)
+ *    Data-dependent faults (page_table entry >= num_blocks, seq_len > max_pages*page_size,
+ *    non-finite inputs) are undefined behaviour, not detected.
+ *    seq_len == 0 is valid: the sequence selects nothing, o = 0, lse = -inf (reading R8).
+ *  - Compiled set: head_dim 64 or 128; page_size in {8, 16, 32, 64} for bf16 and any
+ *    page_size >= 1 for fp32; group size 1..8 for bf16, any for fp32.
+ */
+#ifndef TINYSERVE_H
+#define TINYSERVE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    TS_OK = 0,
+    TS_ERR_CONFIG = 1,
+    TS_ERR_SHAPE = 2,
+    TS_ERR_ALIGN = 3,
+    TS_ERR_UNSUPPORTED = 4,
+    TS_ERR_CUDA = 5,
+    TS_ERR_WORKSPACE = 6
+} ts_status;
+
+typedef enum { TS_F32 = 0, TS_BF16 = 1 } ts_dtype;
+
+typedef struct {
+    int32_t batch;          /* B: sequences in the batch                                   */
+    int32_t num_q_heads;    /* Hq                                                          */
+    int32_t num_kv_heads;   /* Hkv, Hq % Hkv == 0, group size G = Hq / Hkv                  */
+    int32_t head_dim;       /* d                                            */
+    int32_t page_size;      /* S tokens per page                             */
+    int32_t max_pages;      /* row stride of page_table and scores (local pages)           */
+    int32_t num_blocks;     /* physical blocks in k_pool / v_pool / meta                   */
+    int32_t shard_stride;   /* 1 unsharded; G ranks for block-cyclic sequence sharding     */
+    int32_t shard_offset;   /* this rank's residue, 0 <= shard_offset < shard_stride       */
+    int32_t kv_dtype;       /* ts_dtype of q, k_pool, v_pool and meta                      */
+} ts_layout;
+
+/* Metadata maintenance on KV append ("lightweight metadata — channel-wise
+ * min and max values of stored Key vectors — is maintained"; Eq. 1).
+ * For each sequence b with t = seq_lens_before[b]: global page j = t / S, slot = t % S.
+ * If this rank owns j: writes k_new[b] / v_new[b] ([B][Hkv][d], kv_dtype) into slot
+ * `slot` of block page_table[b][j / shard_stride] and sets, per kv head,
+ *   m = slot == 0 ? k : min(m, k),   M = slot == 0 ? k : max(M, k)   (exact, no rounding).
+ * Does not modify seq_lens (the caller advances it). */
+ts_status ts_meta_append(const ts_layout *layout, const void *k_new, const void *v_new,
+                         const int32_t *seq_lens_before, const int32_t *page_table,
+                         void *k_pool, void *v_pool, void *meta, void *stream);
+
+/* Bulk metadata (SPEC.md:65-73 recompute_metadata; prefill / cache import): for every
+ * owned page j < P_b of every sequence, meta of its block = min / max over its valid keys
+ * (tokens t < seq_lens[b]).  Blocks of pages >= P_b are not touched. */
+ts_status ts_meta_build(const ts_layout *layout, const void *k_pool, const int32_t *page_table,
+                        const int32_t *seq_lens, void *meta, void *stream);
+
+/* Page scoring (Eq. 2; Alg. 1 Step 1).  For every sequence b, kv head g
+ * and owned local page jl (global j = jl*stride + offset < P_b = ceil(seq_lens[b]/S)):
+ *   scores[b][g][jl] = max_{h in group(g)} sum_i max(q[b][h][i]*m_i, q[b][h][i]*M_i)
+ * (= Eq. 2 per head; GQA max over the group, reading R9), accumulated in fp32.  Entries
+ * for non-existent pages are -inf.  A page's score depends only on (q, its meta): the same
+ * bits whatever the sharding.  -0.0 is written as +0.0. */
+ts_status ts_score_pages(const ts_layout *layout, const void *q, const void *meta,
+                         const int32_t *page_table, const int32_t *seq_lens, float *scores,
+                         void *stream);
+
+/* Top-K selection (Alg. 1 Step 2 "radix select").
+ * scores [rows][stride] fp32.  Row r's candidates are the entries i < row_len[r]
+ * (row_len NULL: all `stride`) whose score is not -inf.  The id of entry i is
+ * ids_in[r][i] if ids_in != NULL, else i*id_stride + id_offset.  Selects
+ * kk = min(k, #candidates) entries with the largest scores; equal scores go to the lower
+ * id (reading R6).  Outputs: sel_ids [rows][k] int32, the kk ids ascending then -1
+ * padding; sel_scores [rows][k] fp32 (nullable), aligned with sel_ids, -inf padding;
+ * sel_count [rows] int32 = kk.  Deterministic; exact (integer key comparisons). */
+ts_status ts_select_topk(const float *scores, int32_t rows, int32_t stride, const int32_t *row_len,
+                         const int32_t *ids_in, int32_t id_stride, int32_t id_offset, int32_t k,
+                         int32_t *sel_ids, float *sel_scores, int32_t *sel_count, void *stream);
+
+/* Sparse attention (SparseAttn PAPER.md:169-172; Alg. 1 Steps 3-4).
+ * For q head h of sequence b (kv head g = h / G): over the valid tokens (t < seq_lens[b],
+ * reading R7) of the OWNED pages among sel_ids[b][g][0 .. sel_count[b][g]) (global ids,
+ * [B][Hkv][sel_stride]), a_t = scale * q.k_t, o = softmax(a) . V, lse = ln sum exp(a_t),
+ * fp32.  No attended token: o = 0, lse = -inf.  lse may be NULL.  Split-K over CTAs with an
+ * in-kernel log-sum-exp merge; ws (>= ts_attn_workspace_bytes, zero-filled once before
+ * first use; the library leaves it reusable) holds the partials. */
+ts_status ts_sparse_decode_attn(const ts_layout *layout, const void *q, const void *k_pool,
+                                const void *v_pool, const int32_t *page_table,
+                                const int32_t *seq_lens, const int32_t *sel_ids,
+                                const int32_t *sel_count, int32_t sel_stride, float scale,
+                                float *o, float *lse, void *ws, size_t ws_bytes, void *stream);
+
+/* The fused decode step (Alg. 1 end to end): score every page from
+ * meta, select K_b = min(P_b, max(1, floor(budget_tokens/S))) pages per (b, g), attend.
+ * Unsharded layouts only (shard_stride == 1; the sequence-sharded step is composed from
+ * the calls above plus two all-gathers).  sel_ids_out [B][Hkv][Kmax] and
+ * sel_count_out [B][Hkv] (Kmax = max(1, budget_tokens/S)) may be NULL.
+ * ws >= ts_workspace_bytes(layout, budget_tokens), zero-filled once before first use. */
+ts_status ts_decode_step(const ts_layout *layout, const void *q, const void *k_pool,
+                         const void *v_pool, const void *meta, const int32_t *page_table,
+                         const int32_t *seq_lens, int32_t budget_tokens, float scale, float *o,
+                         float *lse, int32_t *sel_ids_out, int32_t *sel_count_out, void *ws,
+                         size_t ws_bytes, void *stream);
+
+/* Log-sum-exp merge of `parts` partial attentions over disjoint token sets:
+ * o_parts [parts][rows][d], lse_parts [parts][rows] ->
+ *   lse = ln sum_p exp(lse_p),   o = sum_p exp(lse_p - lse) * o_p.
+ * Parts with lse = -inf contribute nothing; all -inf gives o = 0, lse = -inf. */
+ts_status ts_lse_merge(int32_t parts, int32_t rows, int32_t d, const float *o_parts,
+                       const float *lse_parts, float *o, float *lse, void *stream);
+
+/* Workspace sizes in bytes (host-only, no CUDA call). */
+size_t ts_workspace_bytes(const ts_layout *layout, int32_t budget_tokens);
+size_t ts_attn_workspace_bytes(const ts_layout *layout, int32_t sel_stride);
+
+/* Static strings (host-only). */
+const char *ts_status_str(ts_status status);
+const char *ts_version(void);
+
+/* Number of kernel launches the last successful host call on this thread enqueued
+ * (bench.py's gpu_launches accounting; host-only). */
+int32_t ts_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TINYSERVE_H */

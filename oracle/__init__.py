@@ -178,7 +178,7 @@ def select_topk(scores, row_len, k, ids_in=None, threads: int = 0):
     """
     sc = np.ascontiguousarray(scores, np.float64)
     rows, stride = sc.shape
-    rl = _i32(row_len)
+    rl = None if row_len is None else _i32(row_len)
     ids = None if ids_in is None else _i32(ids_in)
     out = np.zeros((rows, k), np.int32)
     oscore = np.zeros((rows, k), np.float64)

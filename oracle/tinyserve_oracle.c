@@ -199,7 +199,8 @@ int or_score_pages(const or_layout *L, const void *q, const double *mmin, const 
 /* ------------------------------------------------------------------------------------
  * Step 4 — Top-K (Alg. 1 Step 2): per row, kk = min(k, n) entries with
  * the largest score; equal scores go to the lower id (reading R6); output ids
- * ascending.  ids_in (nullable) gives each entry's id (candidate merge,
+ * ascending.  Entries with score -inf are "no page" and never selected
+ * (reading R8), so kk = min(k, #finite entries among the first row_len).  ids_in (nullable) gives each entry's id (candidate merge,
  * DESIGN.md §6); otherwise the id of entry i is i.  -0.0 and +0.0 compare equal.
  * Implemented as a full sort by (score desc, id asc) — a library sort, no selection trick.
  * ---------------------------------------------------------------------------------- */
@@ -224,13 +225,17 @@ int or_select_topk(const double *scores, int rows, int stride, const int32_t *ro
     set_threads(threads);
 #pragma omp parallel for schedule(dynamic)
     for (int r = 0; r < rows; ++r) {
-        const int n = row_len[r];
-        const int kk = n < k ? n : k;
-        or_cand *c = (or_cand *)malloc(sizeof(or_cand) * (n > 0 ? n : 1));
-        for (int i = 0; i < n; ++i) {
-            c[i].s = scores[(size_t)r * stride + i] + 0.0;  /* -0.0 -> +0.0 */
-            c[i].id = ids_in ? ids_in[(size_t)r * stride + i] : i;
+        const int len = row_len ? row_len[r] : stride;
+        or_cand *c = (or_cand *)malloc(sizeof(or_cand) * (len > 0 ? len : 1));
+        int n = 0;
+        for (int i = 0; i < len; ++i) {
+            const double s = scores[(size_t)r * stride + i];
+            if (s == -INFINITY) continue;       /* -inf = "no page" (reading R8) */
+            c[n].s = s + 0.0;                   /* -0.0 -> +0.0 (reading R6) */
+            c[n].id = ids_in ? ids_in[(size_t)r * stride + i] : i;
+            ++n;
         }
+        const int kk = n < k ? n : k;
         qsort(c, n, sizeof(or_cand), cmp_score_desc_id_asc);
         qsort(c, kk, sizeof(or_cand), cmp_id_asc);
         for (int i = 0; i < k; ++i) {

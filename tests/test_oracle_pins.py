@@ -226,6 +226,14 @@ def test_topk_rank_consistency_and_ids_in(orc):
     assert np.array_equal(ids_a, ids_b)
 
 
+def test_topk_neg_inf_is_no_page(orc):
+    """Reading R8: -inf entries (pages that do not exist) are never selected."""
+    s = np.array([[-np.inf, 1.0, -np.inf, 0.5, -np.inf, -np.inf]])
+    ids, sc, cnt = orc.select_topk(s, None, 4)
+    assert cnt[0] == 2 and ids[0].tolist() == [1, 3, -1, -1]
+    assert np.isneginf(sc[0, 2:]).all()
+
+
 def test_topk_candidate_merge_is_exact(orc):
     """global top-K == top-K of the union of per-shard top-Ks (block-cyclic
     ownership, global ids), on inputs with heavy ties."""
