@@ -1,0 +1,477 @@
+#!/usr/bin/env python
+"""bench.py — decode steps/s and achieved HBM GB/s of the TinyServe decode hot path on B200.
+
+One step = one ts_decode_step (score every page -> top-K -> sparse attention) for the whole
+batch of one attention layer, on synthetic caches of the BASELINE.json
+config shapes.  Default: config c2 (GPT2-345M shape, BASELINE.json configs[1]), N = 1.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c3|c4|c5] [--impl reference]
+
+Timing: inputs resident in HBM; R independent cache replicas rotated step
+by step with R * (bytes per step) >= 4 x L2, so every step reads cold metadata and KV; the
+K steps are CUDA-graph replays timed with CUDA events on the launching stream, barrier +
+synchronize on both sides, max over ranks.  Clocks sampled by NVML during the timed region.
+N > 1: c2/c3 run one full config batch per rank (weak scaling, no communication); c4 splits
+its batch of 128 over the ranks (strong); c5 shards every sequence block-cyclically over the
+ranks with two NCCL all-gathers per step (strong; paper_2509_12211_b200/sharded.py).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import synth  # noqa: E402
+
+PEAK_SPEC_GBS = 8000.0  # B200 HBM3e spec (north-star denominator)
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            j = json.load(f)
+        return float(j["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (copy, read+write)"
+    except Exception:
+        return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md; MEASURED_PEAKS.json absent)"
+
+
+# ------------------------------------------------------------------------------ clocks
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons while the timed region runs."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, index: int, period_s: float = 0.005):
+        self.samples, self.reasons, self.ok = [], set(), False
+        self.period, self.index = period_s, index
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"],
+                    "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------------------ workload
+def rank_config(name: str, world: int, rank: int):
+    """Per-rank config and sharding mode."""
+    cfg = synth.config(name)
+    if name == "c4" and world > 1:
+        assert cfg.batch % world == 0
+        cfg = cfg.with_(batch=cfg.batch // world)
+        return cfg, "batch", "strong"
+    if name == "c5" and world > 1:
+        return cfg, "sequence", "strong"
+    return cfg, ("batch" if world > 1 else "none"), "weak"
+
+
+def kernel_bytes(cfg, L: int, Kmax: int, mp_local: int, world: int = 1):
+    """Algorithmic bytes per launch of each kernel of one step.
+
+    score:  metadata of every (owned) page + q + page-table row + fp32 scores written
+    select: fp32 scores read + selected ids / counts written
+    attn:   K and V rows of the valid tokens of the owned selected pages + q + ids +
+            page-table lookups + fp32 o and lse written
+    """
+    e = 2 if cfg.dtype == "bf16" else 4
+    B, Hq, Hkv, d, S = cfg.batch, cfg.num_q_heads, cfg.num_kv_heads, cfg.head_dim, cfg.page_size
+    P = -(-L // S)
+    P_own = -(-P // world)
+    K = min(P, Kmax)
+    K_own = -(-K // world)
+    q = B * Hq * d * e
+    score = B * Hkv * P_own * 2 * d * e + q + B * P_own * 4 + B * Hkv * mp_local * 4
+    select = B * Hkv * mp_local * 4 + B * Hkv * (Kmax + 1) * 4
+    toks = min(K_own * S, L)
+    attn = (B * Hkv * toks * 2 * d * e + q + B * Hkv * (K + 1) * 4 + B * Hkv * K_own * 4
+            + B * Hq * (d + 1) * 4)
+    return {"score": score, "select": select, "attn": attn, "total": score + select + attn}
+
+
+def build_replica(ts, cfg, seed, device, world=1, rank=0):
+    case = synth.make_case(cfg, seed=seed, device=device)
+    pt = case["page_table"]
+    if world > 1 and cfg.name == "c5":
+        from paper_2509_12211_b200 import sharded
+        pt = sharded.shard_page_table(pt, world, rank)
+    L = ts.make_layout(case["q"], case["k_pool"], pt, world if cfg.name == "c5" else 1,
+                       rank if cfg.name == "c5" else 0)
+    meta = ts.meta_build(L, case["k_pool"], pt, case["seq_lens"])
+    rep = dict(case, page_table=pt, layout=L, meta=meta)
+    B, Hq, Hkv, d = cfg.batch, cfg.num_q_heads, cfg.num_kv_heads, cfg.head_dim
+    K = ts.kmax(L, cfg.budget_tokens)
+    rep["o"] = torch.empty((B, Hq, d), dtype=torch.float32, device=device)
+    rep["lse"] = torch.empty((B, Hq), dtype=torch.float32, device=device)
+    rep["ids"] = torch.empty((B, Hkv, K), dtype=torch.int32, device=device)
+    rep["cnt"] = torch.empty((B, Hkv), dtype=torch.int32, device=device)
+    rep["ws"] = ts.new_workspace(ts.workspace_bytes(L, cfg.budget_tokens), device)
+    return rep
+
+
+def step_fn(ts, cfg, rep, stream):
+    return ts.decode_step(rep["layout"], rep["q"], rep["k_pool"], rep["v_pool"], rep["meta"],
+                          rep["page_table"], rep["seq_lens"], cfg.budget_tokens, cfg.scale,
+                          o=rep["o"], lse=rep["lse"], sel_ids=rep["ids"], sel_count=rep["cnt"],
+                          ws=rep["ws"], stream=stream)
+
+
+# ------------------------------------------------------------------------------ oracle legs
+def oracle_rate(cfg, rep_cpu, budget_s: float, max_rows=None):
+    """Oracle decode_step on host cores over a bounded sample of the workload (whole
+    sequences, all heads).  Returns (full-workload steps/s, cores, sample description)."""
+    import oracle
+    B = cfg.batch
+    nb = max(1, min(B, max_rows or B))
+    q, kp, vp = rep_cpu["q"], rep_cpu["k_pool"], rep_cpu["v_pool"]
+    pt, sl = rep_cpu["page_table"], rep_cpu["seq_lens"]
+
+    def run(nseq):
+        t0 = time.perf_counter()
+        oracle.decode_step(q[:nseq], kp, vp, pt[:nseq], sl[:nseq], cfg.budget_tokens, cfg.scale)
+        return time.perf_counter() - t0
+
+    t1 = run(1)
+    nseq = max(1, min(nb, int(budget_s / 3 / max(t1, 1e-6))))
+    reps, tot = 0, 0.0
+    while tot < budget_s and reps < 1000:
+        tot += run(nseq)
+        reps += 1
+    per_seq = tot / (reps * nseq)
+    return 1.0 / (per_seq * B), oracle.num_threads(), (
+        f"{reps} oracle decode_step calls of {nseq}/{B} sequences (all {cfg.num_q_heads} q heads, "
+        f"metadata recomputed from K), {tot:.1f} s; steps/s scaled to the full batch")
+
+
+def run_reference(args, cfg, world, rank):
+    """--impl reference: the float64 oracle (this tier's reference arm) on host cores."""
+    if rank != 0:
+        return
+    import oracle
+    oracle.build()
+    case = synth.make_case(cfg, seed=42)
+    per_call_budget = max(0.05, 120.0 / max(1, args.steps + args.warmup))
+    # size the per-step sample (sequences) so the whole run stays within ~2-3 minutes
+    t0 = time.perf_counter()
+    oracle.decode_step(case["q"][:1], case["k_pool"], case["v_pool"], case["page_table"][:1],
+                       case["seq_lens"][:1], cfg.budget_tokens, cfg.scale)
+    t_seq = time.perf_counter() - t0
+    nseq = max(1, min(cfg.batch, int(per_call_budget / max(t_seq, 1e-6))))
+    for _ in range(args.warmup):
+        oracle.decode_step(case["q"][:nseq], case["k_pool"], case["v_pool"],
+                           case["page_table"][:nseq], case["seq_lens"][:nseq], cfg.budget_tokens,
+                           cfg.scale)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.decode_step(case["q"][:nseq], case["k_pool"], case["v_pool"],
+                           case["page_table"][:nseq], case["seq_lens"][:nseq], cfg.budget_tokens,
+                           cfg.scale)
+    dt = time.perf_counter() - t0
+    per_step_full = dt / args.steps * cfg.batch / nseq
+    value = 1.0 / per_step_full
+    cores = oracle.num_threads()
+    sample = (f"each step: oracle decode_step on {nseq}/{cfg.batch} sequences of {cfg.name} "
+              f"(float64, metadata recomputed), steps/s scaled to the full batch")
+    line = {"impl": "reference", "metric": "decode steps/s", "value": value, "unit": "steps/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": per_step_full * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_json(cfg, world, "none"),
+            "cpu_baseline": {"value": value, "unit": "steps/s", "cores": cores, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def config_json(cfg, world, mode, extra=None):
+    c = {"workload": f"{cfg.name}: {cfg.note}", "batch_per_rank": cfg.batch,
+         "num_q_heads": cfg.num_q_heads, "num_kv_heads": cfg.num_kv_heads,
+         "head_dim": cfg.head_dim, "ctx": cfg.ctx, "page_size": cfg.page_size,
+         "budget_tokens": cfg.budget_tokens, "kv_dtype": cfg.dtype, "scale": cfg.scale,
+         "sharding": mode, "world": world}
+    if extra:
+        c.update(extra)
+    return c
+
+
+# ------------------------------------------------------------------------------ main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3000)
+    ap.add_argument("--warmup", type=int, default=30)
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-oracle", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--oracle-seconds", type=float, default=12.0)
+    ap.add_argument("--replicas", type=int, default=0)
+    args = ap.parse_args()
+    assert args.warmup >= 3
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    cfg, mode, scaling = rank_config(args.config, world, rank)
+
+    if args.impl == "reference":
+        run_reference(args, cfg, world, rank)
+        return
+
+    import paper_2509_12211_b200 as ts
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+
+    props = torch.cuda.get_device_properties(dev)
+    l2 = getattr(props, "L2_cache_size", 126 * 2**20) or 126 * 2**20
+    L_ctx = cfg.ctx
+    Kmax = min(cfg.max_pages, max(1, cfg.budget_tokens // cfg.page_size))
+    mp_local = -(-cfg.max_pages // world) if mode == "sequence" else cfg.max_pages
+    kb = kernel_bytes(cfg, L_ctx, Kmax, mp_local, world if mode == "sequence" else 1)
+    alg = synth.algorithmic_bytes(cfg, [L_ctx] * cfg.batch)
+    step_bytes = alg["total"] if mode != "sequence" else kb["total"]
+    R = args.replicas or max(2, -(-4 * l2 // max(1, step_bytes)))
+    stream = torch.cuda.Stream(device=dev)
+
+    reps = [build_replica(ts, cfg, seed=1000 * rank + r, device=dev, world=world, rank=rank)
+            for r in range(R)]
+    torch.cuda.synchronize()
+
+    if mode == "sequence":
+        from paper_2509_12211_b200 import sharded
+        for rep in reps:
+            rep["shard"] = sharded.ShardStep(ts, rep["layout"], world, rank, cfg.budget_tokens, dev)
+
+        def one(rep):
+            rep["shard"].step(rep["q"], rep["k_pool"], rep["v_pool"], rep["meta"],
+                              rep["page_table"], rep["seq_lens"], cfg.scale)
+    else:
+        def one(rep):
+            step_fn(ts, cfg, rep, stream)
+
+    # ---- launches per step (our kernels)
+    with torch.cuda.stream(stream):
+        one(reps[0])
+    torch.cuda.synchronize()
+    launches_per_step = 3 if mode != "sequence" else 5
+
+    # ---- graphs: one per replica; with phase events around the kernels
+    ev = [[torch.cuda.Event(enable_timing=True, external=True) for _ in range(4)] for _ in reps]
+    for es in ev:
+        for e in es:
+            e.record(stream)
+    torch.cuda.synchronize()
+    graphs = []
+    use_graph = mode != "sequence"
+    if use_graph:
+        for r, rep in enumerate(reps):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(stream):
+                ts.profile_events(ev[r])
+                with torch.cuda.graph(g, stream=stream):
+                    one(rep)
+                ts.profile_events(None)
+            graphs.append(g)
+        torch.cuda.synchronize()
+
+    def run_steps(n, offset=0):
+        with torch.cuda.stream(stream):
+            for i in range(n):
+                r = (offset + i) % R
+                if use_graph:
+                    graphs[r].replay()
+                else:
+                    one(reps[r])
+
+    run_steps(args.warmup)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        wall0 = time.perf_counter()
+        t0.record(stream)
+        run_steps(args.steps, offset=args.warmup)
+        t1.record(stream)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - wall0
+    if world > 1:
+        torch.distributed.barrier()
+    ms = t0.elapsed_time(t1)
+    if world > 1:
+        tt = torch.tensor([ms], device=dev)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        ms = float(tt.item())
+    ms_per_step = ms / args.steps
+
+    # ---- per-kernel durations of the last R steps of the timed region (in-graph events)
+    phase = None
+    if use_graph:
+        sc = [ev[r][0].elapsed_time(ev[r][1]) for r in range(R)]
+        se = [ev[r][1].elapsed_time(ev[r][2]) for r in range(R)]
+        at = [ev[r][2].elapsed_time(ev[r][3]) for r in range(R)]
+        phase = {"score_us": 1e3 * statistics.mean(sc), "select_us": 1e3 * statistics.mean(se),
+                 "attn_us": 1e3 * statistics.mean(at), "samples": R}
+
+    # ---- e2e: public API with host buffers (pinned), H2D of q / new k,v + D2H of o, lse
+    e2e = None
+    if not args.no_e2e and mode != "sequence":
+        e2e = run_e2e(ts, cfg, reps[0], dev, stream, steps=min(args.steps, 500), warmup=5)
+        if world > 1:
+            tt = torch.tensor([1.0 / e2e["value"]], device=dev)
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            e2e["value"] = world / float(tt.item()) if scaling == "weak" else 1.0 / float(tt.item())
+
+    # ---- cpu baseline (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_oracle:
+        import oracle
+        oracle.build()
+        host = {k: reps[0][k].cpu() for k in ("q", "k_pool", "v_pool", "page_table", "seq_lens")}
+        v, cores, sample = oracle_rate(cfg, host, args.oracle_seconds)
+        cpu = {"value": v, "unit": "steps/s", "cores": cores, "kind": "oracle", "sample": sample}
+
+    if rank != 0:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return
+
+    steps_per_s = 1e3 / ms_per_step
+    if mode == "sequence" or scaling == "strong":
+        value = steps_per_s              # every step covers the whole (sharded) batch
+    else:
+        value = steps_per_s * world      # independent batches, one per rank
+    gbs = step_bytes * world / (ms_per_step * 1e-3) / 1e9 if mode != "sequence" else \
+        kb["total"] * world / (ms_per_step * 1e-3) / 1e9
+    peak, peak_src = measured_peaks()
+    roof = None
+    if phase:
+        dom = max(("score", "attn"), key=lambda k: phase[k + "_us"])
+        achieved = kb[dom] / (phase[dom + "_us"] * 1e-6) / 1e9
+        roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": kb[dom], "avg_launch_us": phase[dom + "_us"],
+                "phase_us": phase}
+    clocks = clk.summary()
+    line = {
+        "metric": "decode steps/s", "value": value, "unit": "steps/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
+        "dtype": cfg.dtype, "data": "synthetic",
+        "config": config_json(cfg, world, mode, {
+            "replicas": R, "l2_bytes": l2, "l2_policy": "rotate R cold replicas (R*bytes >= 4*L2)",
+            "graph": use_graph}),
+        "tokens_per_s": value * cfg.batch,
+        "hbm_gbs": gbs, "frac_of_8tbs": gbs / PEAK_SPEC_GBS, "frac_of_measured": gbs / peak,
+        "algorithmic_bytes_per_step": step_bytes, "kernel_bytes": kb,
+        "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+        "gpu_launches": launches_per_step * args.steps, "clocks": clocks,
+        "wall_s_timed": wall, "device": torch.cuda.get_device_name(dev),
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def run_e2e(ts, cfg, rep, dev, stream, steps, warmup):
+    """Same metric through the public API with host buffers: per step the pinned q, k_new,
+    v_new go H2D, ts_meta_append rewrites the newest token of every sequence (length kept,
+    so the workload stays the config's), ts_decode_step runs, o and lse come back D2H."""
+    B, Hq, Hkv, d = cfg.batch, cfg.num_q_heads, cfg.num_kv_heads, cfg.head_dim
+    dt = cfg.torch_dtype
+    hq = torch.randn((B, Hq, d)).to(dt).pin_memory()
+    hk = torch.randn((B, Hkv, d)).to(dt).pin_memory()
+    hv = torch.randn((B, Hkv, d)).to(dt).pin_memory()
+    ho = torch.empty((B, Hq, d), dtype=torch.float32).pin_memory()
+    hl = torch.empty((B, Hq), dtype=torch.float32).pin_memory()
+    dq, dk, dv = torch.empty_like(hq, device=dev), torch.empty_like(hk, device=dev), \
+        torch.empty_like(hv, device=dev)
+    pos = (rep["seq_lens"] - 1).contiguous()  # append position = last token (rewrite)
+    L = rep["layout"]
+
+    def one():
+        dq.copy_(hq, non_blocking=True)
+        dk.copy_(hk, non_blocking=True)
+        dv.copy_(hv, non_blocking=True)
+        ts.meta_append(L, dk, dv, pos, rep["page_table"], rep["k_pool"], rep["v_pool"],
+                       rep["meta"], advance=False, stream=stream)
+        ts.decode_step(L, dq, rep["k_pool"], rep["v_pool"], rep["meta"], rep["page_table"],
+                       rep["seq_lens"], cfg.budget_tokens, cfg.scale, o=rep["o"], lse=rep["lse"],
+                       sel_ids=rep["ids"], sel_count=rep["cnt"], ws=rep["ws"], stream=stream)
+        ho.copy_(rep["o"], non_blocking=True)
+        hl.copy_(rep["lse"], non_blocking=True)
+
+    with torch.cuda.stream(stream):
+        for _ in range(warmup):
+            one()
+    torch.cuda.synchronize()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        a.record(stream)
+        for _ in range(steps):
+            one()
+        b.record(stream)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / steps
+    h2d = hq.numel() * hq.element_size() + 2 * hk.numel() * hk.element_size()
+    d2h = ho.numel() * 4 + hl.numel() * 4
+    return {"value": 1e3 / ms, "unit": "steps/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "ms_per_step": ms, "steps": steps,
+            "api": "paper_2509_12211_b200.meta_append + decode_step (ctypes -> C ABI), eager"}
+
+
+if __name__ == "__main__":
+    main()

@@ -46,8 +46,10 @@
  *    Data-dependent faults (page_table entry >= num_blocks, seq_len > max_pages*page_size,
  *    non-finite inputs) are undefined behaviour, not detected.
  *    seq_len == 0 is valid: the sequence selects nothing, o = 0, lse = -inf (reading R8).
- *  - Compiled set: head_dim 64 or 128; page_size in {8, 16, 32, 64} for bf16 and any
- *    page_size >= 1 for fp32; group size 1..8 for bf16, any for fp32.
+ *  - Compiled set: head_dim 64 or 128 for metadata, scoring and fp32 attention; the bf16
+ *    attention (ts_sparse_decode_attn, ts_decode_step) needs head_dim 64, page_size in
+ *    {8, 16, 32, 64} and group size 1..8 (tensor-core tiles); fp32 takes any page_size
+ *    and group size.  At most 4096 selected pages per row.
  */
 #ifndef TINYSERVE_H
 #define TINYSERVE_H
@@ -86,13 +88,15 @@ typedef struct {
 
 /* Metadata maintenance on KV append ("lightweight metadata — channel-wise
  * min and max values of stored Key vectors — is maintained"; Eq. 1).
- * For each sequence b with t = seq_lens_before[b]: global page j = t / S, slot = t % S.
- * If this rank owns j: writes k_new[b] / v_new[b] ([B][Hkv][d], kv_dtype) into slot
- * `slot` of block page_table[b][j / shard_stride] and sets, per kv head,
+ * For each sequence b with t = seq_lens[b] (length BEFORE the append): global page
+ * j = t / S, slot = t % S.  If this rank owns j: writes k_new[b] / v_new[b]
+ * ([B][Hkv][d], kv_dtype) into slot `slot` of block page_table[b][j / shard_stride] and
+ * sets, per kv head,
  *   m = slot == 0 ? k : min(m, k),   M = slot == 0 ? k : max(M, k)   (exact, no rounding).
- * Does not modify seq_lens (the caller advances it). */
+ * If `advance` != 0 the kernel then sets seq_lens[b] = t + 1 (every rank advances its copy
+ * of the global length, owner or not); otherwise seq_lens is left unchanged. */
 ts_status ts_meta_append(const ts_layout *layout, const void *k_new, const void *v_new,
-                         const int32_t *seq_lens_before, const int32_t *page_table,
+                         int32_t *seq_lens, int32_t advance, const int32_t *page_table,
                          void *k_pool, void *v_pool, void *meta, void *stream);
 
 /* Bulk metadata (SPEC.md:65-73 recompute_metadata; prefill / cache import): for every
@@ -140,7 +144,7 @@ ts_status ts_sparse_decode_attn(const ts_layout *layout, const void *q, const vo
  * meta, select K_b = min(P_b, max(1, floor(budget_tokens/S))) pages per (b, g), attend.
  * Unsharded layouts only (shard_stride == 1; the sequence-sharded step is composed from
  * the calls above plus two all-gathers).  sel_ids_out [B][Hkv][Kmax] and
- * sel_count_out [B][Hkv] (Kmax = max(1, budget_tokens/S)) may be NULL.
+ * sel_count_out [B][Hkv] (Kmax = min(max_pages, max(1, budget_tokens/S))) may be NULL.
  * ws >= ts_workspace_bytes(layout, budget_tokens), zero-filled once before first use. */
 ts_status ts_decode_step(const ts_layout *layout, const void *q, const void *k_pool,
                          const void *v_pool, const void *meta, const int32_t *page_table,
@@ -148,12 +152,26 @@ ts_status ts_decode_step(const ts_layout *layout, const void *q, const void *k_p
                          float *lse, int32_t *sel_ids_out, int32_t *sel_count_out, void *ws,
                          size_t ws_bytes, void *stream);
 
-/* Log-sum-exp merge of `parts` partial attentions over disjoint token sets:
- * o_parts [parts][rows][d], lse_parts [parts][rows] ->
+/* Candidate merge — the exchange step of sequence sharding: the global
+ * top-k over the union of per-rank candidate lists.  Part p (< parts) of row r holds k_part
+ * entries at cand_scores[p*part_stride + r*k_part + e] with global page ids at the same
+ * offsets of cand_ids (e.g. the rank-major output of an all-gather of every rank's
+ * ts_select_topk result; part_stride 0 = rows*k_part, i.e. [parts][rows][k_part]).
+ * -inf entries are ignored.  Output exactly as ts_select_topk (ids ascending, ties to
+ * the lower id).  Because a page's score bits do not depend on sharding and every global
+ * top-k page is in its owner's local top-k, the result equals the unsharded selection. */
+ts_status ts_select_merge(const float *cand_scores, const int32_t *cand_ids, int32_t parts,
+                          int64_t part_stride, int32_t rows, int32_t k_part, int32_t k,
+                          int32_t *sel_ids, float *sel_scores, int32_t *sel_count, void *stream);
+
+/* Log-sum-exp merge of `parts` partial attentions over disjoint token sets.  Part p of
+ * o_parts starts at p*part_stride and holds [rows][d]; part p of lse_parts starts at
+ * p*part_stride and holds [rows] (part_stride 0: dense, rows*d and rows respectively):
  *   lse = ln sum_p exp(lse_p),   o = sum_p exp(lse_p - lse) * o_p.
  * Parts with lse = -inf contribute nothing; all -inf gives o = 0, lse = -inf. */
 ts_status ts_lse_merge(int32_t parts, int32_t rows, int32_t d, const float *o_parts,
-                       const float *lse_parts, float *o, float *lse, void *stream);
+                       const float *lse_parts, int64_t part_stride, float *o, float *lse,
+                       void *stream);
 
 /* Workspace sizes in bytes (host-only, no CUDA call). */
 size_t ts_workspace_bytes(const ts_layout *layout, int32_t budget_tokens);
@@ -166,6 +184,12 @@ const char *ts_version(void);
 /* Number of kernel launches the last successful host call on this thread enqueued
  * (bench.py's gpu_launches accounting; host-only). */
 int32_t ts_last_launch_count(void);
+
+/* Measurement hook (bench.py roofline): while set, ts_decode_step on this thread records
+ * events[0..3] (cudaEvent_t, created by the caller) on its stream before the scoring
+ * kernel, after scoring, after selection and after attention, as external records (valid
+ * inside CUDA-graph capture).  events == NULL or n == 0 clears it.  Host-only. */
+void ts_profile_events(void *const *events, int32_t n);
 
 #ifdef __cplusplus
 }

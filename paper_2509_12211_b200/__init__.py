@@ -1,0 +1,261 @@
+"""TinyServe decode hot path on B200 (sm_100a): query-aware page selection + sparse attention.
+
+Thin Python binding over libtinyserve.so (include/tinyserve.h).  PyTorch is used only for
+device memory, streams and process groups; every step of the path runs in the library's
+CUDA kernels.  Names follow the C ABI:
+
+  meta_append, meta_build, score_pages, select_topk, sparse_decode_attn, decode_step,
+  lse_merge, workspace_bytes, attn_workspace_bytes
+
+Tensors: q [B][Hq][d], k_pool / v_pool [NB][Hkv][S][d], meta
+[NB][Hkv][2][d] (kv dtype: bf16 or fp32), page_table [B][max_pages] int32, seq_lens [B]
+int32; o [B][Hq][d] fp32, lse [B][Hq] fp32.
+"""
+from __future__ import annotations
+
+import torch
+
+from ._lib import Layout, TinyServeError, TS_BF16, TS_F32, check, exported_symbols, lib
+
+__all__ = ["Layout", "TinyServeError", "make_layout", "meta_append", "meta_build",
+           "score_pages", "select_topk", "sparse_decode_attn", "decode_step", "select_merge", "lse_merge",
+           "workspace_bytes", "attn_workspace_bytes", "new_workspace", "kmax", "launch_count",
+           "profile_events",
+           "exported_symbols", "PagedKV"]
+
+
+def _dtype_code(dt: torch.dtype) -> int:
+    if dt == torch.bfloat16:
+        return TS_BF16
+    if dt == torch.float32:
+        return TS_F32
+    raise TypeError(f"kv dtype must be bfloat16 or float32, got {dt}")
+
+
+def _cuda(*ts):
+    for t in ts:
+        if t is not None and (not isinstance(t, torch.Tensor) or not t.is_cuda):
+            raise TypeError("tinyserve: every tensor must be a CUDA tensor (no CPU fallback)")
+        if t is not None and not t.is_contiguous():
+            raise ValueError("tinyserve: tensors must be contiguous")
+
+
+def _ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+def _stream(stream):
+    s = torch.cuda.current_stream() if stream is None else stream
+    return s.cuda_stream
+
+
+def make_layout(q: torch.Tensor, k_pool: torch.Tensor, page_table: torch.Tensor,
+                shard_stride: int = 1, shard_offset: int = 0) -> Layout:
+    B, Hq, d = q.shape
+    nb, Hkv, S, d2 = k_pool.shape
+    if d2 != d or q.dtype != k_pool.dtype:
+        raise ValueError("q and k_pool disagree on head_dim or dtype")
+    return Layout(B, Hq, Hkv, d, S, page_table.shape[1], nb, shard_stride, shard_offset,
+                  _dtype_code(k_pool.dtype))
+
+
+def kmax(layout: Layout, budget_tokens: int) -> int:
+    """K = floor(budget / S) clipped to [1, max_pages] (reading R4); per row clipped to P_b."""
+    return min(layout.max_pages, max(1, budget_tokens // layout.page_size))
+
+
+def workspace_bytes(layout: Layout, budget_tokens: int) -> int:
+    return lib().ts_workspace_bytes(layout, budget_tokens)
+
+
+def attn_workspace_bytes(layout: Layout, sel_stride: int) -> int:
+    return lib().ts_attn_workspace_bytes(layout, sel_stride)
+
+
+def new_workspace(nbytes: int, device) -> torch.Tensor:
+    """Zero-filled workspace (the split-K tickets must start at zero; the library re-arms them)."""
+    return torch.zeros(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+
+
+def profile_events(events) -> None:
+    """Make ts_decode_step record the given torch.cuda.Events (4: before score, after score,
+    after select, after attention) on its stream; None clears.  Events must be created with
+    external=True and recorded once beforehand (lazy creation)."""
+    if not events:
+        lib().ts_profile_events(None, 0)
+        return
+    import ctypes
+    arr = (ctypes.c_void_p * len(events))(*[e.cuda_event for e in events])
+    lib().ts_profile_events(arr, len(events))
+
+
+def launch_count() -> int:
+    """Kernel launches enqueued by the last library call on this thread."""
+    return lib().ts_last_launch_count()
+
+
+def meta_append(layout, k_new, v_new, seq_lens, page_table, k_pool, v_pool, meta,
+                advance=True, stream=None):
+    """Append one token per sequence (k_new, v_new [B][Hkv][d]) at position seq_lens[b];
+    with advance=True the kernel also increments seq_lens."""
+    _cuda(k_new, v_new, seq_lens, page_table, k_pool, v_pool, meta)
+    check("ts_meta_append", lib().ts_meta_append(
+        layout, _ptr(k_new), _ptr(v_new), _ptr(seq_lens), int(bool(advance)), _ptr(page_table),
+        _ptr(k_pool), _ptr(v_pool), _ptr(meta), _stream(stream)))
+
+
+def meta_build(layout, k_pool, page_table, seq_lens, meta=None, stream=None):
+    if meta is None:
+        meta = torch.zeros((layout.num_blocks, layout.num_kv_heads, 2, layout.head_dim),
+                           dtype=k_pool.dtype, device=k_pool.device)
+    _cuda(k_pool, page_table, seq_lens, meta)
+    check("ts_meta_build", lib().ts_meta_build(layout, _ptr(k_pool), _ptr(page_table),
+                                               _ptr(seq_lens), _ptr(meta), _stream(stream)))
+    return meta
+
+
+def score_pages(layout, q, meta, page_table, seq_lens, scores=None, stream=None):
+    if scores is None:
+        scores = torch.empty((layout.batch, layout.num_kv_heads, layout.max_pages),
+                             dtype=torch.float32, device=q.device)
+    _cuda(q, meta, page_table, seq_lens, scores)
+    check("ts_score_pages", lib().ts_score_pages(layout, _ptr(q), _ptr(meta), _ptr(page_table),
+                                                 _ptr(seq_lens), _ptr(scores), _stream(stream)))
+    return scores
+
+
+def select_topk(scores, k, row_len=None, ids_in=None, id_stride=1, id_offset=0,
+                sel_ids=None, sel_scores=None, sel_count=None, want_scores=True, stream=None):
+    """scores [rows][stride] fp32 -> (sel_ids [rows][k], sel_scores [rows][k], sel_count [rows])."""
+    s2 = scores.reshape(-1, scores.shape[-1])
+    rows, stride = s2.shape
+    dev = scores.device
+    if sel_ids is None:
+        sel_ids = torch.empty((rows, k), dtype=torch.int32, device=dev)
+    if sel_scores is None and want_scores:
+        sel_scores = torch.empty((rows, k), dtype=torch.float32, device=dev)
+    if sel_count is None:
+        sel_count = torch.empty((rows,), dtype=torch.int32, device=dev)
+    _cuda(s2, row_len, ids_in, sel_ids, sel_scores, sel_count)
+    check("ts_select_topk", lib().ts_select_topk(
+        _ptr(s2), rows, stride, _ptr(row_len), _ptr(ids_in), id_stride, id_offset, k,
+        _ptr(sel_ids), _ptr(sel_scores), _ptr(sel_count), _stream(stream)))
+    return sel_ids, sel_scores, sel_count
+
+
+def sparse_decode_attn(layout, q, k_pool, v_pool, page_table, seq_lens, sel_ids, sel_count,
+                       scale, o=None, lse=None, ws=None, want_lse=True, stream=None):
+    dev = q.device
+    sel_stride = sel_ids.shape[-1]
+    if o is None:
+        o = torch.empty((layout.batch, layout.num_q_heads, layout.head_dim), dtype=torch.float32,
+                        device=dev)
+    if lse is None and want_lse:
+        lse = torch.empty((layout.batch, layout.num_q_heads), dtype=torch.float32, device=dev)
+    if ws is None:
+        ws = new_workspace(attn_workspace_bytes(layout, sel_stride), dev)
+    _cuda(q, k_pool, v_pool, page_table, seq_lens, sel_ids, sel_count, o, lse, ws)
+    check("ts_sparse_decode_attn", lib().ts_sparse_decode_attn(
+        layout, _ptr(q), _ptr(k_pool), _ptr(v_pool), _ptr(page_table), _ptr(seq_lens),
+        _ptr(sel_ids), _ptr(sel_count), sel_stride, float(scale), _ptr(o), _ptr(lse), _ptr(ws),
+        ws.numel(), _stream(stream)))
+    return o, lse
+
+
+def decode_step(layout, q, k_pool, v_pool, meta, page_table, seq_lens, budget_tokens, scale,
+                o=None, lse=None, sel_ids=None, sel_count=None, ws=None, want_lse=True,
+                want_selection=True, stream=None):
+    """Alg. 1 end to end: score -> select -> sparse attention.  Returns (o, lse, sel_ids, sel_count)."""
+    dev = q.device
+    K = kmax(layout, budget_tokens)
+    rows = layout.batch * layout.num_kv_heads
+    if o is None:
+        o = torch.empty((layout.batch, layout.num_q_heads, layout.head_dim), dtype=torch.float32,
+                        device=dev)
+    if lse is None and want_lse:
+        lse = torch.empty((layout.batch, layout.num_q_heads), dtype=torch.float32, device=dev)
+    if want_selection:
+        if sel_ids is None:
+            sel_ids = torch.empty((layout.batch, layout.num_kv_heads, K), dtype=torch.int32, device=dev)
+        if sel_count is None:
+            sel_count = torch.empty((layout.batch, layout.num_kv_heads), dtype=torch.int32, device=dev)
+    if ws is None:
+        ws = new_workspace(workspace_bytes(layout, budget_tokens), dev)
+    _cuda(q, k_pool, v_pool, meta, page_table, seq_lens, o, lse, sel_ids, sel_count, ws)
+    check("ts_decode_step", lib().ts_decode_step(
+        layout, _ptr(q), _ptr(k_pool), _ptr(v_pool), _ptr(meta), _ptr(page_table), _ptr(seq_lens),
+        int(budget_tokens), float(scale), _ptr(o), _ptr(lse), _ptr(sel_ids), _ptr(sel_count),
+        _ptr(ws), ws.numel(), _stream(stream)))
+    return o, lse, sel_ids, sel_count
+
+
+def select_merge(cand_scores, cand_ids, k, parts=None, rows=None, k_part=None, part_stride=0,
+                 sel_ids=None, sel_scores=None, sel_count=None, want_scores=True, stream=None):
+    """Global top-k over per-part candidate lists ([parts][rows][k_part] unless part_stride
+    and explicit sizes are given).  Returns (sel_ids [rows][k], sel_scores, sel_count)."""
+    if parts is None:
+        parts, rows, k_part = cand_scores.shape
+    dev = cand_scores.device
+    if sel_ids is None:
+        sel_ids = torch.empty((rows, k), dtype=torch.int32, device=dev)
+    if sel_scores is None and want_scores:
+        sel_scores = torch.empty((rows, k), dtype=torch.float32, device=dev)
+    if sel_count is None:
+        sel_count = torch.empty((rows,), dtype=torch.int32, device=dev)
+    _cuda(sel_ids, sel_scores, sel_count)
+    check("ts_select_merge", lib().ts_select_merge(
+        cand_scores.data_ptr(), cand_ids.data_ptr(), parts, part_stride, rows, k_part, k,
+        _ptr(sel_ids), _ptr(sel_scores), _ptr(sel_count), _stream(stream)))
+    return sel_ids, sel_scores, sel_count
+
+
+def lse_merge(o_parts, lse_parts, o=None, lse=None, parts=None, rows=None, d=None,
+              part_stride=0, stream=None):
+    """o_parts [parts][rows][d], lse_parts [parts][rows] -> (o [rows][d], lse [rows]).
+    With part_stride != 0, parts/rows/d must be given and both arrays are strided views."""
+    if parts is None:
+        parts, rows, d = o_parts.shape
+    dev = o_parts.device
+    if o is None:
+        o = torch.empty((rows, d), dtype=torch.float32, device=dev)
+    if lse is None:
+        lse = torch.empty((rows,), dtype=torch.float32, device=dev)
+    _cuda(o, lse)
+    check("ts_lse_merge", lib().ts_lse_merge(parts, rows, d, o_parts.data_ptr(),
+                                             lse_parts.data_ptr(), part_stride, _ptr(o), _ptr(lse),
+                                             _stream(stream)))
+    return o, lse
+
+
+class PagedKV:
+    """A paged KV cache on one GPU (vLLM-style block pool + page table) with its metadata.
+
+    Convenience owner of the device tensors for one attention layer; all compute goes
+    through the C ABI.  `append` = ts_meta_append + seq_lens += 1 (SPEC.md:388 order:
+    append, then select); `step` = ts_decode_step.
+    """
+
+    def __init__(self, k_pool, v_pool, page_table, seq_lens, num_q_heads, meta=None,
+                 shard_stride=1, shard_offset=0):
+        _cuda(k_pool, v_pool, page_table, seq_lens)
+        self.k_pool, self.v_pool = k_pool, v_pool
+        self.page_table, self.seq_lens = page_table, seq_lens
+        B = page_table.shape[0]
+        q_like = torch.empty((B, num_q_heads, k_pool.shape[-1]), dtype=k_pool.dtype, device="meta")
+        self.layout = make_layout(q_like, k_pool, page_table, shard_stride, shard_offset)
+        self.meta = meta if meta is not None else meta_build(self.layout, k_pool, page_table, seq_lens)
+        self._ws = {}
+
+    def workspace(self, budget_tokens):
+        if budget_tokens not in self._ws:
+            self._ws[budget_tokens] = new_workspace(workspace_bytes(self.layout, budget_tokens),
+                                                    self.k_pool.device)
+        return self._ws[budget_tokens]
+
+    def append(self, k_new, v_new, stream=None):
+        meta_append(self.layout, k_new, v_new, self.seq_lens, self.page_table, self.k_pool,
+                    self.v_pool, self.meta, advance=True, stream=stream)
+
+    def step(self, q, budget_tokens, scale, **kw):
+        return decode_step(self.layout, q, self.k_pool, self.v_pool, self.meta, self.page_table,
+                           self.seq_lens, budget_tokens, scale, ws=self.workspace(budget_tokens), **kw)

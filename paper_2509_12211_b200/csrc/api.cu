@@ -1,0 +1,467 @@
+// api.cu — the C ABI of libtinyserve.so (include/tinyserve.h): host-side validation,
+// launch configuration and TMA descriptor encoding.  Every entry point only enqueues work
+// on the caller's stream; nothing here allocates device memory or synchronises.
+#include <cudaTypedefs.h>
+
+#include <mutex>
+#include <unordered_map>
+
+#include "../../include/tinyserve.h"
+#include "attn.cuh"
+#include "common.cuh"
+#include "meta.cuh"
+#include "score.cuh"
+#include "select.cuh"
+
+using namespace ts;
+
+namespace {
+
+thread_local int g_launches = 0;
+thread_local cudaEvent_t g_phase_ev[4] = {nullptr, nullptr, nullptr, nullptr};
+
+// records phase event i on the stream (external record node when captured in a graph)
+inline void phase_mark(int i, cudaStream_t st) {
+    if (g_phase_ev[i]) cudaEventRecordWithFlags(g_phase_ev[i], st, cudaEventRecordExternal);
+}
+
+constexpr int kMaxSplits = 64;
+constexpr int kMaxSel = 4096;  // max selected pages per row held in the attention page list
+constexpr int kAttnWarps = 4;
+constexpr int kAttnStages = 4;
+
+inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+inline size_t round_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+ts_status check_layout(const ts_layout *L) {
+    if (!L) return TS_ERR_CONFIG;
+    if (L->batch < 0 || L->num_q_heads < 1 || L->num_kv_heads < 1 || L->head_dim < 1 ||
+        L->page_size < 1 || L->max_pages < 1 || L->num_blocks < 1)
+        return TS_ERR_CONFIG;
+    if (L->kv_dtype != TS_F32 && L->kv_dtype != TS_BF16) return TS_ERR_CONFIG;
+    if (L->num_q_heads % L->num_kv_heads) return TS_ERR_SHAPE;
+    if (L->shard_stride < 1 || L->shard_offset < 0 || L->shard_offset >= L->shard_stride)
+        return TS_ERR_SHAPE;
+    if (L->head_dim != 64 && L->head_dim != 128) return TS_ERR_UNSUPPORTED;
+    return TS_OK;
+}
+
+int group_of(const ts_layout *L) { return L->num_q_heads / L->num_kv_heads; }
+
+bool bf16_attn_supported(const ts_layout *L) {
+    const int S = L->page_size;
+    return L->kv_dtype == TS_BF16 && L->head_dim == 64 && group_of(L) <= 8 &&
+           (S == 8 || S == 16 || S == 32 || S == 64);
+}
+
+ts_status launch_status() {
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? TS_OK : TS_ERR_CUDA;
+}
+
+int device_sms() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    static std::mutex mu;
+    static std::unordered_map<int, int> cache;
+    std::lock_guard<std::mutex> g(mu);
+    auto it = cache.find(dev);
+    if (it != cache.end()) return it->second;
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev] = sms;
+    return sms;
+}
+
+// ---------------------------------------------------------------- TMA descriptors
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    return fn;
+}
+
+// Pool [NB][Hkv][S][64] bf16 viewed as a 2-D tensor of NB*Hkv*S rows x 64 columns; box =
+// TT rows x 64 columns (128 B rows), 128-byte swizzle.
+bool make_pool_map(CUtensorMap *map, const void *pool, const ts_layout *L, int TT) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    const cuuint64_t dims[2] = {64, (cuuint64_t)L->num_blocks * L->num_kv_heads * L->page_size};
+    const cuuint64_t strides[1] = {64 * 2};
+    const cuuint32_t box[2] = {64, (cuuint32_t)TT};
+    const cuuint32_t estr[2] = {1, 1};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(pool), dims, strides,
+              box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+              CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// ---------------------------------------------------------------- workspace layout
+struct AttnWs {
+    size_t tickets, part, total;
+};
+AttnWs attn_ws_layout(const ts_layout *L) {
+    const size_t rows = (size_t)L->batch * L->num_kv_heads;
+    AttnWs w;
+    w.tickets = 0;
+    w.part = round_up(rows * 4, 256);
+    const size_t d = L->head_dim;
+    w.total = w.part + round_up(rows * kMaxSplits * 8 * (d + 4) * 4, 256);
+    return w;
+}
+
+struct StepWs {
+    AttnWs attn;
+    size_t scores, sel_ids, sel_count, total;
+};
+StepWs step_ws_layout(const ts_layout *L, int kmax) {
+    StepWs w;
+    w.attn = attn_ws_layout(L);
+    const size_t rows = (size_t)L->batch * L->num_kv_heads;
+    w.scores = w.attn.total;
+    w.sel_ids = w.scores + round_up(rows * L->max_pages * 4, 256);
+    w.sel_count = w.sel_ids + round_up(rows * kmax * 4, 256);
+    w.total = w.sel_count + round_up(rows * 4, 256);
+    return w;
+}
+
+// K = floor(budget / S) clipped to [1, max_pages] (reading R4/R5; P_b <= max_pages)
+int kmax_of(const ts_layout *L, int budget) {
+    const int k = budget / L->page_size > 1 ? budget / L->page_size : 1;
+    return k < L->max_pages ? k : L->max_pages;
+}
+
+// ---------------------------------------------------------------- launchers
+ts_status launch_score(const ts_layout *L, const void *q, const void *meta, const int *pt,
+                       const int *sl, float *scores, cudaStream_t st) {
+    ScoreParams p{L->batch, L->num_q_heads, L->num_kv_heads, group_of(L), L->head_dim,
+                  L->page_size, L->max_pages, L->shard_stride, L->shard_offset};
+    const int rows = L->batch * L->num_kv_heads;
+    if (rows == 0) return TS_OK;
+    if (L->kv_dtype == TS_BF16 && p.G <= 8) {
+        dim3 grid((L->max_pages + kScorePagesPerCta - 1) / kScorePagesPerCta, rows);
+        if (L->head_dim == 64)
+            score_mma_kernel<64><<<grid, kScoreWarps * 32, 0, st>>>(
+                p, (const uint16_t *)q, (const uint16_t *)meta, pt, sl, scores);
+        else
+            score_mma_kernel<128><<<grid, kScoreWarps * 32, 0, st>>>(
+                p, (const uint16_t *)q, (const uint16_t *)meta, pt, sl, scores);
+    } else {
+        dim3 grid((L->max_pages + kSimtPagesPerCta - 1) / kSimtPagesPerCta, rows);
+        const size_t sm = (size_t)p.G * 2 * L->head_dim * 4;
+        if (sm > 200 * 1024) return TS_ERR_UNSUPPORTED;
+        if (L->kv_dtype == TS_BF16) {
+            if (L->head_dim == 64) {
+                cudaFuncSetAttribute(score_simt_kernel<uint16_t, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+                score_simt_kernel<uint16_t, 64><<<grid, kSimtWarps * 32, sm, st>>>(p, (const uint16_t *)q, (const uint16_t *)meta, pt, sl, scores);
+            } else {
+                cudaFuncSetAttribute(score_simt_kernel<uint16_t, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+                score_simt_kernel<uint16_t, 128><<<grid, kSimtWarps * 32, sm, st>>>(p, (const uint16_t *)q, (const uint16_t *)meta, pt, sl, scores);
+            }
+        } else {
+            if (L->head_dim == 64) {
+                cudaFuncSetAttribute(score_simt_kernel<float, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+                score_simt_kernel<float, 64><<<grid, kSimtWarps * 32, sm, st>>>(p, (const float *)q, (const float *)meta, pt, sl, scores);
+            } else {
+                cudaFuncSetAttribute(score_simt_kernel<float, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+                score_simt_kernel<float, 128><<<grid, kSimtWarps * 32, sm, st>>>(p, (const float *)q, (const float *)meta, pt, sl, scores);
+            }
+        }
+    }
+    ++g_launches;
+    return launch_status();
+}
+
+ts_status launch_select(const float *scores, int rows, int stride, const int *row_len,
+                        const int *ids_in, int id_stride, int id_offset, int k, int *sel_ids,
+                        float *sel_scores, int *sel_count, cudaStream_t st, int parts = 1,
+                        long long part_stride = 0) {
+    if (rows == 0) return TS_OK;
+    const size_t n = (size_t)stride * parts;
+    const size_t sm = n * 4 * (ids_in ? 3 : 1);
+    if (sm > 200 * 1024) return TS_ERR_UNSUPPORTED;
+    if (ids_in && n > 16 * kSelThreads) return TS_ERR_UNSUPPORTED;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaFuncSetAttribute(select_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    });
+    SelectParams p{scores, rows, stride * parts, row_len, ids_in, id_stride, id_offset, k,
+                   stride, part_stride, sel_ids, sel_scores, sel_count};
+    select_topk_kernel<<<rows, kSelThreads, sm, st>>>(p);
+    ++g_launches;
+    return launch_status();
+}
+
+template <int TT>
+ts_status launch_attn_mma(const ts_layout *L, AttnParams &p, const void *k_pool, const void *v_pool,
+                          cudaStream_t st) {
+    using SM = AttnSmem<TT, kAttnWarps, kAttnStages>;
+    auto kern = attn_mma_kernel<TT, kAttnWarps, kAttnStages>;
+    const size_t sm = SM::bytes(p.sel_stride);
+    static std::once_flag once;
+    std::call_once(once, [&] {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    });
+    CUtensorMap tmK, tmV;
+    if (!make_pool_map(&tmK, k_pool, L, TT) || !make_pool_map(&tmV, v_pool, L, TT))
+        return TS_ERR_CUDA;
+    const int rows = L->batch * L->num_kv_heads;
+    int occ = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kAttnWarps * 32, sm);
+    if (occ < 1) occ = 1;
+    const int slots = device_sms() * occ;
+    const int kmax = p.sel_stride;
+    const int tiles_per_row = kmax * (L->page_size / TT);
+    int splits = rows >= slots ? 1 : slots / rows;
+    splits = std::min(splits, std::max(1, tiles_per_row / kAttnWarps));
+    splits = std::max(1, std::min(splits, kMaxSplits));
+    p.splits = splits;
+    p.items = rows * splits;
+    const int grid = std::min(p.items, slots);
+    kern<<<grid, kAttnWarps * 32, sm, st>>>(tmK, tmV, p);
+    ++g_launches;
+    return launch_status();
+}
+
+ts_status launch_attn(const ts_layout *L, const void *q, const void *k_pool, const void *v_pool,
+                      const int *pt, const int *sl, const int *sel_ids, const int *sel_count,
+                      int sel_stride, float scale, float *o, float *lse, void *ws, cudaStream_t st) {
+    const int rows = L->batch * L->num_kv_heads;
+    if (rows == 0) return TS_OK;
+    const AttnWs w = attn_ws_layout(L);
+    AttnParams p{};
+    p.q = q;
+    p.page_table = pt;
+    p.seq_lens = sl;
+    p.sel_ids = sel_ids;
+    p.sel_count = sel_count;
+    p.sel_stride = sel_stride;
+    p.B = L->batch;
+    p.Hq = L->num_q_heads;
+    p.Hkv = L->num_kv_heads;
+    p.G = group_of(L);
+    p.D = L->head_dim;
+    p.S = L->page_size;
+    p.max_pages = L->max_pages;
+    p.stride = L->shard_stride;
+    p.offset = L->shard_offset;
+    p.scale = scale;
+    p.o = o;
+    p.lse = lse;
+    p.tickets = reinterpret_cast<unsigned *>(static_cast<char *>(ws) + w.tickets);
+    p.part = reinterpret_cast<float *>(static_cast<char *>(ws) + w.part);
+    p.splits = 1;
+    p.items = rows;
+    if (L->kv_dtype == TS_BF16) {
+        if (!bf16_attn_supported(L) || sel_stride > kMaxSel) return TS_ERR_UNSUPPORTED;
+        if (L->page_size >= 16) return launch_attn_mma<16>(L, p, k_pool, v_pool, st);
+        return launch_attn_mma<8>(L, p, k_pool, v_pool, st);
+    }
+    const int threads = 32 * std::min(p.G, 8);
+    if (L->head_dim == 64)
+        attn_simt_kernel<64><<<rows, threads, 0, st>>>(p, (const float *)k_pool, (const float *)v_pool);
+    else
+        attn_simt_kernel<128><<<rows, threads, 0, st>>>(p, (const float *)k_pool, (const float *)v_pool);
+    ++g_launches;
+    return launch_status();
+}
+
+}  // namespace
+
+// =================================================================== C ABI
+extern "C" {
+
+const char *ts_status_str(ts_status s) {
+    switch (s) {
+        case TS_OK: return "TS_OK";
+        case TS_ERR_CONFIG: return "TS_ERR_CONFIG: invalid size, budget or dtype";
+        case TS_ERR_SHAPE: return "TS_ERR_SHAPE: inconsistent shapes (heads, k, sharding)";
+        case TS_ERR_ALIGN: return "TS_ERR_ALIGN: tensor pointer not 16-byte aligned";
+        case TS_ERR_UNSUPPORTED: return "TS_ERR_UNSUPPORTED: shape outside the compiled set";
+        case TS_ERR_CUDA: return "TS_ERR_CUDA: CUDA launch failure";
+        case TS_ERR_WORKSPACE: return "TS_ERR_WORKSPACE: workspace missing or too small";
+    }
+    return "unknown ts_status";
+}
+
+const char *ts_version(void) { return "tinyserve-b200 0.1 (sm_100a)"; }
+
+int32_t ts_last_launch_count(void) { return g_launches; }
+
+void ts_profile_events(void *const *events, int32_t n) {
+    for (int i = 0; i < 4; ++i)
+        g_phase_ev[i] = (events && i < n) ? static_cast<cudaEvent_t>(events[i]) : nullptr;
+}
+
+size_t ts_attn_workspace_bytes(const ts_layout *L, int32_t sel_stride) {
+    (void)sel_stride;
+    if (check_layout(L) != TS_OK) return 0;
+    return attn_ws_layout(L).total;
+}
+
+size_t ts_workspace_bytes(const ts_layout *L, int32_t budget_tokens) {
+    if (check_layout(L) != TS_OK || budget_tokens < 1) return 0;
+    return step_ws_layout(L, kmax_of(L, budget_tokens)).total;
+}
+
+ts_status ts_meta_append(const ts_layout *L, const void *k_new, const void *v_new,
+                         int32_t *seq_lens, int32_t advance, const int32_t *page_table,
+                         void *k_pool, void *v_pool, void *meta, void *stream) {
+    g_launches = 0;
+    ts_status s = check_layout(L);
+    if (s != TS_OK) return s;
+    if (!aligned16(k_new) || !aligned16(v_new) || !aligned16(k_pool) || !aligned16(v_pool) ||
+        !aligned16(meta))
+        return TS_ERR_ALIGN;
+    if (L->batch == 0) return TS_OK;
+    MetaParams p{L->batch, L->num_kv_heads, L->head_dim, L->page_size, L->max_pages,
+                 L->shard_stride, L->shard_offset};
+    const int threads = L->num_kv_heads * L->head_dim / (L->kv_dtype == TS_BF16 ? 8 : 4);
+    if (threads > 1024) return TS_ERR_UNSUPPORTED;
+    if (L->kv_dtype == TS_BF16)
+        meta_append_kernel<uint16_t><<<L->batch, threads, 0, as_stream(stream)>>>(
+            p, (const uint16_t *)k_new, (const uint16_t *)v_new, seq_lens, advance, page_table,
+            (uint16_t *)k_pool, (uint16_t *)v_pool, (uint16_t *)meta);
+    else
+        meta_append_kernel<float><<<L->batch, threads, 0, as_stream(stream)>>>(
+            p, (const float *)k_new, (const float *)v_new, seq_lens, advance, page_table,
+            (float *)k_pool, (float *)v_pool, (float *)meta);
+    ++g_launches;
+    return launch_status();
+}
+
+ts_status ts_meta_build(const ts_layout *L, const void *k_pool, const int32_t *page_table,
+                        const int32_t *seq_lens, void *meta, void *stream) {
+    g_launches = 0;
+    ts_status s = check_layout(L);
+    if (s != TS_OK) return s;
+    if (!aligned16(k_pool) || !aligned16(meta)) return TS_ERR_ALIGN;
+    if (L->batch == 0) return TS_OK;
+    MetaParams p{L->batch, L->num_kv_heads, L->head_dim, L->page_size, L->max_pages,
+                 L->shard_stride, L->shard_offset};
+    const long long work = (long long)L->batch * L->max_pages * L->num_kv_heads *
+                           (L->head_dim / (L->kv_dtype == TS_BF16 ? 8 : 4));
+    const int grid = (int)std::min<long long>((work + 255) / 256, (long long)device_sms() * 16);
+    if (L->kv_dtype == TS_BF16)
+        meta_build_kernel<uint16_t><<<grid, 256, 0, as_stream(stream)>>>(
+            p, (const uint16_t *)k_pool, page_table, seq_lens, (uint16_t *)meta);
+    else
+        meta_build_kernel<float><<<grid, 256, 0, as_stream(stream)>>>(
+            p, (const float *)k_pool, page_table, seq_lens, (float *)meta);
+    ++g_launches;
+    return launch_status();
+}
+
+ts_status ts_score_pages(const ts_layout *L, const void *q, const void *meta,
+                         const int32_t *page_table, const int32_t *seq_lens, float *scores,
+                         void *stream) {
+    g_launches = 0;
+    ts_status s = check_layout(L);
+    if (s != TS_OK) return s;
+    if (!aligned16(q) || !aligned16(meta)) return TS_ERR_ALIGN;
+    return launch_score(L, q, meta, page_table, seq_lens, scores, as_stream(stream));
+}
+
+ts_status ts_select_topk(const float *scores, int32_t rows, int32_t stride, const int32_t *row_len,
+                         const int32_t *ids_in, int32_t id_stride, int32_t id_offset, int32_t k,
+                         int32_t *sel_ids, float *sel_scores, int32_t *sel_count, void *stream) {
+    g_launches = 0;
+    if (rows < 0 || stride < 1) return TS_ERR_CONFIG;
+    if (k < 1 || id_stride < 1) return TS_ERR_SHAPE;
+    return launch_select(scores, rows, stride, row_len, ids_in, id_stride, id_offset, k, sel_ids,
+                         sel_scores, sel_count, as_stream(stream));
+}
+
+ts_status ts_sparse_decode_attn(const ts_layout *L, const void *q, const void *k_pool,
+                                const void *v_pool, const int32_t *page_table,
+                                const int32_t *seq_lens, const int32_t *sel_ids,
+                                const int32_t *sel_count, int32_t sel_stride, float scale,
+                                float *o, float *lse, void *ws, size_t ws_bytes, void *stream) {
+    g_launches = 0;
+    ts_status s = check_layout(L);
+    if (s != TS_OK) return s;
+    if (sel_stride < 1) return TS_ERR_SHAPE;
+    if (!aligned16(q) || !aligned16(k_pool) || !aligned16(v_pool) || !aligned16(o))
+        return TS_ERR_ALIGN;
+    if (!ws || ws_bytes < attn_ws_layout(L).total) return TS_ERR_WORKSPACE;
+    return launch_attn(L, q, k_pool, v_pool, page_table, seq_lens, sel_ids, sel_count, sel_stride,
+                       scale, o, lse, ws, as_stream(stream));
+}
+
+ts_status ts_decode_step(const ts_layout *L, const void *q, const void *k_pool, const void *v_pool,
+                         const void *meta, const int32_t *page_table, const int32_t *seq_lens,
+                         int32_t budget_tokens, float scale, float *o, float *lse,
+                         int32_t *sel_ids_out, int32_t *sel_count_out, void *ws, size_t ws_bytes,
+                         void *stream) {
+    g_launches = 0;
+    ts_status s = check_layout(L);
+    if (s != TS_OK) return s;
+    if (budget_tokens < 1) return TS_ERR_CONFIG;
+    if (L->shard_stride != 1) return TS_ERR_UNSUPPORTED;
+    if (!aligned16(q) || !aligned16(k_pool) || !aligned16(v_pool) || !aligned16(meta) ||
+        !aligned16(o))
+        return TS_ERR_ALIGN;
+    const int kmax = kmax_of(L, budget_tokens);
+    const StepWs w = step_ws_layout(L, kmax);
+    if (!ws || ws_bytes < w.total) return TS_ERR_WORKSPACE;
+    if (L->kv_dtype == TS_BF16 && (!bf16_attn_supported(L) || kmax > kMaxSel))
+        return TS_ERR_UNSUPPORTED;
+    char *wb = static_cast<char *>(ws);
+    float *scores = reinterpret_cast<float *>(wb + w.scores);
+    int *ids = sel_ids_out ? sel_ids_out : reinterpret_cast<int *>(wb + w.sel_ids);
+    int *cnt = sel_count_out ? sel_count_out : reinterpret_cast<int *>(wb + w.sel_count);
+    const cudaStream_t st = as_stream(stream);
+    const int rows = L->batch * L->num_kv_heads;
+    int launches = 0;
+    phase_mark(0, st);
+    if ((s = launch_score(L, q, meta, page_table, seq_lens, scores, st)) != TS_OK) return s;
+    phase_mark(1, st);
+    launches += g_launches;
+    g_launches = 0;
+    if ((s = launch_select(scores, rows, L->max_pages, nullptr, nullptr, 1, 0, kmax, ids, nullptr,
+                           cnt, st)) != TS_OK)
+        return s;
+    phase_mark(2, st);
+    launches += g_launches;
+    g_launches = 0;
+    if ((s = launch_attn(L, q, k_pool, v_pool, page_table, seq_lens, ids, cnt, kmax, scale, o, lse,
+                         ws, st)) != TS_OK)
+        return s;
+    phase_mark(3, st);
+    g_launches += launches;
+    return TS_OK;
+}
+
+ts_status ts_select_merge(const float *cand_scores, const int32_t *cand_ids, int32_t parts,
+                          int64_t part_stride, int32_t rows, int32_t k_part, int32_t k,
+                          int32_t *sel_ids, float *sel_scores, int32_t *sel_count, void *stream) {
+    g_launches = 0;
+    if (rows < 0 || parts < 1 || k_part < 1 || part_stride < 0) return TS_ERR_CONFIG;
+    if (k < 1 || !cand_ids) return TS_ERR_SHAPE;
+    if (part_stride == 0) part_stride = (int64_t)rows * k_part;
+    return launch_select(cand_scores, rows, k_part, nullptr, cand_ids, 1, 0, k, sel_ids, sel_scores,
+                         sel_count, as_stream(stream), parts, part_stride);
+}
+
+ts_status ts_lse_merge(int32_t parts, int32_t rows, int32_t d, const float *o_parts,
+                       const float *lse_parts, int64_t part_stride, float *o, float *lse,
+                       void *stream) {
+    g_launches = 0;
+    if (parts < 1 || rows < 0 || d < 1 || part_stride < 0) return TS_ERR_CONFIG;
+    if (rows == 0) return TS_OK;
+    const long long so = part_stride ? part_stride : (long long)rows * d;
+    const long long sl = part_stride ? part_stride : (long long)rows;
+    lse_merge_kernel<<<rows, 64, 0, as_stream(stream)>>>(parts, rows, d, o_parts, lse_parts, so, sl,
+                                                         o, lse);
+    ++g_launches;
+    return launch_status();
+}
+
+}  // extern "C"

@@ -1,0 +1,348 @@
+"""GPU parity: every C-ABI entry point vs the float64 oracle on the same seeded inputs.
+
+Bars (BASELINE.json north_star): metadata and page sets bit-exact (integer / byte work);
+attention output max-abs <= 2e-3 for bf16 K/V and <= 1e-5 for fp32 K/V; scores within
+1e-5 * L1 (4x the fp32 accumulation bound d * 2^-24 * L1 at d = 64).
+Page-set comparisons use margin-enforced inputs (oracle.margin) except where ties are the
+point (integer inputs, compared against the oracle's own tie rule).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import oracle.margin
+import synth
+
+pytestmark = pytest.mark.gpu
+
+DEV = "cuda:0"
+ATOL = {"bf16": 2e-3, "f32": 1e-5}
+
+
+@pytest.fixture(scope="module")
+def ts():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2509_12211_b200 import _build
+    _build.build()
+    import paper_2509_12211_b200 as ts
+    return ts
+
+
+def on_dev(case):
+    return {k: (v.to(DEV) if isinstance(v, torch.Tensor) else v) for k, v in case.items()}
+
+
+def gpu_meta(ts, d):
+    L = ts.make_layout(d["q"], d["k_pool"], d["page_table"])
+    return L, ts.meta_build(L, d["k_pool"], d["page_table"], d["seq_lens"])
+
+
+def logical_meta(meta, page_table, seq_lens, S):
+    """GPU meta [NB][Hkv][2][d] -> oracle's logical [B][Hkv][mp][d] (valid pages only)."""
+    m = oracle.widen(meta.cpu())
+    pt = page_table.cpu().numpy()
+    B, mp = pt.shape
+    out_min = np.zeros((B, m.shape[1], mp, m.shape[3]))
+    out_max = np.zeros_like(out_min)
+    for b, L in enumerate(seq_lens.tolist()):
+        P = -(-L // S)
+        out_min[b, :, :P] = m[pt[b, :P], :, 0].transpose(1, 0, 2)
+        out_max[b, :, :P] = m[pt[b, :P], :, 1].transpose(1, 0, 2)
+    return out_min, out_max
+
+
+CASES = {
+    # name: (config, overrides, ragged)
+    "c1": ("c1", {}, False),
+    "c1_ragged": ("c1", dict(batch=3, ctx=200), True),
+    "c2_small": ("c2", dict(batch=4, ctx=1500), True),
+    "c3_small": ("c3", dict(batch=2, ctx=3000, budget_tokens=512), True),
+    "g4_s32": ("c3", dict(batch=2, num_q_heads=16, ctx=2500, page_size=32, budget_tokens=512), True),
+    "g2_s8": ("c3", dict(batch=3, num_q_heads=8, ctx=900, page_size=8, budget_tokens=128), True),
+    "c5_like": ("c5", dict(batch=1, ctx=40000, budget_tokens=1024), True),
+    "f32_gqa": ("c1", dict(batch=2, num_q_heads=8, num_kv_heads=2, ctx=700, page_size=16,
+                           budget_tokens=160), True),
+    "bf16_d128_score": ("c3", dict(batch=2, head_dim=128, ctx=900, budget_tokens=128), True),
+}
+
+
+def make(name, seed=7, **kw):
+    cname, over, ragged = CASES[name]
+    cfg = synth.config(cname, **over)
+    return cfg, synth.make_case(cfg, seed=seed, ragged=ragged, poison_tail=True, **kw)
+
+
+# ------------------------------------------------------------------ a1: metadata
+@pytest.mark.parametrize("name", ["c1_ragged", "c2_small", "g4_s32", "g2_s8", "bf16_d128_score"])
+def test_meta_build_bit_exact(ts, name):
+    cfg, case = make(name)
+    d = on_dev(case)
+    L, meta = gpu_meta(ts, d)
+    gmin, gmax = logical_meta(meta, case["page_table"], case["seq_lens"], cfg.page_size)
+    omin, omax = oracle.meta_build(case["k_pool"], case["page_table"], case["seq_lens"])
+    assert np.array_equal(gmin, omin) and np.array_equal(gmax, omax)
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_meta_append_incremental_equals_oracle(ts, dtype):
+    """ts_meta_append over a whole prefill, token by token (advance=True), == batch oracle
+    metadata bit-exactly, and the pools hold exactly the appended bytes."""
+    cfg = synth.config("c2", batch=3, num_q_heads=4, num_kv_heads=2, ctx=100, page_size=16,
+                       dtype=dtype)
+    src = synth.make_case(cfg, seed=11)
+    d = on_dev(src)
+    kp = torch.zeros_like(d["k_pool"])
+    vp = torch.zeros_like(d["v_pool"])
+    meta = torch.zeros((src["num_blocks"], 2, 2, 64), dtype=kp.dtype, device=DEV)
+    lens = torch.zeros(3, dtype=torch.int32, device=DEV)
+    L = ts.make_layout(d["q"], kp, d["page_table"])
+    pt = src["page_table"].numpy()
+    for t in range(cfg.ctx):
+        kn = torch.stack([src["k_pool"][pt[b, t // 16], :, t % 16] for b in range(3)]).to(DEV)
+        vn = torch.stack([src["v_pool"][pt[b, t // 16], :, t % 16] for b in range(3)]).to(DEV)
+        ts.meta_append(L, kn.contiguous(), vn.contiguous(), lens, d["page_table"], kp, vp, meta)
+    assert lens.tolist() == [cfg.ctx] * 3
+    ek, ev = torch.zeros_like(src["k_pool"]), torch.zeros_like(src["v_pool"])
+    for b in range(3):  # expected pools: exactly the appended slots, zeros elsewhere
+        for t in range(cfg.ctx):
+            ek[pt[b, t // 16], :, t % 16] = src["k_pool"][pt[b, t // 16], :, t % 16]
+            ev[pt[b, t // 16], :, t % 16] = src["v_pool"][pt[b, t // 16], :, t % 16]
+    assert torch.equal(kp.cpu(), ek) and torch.equal(vp.cpu(), ev)
+    gmin, gmax = logical_meta(meta, src["page_table"], lens.cpu(), 16)
+    omin, omax = oracle.meta_build(src["k_pool"], src["page_table"], lens.cpu())
+    assert np.array_equal(gmin, omin) and np.array_equal(gmax, omax)
+
+
+# ------------------------------------------------------------------ a2: scores
+@pytest.mark.parametrize("name", list(CASES))
+def test_score_pages(ts, name):
+    cfg, case = make(name)
+    d = on_dev(case)
+    L, meta = gpu_meta(ts, d)
+    sc = ts.score_pages(L, d["q"], meta, d["page_table"], d["seq_lens"]).cpu().numpy()
+    omin, omax = oracle.meta_build(case["k_pool"], case["page_table"], case["seq_lens"])
+    ref = oracle.score_pages(case["q"], omin, omax, case["seq_lens"], cfg.page_size)
+    l1 = oracle.margin.l1_bounds(case["q"], omin, omax, cfg.group)
+    fin = np.isfinite(ref)
+    assert np.array_equal(np.isneginf(sc), ~fin)
+    err = np.abs(sc[fin] - ref[fin]) / np.maximum(l1[fin], 1e-30)
+    assert err.max() <= 1e-5, err.max()
+    assert not np.any(np.signbit(sc[fin]) & (sc[fin] == 0))  # -0.0 canonicalised
+
+
+# ------------------------------------------------------------------ a3: top-K
+def _cmp_select(ts, scores_np, k, row_len=None, ids=None):
+    s = torch.from_numpy(scores_np.astype(np.float32))
+    ref_ids, ref_sc, ref_cnt = oracle.select_topk(s.numpy().astype(np.float64), row_len, k, ids_in=ids)
+    gi, gs, gc = ts.select_topk(s.to(DEV), k,
+                                row_len=None if row_len is None else torch.tensor(row_len, dtype=torch.int32, device=DEV),
+                                ids_in=None if ids is None else torch.from_numpy(ids).to(DEV))
+    assert np.array_equal(gc.cpu().numpy(), ref_cnt)
+    assert np.array_equal(gi.cpu().numpy(), ref_ids)
+    g = gs.cpu().numpy()
+    assert np.array_equal(g, ref_sc.astype(np.float32))
+
+
+@pytest.mark.parametrize("n,k", [(16, 4), (256, 32), (2048, 128), (8192, 64), (500, 500), (37, 50)])
+def test_select_topk_exact(ts, n, k):
+    rng = np.random.default_rng(n + k)
+    rows = 24
+    s = rng.standard_normal((rows, n)).astype(np.float32)
+    s[1] = np.round(s[1] * 2)          # heavy ties
+    s[2] = 0.0
+    s[2, ::3] = -0.0                   # -0.0 == +0.0
+    s[3, n // 2:] = -np.inf            # missing pages
+    s[4] = 1.0
+    _cmp_select(ts, s, k)
+    lens = rng.integers(0, n + 1, rows).tolist()
+    _cmp_select(ts, s, k, row_len=lens)
+
+
+def test_select_topk_ids_in_and_merge(ts):
+    rng = np.random.default_rng(5)
+    rows, n, k = 16, 512, 48
+    s = np.round(rng.standard_normal((rows, n)) * 3).astype(np.float32)
+    ids = np.stack([rng.permutation(4 * n)[:n] for _ in range(rows)]).astype(np.int32)
+    _cmp_select(ts, s, k, ids=ids)
+    # select_merge over [parts][rows][k_part] candidates == oracle over the concatenation
+    parts, kp = 4, 64
+    cs = np.round(rng.standard_normal((parts, rows, kp)) * 2).astype(np.float32)
+    cs[:, :, -5:] = -np.inf
+    ci = rng.integers(0, 10_000, (parts, rows, kp)).astype(np.int32)
+    for r in range(rows):  # unique ids per row
+        ci[:, r, :] = rng.permutation(10_000)[: parts * kp].reshape(parts, kp)
+    gi, gs, gc = ts.select_merge(torch.from_numpy(cs).to(DEV), torch.from_numpy(ci).to(DEV), k)
+    flat_s = cs.transpose(1, 0, 2).reshape(rows, -1).astype(np.float64)
+    flat_i = ci.transpose(1, 0, 2).reshape(rows, -1)
+    ri, rsc, rc = oracle.select_topk(flat_s, None, k, ids_in=flat_i)
+    assert np.array_equal(gc.cpu().numpy(), rc) and np.array_equal(gi.cpu().numpy(), ri)
+
+
+# ------------------------------------------------------------------ a4: sparse attention
+@pytest.mark.parametrize("name", [n for n in CASES if n != "bf16_d128_score"])
+@pytest.mark.parametrize("scale", [None, 1.0])
+def test_sparse_attention(ts, name, scale):
+    cfg, case = make(name, seed=3)
+    scale = cfg.scale if scale is None else scale
+    ref = oracle.decode_step(case["q"], case["k_pool"], case["v_pool"], case["page_table"],
+                             case["seq_lens"], cfg.budget_tokens, scale)
+    d = on_dev(case)
+    L = ts.make_layout(d["q"], d["k_pool"], d["page_table"])
+    ids = torch.from_numpy(ref["sel_ids"]).to(DEV)
+    cnt = torch.from_numpy(ref["sel_count"]).to(DEV)
+    o, lse = ts.sparse_decode_attn(L, d["q"], d["k_pool"], d["v_pool"], d["page_table"],
+                                   d["seq_lens"], ids, cnt, scale)
+    err = np.abs(o.cpu().numpy() - ref["o"]).max()
+    assert err <= ATOL[cfg.dtype], err
+    lerr = np.abs(lse.cpu().numpy() - ref["lse"]).max()
+    assert lerr <= (1e-3 if cfg.dtype == "bf16" else 1e-5), lerr
+
+
+def test_attention_k_equals_p_is_dense(ts):
+    """K = P: sparse attention == dense attention (PAPER.md:141-145 vs 169-172)."""
+    cfg = synth.config("c3", batch=2, ctx=1000, budget_tokens=1 << 20)
+    case = synth.make_case(cfg, seed=9, ragged=True, poison_tail=True)
+    ref = oracle.decode_step(case["q"], case["k_pool"], case["v_pool"], case["page_table"],
+                             case["seq_lens"], cfg.budget_tokens, cfg.scale)
+    d = on_dev(case)
+    L, meta = gpu_meta(ts, d)
+    o, lse, ids, cnt = ts.decode_step(L, d["q"], d["k_pool"], d["v_pool"], meta, d["page_table"],
+                                      d["seq_lens"], cfg.budget_tokens, cfg.scale)
+    P = [-(-x // 16) for x in case["seq_lens"].tolist()]
+    assert cnt.cpu().numpy().tolist() == [[p] * 4 for p in P]
+    assert np.abs(o.cpu().numpy() - ref["o"]).max() <= 2e-3
+
+
+# ------------------------------------------------------------------ a5: fused step
+def _step_parity(ts, cfg, case, ref):
+    d = on_dev(case)
+    L, meta = gpu_meta(ts, d)
+    o, lse, ids, cnt = ts.decode_step(L, d["q"], d["k_pool"], d["v_pool"], meta, d["page_table"],
+                                      d["seq_lens"], cfg.budget_tokens, cfg.scale)
+    assert np.array_equal(cnt.cpu().numpy(), ref["sel_count"])
+    K = ids.shape[2]  # min(max_pages, budget / S); the oracle's array may be wider
+    assert np.all(ref["sel_ids"][:, :, K:] == -1)
+    assert np.array_equal(ids.cpu().numpy(), ref["sel_ids"][:, :, :K])
+    err = np.abs(o.cpu().numpy() - ref["o"]).max()
+    assert err <= ATOL[cfg.dtype], err
+    fin = np.isfinite(ref["lse"])
+    assert np.array_equal(np.isfinite(lse.cpu().numpy()), fin)
+    return err
+
+
+@pytest.mark.parametrize("name", [n for n in CASES if n != "bf16_d128_score"])
+def test_decode_step(ts, name):
+    cfg, case = make(name, seed=21)
+    ref = oracle.margin.enforce(case, cfg.budget_tokens)
+    _step_parity(ts, cfg, case, ref)
+
+
+@pytest.mark.parametrize("lens", [[0, 5, 16, 17], [1, 1, 1, 1], [0, 0, 0, 0], [31, 64, 2, 48]])
+def test_decode_step_edge_lengths(ts, lens):
+    """seq_len 0 (o = 0, lse = -inf), seq_len < S, exact page multiples, K >= P."""
+    cfg = synth.config("c3", batch=4, ctx=64, budget_tokens=32)
+    case = synth.make_case(cfg, seed=2, seq_lens=lens, poison_tail=True)
+    ref = oracle.margin.enforce(case, cfg.budget_tokens)
+    _step_parity(ts, cfg, case, ref)
+    d = on_dev(case)
+
+
+@pytest.mark.parametrize("budget", [1, 15, 16, 17, 4096])
+def test_decode_step_budget_edges(ts, budget):
+    cfg = synth.config("c2", batch=2, num_q_heads=2, num_kv_heads=2, ctx=500, budget_tokens=budget)
+    case = synth.make_case(cfg, seed=4, ragged=True)
+    ref = oracle.margin.enforce(case, budget)
+    _step_parity(ts, cfg, case, ref)
+
+
+def test_decode_step_integer_ties(ts):
+    """Real ties (integer q, k): the GPU must apply the oracle's lower-id rule exactly."""
+    cfg = synth.config("c3", batch=2, ctx=2048, budget_tokens=256)
+    case = synth.make_case(cfg, seed=6, mode="int")
+    ref = oracle.decode_step(case["q"], case["k_pool"], case["v_pool"], case["page_table"],
+                             case["seq_lens"], cfg.budget_tokens, cfg.scale, want_scores=True)
+    s = ref["scores"]
+    assert any(len(np.unique(s[b, g])) < s.shape[2] for b in range(2) for g in range(4))
+    _step_parity(ts, cfg, case, ref)
+
+
+@pytest.mark.parametrize("cname", ["c2", "c3"])
+def test_decode_step_full_size(ts, cname):
+    """BASELINE configs at full size, in bench.py's launch configuration."""
+    cfg = synth.config(cname)
+    case = synth.make_case(cfg, seed=42, ragged=True)
+    ref = oracle.margin.enforce(case, cfg.budget_tokens)
+    _step_parity(ts, cfg, case, ref)
+
+
+def test_decode_step_c5_full_context(ts):
+    """C5 shape (512k ctx, S = 64, budget 4096) at batch 1."""
+    cfg = synth.config("c5", batch=1)
+    case = synth.make_case(cfg, seed=42, ragged=True)
+    ref = oracle.margin.enforce(case, cfg.budget_tokens)
+    _step_parity(ts, cfg, case, ref)
+
+
+def test_cuda_graph_and_determinism(ts):
+    cfg, case = make("c3_small", seed=8)
+    d = on_dev(case)
+    L, meta = gpu_meta(ts, d)
+    ws = ts.new_workspace(ts.workspace_bytes(L, cfg.budget_tokens), DEV)
+    o1, l1, i1, c1 = ts.decode_step(L, d["q"], d["k_pool"], d["v_pool"], meta, d["page_table"],
+                                    d["seq_lens"], cfg.budget_tokens, cfg.scale, ws=ws)
+    o1, i1 = o1.clone(), i1.clone()
+    o2 = torch.empty_like(o1)
+    i2 = torch.empty_like(i1)
+    c2 = torch.empty_like(c1)
+    l2 = torch.empty_like(l1)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            ts.decode_step(L, d["q"], d["k_pool"], d["v_pool"], meta, d["page_table"],
+                           d["seq_lens"], cfg.budget_tokens, cfg.scale, o=o2, lse=l2,
+                           sel_ids=i2, sel_count=c2, ws=ws)
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(o1, o2) and torch.equal(i1, i2)
+
+
+# ------------------------------------------------------------------ e: shard emulation
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
+def test_shard_emulation_matches_unsharded(ts, world):
+    """Block-cyclic G-way sequence sharding on one GPU (exchanges = concatenation): the
+    selection is bit-identical to the unsharded kernel's (any input, ties included) and o
+    matches the oracle."""
+    from paper_2509_12211_b200 import sharded
+    cfg = synth.config("c5", batch=2, ctx=20000, budget_tokens=1024)
+    case = synth.make_case(cfg, seed=33, ragged=True, poison_tail=True)
+    ref = oracle.margin.enforce(case, cfg.budget_tokens)
+    d = on_dev(case)
+    L, meta = gpu_meta(ts, d)
+    o1, l1, i1, c1 = ts.decode_step(L, d["q"], d["k_pool"], d["v_pool"], meta, d["page_table"],
+                                    d["seq_lens"], cfg.budget_tokens, cfg.scale)
+    o, lse, ids, cnts = sharded.emulate(ts, L, world, d["q"], d["k_pool"], d["v_pool"],
+                                        d["page_table"], d["seq_lens"], cfg.budget_tokens, cfg.scale)
+    for r in range(world):
+        assert torch.equal(ids[r], i1) and torch.equal(cnts[r], c1)
+    assert np.array_equal(i1.cpu().numpy(), ref["sel_ids"])
+    assert np.abs(o.cpu().numpy() - ref["o"]).max() <= 2e-3
+    assert torch.allclose(o, o1, atol=1e-5, rtol=0)
+
+
+def test_lse_merge_kernel(ts):
+    rng = np.random.default_rng(1)
+    parts, rows, d = 5, 33, 64
+    op = rng.standard_normal((parts, rows, d))
+    lp = rng.standard_normal((parts, rows)) * 3
+    lp[1, :4] = -np.inf
+    lp[:, 7] = -np.inf
+    ro, rl = oracle.lse_merge(op, lp)
+    go, gl = ts.lse_merge(torch.tensor(op, dtype=torch.float32, device=DEV),
+                          torch.tensor(lp, dtype=torch.float32, device=DEV))
+    assert np.abs(go.cpu().numpy() - ro).max() < 1e-5
+    g = gl.cpu().numpy()
+    assert np.isneginf(g[7]) and np.abs(np.delete(g, 7) - np.delete(rl, 7)).max() < 1e-5
