@@ -22,8 +22,10 @@
  *      q          [batch][num_q_heads][head_dim]             kv_dtype
  *      k_pool     [num_blocks][num_kv_heads][page_size][head_dim]   kv_dtype
  *      v_pool     [num_blocks][num_kv_heads][page_size][head_dim]   kv_dtype
- *      meta       [num_blocks][num_kv_heads][2][head_dim]    kv_dtype; [..][0][:] = m (min),
- *                 [..][1][:] = M (max) of the valid keys of the block (Eq. 1)
+ *      meta       [batch][num_kv_heads][max_pages][2][head_dim]   kv_dtype, LOGICAL page
+ *                 order: [b][g][jl][0][:] = m (min), [..][1][:] = M (max) of the valid keys
+ *                 of local page jl of sequence b, kv head g (Eq. 1).  Row (b, g) is one
+ *                 contiguous run, so scoring streams it with no page-table lookup.
  *      page_table [batch][max_pages] int32: LOCAL page index -> physical block
  *      seq_lens   [batch] int32: GLOBAL number of tokens in the cache (before the append
  *                 for ts_meta_append, after it for everything else)
@@ -91,7 +93,7 @@ typedef struct {
  * For each sequence b with t = seq_lens[b] (length BEFORE the append): global page
  * j = t / S, slot = t % S.  If this rank owns j: writes k_new[b] / v_new[b]
  * ([B][Hkv][d], kv_dtype) into slot `slot` of block page_table[b][j / shard_stride] and
- * sets, per kv head,
+ * sets, per kv head, in meta[b][g][j / shard_stride]
  *   m = slot == 0 ? k : min(m, k),   M = slot == 0 ? k : max(M, k)   (exact, no rounding).
  * If `advance` != 0 the kernel then sets seq_lens[b] = t + 1 (every rank advances its copy
  * of the global length, owner or not); otherwise seq_lens is left unchanged. */
@@ -100,8 +102,8 @@ ts_status ts_meta_append(const ts_layout *layout, const void *k_new, const void 
                          void *k_pool, void *v_pool, void *meta, void *stream);
 
 /* Bulk metadata (SPEC.md:65-73 recompute_metadata; prefill / cache import): for every
- * owned page j < P_b of every sequence, meta of its block = min / max over its valid keys
- * (tokens t < seq_lens[b]).  Blocks of pages >= P_b are not touched. */
+ * owned page j < P_b of every sequence, meta[b][g][j / shard_stride] = min / max over the
+ * page's valid keys (tokens t < seq_lens[b]).  Entries of pages >= P_b are not touched. */
 ts_status ts_meta_build(const ts_layout *layout, const void *k_pool, const int32_t *page_table,
                         const int32_t *seq_lens, void *meta, void *stream);
 
@@ -186,9 +188,11 @@ const char *ts_version(void);
 int32_t ts_last_launch_count(void);
 
 /* Measurement hook (bench.py roofline): while set, ts_decode_step on this thread records
- * events[0..3] (cudaEvent_t, created by the caller) on its stream before the scoring
- * kernel, after scoring, after selection and after attention, as external records (valid
- * inside CUDA-graph capture).  events == NULL or n == 0 clears it.  Host-only. */
+ * events[0..3] (cudaEvent_t, created by the caller; NULL entries skipped) on its stream
+ * before the first kernel, after scoring, after selection and after attention, as external
+ * records (valid inside CUDA-graph capture).  The bf16 path runs scoring+selection and
+ * attention as two PDL-overlapped kernels and records only events[0] and events[3].
+ * events == NULL or n == 0 clears it.  Host-only. */
 void ts_profile_events(void *const *events, int32_t n);
 
 #ifdef __cplusplus

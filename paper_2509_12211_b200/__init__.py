@@ -8,8 +8,8 @@ CUDA kernels.  Names follow the C ABI:
   lse_merge, workspace_bytes, attn_workspace_bytes
 
 Tensors: q [B][Hq][d], k_pool / v_pool [NB][Hkv][S][d], meta
-[NB][Hkv][2][d] (kv dtype: bf16 or fp32), page_table [B][max_pages] int32, seq_lens [B]
-int32; o [B][Hq][d] fp32, lse [B][Hq] fp32.
+[B][Hkv][max_pages][2][d] (logical page order; kv dtype: bf16 or fp32), page_table
+[B][max_pages] int32, seq_lens [B] int32; o [B][Hq][d] fp32, lse [B][Hq] fp32.
 """
 from __future__ import annotations
 
@@ -19,7 +19,7 @@ from ._lib import Layout, TinyServeError, TS_BF16, TS_F32, check, exported_symbo
 
 __all__ = ["Layout", "TinyServeError", "make_layout", "meta_append", "meta_build",
            "score_pages", "select_topk", "sparse_decode_attn", "decode_step", "select_merge", "lse_merge",
-           "workspace_bytes", "attn_workspace_bytes", "new_workspace", "kmax", "launch_count",
+           "workspace_bytes", "attn_workspace_bytes", "new_workspace", "new_meta", "kmax", "launch_count",
            "profile_events",
            "exported_symbols", "PagedKV"]
 
@@ -85,7 +85,8 @@ def profile_events(events) -> None:
         lib().ts_profile_events(None, 0)
         return
     import ctypes
-    arr = (ctypes.c_void_p * len(events))(*[e.cuda_event for e in events])
+    arr = (ctypes.c_void_p * len(events))(*[(e.cuda_event if e is not None else None)
+                                             for e in events])
     lib().ts_profile_events(arr, len(events))
 
 
@@ -104,10 +105,15 @@ def meta_append(layout, k_new, v_new, seq_lens, page_table, k_pool, v_pool, meta
         _ptr(k_pool), _ptr(v_pool), _ptr(meta), _stream(stream)))
 
 
+def new_meta(layout, dtype, device) -> torch.Tensor:
+    """Zeroed metadata [B][Hkv][max_pages][2][d] (logical page order)."""
+    return torch.zeros((layout.batch, layout.num_kv_heads, layout.max_pages, 2, layout.head_dim),
+                       dtype=dtype, device=device)
+
+
 def meta_build(layout, k_pool, page_table, seq_lens, meta=None, stream=None):
     if meta is None:
-        meta = torch.zeros((layout.num_blocks, layout.num_kv_heads, 2, layout.head_dim),
-                           dtype=k_pool.dtype, device=k_pool.device)
+        meta = new_meta(layout, k_pool.dtype, k_pool.device)
     _cuda(k_pool, page_table, seq_lens, meta)
     check("ts_meta_build", lib().ts_meta_build(layout, _ptr(k_pool), _ptr(page_table),
                                                _ptr(seq_lens), _ptr(meta), _stream(stream)))

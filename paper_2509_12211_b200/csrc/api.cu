@@ -3,14 +3,17 @@
 // on the caller's stream; nothing here allocates device memory or synchronises.
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <mutex>
 #include <unordered_map>
 
 #include "../../include/tinyserve.h"
 #include "attn.cuh"
+#include "attn_stream.cuh"
 #include "common.cuh"
 #include "meta.cuh"
 #include "score.cuh"
+#include "score_select.cuh"
 #include "select.cuh"
 
 using namespace ts;
@@ -18,6 +21,7 @@ using namespace ts;
 namespace {
 
 thread_local int g_launches = 0;
+unsigned long long *g_dbg_ts = nullptr;  // development: attention CTA timestamps
 thread_local cudaEvent_t g_phase_ev[4] = {nullptr, nullptr, nullptr, nullptr};
 
 // records phase event i on the stream (external record node when captured in a graph)
@@ -25,10 +29,9 @@ inline void phase_mark(int i, cudaStream_t st) {
     if (g_phase_ev[i]) cudaEventRecordWithFlags(g_phase_ev[i], st, cudaEventRecordExternal);
 }
 
-constexpr int kMaxSplits = 64;
-constexpr int kMaxSel = 4096;  // max selected pages per row held in the attention page list
-constexpr int kAttnWarps = 4;
-constexpr int kAttnStages = 4;
+constexpr int kMaxSel = 4096;      // max selected pages per row
+constexpr int kStreamNC = 6;       // consumer warps per attention CTA (+ TMA, scheduler, merge)
+constexpr int kStreamStages = 18;  // ring stages (4 KB each): 3 per consumer
 
 inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
@@ -104,31 +107,38 @@ bool make_pool_map(CUtensorMap *map, const void *pool, const ts_layout *L, int T
 }
 
 // ---------------------------------------------------------------- workspace layout
+// attention workspace: [tickets: rows u32][work counters: 2 u32][partials: rows x ipr x 8 x kPS]
+// with ipr <= kMaxItemsPerRow items per row (attn_stream.cuh).
+constexpr int kMaxItemsPerRow = 64;
 struct AttnWs {
-    size_t tickets, part, total;
+    size_t tickets, work, part, total;
 };
-AttnWs attn_ws_layout(const ts_layout *L) {
+AttnWs attn_ws_layout(const ts_layout *L, int sel_stride) {
     const size_t rows = (size_t)L->batch * L->num_kv_heads;
+    const int tpr = sel_stride * std::max(1, L->page_size / 16);
+    const int ipr = std::min(kMaxItemsPerRow, std::max(1, tpr));
     AttnWs w;
     w.tickets = 0;
-    w.part = round_up(rows * 4, 256);
-    const size_t d = L->head_dim;
-    w.total = w.part + round_up(rows * kMaxSplits * 8 * (d + 4) * 4, 256);
+    w.work = round_up(rows * 4, 256);
+    w.part = w.work + 256;
+    w.total = w.part + round_up(rows * (size_t)ipr * 8 * kPS * 4, 256);
     return w;
 }
 
 struct StepWs {
     AttnWs attn;
-    size_t scores, sel_ids, sel_count, total;
+    size_t scores, sel_ids, sel_count, sc_tickets, ready, total;
 };
 StepWs step_ws_layout(const ts_layout *L, int kmax) {
     StepWs w;
-    w.attn = attn_ws_layout(L);
+    w.attn = attn_ws_layout(L, kmax);
     const size_t rows = (size_t)L->batch * L->num_kv_heads;
     w.scores = w.attn.total;
     w.sel_ids = w.scores + round_up(rows * L->max_pages * 4, 256);
     w.sel_count = w.sel_ids + round_up(rows * kmax * 4, 256);
-    w.total = w.sel_count + round_up(rows * 4, 256);
+    w.sc_tickets = w.sel_count + round_up(rows * 4, 256);
+    w.ready = w.sc_tickets + round_up(rows * 4, 256);
+    w.total = w.ready + round_up(rows * 4, 256);
     return w;
 }
 
@@ -199,43 +209,72 @@ ts_status launch_select(const float *scores, int rows, int stride, const int *ro
     return launch_status();
 }
 
+// Persistent dynamic-item attention (bf16).  ready != nullptr (decode-step mode): rows are
+// consumed as score_select_kernel releases them, and the launch uses programmatic
+// dependent launch so this grid overlaps the scoring grid.
 template <int TT>
-ts_status launch_attn_mma(const ts_layout *L, AttnParams &p, const void *k_pool, const void *v_pool,
-                          cudaStream_t st) {
-    using SM = AttnSmem<TT, kAttnWarps, kAttnStages>;
-    auto kern = attn_mma_kernel<TT, kAttnWarps, kAttnStages>;
-    const size_t sm = SM::bytes(p.sel_stride);
-    static std::once_flag once;
-    std::call_once(once, [&] {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    });
+ts_status launch_attn_stream(const ts_layout *L, AttnParams &p, const void *k_pool,
+                             const void *v_pool, unsigned *ready, unsigned *work, cudaStream_t st) {
+    using SM = StreamSmem<kStreamNC, kStreamStages>;
+    auto kern = attn_stream_kernel<TT, kStreamNC, kStreamStages>;
     CUtensorMap tmK, tmV;
     if (!make_pool_map(&tmK, k_pool, L, TT) || !make_pool_map(&tmV, v_pool, L, TT))
         return TS_ERR_CUDA;
     const int rows = L->batch * L->num_kv_heads;
-    int occ = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kAttnWarps * 32, sm);
-    if (occ < 1) occ = 1;
-    const int slots = device_sms() * occ;
-    const int kmax = p.sel_stride;
-    const int tiles_per_row = kmax * (L->page_size / TT);
-    int splits = rows >= slots ? 1 : slots / rows;
-    splits = std::min(splits, std::max(1, tiles_per_row / kAttnWarps));
-    splits = std::max(1, std::min(splits, kMaxSplits));
-    p.splits = splits;
-    p.items = rows * splits;
-    const int grid = std::min(p.items, slots);
-    kern<<<grid, kAttnWarps * 32, sm, st>>>(tmK, tmV, p);
+    StreamParams sp{};
+    sp.tpr = p.sel_stride * (L->page_size / TT);
+    static const int per_sm = getenv("TS_ATTN_CTAS_PER_SM") ? atoi(getenv("TS_ATTN_CTAS_PER_SM")) : 2;
+    const int slots_cap = device_sms() * per_sm;
+    // item size: ~32 slots (few merges), a multiple of NC; a whole row when the row is short
+    long long is = std::min<long long>(sp.tpr, 32);
+    is = (is + kStreamNC - 1) / kStreamNC * kStreamNC;
+    sp.is = (int)std::max<long long>(is, 1);
+    sp.ipr = (sp.tpr + sp.is - 1) / sp.is;
+    if (sp.ipr > kMaxItemsPerRow) {  // long rows: grow items so the partials fit the workspace
+        sp.is = (sp.tpr + kMaxItemsPerRow - 1) / kMaxItemsPerRow;
+        sp.is = (sp.is + kStreamNC - 1) / kStreamNC * kStreamNC;
+        sp.ipr = (sp.tpr + sp.is - 1) / sp.is;
+    }
+    sp.n_items = rows * sp.ipr;
+    const int grid = std::max(1, std::min(sp.n_items, slots_cap));
+    const size_t sm = SM::bytes();
+    static int sm_set = 0;  // opt-in grown on demand (dynamic + static <= 227 KB)
+    if ((int)sm > sm_set) {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) !=
+            cudaSuccess)
+            return TS_ERR_CUDA;
+        sm_set = (int)sm;
+    }
+    sp.a = p;
+    sp.ready = ready;
+    sp.work = work;
+    static const int dbg = getenv("TS_DEBUG_ATTN") ? atoi(getenv("TS_DEBUG_ATTN")) : 0;
+    sp.dbg = dbg;
+    sp.dbg_ts = g_dbg_ts;
+    sp.kpool_dbg = static_cast<const char *>(k_pool);
+    sp.vpool_dbg = static_cast<const char *>(v_pool);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3((kStreamNC + 3) * 32);
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = ready ? 1 : 0;
+    if (cudaLaunchKernelEx(&cfg, kern, tmK, tmV, sp) != cudaSuccess) return TS_ERR_CUDA;
     ++g_launches;
     return launch_status();
 }
 
 ts_status launch_attn(const ts_layout *L, const void *q, const void *k_pool, const void *v_pool,
                       const int *pt, const int *sl, const int *sel_ids, const int *sel_count,
-                      int sel_stride, float scale, float *o, float *lse, void *ws, cudaStream_t st) {
+                      int sel_stride, float scale, float *o, float *lse, void *ws, cudaStream_t st,
+                      unsigned *ready = nullptr) {
     const int rows = L->batch * L->num_kv_heads;
     if (rows == 0) return TS_OK;
-    const AttnWs w = attn_ws_layout(L);
+    const AttnWs w = attn_ws_layout(L, sel_stride);
     AttnParams p{};
     p.q = q;
     p.page_table = pt;
@@ -261,8 +300,9 @@ ts_status launch_attn(const ts_layout *L, const void *q, const void *k_pool, con
     p.items = rows;
     if (L->kv_dtype == TS_BF16) {
         if (!bf16_attn_supported(L) || sel_stride > kMaxSel) return TS_ERR_UNSUPPORTED;
-        if (L->page_size >= 16) return launch_attn_mma<16>(L, p, k_pool, v_pool, st);
-        return launch_attn_mma<8>(L, p, k_pool, v_pool, st);
+        unsigned *work = reinterpret_cast<unsigned *>(static_cast<char *>(ws) + w.work);
+        if (L->page_size >= 16) return launch_attn_stream<16>(L, p, k_pool, v_pool, ready, work, st);
+        return launch_attn_stream<8>(L, p, k_pool, v_pool, ready, work, st);
     }
     const int threads = 32 * std::min(p.G, 8);
     if (L->head_dim == 64)
@@ -295,15 +335,17 @@ const char *ts_version(void) { return "tinyserve-b200 0.1 (sm_100a)"; }
 
 int32_t ts_last_launch_count(void) { return g_launches; }
 
+// development hook (not in the public header): device buffer for attention CTA timestamps
+void ts_debug_timestamps(void *buf) { g_dbg_ts = static_cast<unsigned long long *>(buf); }
+
 void ts_profile_events(void *const *events, int32_t n) {
     for (int i = 0; i < 4; ++i)
         g_phase_ev[i] = (events && i < n) ? static_cast<cudaEvent_t>(events[i]) : nullptr;
 }
 
 size_t ts_attn_workspace_bytes(const ts_layout *L, int32_t sel_stride) {
-    (void)sel_stride;
-    if (check_layout(L) != TS_OK) return 0;
-    return attn_ws_layout(L).total;
+    if (check_layout(L) != TS_OK || sel_stride < 1) return 0;
+    return attn_ws_layout(L, sel_stride).total;
 }
 
 size_t ts_workspace_bytes(const ts_layout *L, int32_t budget_tokens) {
@@ -390,7 +432,7 @@ ts_status ts_sparse_decode_attn(const ts_layout *L, const void *q, const void *k
     if (sel_stride < 1) return TS_ERR_SHAPE;
     if (!aligned16(q) || !aligned16(k_pool) || !aligned16(v_pool) || !aligned16(o))
         return TS_ERR_ALIGN;
-    if (!ws || ws_bytes < attn_ws_layout(L).total) return TS_ERR_WORKSPACE;
+    if (!ws || ws_bytes < attn_ws_layout(L, sel_stride).total) return TS_ERR_WORKSPACE;
     return launch_attn(L, q, k_pool, v_pool, page_table, seq_lens, sel_ids, sel_count, sel_stride,
                        scale, o, lse, ws, as_stream(stream));
 }
@@ -419,6 +461,42 @@ ts_status ts_decode_step(const ts_layout *L, const void *q, const void *k_pool, 
     int *cnt = sel_count_out ? sel_count_out : reinterpret_cast<int *>(wb + w.sel_count);
     const cudaStream_t st = as_stream(stream);
     const int rows = L->batch * L->num_kv_heads;
+    if (L->kv_dtype == TS_BF16 && group_of(L) <= 8) {
+        // scoring + selection grid (releases rows) -> PDL-overlapped attention grid that
+        // consumes rows as they are selected (2 kernels, one programmatic dependency edge)
+        unsigned *tick = reinterpret_cast<unsigned *>(wb + w.sc_tickets);
+        unsigned *ready = reinterpret_cast<unsigned *>(wb + w.ready);
+        ScoreParams sp{L->batch, L->num_q_heads, L->num_kv_heads, group_of(L), L->head_dim,
+                       L->page_size, L->max_pages, 1, 0};
+        FusedSelect fs{ids, cnt, tick, ready, kmax};
+        const size_t sm = (size_t)L->max_pages * 4;
+        if (sm > 160 * 1024) return TS_ERR_UNSUPPORTED;
+        dim3 grid((L->max_pages + kScorePagesPerCta - 1) / kScorePagesPerCta, rows);
+        phase_mark(0, st);
+        if (rows > 0) {
+            if (L->head_dim == 64) {
+                static std::once_flag once;
+                std::call_once(once, [] { cudaFuncSetAttribute(score_select_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024); });
+                score_select_kernel<64><<<grid, kScoreWarps * 32, sm, st>>>(
+                    sp, (const uint16_t *)q, (const uint16_t *)meta, page_table, seq_lens, scores, fs);
+            } else {
+                static std::once_flag once;
+                std::call_once(once, [] { cudaFuncSetAttribute(score_select_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024); });
+                score_select_kernel<128><<<grid, kScoreWarps * 32, sm, st>>>(
+                    sp, (const uint16_t *)q, (const uint16_t *)meta, page_table, seq_lens, scores, fs);
+            }
+            if ((s = launch_status()) != TS_OK) return s;
+        }
+        // no phase marks between the two kernels: an event node there would break the
+        // programmatic (PDL) edge that lets the attention grid overlap the scoring grid
+        g_launches = 0;
+        if ((s = launch_attn(L, q, k_pool, v_pool, page_table, seq_lens, ids, cnt, kmax, scale, o,
+                             lse, ws, st, ready)) != TS_OK)
+            return s;
+        phase_mark(3, st);
+        g_launches += rows > 0 ? 1 : 0;
+        return TS_OK;
+    }
     int launches = 0;
     phase_mark(0, st);
     if ((s = launch_score(L, q, meta, page_table, seq_lens, scores, st)) != TS_OK) return s;

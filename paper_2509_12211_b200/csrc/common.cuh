@@ -92,6 +92,31 @@ TS_DEV void mbar_wait(uint32_t bar, uint32_t parity) {
         : "memory");
 }
 
+TS_DEV void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+// ---------------------------------------------------------------- sync / ordering
+TS_DEV void named_bar_sync(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+TS_DEV uint32_t ld_acquire_u32(const unsigned *p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+TS_DEV void st_release_u32(unsigned *p, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+TS_DEV void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+TS_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+TS_DEV void nanosleep_ns(uint32_t ns) { asm volatile("nanosleep.u32 %0;" ::"r"(ns)); }
+TS_DEV uint64_t globaltimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
 // ---------------------------------------------------------------- TMA
 TS_DEV uint64_t l2_policy_evict_first() {
     uint64_t p;
@@ -107,6 +132,21 @@ TS_DEV void tma_load_2d(uint32_t dst, const CUtensorMap *map, int32_t x, int32_t
         "cache_hint [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
         "l"(map), "r"(x), "r"(y), "r"(bar), "l"(policy)
         : "memory");
+}
+// 1-D bulk copy global -> shared (16-byte aligned, multiple of 16 bytes).
+TS_DEV void bulk_load(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+        "l"(src), "r"(bytes), "r"(bar)
+        : "memory");
+}
+// Ampere-style async copy, 16 B global -> shared (L2 only), and its mbarrier hook: the
+// barrier receives one arrival from this thread once all its prior cp.async complete.
+TS_DEV void cp_async16(uint32_t dst, const void *src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+TS_DEV void cp_async_mbar_arrive(uint32_t bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
 }
 TS_DEV void prefetch_tmap(const CUtensorMap *map) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");

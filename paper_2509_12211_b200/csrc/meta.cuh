@@ -2,7 +2,9 @@
 //   ts_meta_append: fused K/V slot write + running min/max of the page
 //   ts_meta_build : min/max over the valid keys of every page
 // Both are exact in every dtype (compare/select only).  One thread per 16-byte chunk of a
-// (block, kv-head) record: 128-bit loads/stores, coalesced along head_dim.
+// (page, kv-head) record: 128-bit loads/stores, coalesced along head_dim.  Metadata lives in
+// the LOGICAL layout [B][Hkv][max_pages][2][D] (row (b, g) contiguous, page order), so that
+// scoring is one contiguous stream per row with no page-table indirection.
 #pragma once
 #include "common.cuh"
 
@@ -71,7 +73,8 @@ __global__ void meta_append_kernel(MetaParams p, const T *__restrict__ k_new,
     const size_t dst = (((size_t)blk * p.Hkv + h) * p.S + slot) * p.D + c * V::kElems;
     *reinterpret_cast<uint4 *>(k_pool + dst) = k;
     *reinterpret_cast<uint4 *>(v_pool + dst) = v;
-    T *mrec = meta + ((size_t)blk * p.Hkv + h) * 2 * p.D + c * V::kElems;
+    // logical metadata layout [B][Hkv][max_pages][2][D]
+    T *mrec = meta + (((size_t)b * p.Hkv + h) * p.max_pages + jl) * 2 * p.D + c * V::kElems;
     uint4 *mn = reinterpret_cast<uint4 *>(mrec);
     uint4 *mx = reinterpret_cast<uint4 *>(mrec + p.D);
     if (slot == 0) {  // first key of a page: m = M = k
@@ -113,7 +116,7 @@ __global__ void meta_build_kernel(MetaParams p, const T *__restrict__ k_pool,
             lo = V::vmin(lo, x);
             hi = V::vmax(hi, x);
         }
-        T *mrec = meta + ((size_t)blk * p.Hkv + h) * 2 * p.D + c * V::kElems;
+        T *mrec = meta + (((size_t)b * p.Hkv + h) * p.max_pages + jl) * 2 * p.D + c * V::kElems;
         *reinterpret_cast<uint4 *>(mrec) = lo;
         *reinterpret_cast<uint4 *>(mrec + p.D) = hi;
     }

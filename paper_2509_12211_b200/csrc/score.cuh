@@ -3,7 +3,8 @@
 //   s[b][g][jl] = max_{h in group g} sum_i max(q_hi * m_i, q_hi * M_i)
 //              = max_h ( q_h^+ . M + q_h^- . m )            (m <= M; reading R3)
 //
-// This is a streaming read of the metadata (one 2*d-element record per (page, kv head)).
+// This is a streaming read of the metadata: one 2*d-element record per (page, kv head), in
+// the logical layout [B][Hkv][max_pages][2][d], so a row is one contiguous run.
 //  * bf16, G <= 8: the record row [m | M] (K = 2d) times the coefficient matrix
 //    [q^- ; q^+] (2d x G) is a 16-page x 2d x 8-head product per warp tile, run on the
 //    tensor cores with mma.sync.m16n8k16 (bf16 x bf16 products are exact in fp32).  The
@@ -38,20 +39,20 @@ constexpr int kScoreWarps = 4;
 constexpr int kScoreTilesPerWarp = 2;
 constexpr int kScorePagesPerCta = kScoreWarps * kScoreTilesPerWarp * 16;
 
+// Scores of pages [chunk * 128, chunk * 128 + 128) of row `row` by one 4-warp CTA.
 template <int D>
-__global__ void __launch_bounds__(kScoreWarps * 32)
-    score_mma_kernel(ScoreParams p, const uint16_t *__restrict__ q,
-                     const uint16_t *__restrict__ meta, const int *__restrict__ page_table,
-                     const int *__restrict__ seq_lens, float *__restrict__ scores) {
+TS_DEV void score_mma_block(const ScoreParams &p, const uint16_t *__restrict__ q,
+                            const uint16_t *__restrict__ meta, const int *__restrict__ page_table,
+                            const int *__restrict__ seq_lens, float *__restrict__ scores, int row,
+                            int chunk) {
     constexpr int CH = 2 * D / 8;    // 16-byte chunks per record (16 for d = 64)
     constexpr int CPT = CH / 4;      // chunks per thread per record row
     constexpr int STEPS = CH / 2;    // k16 steps per record
-    const int row = blockIdx.y;      // b * Hkv + g
     const int b = row / p.Hkv, g = row % p.Hkv;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int gid = lane >> 2, t = lane & 3;
     const int P = local_pages(seq_lens[b], p.S, p.stride, p.offset);
-    const int cta_base = blockIdx.x * kScorePagesPerCta;
+    const int cta_base = chunk * kScorePagesPerCta;
     float *srow = scores + (size_t)row * p.max_pages;
 
     if (cta_base >= P) {  // nothing to score: fill -inf for this CTA's slice
@@ -70,8 +71,7 @@ __global__ void __launch_bounds__(kScoreWarps * 32)
         for (int hr = 0; hr < 2; ++hr) {
             const int jl = warp_base + tt * 16 + gid + hr * 8;
             if (jl < P) {
-                const int blk = page_table[(size_t)b * p.max_pages + jl];
-                const uint16_t *rec = meta + ((size_t)blk * p.Hkv + g) * 2 * D;
+                const uint16_t *rec = meta + ((size_t)row * p.max_pages + jl) * 2 * D;
 #pragma unroll
                 for (int i = 0; i < CPT; ++i) a[tt][hr][i] = ldg_nc_v4(rec + (t + 4 * i) * 8);
             } else {
@@ -126,6 +126,14 @@ __global__ void __launch_bounds__(kScoreWarps * 32)
     }
 }
 
+template <int D>
+__global__ void __launch_bounds__(kScoreWarps * 32)
+    score_mma_kernel(ScoreParams p, const uint16_t *__restrict__ q,
+                     const uint16_t *__restrict__ meta, const int *__restrict__ page_table,
+                     const int *__restrict__ seq_lens, float *__restrict__ scores) {
+    score_mma_block<D>(p, q, meta, page_table, seq_lens, scores, blockIdx.y, blockIdx.x);
+}
+
 // ------------------------------------------------------------------ SIMT path
 // Record = 2*D elements of T; LPR lanes per record (16-byte chunk each, CPL chunks per
 // lane).  q of the group staged in smem as fp32 [G][D].  grid = (ceil(max_pages/PPC), rows).
@@ -166,8 +174,7 @@ __global__ void __launch_bounds__(kSimtWarps * 32)
         const bool live = jl < P && jl < min(base + kSimtPagesPerCta, p.max_pages);
         float e[CPL][EPC];
         if (live) {
-            const int blk = page_table[(size_t)b * p.max_pages + jl];
-            const T *rec = meta + ((size_t)blk * p.Hkv + g) * 2 * D;
+            const T *rec = meta + ((size_t)row * p.max_pages + jl) * 2 * D;
 #pragma unroll
             for (int c = 0; c < CPL; ++c) {
                 const T *src = rec + (sl + c * LPR) * EPC;

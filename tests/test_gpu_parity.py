@@ -40,16 +40,15 @@ def gpu_meta(ts, d):
 
 
 def logical_meta(meta, page_table, seq_lens, S):
-    """GPU meta [NB][Hkv][2][d] -> oracle's logical [B][Hkv][mp][d] (valid pages only)."""
+    """GPU meta [B][Hkv][mp][2][d] -> oracle's (min, max) [B][Hkv][mp][d], valid pages only
+    (entries of pages >= P_b are left zero on both sides)."""
     m = oracle.widen(meta.cpu())
-    pt = page_table.cpu().numpy()
-    B, mp = pt.shape
-    out_min = np.zeros((B, m.shape[1], mp, m.shape[3]))
+    out_min = np.zeros(m.shape[:3] + m.shape[4:])
     out_max = np.zeros_like(out_min)
     for b, L in enumerate(seq_lens.tolist()):
         P = -(-L // S)
-        out_min[b, :, :P] = m[pt[b, :P], :, 0].transpose(1, 0, 2)
-        out_max[b, :, :P] = m[pt[b, :P], :, 1].transpose(1, 0, 2)
+        out_min[b, :, :P] = m[b, :, :P, 0]
+        out_max[b, :, :P] = m[b, :, :P, 1]
     return out_min, out_max
 
 
@@ -95,9 +94,9 @@ def test_meta_append_incremental_equals_oracle(ts, dtype):
     d = on_dev(src)
     kp = torch.zeros_like(d["k_pool"])
     vp = torch.zeros_like(d["v_pool"])
-    meta = torch.zeros((src["num_blocks"], 2, 2, 64), dtype=kp.dtype, device=DEV)
     lens = torch.zeros(3, dtype=torch.int32, device=DEV)
     L = ts.make_layout(d["q"], kp, d["page_table"])
+    meta = ts.new_meta(L, kp.dtype, DEV)
     pt = src["page_table"].numpy()
     for t in range(cfg.ctx):
         kn = torch.stack([src["k_pool"][pt[b, t // 16], :, t % 16] for b in range(3)]).to(DEV)
@@ -330,7 +329,9 @@ def test_shard_emulation_matches_unsharded(ts, world):
         assert torch.equal(ids[r], i1) and torch.equal(cnts[r], c1)
     assert np.array_equal(i1.cpu().numpy(), ref["sel_ids"])
     assert np.abs(o.cpu().numpy() - ref["o"]).max() <= 2e-3
-    assert torch.allclose(o, o1, atol=1e-5, rtol=0)
+    # P . V runs with tf32 P, rounded relative to each shard's own running max, so the
+    # sharded and unsharded outputs differ by O(2^-11) relative, not fp32 ulps
+    assert torch.allclose(o, o1, atol=5e-4, rtol=0)
 
 
 def test_lse_merge_kernel(ts):
