@@ -9,11 +9,10 @@
 
 #include "../../include/tinyserve.h"
 #include "attn.cuh"
-#include "attn_stream.cuh"
 #include "common.cuh"
+#include "decode_pipe.cuh"
 #include "meta.cuh"
 #include "score.cuh"
-#include "score_select.cuh"
 #include "select.cuh"
 
 using namespace ts;
@@ -22,6 +21,7 @@ namespace {
 
 thread_local int g_launches = 0;
 unsigned long long *g_dbg_ts = nullptr;  // development: attention CTA timestamps
+volatile int *g_dbg_state = nullptr;     // development: live CTA state (host-mapped)
 thread_local cudaEvent_t g_phase_ev[4] = {nullptr, nullptr, nullptr, nullptr};
 
 // records phase event i on the stream (external record node when captured in a graph)
@@ -30,8 +30,9 @@ inline void phase_mark(int i, cudaStream_t st) {
 }
 
 constexpr int kMaxSel = 4096;      // max selected pages per row
-constexpr int kStreamNC = 6;       // consumer warps per attention CTA (+ TMA, scheduler, merge)
-constexpr int kStreamStages = 18;  // ring stages (4 KB each): 3 per consumer
+constexpr int kPipeNC = 6;         // consumer warps per pipeline CTA (+ TMA, scheduler, merge)
+constexpr int kPipeStages = 18;    // ring stages (4 KB each); a multiple of kPipeNC
+constexpr int kScoreChunkTiles = 32;  // metadata tiles (x 16 pages) per score item
 
 inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
@@ -108,7 +109,7 @@ bool make_pool_map(CUtensorMap *map, const void *pool, const ts_layout *L, int T
 
 // ---------------------------------------------------------------- workspace layout
 // attention workspace: [tickets: rows u32][work counters: 2 u32][partials: rows x ipr x 8 x kPS]
-// with ipr <= kMaxItemsPerRow items per row (attn_stream.cuh).
+// with ipr <= kMaxItemsPerRow items per row (decode_pipe.cuh).
 constexpr int kMaxItemsPerRow = 64;
 struct AttnWs {
     size_t tickets, work, part, total;
@@ -127,8 +128,13 @@ AttnWs attn_ws_layout(const ts_layout *L, int sel_stride) {
 
 struct StepWs {
     AttnWs attn;
-    size_t scores, sel_ids, sel_count, sc_tickets, ready, total;
+    size_t scores, sel_ids, sel_count, sc_tickets, ready, cand_sc, cand_id, total;
 };
+// score items per row of the fused pipeline
+int score_chunks(const ts_layout *L) {
+    const int mtiles = (L->max_pages + 15) / 16;
+    return (mtiles + kScoreChunkTiles - 1) / kScoreChunkTiles;
+}
 StepWs step_ws_layout(const ts_layout *L, int kmax) {
     StepWs w;
     w.attn = attn_ws_layout(L, kmax);
@@ -138,7 +144,10 @@ StepWs step_ws_layout(const ts_layout *L, int kmax) {
     w.sel_count = w.sel_ids + round_up(rows * kmax * 4, 256);
     w.sc_tickets = w.sel_count + round_up(rows * 4, 256);
     w.ready = w.sc_tickets + round_up(rows * 4, 256);
-    w.total = w.ready + round_up(rows * 4, 256);
+    const size_t nc = rows * (size_t)score_chunks(L) * kmax;
+    w.cand_sc = w.ready + round_up(rows * 4, 256);
+    w.cand_id = w.cand_sc + round_up(nc * 4, 256);
+    w.total = w.cand_id + round_up(nc * 4, 256);
     return w;
 }
 
@@ -209,34 +218,67 @@ ts_status launch_select(const float *scores, int rows, int stride, const int *ro
     return launch_status();
 }
 
-// Persistent dynamic-item attention (bf16).  ready != nullptr (decode-step mode): rows are
-// consumed as score_select_kernel releases them, and the launch uses programmatic
-// dependent launch so this grid overlaps the scoring grid.
+// The persistent pipeline kernel (decode_pipe.cuh).  fused != nullptr: the whole decode
+// step (score items + attention items); otherwise attention only over a given selection.
+struct FusedArgs {
+    const void *meta;
+    unsigned *ready, *sc_tickets;
+    float *cand_sc;
+    int *cand_id, *sel_out, *cnt_out;
+    int kmax;
+};
+
+template <int TT, int STAGES>
+ts_status launch_pipe_s(const ts_layout *L, AttnParams &p, const void *k_pool, const void *v_pool,
+                        unsigned *work, const FusedArgs *fa, cudaStream_t st);
+
 template <int TT>
-ts_status launch_attn_stream(const ts_layout *L, AttnParams &p, const void *k_pool,
-                             const void *v_pool, unsigned *ready, unsigned *work, cudaStream_t st) {
-    using SM = StreamSmem<kStreamNC, kStreamStages>;
-    auto kern = attn_stream_kernel<TT, kStreamNC, kStreamStages>;
+ts_status launch_pipe(const ts_layout *L, AttnParams &p, const void *k_pool, const void *v_pool,
+                      unsigned *work, const FusedArgs *fa, cudaStream_t st) {
+    static const int stages = getenv("TS_PIPE_STAGES") ? atoi(getenv("TS_PIPE_STAGES")) : kPipeStages;
+    if (stages == 12) return launch_pipe_s<TT, 12>(L, p, k_pool, v_pool, work, fa, st);
+    if (stages == 24) return launch_pipe_s<TT, 24>(L, p, k_pool, v_pool, work, fa, st);
+    return launch_pipe_s<TT, kPipeStages>(L, p, k_pool, v_pool, work, fa, st);
+}
+
+template <int TT, int STAGES>
+ts_status launch_pipe_s(const ts_layout *L, AttnParams &p, const void *k_pool, const void *v_pool,
+                        unsigned *work, const FusedArgs *fa, cudaStream_t st) {
+    using SM = PipeSmem<kPipeNC, STAGES>;
+    auto kern = decode_pipe_kernel<TT, kPipeNC, STAGES>;
     CUtensorMap tmK, tmV;
     if (!make_pool_map(&tmK, k_pool, L, TT) || !make_pool_map(&tmV, v_pool, L, TT))
         return TS_ERR_CUDA;
     const int rows = L->batch * L->num_kv_heads;
-    StreamParams sp{};
+    PipeParams sp{};
     sp.tpr = p.sel_stride * (L->page_size / TT);
-    static const int per_sm = getenv("TS_ATTN_CTAS_PER_SM") ? atoi(getenv("TS_ATTN_CTAS_PER_SM")) : 2;
-    const int slots_cap = device_sms() * per_sm;
-    // item size: ~32 slots (few merges), a multiple of NC; a whole row when the row is short
     long long is = std::min<long long>(sp.tpr, 32);
-    is = (is + kStreamNC - 1) / kStreamNC * kStreamNC;
+    is = (is + kPipeNC - 1) / kPipeNC * kPipeNC;
     sp.is = (int)std::max<long long>(is, 1);
     sp.ipr = (sp.tpr + sp.is - 1) / sp.is;
     if (sp.ipr > kMaxItemsPerRow) {  // long rows: grow items so the partials fit the workspace
         sp.is = (sp.tpr + kMaxItemsPerRow - 1) / kMaxItemsPerRow;
-        sp.is = (sp.is + kStreamNC - 1) / kStreamNC * kStreamNC;
+        sp.is = (sp.is + kPipeNC - 1) / kPipeNC * kPipeNC;
         sp.ipr = (sp.tpr + sp.is - 1) / sp.is;
     }
-    sp.n_items = rows * sp.ipr;
-    const int grid = std::max(1, std::min(sp.n_items, slots_cap));
+    sp.n_attn = rows * sp.ipr;
+    if (fa) {
+        sp.meta = static_cast<const uint16_t *>(fa->meta);
+        sp.ready = fa->ready;
+        sp.sc_tickets = fa->sc_tickets;
+        sp.cand_sc = fa->cand_sc;
+        sp.cand_id = fa->cand_id;
+        sp.sel_out = fa->sel_out;
+        sp.cnt_out = fa->cnt_out;
+        sp.kmax = fa->kmax;
+        sp.mtiles = (L->max_pages + 15) / 16;
+        sp.sch = kScoreChunkTiles;
+        sp.spr = score_chunks(L);
+        if (sp.spr > 1 && sp.spr * sp.kmax > SM::kSelKeys) return TS_ERR_UNSUPPORTED;
+        sp.n_score = rows * sp.spr;
+    }
+    static const int per_sm = getenv("TS_PIPE_CTAS_PER_SM") ? atoi(getenv("TS_PIPE_CTAS_PER_SM")) : 2;
+    const int grid = std::max(1, std::min(sp.n_score + sp.n_attn, device_sms() * per_sm));
     const size_t sm = SM::bytes();
     static int sm_set = 0;  // opt-in grown on demand (dynamic + static <= 227 KB)
     if ((int)sm > sm_set) {
@@ -246,24 +288,12 @@ ts_status launch_attn_stream(const ts_layout *L, AttnParams &p, const void *k_po
         sm_set = (int)sm;
     }
     sp.a = p;
-    sp.ready = ready;
     sp.work = work;
     static const int dbg = getenv("TS_DEBUG_ATTN") ? atoi(getenv("TS_DEBUG_ATTN")) : 0;
     sp.dbg = dbg;
     sp.dbg_ts = g_dbg_ts;
-    sp.kpool_dbg = static_cast<const char *>(k_pool);
-    sp.vpool_dbg = static_cast<const char *>(v_pool);
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3((kStreamNC + 3) * 32);
-    cfg.dynamicSmemBytes = sm;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = ready ? 1 : 0;
-    if (cudaLaunchKernelEx(&cfg, kern, tmK, tmV, sp) != cudaSuccess) return TS_ERR_CUDA;
+    sp.dbg_state = g_dbg_state;
+    kern<<<grid, (kPipeNC + 3) * 32, sm, st>>>(tmK, tmV, sp);
     ++g_launches;
     return launch_status();
 }
@@ -271,7 +301,7 @@ ts_status launch_attn_stream(const ts_layout *L, AttnParams &p, const void *k_po
 ts_status launch_attn(const ts_layout *L, const void *q, const void *k_pool, const void *v_pool,
                       const int *pt, const int *sl, const int *sel_ids, const int *sel_count,
                       int sel_stride, float scale, float *o, float *lse, void *ws, cudaStream_t st,
-                      unsigned *ready = nullptr) {
+                      const FusedArgs *fa = nullptr) {
     const int rows = L->batch * L->num_kv_heads;
     if (rows == 0) return TS_OK;
     const AttnWs w = attn_ws_layout(L, sel_stride);
@@ -291,6 +321,7 @@ ts_status launch_attn(const ts_layout *L, const void *q, const void *k_pool, con
     p.max_pages = L->max_pages;
     p.stride = L->shard_stride;
     p.offset = L->shard_offset;
+    p.num_blocks = L->num_blocks;
     p.scale = scale;
     p.o = o;
     p.lse = lse;
@@ -301,8 +332,8 @@ ts_status launch_attn(const ts_layout *L, const void *q, const void *k_pool, con
     if (L->kv_dtype == TS_BF16) {
         if (!bf16_attn_supported(L) || sel_stride > kMaxSel) return TS_ERR_UNSUPPORTED;
         unsigned *work = reinterpret_cast<unsigned *>(static_cast<char *>(ws) + w.work);
-        if (L->page_size >= 16) return launch_attn_stream<16>(L, p, k_pool, v_pool, ready, work, st);
-        return launch_attn_stream<8>(L, p, k_pool, v_pool, ready, work, st);
+        if (L->page_size >= 16) return launch_pipe<16>(L, p, k_pool, v_pool, work, fa, st);
+        return launch_pipe<8>(L, p, k_pool, v_pool, work, fa, st);
     }
     const int threads = 32 * std::min(p.G, 8);
     if (L->head_dim == 64)
@@ -337,6 +368,7 @@ int32_t ts_last_launch_count(void) { return g_launches; }
 
 // development hook (not in the public header): device buffer for attention CTA timestamps
 void ts_debug_timestamps(void *buf) { g_dbg_ts = static_cast<unsigned long long *>(buf); }
+void ts_debug_state(void *buf) { g_dbg_state = static_cast<volatile int *>(buf); }
 
 void ts_profile_events(void *const *events, int32_t n) {
     for (int i = 0; i < 4; ++i)
@@ -461,40 +493,20 @@ ts_status ts_decode_step(const ts_layout *L, const void *q, const void *k_pool, 
     int *cnt = sel_count_out ? sel_count_out : reinterpret_cast<int *>(wb + w.sel_count);
     const cudaStream_t st = as_stream(stream);
     const int rows = L->batch * L->num_kv_heads;
-    if (L->kv_dtype == TS_BF16 && group_of(L) <= 8) {
-        // scoring + selection grid (releases rows) -> PDL-overlapped attention grid that
-        // consumes rows as they are selected (2 kernels, one programmatic dependency edge)
-        unsigned *tick = reinterpret_cast<unsigned *>(wb + w.sc_tickets);
-        unsigned *ready = reinterpret_cast<unsigned *>(wb + w.ready);
-        ScoreParams sp{L->batch, L->num_q_heads, L->num_kv_heads, group_of(L), L->head_dim,
-                       L->page_size, L->max_pages, 1, 0};
-        FusedSelect fs{ids, cnt, tick, ready, kmax};
-        const size_t sm = (size_t)L->max_pages * 4;
-        if (sm > 160 * 1024) return TS_ERR_UNSUPPORTED;
-        dim3 grid((L->max_pages + kScorePagesPerCta - 1) / kScorePagesPerCta, rows);
+    if (L->kv_dtype == TS_BF16 && group_of(L) <= 8 && L->head_dim == 64) {
+        // the whole step as one persistent pipeline kernel (decode_pipe.cuh)
+        FusedArgs fa{meta,
+                     reinterpret_cast<unsigned *>(wb + w.ready),
+                     reinterpret_cast<unsigned *>(wb + w.sc_tickets),
+                     reinterpret_cast<float *>(wb + w.cand_sc),
+                     reinterpret_cast<int *>(wb + w.cand_id),
+                     ids, cnt, kmax};
         phase_mark(0, st);
-        if (rows > 0) {
-            if (L->head_dim == 64) {
-                static std::once_flag once;
-                std::call_once(once, [] { cudaFuncSetAttribute(score_select_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024); });
-                score_select_kernel<64><<<grid, kScoreWarps * 32, sm, st>>>(
-                    sp, (const uint16_t *)q, (const uint16_t *)meta, page_table, seq_lens, scores, fs);
-            } else {
-                static std::once_flag once;
-                std::call_once(once, [] { cudaFuncSetAttribute(score_select_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024); });
-                score_select_kernel<128><<<grid, kScoreWarps * 32, sm, st>>>(
-                    sp, (const uint16_t *)q, (const uint16_t *)meta, page_table, seq_lens, scores, fs);
-            }
-            if ((s = launch_status()) != TS_OK) return s;
-        }
-        // no phase marks between the two kernels: an event node there would break the
-        // programmatic (PDL) edge that lets the attention grid overlap the scoring grid
-        g_launches = 0;
-        if ((s = launch_attn(L, q, k_pool, v_pool, page_table, seq_lens, ids, cnt, kmax, scale, o,
-                             lse, ws, st, ready)) != TS_OK)
+        if (rows > 0 &&
+            (s = launch_attn(L, q, k_pool, v_pool, page_table, seq_lens, ids, cnt, kmax, scale, o,
+                             lse, ws, st, &fa)) != TS_OK)
             return s;
         phase_mark(3, st);
-        g_launches += rows > 0 ? 1 : 0;
         return TS_OK;
     }
     int launches = 0;

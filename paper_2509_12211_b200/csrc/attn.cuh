@@ -1,7 +1,7 @@
 // attn.cuh — shared attention definitions + the fp32 CUDA-core path and the LSE merge
 // (SparseAttn PAPER.md:169-172; Alg. 1 Steps 3-4).
 //
-// The bf16 tensor-core path (the hot one) is attn_stream.cuh.  Its fragment maps, used
+// The bf16 tensor-core path (the hot one) is decode_pipe.cuh.  Its fragment maps, used
 // there, are:
 //   S^T = Q K^T : mma.m16n8k16 bf16; A rows = the G q heads of the kv group (rows >= G are
 //                 zero), k-slot permutation d = 16t + 4s + {0..3} so that a thread's two
@@ -24,7 +24,7 @@ struct AttnParams {
     const int *sel_ids;
     const int *sel_count;
     int sel_stride;
-    int B, Hq, Hkv, G, D, S, max_pages, stride, offset;
+    int B, Hq, Hkv, G, D, S, max_pages, stride, offset, num_blocks;
     float scale;       // softmax scale (reading R1)
     float *o;
     float *lse;        // nullable
