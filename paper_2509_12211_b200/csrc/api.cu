@@ -13,7 +13,9 @@
 #include "decode_pipe.cuh"
 #include "meta.cuh"
 #include "score.cuh"
+#include "score_select.cuh"
 #include "select.cuh"
+#include "sparse_attn.cuh"
 
 using namespace ts;
 
@@ -21,6 +23,7 @@ namespace {
 
 thread_local int g_launches = 0;
 unsigned long long *g_dbg_ts = nullptr;  // development: attention CTA timestamps
+unsigned long long *g_dbg_ss = nullptr;  // development: score/select CTA timestamps
 volatile int *g_dbg_state = nullptr;     // development: live CTA state (host-mapped)
 thread_local cudaEvent_t g_phase_ev[4] = {nullptr, nullptr, nullptr, nullptr};
 
@@ -78,6 +81,39 @@ int device_sms() {
     return sms;
 }
 
+// Co-resident clusters of `cluster` CTAs for a kernel configuration (cached; host only).
+template <typename K>
+int max_active_clusters(K kern, int threads, size_t smem, int cluster) {
+    static std::mutex mu;
+    static std::unordered_map<unsigned long long, int> cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const unsigned long long key = (reinterpret_cast<uintptr_t>((const void *)kern) * 1315423911ull) ^
+                                   ((unsigned long long)smem << 20) ^ ((unsigned long long)cluster << 8) ^
+                                   (unsigned long long)threads ^ ((unsigned long long)dev << 56);
+    std::lock_guard<std::mutex> g(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(cluster * 64);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cluster;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, (const void *)kern, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        n = 0;
+    }
+    cache[key] = n;
+    return n;
+}
+
 // ---------------------------------------------------------------- TMA descriptors
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -128,7 +164,7 @@ AttnWs attn_ws_layout(const ts_layout *L, int sel_stride) {
 
 struct StepWs {
     AttnWs attn;
-    size_t scores, sel_ids, sel_count, sc_tickets, ready, cand_sc, cand_id, total;
+    size_t scores, sel_ids, sel_count, sc_tickets, ready, cand_sc, cand_id, sel_blk, total;
 };
 // score items per row of the fused pipeline
 int score_chunks(const ts_layout *L) {
@@ -147,7 +183,8 @@ StepWs step_ws_layout(const ts_layout *L, int kmax) {
     const size_t nc = rows * (size_t)score_chunks(L) * kmax;
     w.cand_sc = w.ready + round_up(rows * 4, 256);
     w.cand_id = w.cand_sc + round_up(nc * 4, 256);
-    w.total = w.cand_id + round_up(nc * 4, 256);
+    w.sel_blk = w.cand_id + round_up(nc * 4, 256);
+    w.total = w.sel_blk + round_up(rows * kmax * 4, 256);
     return w;
 }
 
@@ -298,19 +335,180 @@ ts_status launch_pipe_s(const ts_layout *L, AttnParams &p, const void *k_pool, c
     return launch_status();
 }
 
-ts_status launch_attn(const ts_layout *L, const void *q, const void *k_pool, const void *v_pool,
-                      const int *pt, const int *sl, const int *sel_ids, const int *sel_count,
-                      int sel_stride, float scale, float *o, float *lse, void *ws, cudaStream_t st,
-                      const FusedArgs *fa = nullptr) {
+// bf16 sparse attention (sparse_attn.cuh): grid = rows x C CTAs, one cluster per row.
+// W warps per CTA: 4 when the rows alone fill the GPU (4 CTAs / SM), 8 otherwise, 16 for
+// very few rows; C = CTAs per row so that rows x C ~ one wave, each warp keeping >= 2
+// octets.  pdl: launched as a programmatic dependent of the previous kernel.
+template <int W, int DP>
+ts_status prepare_sa(size_t sm) {
+    auto kern = sparse_attn_kernel<W, DP>;
+    static std::mutex mu;
+    static size_t sm_set = 0;
+    static bool np_set = false;
+    std::lock_guard<std::mutex> g(mu);
+    if (sm > sm_set) {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) !=
+            cudaSuccess)
+            return TS_ERR_CUDA;
+        sm_set = sm;
+    }
+    if (!np_set) {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+            cudaSuccess)
+            return TS_ERR_CUDA;
+        np_set = true;
+    }
+    return TS_OK;
+}
+
+// C = CTAs per row: the largest C <= cdesired whose clusters all fit on the GPU at once
+template <int W, int DP>
+ts_status launch_sa(const AttnParams &p, int rows, int cdesired, bool pdl, cudaStream_t st) {
+    auto kern = sparse_attn_kernel<W, DP>;
+    const size_t sm = SaSmem<W>::bytes(p.sel_stride);
+    ts_status s = prepare_sa<W, DP>(sm);
+    if (s != TS_OK) return s;
+    int C = std::max(1, cdesired);
+    while (C > 1 && max_active_clusters(kern, W * 32, sm, C) < rows) --C;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(rows * C);
+    cfg.blockDim = dim3(W * 32);
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    int na = 0;
+    at[na].id = cudaLaunchAttributeClusterDimension;
+    at[na].val.clusterDim.x = C;
+    at[na].val.clusterDim.y = 1;
+    at[na].val.clusterDim.z = 1;
+    ++na;
+    if (pdl) {
+        at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    cfg.attrs = at;
+    cfg.numAttrs = na;
+    if (cudaLaunchKernelEx(&cfg, kern, p, C) != cudaSuccess) return TS_ERR_CUDA;
+    ++g_launches;
+    return launch_status();
+}
+
+ts_status launch_sparse_attn(const ts_layout *L, const AttnParams &p, bool pdl, cudaStream_t st) {
+    const int rows = L->batch * L->num_kv_heads;
+    const int sms = device_sms();
+    const int n_oct = p.sel_stride * (L->page_size / 8);  // upper bound per row
+    static const int cmax_env = getenv("TS_SA_CMAX") ? atoi(getenv("TS_SA_CMAX")) : 16;
+    int W = rows >= 2 * sms ? 4 : (rows * 16 < sms ? 16 : 8);
+    static const int w_env = getenv("TS_SA_W") ? atoi(getenv("TS_SA_W")) : 0;
+    if (w_env == 4 || w_env == 8 || w_env == 16) W = w_env;
+    const int per_sm = W == 4 ? 4 : (W == 8 ? 2 : 1);
+    int C = std::max(1, std::min(cmax_env, sms * per_sm / std::max(1, rows)));
+    C = std::max(1, std::min(C, n_oct / (2 * W)));
+    if (W == 4) return launch_sa<4, 3>(p, rows, C, pdl, st);
+    if (W == 8) return launch_sa<8, 3>(p, rows, C, pdl, st);
+    return launch_sa<16, 3>(p, rows, C, pdl, st);
+}
+
+// Fused score + select (score_select.cuh): grid = rows x C CTAs (cluster per row), each
+// CTA a contiguous chunk of the row's pages; C so that rows x C ~ 3 CTAs per SM.
+template <int W, int R>
+ts_status launch_ss_t(ScoreSelParams &p, int rows, int cdesired, cudaStream_t st) {
+    auto kern = score_select_kernel<W, R>;
+    const size_t sm = SsSmem<W, R>::bytes(p.max_pages);
+    if (sm > 227 * 1024) return TS_ERR_UNSUPPORTED;
+    {
+        static std::mutex mu;
+        static size_t sm_set = 0;
+        static bool np_set = false;
+        std::lock_guard<std::mutex> g(mu);
+        if (sm > sm_set) {
+            if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) !=
+                cudaSuccess)
+                return TS_ERR_CUDA;
+            sm_set = sm;
+        }
+        if (!np_set) {
+            if (cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+                cudaSuccess)
+                return TS_ERR_CUDA;
+            np_set = true;
+        }
+    }
+    // chunk per CTA (a multiple of the stage), C = CTAs per row; the largest C <= cdesired
+    // whose clusters all fit at once (one wave: no row waits for another row's CTAs)
+    int C = std::max(1, cdesired), chunk = 0;
+    for (;; --C) {
+        chunk = (p.max_pages + C - 1) / C;
+        chunk = (chunk + kSsStagePages - 1) / kSsStagePages * kSsStagePages;
+        const int c = (p.max_pages + chunk - 1) / chunk;
+        if (C == 1 || max_active_clusters(kern, (W + 1) * 32, sm, c) >= rows) {
+            C = c;
+            break;
+        }
+    }
+    p.C = C;
+    p.chunk = chunk;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(rows * p.C);
+    cfg.blockDim = dim3((W + 1) * 32);
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = p.C;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, kern, p) != cudaSuccess) return TS_ERR_CUDA;
+    ++g_launches;
+    return launch_status();
+}
+
+ts_status launch_score_select(const ts_layout *L, const void *q, const void *meta, const int *pt,
+                              const int *sl, int *ids, int *blk, int *cnt, int kmax, unsigned *ready,
+                              cudaStream_t st) {
     const int rows = L->batch * L->num_kv_heads;
     if (rows == 0) return TS_OK;
+    ScoreSelParams p{};
+    p.q = static_cast<const uint16_t *>(q);
+    p.meta = static_cast<const uint16_t *>(meta);
+    p.page_table = pt;
+    p.seq_lens = sl;
+    p.sel_ids = ids;
+    p.sel_blk = blk;
+    p.sel_count = cnt;
+    p.B = L->batch;
+    p.Hq = L->num_q_heads;
+    p.Hkv = L->num_kv_heads;
+    p.G = group_of(L);
+    p.S = L->page_size;
+    p.max_pages = L->max_pages;
+    p.kmax = kmax;
+    p.dbg = g_dbg_ss;
+    static const int per_sm = getenv("TS_SS_PER_SM") ? atoi(getenv("TS_SS_PER_SM")) : 3;
+    static const int cmax = getenv("TS_SS_CMAX") ? atoi(getenv("TS_SS_CMAX")) : 16;
+    const int target = device_sms() * per_sm;
+    const int max_c = std::max(1, std::min(cmax, (L->max_pages + 63) / 64));  // >= 64 pages per CTA
+    const int C = std::max(1, std::min(max_c, (target + rows - 1) / rows));
+    p.ready = ready;
+    return launch_ss_t<4, 4>(p, rows, C, st);
+}
+
+AttnParams attn_params(const ts_layout *L, const void *q, const void *k_pool, const void *v_pool,
+                       const int *pt, const int *sl, const int *sel_ids, const int *sel_count,
+                       int sel_stride, float scale, float *o, float *lse, void *ws) {
     const AttnWs w = attn_ws_layout(L, sel_stride);
     AttnParams p{};
     p.q = q;
+    p.k_pool = k_pool;
+    p.v_pool = v_pool;
     p.page_table = pt;
     p.seq_lens = sl;
     p.sel_ids = sel_ids;
     p.sel_count = sel_count;
+    p.sel_blk = nullptr;
     p.sel_stride = sel_stride;
     p.B = L->batch;
     p.Hq = L->num_q_heads;
@@ -328,9 +526,24 @@ ts_status launch_attn(const ts_layout *L, const void *q, const void *k_pool, con
     p.tickets = reinterpret_cast<unsigned *>(static_cast<char *>(ws) + w.tickets);
     p.part = reinterpret_cast<float *>(static_cast<char *>(ws) + w.part);
     p.splits = 1;
-    p.items = rows;
+    p.items = L->batch * L->num_kv_heads;
+    p.dbg = g_dbg_ts;
+    return p;
+}
+
+ts_status launch_attn(const ts_layout *L, const void *q, const void *k_pool, const void *v_pool,
+                      const int *pt, const int *sl, const int *sel_ids, const int *sel_count,
+                      int sel_stride, float scale, float *o, float *lse, void *ws, cudaStream_t st,
+                      const FusedArgs *fa = nullptr) {
+    const int rows = L->batch * L->num_kv_heads;
+    if (rows == 0) return TS_OK;
+    const AttnWs w = attn_ws_layout(L, sel_stride);
+    AttnParams p = attn_params(L, q, k_pool, v_pool, pt, sl, sel_ids, sel_count, sel_stride, scale,
+                               o, lse, ws);
     if (L->kv_dtype == TS_BF16) {
         if (!bf16_attn_supported(L) || sel_stride > kMaxSel) return TS_ERR_UNSUPPORTED;
+        static const bool use_pipe = getenv("TS_ATTN_PIPE") && atoi(getenv("TS_ATTN_PIPE"));
+        if (!fa && !use_pipe) return launch_sparse_attn(L, p, false, st);
         unsigned *work = reinterpret_cast<unsigned *>(static_cast<char *>(ws) + w.work);
         if (L->page_size >= 16) return launch_pipe<16>(L, p, k_pool, v_pool, work, fa, st);
         return launch_pipe<8>(L, p, k_pool, v_pool, work, fa, st);
@@ -368,6 +581,7 @@ int32_t ts_last_launch_count(void) { return g_launches; }
 
 // development hook (not in the public header): device buffer for attention CTA timestamps
 void ts_debug_timestamps(void *buf) { g_dbg_ts = static_cast<unsigned long long *>(buf); }
+void ts_debug_ss_timestamps(void *buf) { g_dbg_ss = static_cast<unsigned long long *>(buf); }
 void ts_debug_state(void *buf) { g_dbg_state = static_cast<volatile int *>(buf); }
 
 void ts_profile_events(void *const *events, int32_t n) {
@@ -493,7 +707,8 @@ ts_status ts_decode_step(const ts_layout *L, const void *q, const void *k_pool, 
     int *cnt = sel_count_out ? sel_count_out : reinterpret_cast<int *>(wb + w.sel_count);
     const cudaStream_t st = as_stream(stream);
     const int rows = L->batch * L->num_kv_heads;
-    if (L->kv_dtype == TS_BF16 && group_of(L) <= 8 && L->head_dim == 64) {
+    static const bool use_pipe = getenv("TS_STEP_PIPE") && atoi(getenv("TS_STEP_PIPE"));
+    if (L->kv_dtype == TS_BF16 && group_of(L) <= 8 && L->head_dim == 64 && use_pipe) {
         // the whole step as one persistent pipeline kernel (decode_pipe.cuh)
         FusedArgs fa{meta,
                      reinterpret_cast<unsigned *>(wb + w.ready),
@@ -507,6 +722,29 @@ ts_status ts_decode_step(const ts_layout *L, const void *q, const void *k_pool, 
                              lse, ws, st, &fa)) != TS_OK)
             return s;
         phase_mark(3, st);
+        return TS_OK;
+    }
+    if (L->kv_dtype == TS_BF16 && group_of(L) <= 8 && L->head_dim == 64) {
+        // score + select (cluster per row) -> sparse attention (PDL, blocks pre-resolved)
+        int *blk = reinterpret_cast<int *>(wb + w.sel_blk);
+        static const bool flags = !getenv("TS_NO_FLAGS");
+        unsigned *ready = flags ? reinterpret_cast<unsigned *>(wb + w.ready) : nullptr;
+        phase_mark(0, st);
+        if ((s = launch_score_select(L, q, meta, page_table, seq_lens, ids, blk, cnt, kmax, ready,
+                                     st)) != TS_OK)
+            return s;
+        phase_mark(1, st);
+        phase_mark(2, st);
+        if (rows > 0) {
+            AttnParams p = attn_params(L, q, k_pool, v_pool, page_table, seq_lens, ids, cnt, kmax,
+                                       scale, o, lse, ws);
+            p.sel_blk = blk;
+            p.ready = ready;
+            static const bool pdl = !getenv("TS_NO_PDL");
+            if ((s = launch_sparse_attn(L, p, pdl, st)) != TS_OK) return s;
+        }
+        phase_mark(3, st);
+        g_launches = rows > 0 ? 2 : 1;
         return TS_OK;
     }
     int launches = 0;

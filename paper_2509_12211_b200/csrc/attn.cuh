@@ -19,10 +19,14 @@ namespace ts {
 
 struct AttnParams {
     const void *q;
+    const void *k_pool;  // [NB][Hkv][S][D] (sparse_attn.cuh; the SIMT / pipeline kernels take them as arguments)
+    const void *v_pool;
     const int *page_table;
     const int *seq_lens;
     const int *sel_ids;
     const int *sel_count;
+    const int *sel_blk;  // nullable: physical block of each selected page (fused step)
+    unsigned *ready;     // nullable: per-row selection flags (fused step; reset after use)
     int sel_stride;
     int B, Hq, Hkv, G, D, S, max_pages, stride, offset, num_blocks;
     float scale;       // softmax scale (reading R1)
@@ -31,6 +35,7 @@ struct AttnParams {
     float *part;       // [rows][splits][8][kPS]
     unsigned *tickets; // [rows]
     int splits, items;
+    unsigned long long *dbg;  // development: per-CTA globaltimer stamps (nullable)
 };
 
 constexpr int kAttnD = 64;        // head_dim of the tensor-core path

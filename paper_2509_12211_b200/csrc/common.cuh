@@ -2,6 +2,7 @@
 // PTX wrappers: mbarrier, TMA tile loads (cp.async.bulk.tensor), legacy-tensor-core
 // mma.sync (bf16 m16n8k16, tf32 m16n8k8), bf16 <-> fp32 bit conversions.
 #pragma once
+#include <cooperative_groups.h>
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -9,6 +10,8 @@
 #define TS_DEV __device__ __forceinline__
 
 namespace ts {
+
+namespace cg = cooperative_groups;
 
 constexpr float kNegInf = -__builtin_huge_valf();
 constexpr float kLog2e = 1.4426950408889634f;
@@ -105,6 +108,12 @@ TS_DEV uint32_t ld_acquire_u32(const unsigned *p) {
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+TS_DEV uint32_t ld_relaxed_u32(const unsigned *p) {
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+TS_DEV void fence_acquire_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 TS_DEV void st_release_u32(unsigned *p, uint32_t v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -138,6 +147,15 @@ TS_DEV void bulk_load(uint32_t dst, const void *src, uint32_t bytes, uint32_t ba
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
         "l"(src), "r"(bytes), "r"(bar)
+        : "memory");
+}
+// 1-D bulk copy with an L2 cache-policy hint (streaming data: evict_first).
+TS_DEV void bulk_load_hint(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar,
+                           uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], "
+        "[%1], %2, [%3], %4;" ::"r"(dst),
+        "l"(src), "r"(bytes), "r"(bar), "l"(policy)
         : "memory");
 }
 // Ampere-style async copy, 16 B global -> shared (L2 only), and its mbarrier hook: the

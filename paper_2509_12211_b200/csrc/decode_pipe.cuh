@@ -75,9 +75,10 @@ struct PipeSmem {
     static constexpr int kSlotFloats = NC * 8 * kPS;               // partials or chunk scores
     static constexpr int kScratch = kQ + 2 * 8 * kRowBytes;
     static constexpr int kSelKeys = 1024;                          // candidate-merge entries
-    static constexpr int kHist = kScratch + kNSlot * kSlotFloats * 4;  // 256-int histogram
+    static constexpr int kMaxParts = 64;                           // = kMaxItemsPerRow (api.cu)
+    static constexpr int kHist = kScratch + kNSlot * kSlotFloats * 4;  // merge weights [parts][8]
     static constexpr int kDR = 256;                                // descriptor ring entries
-    static constexpr int kDesc = kHist + 256 * 4;
+    static constexpr int kDesc = kHist + kMaxParts * 8 * 4;
     static constexpr int kBars = kDesc + kDR * 16;
     static constexpr int kInfo = kBars + (2 * STAGES + 4) * 8;     // per-stage int4 info
     static constexpr int kItemRing = 64;                           // > items in flight
@@ -106,71 +107,101 @@ constexpr int kFirst = 1 << 8, kLast = 1 << 9, kEnd = 1 << 10, kScoreTile = 1 <<
 // ids ? ids[i] : id0 + i).  -inf entries are "no page" and never selected.  Ties at the
 // threshold go to the lower index (= lower page id, reading R6).  Writes the kk selected
 // ids (ascending) and scores to out_id / out_sc (global or shared), pads up to k with
-// (-1, -inf), returns kk.  8-bit radix passes with a warp-private smem histogram.
-TS_DEV int warp_topk(const float *sc, const int *ids, int id0, int n, int k, int *hist,
-                     int *out_id, float *out_sc) {
+// (-1, -inf), returns kk.
+//
+// Threshold search, no histogram: T = the kk-th largest orderable key is the largest t
+// with #{key >= t} >= kk, found bit by bit from the highest bit in which the smallest and
+// the largest valid key differ (the bits above are common to every candidate threshold).
+// Each step is one compare per key + one warp reduction (REDUX); keys live in registers
+// (KR per lane) when n <= 32 * KR, else they are re-read from smem.  It stops early when a
+// prefix bin is taken whole (#{key >= t} == kk).
+template <int KR>
+TS_DEV int warp_topk(const float *sc, const int *ids, int id0, int n, int k, int *out_id,
+                     float *out_sc) {
     const int lane = threadIdx.x & 31;
+    const bool inreg = n <= 32 * KR;
+    uint32_t kr[KR];
     int nvalid = 0;
-    for (int i = lane; i < n; i += 32) nvalid += score_key(sc[i]) != kKeyNegInf;
+    uint32_t kmin = 0xffffffffu, kmax = 0u;
+#pragma unroll
+    for (int j = 0; j < KR; ++j) {
+        const int i = lane + 32 * j;
+        kr[j] = (inreg && i < n) ? score_key(sc[i]) : 0u;
+    }
+    if (inreg) {
+#pragma unroll
+        for (int j = 0; j < KR; ++j)
+            if (kr[j] > kKeyNegInf) {
+                ++nvalid;
+                kmin = min(kmin, kr[j]);
+                kmax = max(kmax, kr[j]);
+            }
+    } else {
+        for (int i = lane; i < n; i += 32) {
+            const uint32_t key = score_key(sc[i]);
+            if (key > kKeyNegInf) {
+                ++nvalid;
+                kmin = min(kmin, key);
+                kmax = max(kmax, key);
+            }
+        }
+    }
     nvalid = __reduce_add_sync(0xffffffffu, nvalid);
+    kmin = __reduce_min_sync(0xffffffffu, kmin);
+    kmax = __reduce_max_sync(0xffffffffu, kmax);
     const int kk = min(k, nvalid);
-    uint32_t T = kKeyNegInf, pmask = 0xffffffffu;
-    int need_eq = 0;  // kk == nvalid: take every valid entry
-    if (kk < nvalid) {
-        uint32_t prefix = 0;
-        pmask = 0;
-        int rem = kk;
+    // count of keys >= t over the warp
+    auto count_ge = [&](uint32_t t) -> int {
+        int c = 0;
+        if (inreg) {
+#pragma unroll
+            for (int j = 0; j < KR; ++j) c += kr[j] >= t;
+        } else {
+            for (int i = lane; i < n; i += 32) c += score_key(sc[i]) >= t;
+        }
+        return __reduce_add_sync(0xffffffffu, c);
+    };
+    // take every key > tgt, plus the first need_eq keys == teq in index order
+    uint32_t tgt = kKeyNegInf, teq = 0xffffffffu;
+    int need_eq = 0;
+    if (kk > 0 && kk < nvalid) {
+        uint32_t T = kmin;
+        if (kmin != kmax) {
+            const int h = 31 - __clz(kmin ^ kmax);
+            T = kmax & ~((2u << h) - 1u);  // 2u << 31 == 0: T = 0 when h == 31
+            bool whole = false;
 #pragma unroll 1
-        for (int shift = 24; shift >= 0; shift -= 8) {
-            for (int i = lane; i < 256; i += 32) hist[i] = 0;
-            __syncwarp();
-            for (int i = lane; i < n; i += 32) {
-                const uint32_t key = score_key(sc[i]);
-                if ((key & pmask) == prefix) atomicAdd(&hist[(key >> shift) & 255], 1);
-            }
-            __syncwarp();
-            int c[8], s = 0;
-#pragma unroll
-            for (int e = 7; e >= 0; --e) { c[e] = hist[lane * 8 + e]; s += c[e]; }
-            int suf = s;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int y = __shfl_down_sync(0xffffffffu, suf, o);
-                if (lane + o < 32) suf += y;
-            }
-            const int above = suf - s;
-            const unsigned ball = __ballot_sync(0xffffffffu, suf >= rem && above < rem);
-            const int Lw = 31 - __clz(ball);
-            int d = 0, acc = 0, cd = 0;
-            if (lane == Lw) {
-                acc = above;
-                d = 8 * Lw;
-#pragma unroll
-                for (int e = 7; e >= 0; --e) {
-                    if (acc + c[e] >= rem) { d = 8 * Lw + e; cd = c[e]; break; }
-                    acc += c[e];
+            for (int bit = h; bit >= 0; --bit) {
+                const uint32_t cand = T | (1u << bit);
+                const int c = count_ge(cand);
+                if (c >= kk) {
+                    T = cand;
+                    if (c == kk) { whole = true; break; }  // keys >= T are exactly kk
                 }
             }
-            d = __shfl_sync(0xffffffffu, d, Lw);
-            acc = __shfl_sync(0xffffffffu, acc, Lw);
-            cd = __shfl_sync(0xffffffffu, cd, Lw);
-            prefix |= uint32_t(d) << shift;
-            pmask |= 0xffu << shift;
-            rem -= acc;
-            __syncwarp();
-            if (cd == rem) break;  // the whole bin is taken
+            if (whole) {
+                tgt = T - 1u;  // key > T - 1  <=>  key >= T
+            } else {
+                tgt = T;
+                teq = T;
+                need_eq = kk - count_ge(T + 1u);
+            }
+        } else {  // every valid key is equal: take the first kk in index order
+            teq = T;
+            need_eq = kk;
+            tgt = T;
         }
-        T = prefix;
-        need_eq = rem;
     }
     // compaction in index order: lane owns the contiguous segment [lane*per, +per)
     const int per = (n + 31) / 32;
     const int lo = lane * per, hi = min(n, lo + per);
     int n_gt = 0, n_eq = 0;
-    for (int i = lo; i < hi; ++i) {
-        const uint32_t key = score_key(sc[i]) & pmask;
-        n_gt += key > T;
-        n_eq += key == T;
+    if (kk > 0) {
+        for (int i = lo; i < hi; ++i) {
+            const uint32_t key = score_key(sc[i]);
+            n_gt += key > tgt;
+            n_eq += key == teq;
+        }
     }
     int eq_inc = n_eq;
 #pragma unroll
@@ -187,15 +218,17 @@ TS_DEV int warp_topk(const float *sc, const int *ids, int id0, int n, int k, int
         if (lane >= o) pos_inc += y;
     }
     int pos = pos_inc - mine, seen = 0;
-    for (int i = lo; i < hi; ++i) {
-        const float s = sc[i];
-        const uint32_t key = score_key(s) & pmask;
-        bool take_i = key > T;
-        if (key == T) { take_i = seen < take; ++seen; }
-        if (take_i) {
-            out_id[pos] = ids ? ids[i] : id0 + i;
-            if (out_sc) out_sc[pos] = s + 0.0f;
-            ++pos;
+    if (mine > 0) {
+        for (int i = lo; i < hi; ++i) {
+            const float s = sc[i];
+            const uint32_t key = score_key(s);
+            bool take_i = key > tgt;
+            if (key == teq) { take_i = seen < take; ++seen; }
+            if (take_i) {
+                out_id[pos] = ids ? ids[i] : id0 + i;
+                if (out_sc) out_sc[pos] = s + 0.0f;
+                ++pos;
+            }
         }
     }
     for (int i = kk + lane; i < k; i += 32) {
@@ -275,10 +308,12 @@ __global__ void __launch_bounds__((NC + 3) * 32, 2)
         int head = 0, seq = 0;
         const int n_items = sp.n_score + sp.n_attn;
         for (;;) {
-            int item = 0;
-            if (lane == 0) {
+            // the first item of CTA x is item x (grid <= items); later ones come from the
+            // global counter, which therefore counts from gridDim.x
+            int item = blockIdx.x;
+            if (seq > 0 && lane == 0) {
                 while (head - *vdtail > STAGES) nanosleep_ns(64);  // ~one item of look-ahead
-                item = (int)atomicAdd(sp.work, 1u);
+                item = (int)gridDim.x + (int)atomicAdd(sp.work, 1u);
             }
             item = __shfl_sync(0xffffffffu, item, 0);
             if (sp.dbg_state && lane == 0) { sp.dbg_state[blockIdx.x * 16 + 0] = item; sp.dbg_state[blockIdx.x * 16 + 1] = seq; }
@@ -441,7 +476,7 @@ __global__ void __launch_bounds__((NC + 3) * 32, 2)
                         PIPE_CHECK(d.x + nv <= p.B * p.Hkv * p.max_pages, 7, d.x);
                         const uint32_t bytes = nv * 2 * kRowBytes;
                         mbar_arrive_expect_tx(full0 + 8 * st, bytes);
-                        bulk_load(dst, sp.meta + (size_t)d.x * 2 * kAttnD, bytes, full0 + 8 * st);
+                        bulk_load_hint(dst, sp.meta + (size_t)d.x * 2 * kAttnD, bytes, full0 + 8 * st, pol);
                     } else {
                         mbar_arrive_expect_tx(full0 + 8 * st, kStageTx);
                         tma_load_2d(dst, &tmK, 0, d.x, full0 + 8 * st, pol);
@@ -655,7 +690,6 @@ TS_DEV void pipe_merge_warp(const PipeParams &sp, uint8_t *smem, int *s_arrive, 
     const int lane = threadIdx.x & 31;
     const int4 *items = reinterpret_cast<const int4 *>(smem + SM::kItems);
     float *scratch = reinterpret_cast<float *>(smem + SM::kScratch);
-    int *hist = reinterpret_cast<int *>(smem + SM::kHist);
     static_assert(SM::kSlotFloats >= 2 * SM::kSelKeys, "candidate merge reuses the item slot");
     for (int seq = 0;; ++seq) {
         const int sl = seq % SM::kNSlot;
@@ -680,13 +714,20 @@ TS_DEV void pipe_merge_warp(const PipeParams &sp, uint8_t *smem, int *s_arrive, 
             const int page0 = part * sp.sch * 16;
             const int n = max(0, min(P - page0, sp.sch * 16));
             bool publish = sp.spr == 1;
+            // development: merge-warp stamps per score item (dbg_ts[12288 + item * 4 + e])
+#define STAMP(e)                                                                              \
+    if (sp.dbg_ts && lane == 0 && (row * sp.spr + part) < 1024)                               \
+        sp.dbg_ts[12288 + (row * sp.spr + part) * 4 + (e)] = globaltimer();
+            STAMP(0);
             if (publish) {
-                const int kk = warp_topk(slot, nullptr, page0, n, sp.kmax, hist,
-                                         sp.sel_out + (size_t)row * sp.kmax, nullptr);
+                const int kk = warp_topk<16>(slot, nullptr, page0, n, sp.kmax,
+                                             sp.sel_out + (size_t)row * sp.kmax, nullptr);
                 if (lane == 0) sp.cnt_out[row] = kk;
+                STAMP(1);
             } else {
                 const size_t cb = ((size_t)row * sp.spr + part) * sp.kmax;
-                warp_topk(slot, nullptr, page0, n, sp.kmax, hist, sp.cand_id + cb, sp.cand_sc + cb);
+                warp_topk<16>(slot, nullptr, page0, n, sp.kmax, sp.cand_id + cb, sp.cand_sc + cb);
+                STAMP(1);
                 __threadfence();
                 __syncwarp();
                 int fin = 0;
@@ -698,19 +739,36 @@ TS_DEV void pipe_merge_warp(const PipeParams &sp, uint8_t *smem, int *s_arrive, 
                     const size_t c0 = (size_t)row * sp.spr * sp.kmax;
                     float *csc = slot;  // the chunk scores are consumed: reuse the slot
                     int *cid = reinterpret_cast<int *>(slot + SM::kSelKeys);
-                    for (int i = lane; i < nc; i += 32) {
-                        csc[i] = __ldcg(sp.cand_sc + c0 + i);
-                        cid[i] = __ldcg(sp.cand_id + c0 + i);
+                    // batches of 8 independent loads per lane (one L2 round trip each)
+                    for (int i0 = 0; i0 < nc; i0 += 256) {
+                        float vs[8];
+                        int vi[8];
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) {
+                            const int i = i0 + 32 * e + lane;
+                            vs[e] = i < nc ? __ldcg(sp.cand_sc + c0 + i) : 0.f;
+                            vi[e] = i < nc ? __ldcg(sp.cand_id + c0 + i) : 0;
+                        }
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) {
+                            const int i = i0 + 32 * e + lane;
+                            if (i < nc) {
+                                csc[i] = vs[e];
+                                cid[i] = vi[e];
+                            }
+                        }
                     }
                     __syncwarp();
+                    STAMP(2);
                     // candidates are ordered by chunk, ids ascending inside a chunk, and the
                     // chunks cover ascending page ranges: index order == page-id order
-                    const int kk = warp_topk(csc, cid, 0, nc, sp.kmax, hist,
+                    const int kk = warp_topk<16>(csc, cid, 0, nc, sp.kmax,
                                              sp.sel_out + (size_t)row * sp.kmax, nullptr);
                     if (lane == 0) {
                         sp.cnt_out[row] = kk;
                         sp.sc_tickets[row] = 0u;
                     }
+                    STAMP(3);
                     publish = true;
                 }
             }
@@ -791,29 +849,53 @@ TS_DEV void pipe_merge_warp(const PipeParams &sp, uint8_t *smem, int *s_arrive, 
         fin = __shfl_sync(0xffffffffu, fin, 0);
         if (!fin) continue;
         __threadfence();
+        // Row merge of the ipr item partials, written for memory-level parallelism (every
+        // load of a phase is independent): (1) lanes (sub, h) = (lane / 8, lane % 8) reduce
+        // m and l of parts s = sub (mod 4) -> per-head max M_h and l-sum, weights
+        // f[s][h] = exp2(m - M_h) into merge-private smem; (2) each lane accumulates its
+        // float4 outputs over all parts.
         const float *pbase = p.part + (size_t)row * sp.ipr * 8 * kPS;
+        float *wf = reinterpret_cast<float *>(smem + SM::kHist);
+        const int sub = lane >> 3, h8 = lane & 7;
+        float Mh = kNegInf;
+        if (h8 < p.G)
+            for (int s2 = sub; s2 < sp.ipr; s2 += 4)
+                Mh = fmaxf(Mh, __ldcg(pbase + (s2 * 8 + h8) * kPS + kAttnD));
+        Mh = fmaxf(Mh, __shfl_xor_sync(0xffffffffu, Mh, 8));
+        Mh = fmaxf(Mh, __shfl_xor_sync(0xffffffffu, Mh, 16));
+        float lh = 0.f;
+        if (h8 < p.G)
+            for (int s2 = sub; s2 < sp.ipr; s2 += 4) {
+                const float *pr = pbase + (s2 * 8 + h8) * kPS;
+                const float ms = __ldcg(pr + kAttnD), ls = __ldcg(pr + kAttnD + 1);
+                const float f = ms == kNegInf ? 0.f : exp2f(ms - Mh);
+                wf[s2 * 8 + h8] = f;
+                lh += ls * f;
+            }
+        lh += __shfl_xor_sync(0xffffffffu, lh, 8);
+        lh += __shfl_xor_sync(0xffffffffu, lh, 16);
+        __syncwarp();
         for (int xw = lane; xw < p.G * (kAttnD / 4); xw += 32) {
             const int h = xw / (kAttnD / 4), d0 = (xw % (kAttnD / 4)) * 4;
-            float M = kNegInf;
-            for (int s2 = 0; s2 < sp.ipr; ++s2)
-                M = fmaxf(M, __ldcg(pbase + (s2 * 8 + h) * kPS + kAttnD));
-            float acc[4] = {0.f, 0.f, 0.f, 0.f}, l = 0.f;
-            if (M != kNegInf)
+            const float M = __shfl_sync(0xffffffffu, Mh, h);
+            const float l = __shfl_sync(0xffffffffu, lh, h);
+            float acc[4] = {0.f, 0.f, 0.f, 0.f};
+            if (M != kNegInf) {
+#pragma unroll 4
                 for (int s2 = 0; s2 < sp.ipr; ++s2) {
-                    const float *pr = pbase + (s2 * 8 + h) * kPS;
-                    const float ms = __ldcg(pr + kAttnD);
-                    const float ls = __ldcg(pr + kAttnD + 1);
-                    const float4 v = __ldcg(reinterpret_cast<const float4 *>(pr + d0));
-                    const float f = ms == kNegInf ? 0.f : exp2f(ms - M);
-                    l += ls * f;
+                    const float f = wf[s2 * 8 + h];
+                    const float4 v =
+                        __ldcg(reinterpret_cast<const float4 *>(pbase + (s2 * 8 + h) * kPS + d0));
                     acc[0] += v.x * f; acc[1] += v.y * f; acc[2] += v.z * f; acc[3] += v.w * f;
                 }
+            }
             const size_t oh = (size_t)b * p.Hq + g * p.G + h;
             const float inv = l > 0.f ? 1.f / l : 0.f;
             *reinterpret_cast<float4 *>(p.o + oh * kAttnD + d0) =
                 make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
             if (p.lse && d0 == 0) p.lse[oh] = l > 0.f ? (M + log2f(l)) * kLn2 : kNegInf;
         }
+        __syncwarp();
         if (lane == 0) {
             p.tickets[row] = 0u;
             if (sp.ready) sp.ready[row] = 0u;

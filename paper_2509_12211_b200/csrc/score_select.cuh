@@ -1,0 +1,524 @@
+// score_select.cuh — fused page scoring + top-K selection (Alg. 1 Steps 1-2,
+// PAPER.md:217-228; Eq. 2; TopK PAPER.md:162-167), the first kernel of
+// the bf16 decode step (head_dim 64, GQA group G <= 8).
+//
+//  * grid = rows x C CTAs; the C CTAs of one row (b, kv head g) form a thread-block
+//    cluster and split the row's pages into contiguous chunks of `chunk` pages;
+//  * per CTA one producer lane streams the chunk's metadata records (logical layout: one
+//    contiguous run per row) with 1-D bulk copies (cp.async.bulk, L2 evict-first) into a
+//    ring of 8 KB stages (32 pages) tracked by mbarriers; W consumer warps take the stages
+//    round-robin and compute Eq. 2 for 16 pages x G heads per mma.m16n8k16:
+//    [m | M] rows (K = 2d) times [q^- ; q^+] columns, exact bf16 products, fp32 sums,
+//    then the max over the group (reading R9) by quad shuffles.  Pages >= P_b: -inf;
+//  * the chunk scores are pushed into the cluster leader's shared memory (DSMEM); the
+//    leader runs an exact CTA-wide top-K (cta_topk below) and writes the selection
+//    (ascending page ids), its count and the physical block of every selected page
+//    (page-table row prefetched into smem at kernel start) for the attention kernel;
+//  * every CTA triggers its programmatic dependents at once, so the attention kernel's
+//    prologue runs while pages are still being scored (PDL).
+// A page's score depends only on (q, its record): fixed fragment assignment and reduction
+// order, independent of the chunk / cluster split.
+#pragma once
+
+
+#include "attn.cuh"
+#include "common.cuh"
+
+namespace ts {
+
+
+struct ScoreSelParams {
+    const uint16_t *q;        // [B][Hq][64]
+    const uint16_t *meta;     // [B][Hkv][max_pages][2][64]
+    const int *page_table;    // [B][max_pages]
+    const int *seq_lens;      // [B]
+    int *sel_ids;             // [rows][kmax] ascending, -1 padding
+    int *sel_blk;             // [rows][kmax] physical block of each selected page
+    int *sel_count;           // [rows]
+    int B, Hq, Hkv, G, S, max_pages, kmax;
+    unsigned *ready;          // [rows] set to 1 once the row's selection is written (nullable)
+    int C;                    // CTAs per row (cluster size)
+    int chunk;                // pages per CTA (multiple of 32)
+    unsigned long long *dbg;  // development: per-CTA stamps (nullable)
+};
+
+constexpr int kSsStagePages = 32;                         // pages per ring stage
+constexpr int kSsStageBytes = kSsStagePages * 2 * kRowBytes;  // 8 KB
+constexpr int kSsHist = 2048;                             // radix bins per pass (11 bits)
+
+template <int W, int R>
+struct SsSmem {
+    static constexpr int NT = (W + 1) * 32;
+    static constexpr int kRing = 0;                                 // R x 8 KB
+    static constexpr int kQ = kRing + R * kSsStageBytes;           // [8][64] bf16
+    static constexpr int kHist = kQ + 8 * kRowBytes;                // [2048] int
+    static constexpr int kRed = kHist + kSsHist * 4;                // [64] int scratch
+    static constexpr int kBars = kRed + 64 * 4;                     // full[R], empty[R], q, pt
+    static constexpr int kScores = (kBars + (2 * R + 2) * 8 + 127) / 128 * 128;  // [max_pages] fp32 / keys
+    static size_t bytes(int max_pages) {
+        return kScores + (size_t)((max_pages + 3) & ~3) * 4 /* scores */ + (size_t)max_pages * 4 /* page table */ + 16;
+    }
+};
+
+// ---------------------------------------------------------------------------------------
+// Block reductions (NT threads, scratch red[>= NT/32 + 2]).
+template <int NT>
+TS_DEV int block_sum(int v, int *red) {
+    v = __reduce_add_sync(0xffffffffu, v);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    int s = 0;
+#pragma unroll
+    for (int w = 0; w < NT / 32; ++w) s += red[w];
+    __syncthreads();
+    return s;
+}
+template <int NT>
+TS_DEV void block_minmax(uint32_t &mn, uint32_t &mx, int *red) {
+    mn = __reduce_min_sync(0xffffffffu, mn);
+    mx = __reduce_max_sync(0xffffffffu, mx);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) {
+        red[warp] = (int)mn;
+        red[32 + warp] = (int)mx;
+    }
+    __syncthreads();
+    uint32_t a = 0xffffffffu, b = 0u;
+#pragma unroll
+    for (int w = 0; w < NT / 32; ++w) {
+        a = min(a, (uint32_t)red[w]);
+        b = max(b, (uint32_t)red[32 + w]);
+    }
+    mn = a;
+    mx = b;
+    __syncthreads();
+}
+// exclusive scan of one int per thread in thread order; *total = sum
+template <int NT>
+TS_DEV int block_scan(int v, int *red, int *total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) red[warp] = x;
+    __syncthreads();
+    int before = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < NT / 32; ++w) {
+        const int s = red[w];
+        before += w < warp ? s : 0;
+        tot += s;
+    }
+    __syncthreads();
+    *total = tot;
+    return before + x - v;
+}
+
+// ---------------------------------------------------------------------------------------
+// Exact top-k of the orderable keys[0..n) in shared memory by a whole CTA (NT threads).
+// Every key is valid (> key(-inf)); kmin / kmax are their smallest / largest values and
+// hist[0..2048) is zero on entry.  Selects kk = min(k, n) entries with the largest keys;
+// equal keys go to the lower index (reading R6).  Emits the selected indices in ascending
+// order through emit(pos, index) and returns kk.
+//
+// Adaptive radix select: the candidates are the keys in [kmin, kmax]; a pass buckets them
+// by (key - kmin) >> shift into <= 2048 bins (shift makes the range fit), one warp finds
+// the bin holding the rem-th largest candidate, and every key above that bin is taken.
+// Then either the whole bin is taken, or it is a single key value (ties by index), or its
+// <= 64 keys are ranked exactly by one warp, or the search recurses into the bin (each
+// pass removes >= 11 bits of the key range, so <= 3 passes).  Scores are spread, so one
+// pass plus the ranking is the common case.  The final compaction is one block scan of
+// packed (greater, equal) counts over contiguous per-thread segments (ascending output).
+#ifndef TS_TOPK_PROF
+#define TS_TOPK_PROF(i)
+#endif
+template <int NT, typename Emit>
+TS_DEV int cta_topk(const uint32_t *keys, int n, int k, uint32_t kmin, uint32_t kmax, int *hist,
+                    int *red, uint32_t *cand, Emit emit, unsigned long long *dts = nullptr) {
+    // keys[] is 16-byte aligned and zero-padded to a multiple of 4 (0 < every valid key):
+    // the scans below read it as uint4 for memory-level parallelism (smem latency ~30 cycles)
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int kk = min(k, n);
+    TS_TOPK_PROF(0);
+    if (kk <= 0) return 0;
+    const uint4 *k4 = reinterpret_cast<const uint4 *>(keys);
+    const int n4 = (n + 3) >> 2;
+    // selected = {key > tgt} + the first need_eq (lowest index) keys == teq
+    uint32_t tgt = 0u, teq = 0xffffffffu;
+    int need_eq = 0;
+    if (kk < n) {
+        int rem = kk;
+#pragma unroll 1
+        for (int pass = 0;; ++pass) {
+            if (kmin == kmax) {  // every candidate has the same key: ties by index
+                tgt = kmin;
+                teq = kmin;
+                need_eq = rem;
+                break;
+            }
+            const uint32_t span = kmax - kmin;
+            const int bits = 32 - __clz(span);
+            const int shift = bits > 11 ? bits - 11 : 0;
+            if (pass > 0) {
+                for (int i = tid; i < kSsHist; i += NT) hist[i] = 0;
+                __syncthreads();
+            }
+#pragma unroll 2
+            for (int i = tid; i < n4; i += NT) {
+                const uint4 v = k4[i];
+                const uint32_t e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (e[j] >= kmin && e[j] <= kmax) atomicAdd(&hist[(e[j] - kmin) >> shift], 1);
+            }
+            __syncthreads();
+            TS_TOPK_PROF(1);
+            if (warp == 0) {  // boundary bin: lane owns bins [64 lane, +64), scanned from the top
+                const int4 *h4 = reinterpret_cast<const int4 *>(hist) + lane * 16;
+                int c[64];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    const int4 v = h4[j];
+                    c[4 * j] = v.x; c[4 * j + 1] = v.y; c[4 * j + 2] = v.z; c[4 * j + 3] = v.w;
+                }
+                int s = 0;
+#pragma unroll
+                for (int j = 0; j < 64; ++j) s += c[j];
+                int suf = s;  // inclusive suffix over lanes >= lane
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_down_sync(0xffffffffu, suf, o);
+                    if (lane + o < 32) suf += y;
+                }
+                const int above_run = suf - s;
+                if (above_run < rem && suf >= rem) {  // exactly one lane
+                    int acc = above_run, bsel = 0, cb = 0, ab = 0;
+                    bool done = false;
+#pragma unroll
+                    for (int j = 63; j >= 0; --j) {
+                        if (!done && acc + c[j] >= rem) {
+                            bsel = j;
+                            cb = c[j];
+                            ab = acc;
+                            done = true;
+                        }
+                        acc += c[j];
+                    }
+                    red[48] = lane * 64 + bsel;
+                    red[49] = ab;
+                    red[50] = cb;
+                }
+                if (lane == 0) red[51] = 0;  // candidate counter
+            }
+            __syncthreads();
+            if (dts && tid == 0 && pass == 0) dts[5] = globaltimer();
+            TS_TOPK_PROF(2);
+            const int bsel = red[48], above = red[49], cnt = red[50];
+            const uint32_t blo = kmin + ((uint32_t)bsel << shift);
+            const uint32_t bhi = shift ? min(kmax, blo + ((1u << shift) - 1u)) : blo;
+            rem -= above;
+            if (cnt == rem) {  // the whole bin is taken: keys >= blo
+                tgt = blo - 1u;
+                break;
+            }
+            if (shift == 0) {  // the bin is one key value
+                tgt = blo;
+                teq = blo;
+                need_eq = rem;
+                break;
+            }
+            if (cnt <= 64) {  // rank the bin's keys exactly in one warp
+#pragma unroll 2
+                for (int i = tid; i < n4; i += NT) {
+                    const uint4 v = k4[i];
+                    const uint32_t e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        if (e[j] >= blo && e[j] <= bhi) {
+                            const int at = atomicAdd(&red[51], 1);
+                            cand[2 * at] = e[j];
+                            cand[2 * at + 1] = (uint32_t)(4 * i + j);
+                        }
+                }
+                __syncthreads();
+                TS_TOPK_PROF(3);
+                if (warp == 0) {
+                    // rank(c) = #{x : key_x > key_c or (key_x == key_c and idx_x < idx_c)}
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int c = lane + 32 * h;
+                        if (c < cnt) {
+                            const uint32_t kc = cand[2 * c], ic = cand[2 * c + 1];
+                            int rk = 0, gt = 0;
+                            for (int x = 0; x < cnt; ++x) {
+                                const uint2 cx = reinterpret_cast<const uint2 *>(cand)[x];
+                                rk += cx.x > kc || (cx.x == kc && cx.y < ic);
+                                gt += cx.x > kc;
+                            }
+                            if (rk == rem - 1) {  // the last selected candidate
+                                red[52] = (int)kc;
+                                red[53] = rem - gt;  // ties at kc still to take (by index)
+                            }
+                        }
+                    }
+                }
+                __syncthreads();
+                tgt = (uint32_t)red[52];
+                teq = tgt;
+                need_eq = red[53];
+                break;
+            }
+            // recurse into the bin
+            kmin = 0xffffffffu;
+            kmax = 0u;
+            for (int i = tid; i < n4; i += NT) {
+                const uint4 v = k4[i];
+                const uint32_t e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (e[j] >= blo && e[j] <= bhi) {
+                        kmin = min(kmin, e[j]);
+                        kmax = max(kmax, e[j]);
+                    }
+            }
+            block_minmax<NT>(kmin, kmax, red);
+        }
+    }
+    if (dts && tid == 0) dts[6] = globaltimer();
+    TS_TOPK_PROF(4);
+    // compaction in index order: thread owns the contiguous run of uint4 [tid*per4, +per4);
+    // one scan of packed (greater, equal) counts: before me, min(need_eq, eq_before) ties
+    const int per4 = (n4 + NT - 1) / NT;
+    const int i0 = tid * per4, i1 = min(n4, i0 + per4);
+    int n_gt = 0, n_eq = 0;
+#pragma unroll 4
+    for (int i = i0; i < i1; ++i) {
+        const uint4 v = k4[i];
+        n_gt += (v.x > tgt) + (v.y > tgt) + (v.z > tgt) + (v.w > tgt);
+        n_eq += (v.x == teq) + (v.y == teq) + (v.z == teq) + (v.w == teq);
+    }
+    int tot;
+    const int before = block_scan<NT>((n_gt << 16) | n_eq, red, &tot);
+    const int eq_before = before & 0xffff, gt_before = before >> 16;
+    TS_TOPK_PROF(5);
+    int pos = gt_before + min(need_eq, eq_before);
+    int taken = eq_before;
+    if (n_gt + n_eq > 0)
+        for (int i = i0; i < i1; ++i) {
+            const uint4 v = k4[i];
+            const uint32_t e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                bool sel = e[j] > tgt;
+                if (e[j] == teq) sel = taken++ < need_eq;
+                if (sel) emit(pos++, 4 * i + j);
+            }
+        }
+    TS_TOPK_PROF(6);
+    return kk;
+}
+
+TS_DEV void cluster_arrive_relaxed() {
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+TS_DEV void cluster_arrive_release() {
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+TS_DEV void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
+
+template <int W, int R>
+__global__ void __launch_bounds__((W + 1) * 32) score_select_kernel(ScoreSelParams p) {
+    using SM = SsSmem<W, R>;
+    constexpr int NT = SM::NT;
+    extern __shared__ __align__(128) uint8_t ss_smem[];
+    uint8_t *smem = ss_smem;
+    const uint32_t sb = smem_u32(smem);
+    const uint32_t full0 = sb + SM::kBars, empty0 = full0 + 8 * R;
+    const uint32_t qbar = empty0 + 8 * R, ptbar = qbar + 8;
+    float *sc = reinterpret_cast<float *>(smem + SM::kScores);
+    int *pt_s = reinterpret_cast<int *>(smem + SM::kScores) + ((p.max_pages + 3) & ~3);
+    int *hist = reinterpret_cast<int *>(smem + SM::kHist);
+    int *red = reinterpret_cast<int *>(smem + SM::kRed);
+    unsigned *s_kmin = reinterpret_cast<unsigned *>(red + 60), *s_kmax = s_kmin + 1;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int row = blockIdx.x / p.C, rank = blockIdx.x % p.C;
+    const int b = row / p.Hkv, g = row % p.Hkv;
+    unsigned long long *dts = p.dbg && blockIdx.x < 4096 ? p.dbg + blockIdx.x * 8 : nullptr;
+#define SS_STAMP(e) \
+    if (dts && tid == 0) dts[e] = globaltimer();
+    SS_STAMP(0);
+    pdl_launch_dependents();  // the attention kernel may be scheduled from now on
+    if (tid == 0) {
+        for (int i = 0; i < R; ++i) {
+            mbar_init(full0 + 8 * i, 1);
+            mbar_init(empty0 + 8 * i, 1);
+        }
+        mbar_init(qbar, 1);
+        mbar_init(ptbar, 1);
+        fence_mbar_init();
+        *s_kmin = 0xffffffffu;
+        *s_kmax = 0u;
+    }
+    if (rank == 0)  // the leader's first radix pass histogram
+        for (int i = tid; i < kSsHist; i += NT) hist[i] = 0;
+    __syncthreads();
+    if (p.C > 1) cluster_arrive_relaxed();  // "this CTA is running" (before any DSMEM access)
+
+    const int L = p.seq_lens[b];
+    const int P = (L + p.S - 1) / p.S;
+    const int j0 = rank * p.chunk;
+    const bool pt_bulk = (p.max_pages & 3) == 0;  // row start 16-byte aligned
+    const int nloc = max(0, min(P - j0, p.chunk));  // valid pages of this CTA
+    const int nst = (nloc + kSsStagePages - 1) / kSsStagePages;
+
+    if (warp == W) {
+        // ================================ producer ================================
+        if (lane == 0) {
+            const uint64_t pol = l2_policy_evict_first();
+            mbar_arrive_expect_tx(qbar, p.G * kRowBytes);
+            bulk_load(sb + SM::kQ, p.q + ((size_t)b * p.Hq + g * p.G) * kAttnD, p.G * kRowBytes, qbar);
+            if (rank == 0 && P > 0 && pt_bulk) {  // page-table row -> smem (page -> block)
+                const uint32_t ptb = min(((uint32_t)P * 4 + 15) & ~15u, (uint32_t)p.max_pages * 4);
+                mbar_arrive_expect_tx(ptbar, ptb);
+                bulk_load(sb + SM::kScores + (uint32_t)((p.max_pages + 3) & ~3) * 4,
+                          p.page_table + (size_t)b * p.max_pages, ptb, ptbar);
+            }
+            const uint16_t *mrow = p.meta + ((size_t)row * p.max_pages + j0) * 2 * kAttnD;
+            for (int i = 0; i < nst; ++i) {
+                const int st = i % R;
+                mbar_wait(empty0 + 8 * st, ((i / R) & 1) ^ 1);
+                const int np = min(kSsStagePages, nloc - i * kSsStagePages);
+                const uint32_t bytes = np * 2 * kRowBytes;
+                mbar_arrive_expect_tx(full0 + 8 * st, bytes);
+                bulk_load_hint(sb + st * kSsStageBytes, mrow + (size_t)i * kSsStagePages * 2 * kAttnD,
+                               bytes, full0 + 8 * st, pol);
+            }
+        }
+    } else {
+        // ================================ consumers ===============================
+        const int gid = lane >> 2, t = lane & 3;
+        mbar_wait(qbar, 0);
+        uint32_t qa[8], qp[8];  // [q^- ; q^+] coefficients of head gid, channels 8t.., 8(t+4)..
+        {
+            const bool live = gid < p.G;
+            const uint32_t qrow = sb + SM::kQ + gid * kRowBytes;
+            const uint4 x0 = live ? lds_v4(qrow + 16 * t) : make_uint4(0, 0, 0, 0);
+            const uint4 x1 = live ? lds_v4(qrow + 16 * (t + 4)) : make_uint4(0, 0, 0, 0);
+            const uint32_t w0[4] = {x0.x, x0.y, x0.z, x0.w}, w1[4] = {x1.x, x1.y, x1.z, x1.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                qa[e] = bf16x2_min0(w0[e]);
+                qa[4 + e] = bf16x2_min0(w1[e]);
+                qp[e] = bf16x2_max0(w0[e]);
+                qp[4 + e] = bf16x2_max0(w1[e]);
+            }
+        }
+        const bool c0 = 2 * t < p.G, c1 = 2 * t + 1 < p.G;
+        uint32_t kmn = 0xffffffffu, kmx = 0u;  // key range of the valid pages (lanes t < 2)
+        for (int i = warp; i < nst; i += W) {
+            const int st = i % R;
+            mbar_wait(full0 + 8 * st, (i / R) & 1);
+            const uint32_t kb = sb + st * kSsStageBytes;
+#pragma unroll
+            for (int tile = 0; tile < 2; ++tile) {
+                const uint32_t tb = kb + tile * 16 * 2 * kRowBytes;
+                float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                for (int ci = 0; ci < 4; ++ci) {
+                    const uint4 a = lds_v4(tb + gid * 2 * kRowBytes + 16 * (t + 4 * ci));
+                    const uint4 h = lds_v4(tb + (gid + 8) * 2 * kRowBytes + 16 * (t + 4 * ci));
+                    const uint32_t *cf = ci < 2 ? qa + 4 * ci : qp + 4 * (ci - 2);
+                    mma_bf16_16816(acc, a.x, h.x, a.y, h.y, cf[0], cf[1]);
+                    mma_bf16_16816(acc, a.z, h.z, a.w, h.w, cf[2], cf[3]);
+                }
+                float m0 = fmaxf(c0 ? acc[0] : kNegInf, c1 ? acc[1] : kNegInf);
+                float m1 = fmaxf(c0 ? acc[2] : kNegInf, c1 ? acc[3] : kNegInf);
+                m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, 1));
+                m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, 2));
+                m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, 1));
+                m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, 2));
+                if (t < 2) {
+                    const int pg = i * kSsStagePages + tile * 16 + gid + 8 * t;  // local page
+                    if (j0 + pg < p.max_pages) {
+                        const bool valid = pg < nloc;
+                        const float v = valid ? (t ? m1 : m0) + 0.0f : kNegInf;
+                        sc[j0 + pg] = v;
+                        if (valid) {
+                            const uint32_t key = score_key(v);
+                            kmn = min(kmn, key);
+                            kmx = max(kmx, key);
+                        }
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty0 + 8 * st);
+        }
+        kmn = __reduce_min_sync(0xffffffffu, kmn);
+        kmx = __reduce_max_sync(0xffffffffu, kmx);
+        if (lane == 0 && kmn <= kmx) {
+            atomicMin(s_kmin, kmn);
+            atomicMax(s_kmax, kmx);
+        }
+    }
+    // pages of the chunk past P_b (no stage covered them)
+    for (int pg = nst * kSsStagePages + tid; pg < p.chunk; pg += NT)
+        if (j0 + pg < p.max_pages) sc[j0 + pg] = kNegInf;
+    __syncthreads();
+    SS_STAMP(1);
+
+    // ---- chunk scores (and key range) -> the leader's shared memory, then the leader selects
+    if (p.C > 1) {
+        cg::cluster_group cl = cg::this_cluster();
+        cluster_wait();  // every CTA of the cluster is running
+        if (rank != 0) {
+            float *dst = cl.map_shared_rank(sc, 0);
+            const int n = min(p.chunk, p.max_pages - j0);
+            for (int i = tid; i < n; i += NT) dst[j0 + i] = sc[j0 + i];
+            if (tid == 0 && *s_kmin <= *s_kmax) {
+                atomicMin(cl.map_shared_rank(s_kmin, 0), *s_kmin);
+                atomicMax(cl.map_shared_rank(s_kmax, 0), *s_kmax);
+            }
+        }
+        cluster_arrive_release();
+        cluster_wait();
+        if (rank != 0) return;
+    }
+    SS_STAMP(2);
+    // ---- leader: exact top-K over the row's P pages (keys in place of the scores)
+    uint32_t *keys = reinterpret_cast<uint32_t *>(sc);
+    for (int i = tid; i < ((P + 3) & ~3); i += NT) keys[i] = i < P ? score_key(sc[i]) : 0u;
+    if (P > 0 && pt_bulk) mbar_wait(ptbar, 0);
+    const int *ptrow = pt_bulk ? pt_s : p.page_table + (size_t)b * p.max_pages;
+    __syncthreads();
+    SS_STAMP(4);
+    int *out_id = p.sel_ids + (size_t)row * p.kmax;
+    int *out_blk = p.sel_blk + (size_t)row * p.kmax;
+    uint32_t *cand = reinterpret_cast<uint32_t *>(smem + SM::kQ);  // q is in registers by now
+    const int kk = cta_topk<NT>(keys, P, p.kmax, *s_kmin, *s_kmax, hist, red, cand,
+                                [&](int pos, int i) {
+                                    out_id[pos] = i;
+                                    out_blk[pos] = ptrow[i];
+                                }, dts);
+    SS_STAMP(7);
+    for (int i = kk + tid; i < p.kmax; i += NT) {
+        out_id[i] = -1;
+        out_blk[i] = 0;
+    }
+    if (tid == 0) p.sel_count[row] = kk;
+    SS_STAMP(3);
+    if (p.ready) {  // release the row to the attention kernel
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence();
+            st_release_u32(p.ready + row, 1u);
+        }
+    }
+}
+
+}  // namespace ts

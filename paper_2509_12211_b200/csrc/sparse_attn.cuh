@@ -1,0 +1,283 @@
+// sparse_attn.cuh — masked softmax attention over the selected pages (SparseAttn,
+// PAPER.md:169-172; Alg. 1 Steps 3-4 "gather K/V of the selected pages, attention",
+// PAPER.md:231-244), bf16 KV, head_dim 64, GQA group G <= 8.
+//
+// Split-K flash-decode with the split merged inside a thread-block cluster:
+//  * grid = rows x C CTAs, cluster = the C CTAs of one row (b, kv head g); the row's
+//    OWNED selected pages (global ids, sharding filter) are cut into 8-token "octets" and
+//    the octets are dealt out in contiguous ranges to the C x W warps of the cluster;
+//  * every warp streams its octets global -> registers with 128-bit loads, DP octets in
+//    flight (software pipeline, no shared-memory staging, no cross-warp synchronisation
+//    in the main loop): per octet a lane loads 32 B of K (token gid, channels
+//    [16t, 16t+16)) and 2 x 16 B of V (tokens 2t, 2t+1, channels [8 gid, 8 gid + 8));
+//  * S = Q K^T on mma.m16n8k16 (bf16 in, fp32 out; A rows = the G q heads, rows >= G
+//    zero; channel permutation d = 16t + 4s + {0..3} so the 32 B of K feed all four
+//    k-steps), fp32 online softmax in exp2, O += P V on mma.m16n8k8 with tf32 P (reading
+//    R10; bf16 V widened exactly; token permutation k-slot t <-> token 2t, t+4 <-> 2t+1
+//    so the lane's two P values are its A fragment and its V rows are the same tokens);
+//  * tokens t >= seq_len are masked (score -inf, V zeroed: the tail of a partial page may
+//    hold anything — reading R7);
+//  * warp partials (o, m, l) merge in shared memory, CTA partials across the cluster
+//    through distributed shared memory; the cluster writes o (fp32) and lse.
+// With PDL (the fused step) everything up to the first read of the selection overlaps
+// the tail of the score/select kernel: griddepcontrol.wait sits just before it.
+#pragma once
+
+
+#include "attn.cuh"
+#include "common.cuh"
+
+namespace ts {
+
+
+
+constexpr int kSaPart = 68;  // floats per (head) partial in smem: o[64], m, l, pad
+
+template <int W>
+struct SaSmem {
+    // warp partials [W][8 heads][kSaPart] then the CTA partial [8][kSaPart]; page lists
+    // (block element base, first token) follow dynamically.
+    static constexpr int kWarpPart = 0;
+    static constexpr int kCtaPart = W * 8 * kSaPart * 4;
+    static constexpr int kPages = kCtaPart + 8 * kSaPart * 4;
+    static size_t bytes(int max_pages) { return kPages + (size_t)max_pages * 8; }
+};
+
+template <int W, int DP>
+__global__ void __launch_bounds__(W * 32, 512 / (W * 32)) sparse_attn_kernel(AttnParams p, int C) {
+    using SM = SaSmem<W>;
+    extern __shared__ __align__(16) uint8_t sa_smem[];
+    float *wpart = reinterpret_cast<float *>(sa_smem + SM::kWarpPart);
+    float *cpart = reinterpret_cast<float *>(sa_smem + SM::kCtaPart);
+    int *s_base = reinterpret_cast<int *>(sa_smem + SM::kPages);  // [n_own] element base / 64
+    int *s_tok = s_base + p.sel_stride;                             // [n_own] first token
+    __shared__ int s_nown;
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int gid = lane >> 2, t = lane & 3;
+    const int row = blockIdx.x / C, rank = blockIdx.x % C;
+    unsigned long long *dts = p.dbg && blockIdx.x < 2048 ? p.dbg + blockIdx.x * 8 : nullptr;
+#define SA_STAMP(e) \
+    if (dts && threadIdx.x == 0) dts[e] = globaltimer();
+    SA_STAMP(0);
+    const int b = row / p.Hkv, g = row % p.Hkv;
+    const int L = p.seq_lens[b];
+
+    // ---- Q fragments (independent of the selection): q heads g*G + gid, channels [16t, +16)
+    uint32_t qa[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (gid < p.G) {
+        const uint16_t *qr =
+            static_cast<const uint16_t *>(p.q) + ((size_t)b * p.Hq + g * p.G + gid) * kAttnD + 16 * t;
+        const uint4 x0 = ldg_nc_v4(qr), x1 = ldg_nc_v4(qr + 8);
+        qa[0] = x0.x; qa[1] = x0.y; qa[2] = x0.z; qa[3] = x0.w;
+        qa[4] = x1.x; qa[5] = x1.y; qa[6] = x1.z; qa[7] = x1.w;
+    }
+    if (dts && threadIdx.x == 0) dts[1] = globaltimer() + (qa[0] & 0u);  // q arrived
+    // the selection is produced by the previous kernel (fused step): either wait for this
+    // row's flag (released by the selector as soon as the row is done) or for the grid
+    if (p.ready) {
+        if (threadIdx.x == 0) {
+            while (ld_relaxed_u32(p.ready + row) == 0u) nanosleep_ns(64);
+            fence_acquire_gpu();
+        }
+        __syncthreads();
+    } else {
+        pdl_wait();
+    }
+
+    // ---- owned selected pages of the row -> (block base, first token), in id order
+    const int cnt = __ldcg(p.sel_count + row);
+    const int *ids = p.sel_ids + (size_t)row * p.sel_stride;
+    if (p.sel_blk) {  // fused step: the selector already resolved the blocks
+        const int *blks = p.sel_blk + (size_t)row * p.sel_stride;
+        for (int u = threadIdx.x; u < cnt; u += blockDim.x) {
+            s_base[u] = (__ldcg(blks + u) * p.Hkv + g) * p.S;
+            s_tok[u] = __ldcg(ids + u) * p.S;
+        }
+        if (threadIdx.x == 0) s_nown = cnt;
+    } else if (p.stride == 1) {
+        for (int u = threadIdx.x; u < cnt; u += blockDim.x) {
+            const int j = __ldg(ids + u);
+            const int blk = __ldg(p.page_table + (size_t)b * p.max_pages + j);
+            s_base[u] = (blk * p.Hkv + g) * p.S;  // in 64-channel rows
+            s_tok[u] = j * p.S;
+        }
+        if (threadIdx.x == 0) s_nown = cnt;
+    } else {  // sequence sharding: keep the pages this rank owns (warp 0 compacts in order)
+        if (warp == 0) {
+            int n = 0;
+            for (int u0 = 0; u0 < cnt; u0 += 32) {
+                const int u = u0 + lane;
+                const int j = u < cnt ? __ldg(ids + u) : -1;
+                const bool own = j >= 0 && j % p.stride == p.offset;
+                const unsigned m = __ballot_sync(0xffffffffu, own);
+                if (own) {
+                    const int pos = n + __popc(m & ((1u << lane) - 1u));
+                    const int blk = __ldg(p.page_table + (size_t)b * p.max_pages + j / p.stride);
+                    s_base[pos] = (blk * p.Hkv + g) * p.S;
+                    s_tok[pos] = j * p.S;
+                }
+                n += __popc(m);
+            }
+            if (lane == 0) s_nown = n;
+        }
+    }
+    __syncthreads();
+    SA_STAMP(2);
+    const int n_own = s_nown;
+    const int ops = p.S >> 3;  // octets per page
+    const int n_oct = n_own * ops;
+    const int nw = C * W, wg = rank * W + warp;
+    const int o0 = (int)((long long)n_oct * wg / nw), o1 = (int)((long long)n_oct * (wg + 1) / nw);
+
+    const uint16_t *kp = static_cast<const uint16_t *>(p.k_pool);
+    const uint16_t *vp = static_cast<const uint16_t *>(p.v_pool);
+    const float sl2 = p.scale * kLog2e;
+    float m = kNegInf, lp = 0.f;
+    float oacc[8][4];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) oacc[j][0] = oacc[j][1] = oacc[j][2] = oacc[j][3] = 0.f;
+
+    // octet o -> element offset of its first token row, and its first global token
+    auto octet_addr = [&](int o, int &tok0) -> size_t {
+        const int u = o / ops, sub = o - u * ops;
+        tok0 = s_tok[u] + 8 * sub;
+        return ((size_t)s_base[u] + 8 * sub) * kAttnD;
+    };
+    uint4 kb[DP][2], vb[DP][2];
+    int tk[DP];
+    auto issue = [&](int j, int o) {
+        if (o < o1) {
+            const size_t e = octet_addr(o, tk[j]);
+            const uint16_t *kr = kp + e + gid * kAttnD + 16 * t;
+            kb[j][0] = ldg_nc_v4(kr);
+            kb[j][1] = ldg_nc_v4(kr + 8);
+            const uint16_t *vr = vp + e + (2 * t) * kAttnD + 8 * gid;
+            vb[j][0] = ldg_nc_v4(vr);
+            vb[j][1] = ldg_nc_v4(vr + kAttnD);
+        }
+    };
+#pragma unroll
+    for (int j = 0; j < DP; ++j) issue(j, o0 + j);
+
+    for (int ob = o0; ob < o1; ob += DP) {
+#pragma unroll
+        for (int j = 0; j < DP; ++j) {
+            const int o = ob + j;
+            if (o >= o1) break;
+            // ---- S^T tile: heads (rows gid) x tokens (2t, 2t+1) of the octet
+            float s[4] = {0.f, 0.f, 0.f, 0.f};
+            mma_bf16_16816(s, qa[0], 0u, qa[1], 0u, kb[j][0].x, kb[j][0].y);
+            mma_bf16_16816(s, qa[2], 0u, qa[3], 0u, kb[j][0].z, kb[j][0].w);
+            mma_bf16_16816(s, qa[4], 0u, qa[5], 0u, kb[j][1].x, kb[j][1].y);
+            mma_bf16_16816(s, qa[6], 0u, qa[7], 0u, kb[j][1].z, kb[j][1].w);
+            const int tok = tk[j] + 2 * t;
+            const bool ok0 = tok < L, ok1 = tok + 1 < L;
+            const float x0 = ok0 ? s[0] * sl2 : kNegInf;
+            const float x1 = ok1 ? s[1] * sl2 : kNegInf;
+            float tmax = fmaxf(x0, x1);
+            tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 1));
+            tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 2));
+            const float mnew = fmaxf(m, tmax);
+            // an octet past seq_len (tail of a partial page) has no valid token: keep the
+            // exponents finite (mref) so it contributes exactly nothing
+            const float mref = mnew == kNegInf ? 0.f : mnew;
+            const float corr = exp2f(m - mref);  // m = -inf -> 0
+            m = mnew;
+            const float p0 = exp2f(x0 - mref), p1 = exp2f(x1 - mref);
+            lp = lp * corr + p0 + p1;
+            const uint32_t a0 = f32_to_tf32(p0), a2 = f32_to_tf32(p1);
+            const uint4 v0 = vb[j][0], v1 = vb[j][1];
+            const uint32_t w0[4] = {ok0 ? v0.x : 0u, ok0 ? v0.y : 0u, ok0 ? v0.z : 0u, ok0 ? v0.w : 0u};
+            const uint32_t w1[4] = {ok1 ? v1.x : 0u, ok1 ? v1.y : 0u, ok1 ? v1.z : 0u, ok1 ? v1.w : 0u};
+            issue(j, o + DP);  // refill this slot while the tensor cores work
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj) {
+                oacc[jj][0] *= corr;
+                oacc[jj][1] *= corr;
+                const uint32_t b0 = (jj & 1) ? (w0[jj >> 1] & 0xffff0000u) : (w0[jj >> 1] << 16);
+                const uint32_t b1 = (jj & 1) ? (w1[jj >> 1] & 0xffff0000u) : (w1[jj >> 1] << 16);
+                mma_tf32_1688(oacc[jj], a0, 0u, a2, 0u, b0, b1);
+            }
+        }
+    }
+
+    if (dts && threadIdx.x == 0) dts[3] = globaltimer() + (__float_as_uint(oacc[0][0]) & 0u);
+    // ---- warp partial -> smem: head gid, channels 16t + j (c0) and 16t + 8 + j (c1)
+    lp += __shfl_xor_sync(0xffffffffu, lp, 1);
+    lp += __shfl_xor_sync(0xffffffffu, lp, 2);
+    if (gid < p.G) {
+        float *wr = wpart + (warp * 8 + gid) * kSaPart;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            wr[16 * t + j] = oacc[j][0];
+            wr[16 * t + 8 + j] = oacc[j][1];
+        }
+        if (t == 0) {
+            wr[kAttnD] = m;
+            wr[kAttnD + 1] = lp;
+        }
+    }
+    __syncthreads();
+    // ---- CTA merge: thread -> (head, 4 channels)
+    for (int x = threadIdx.x; x < p.G * 16; x += blockDim.x) {
+        const int h = x >> 4, d0 = (x & 15) * 4;
+        float M = kNegInf;
+#pragma unroll
+        for (int w = 0; w < W; ++w) M = fmaxf(M, wpart[(w * 8 + h) * kSaPart + kAttnD]);
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        float l = 0.f;
+        if (M != kNegInf) {
+#pragma unroll
+            for (int w = 0; w < W; ++w) {
+                const float *wr = wpart + (w * 8 + h) * kSaPart;
+                const float mw = wr[kAttnD];
+                const float f = mw == kNegInf ? 0.f : exp2f(mw - M);
+                l += wr[kAttnD + 1] * f;
+                const float4 v = *reinterpret_cast<const float4 *>(wr + d0);
+                acc.x += v.x * f; acc.y += v.y * f; acc.z += v.z * f; acc.w += v.w * f;
+            }
+        }
+        float *cr = cpart + h * kSaPart;
+        *reinterpret_cast<float4 *>(cr + d0) = acc;
+        if (d0 == 0) {
+            cr[kAttnD] = M;
+            cr[kAttnD + 1] = l;
+        }
+    }
+    // ---- cluster merge through DSMEM: CTA `rank` finalises outputs x = rank, rank + C, ...
+    cg::cluster_group cl = cg::this_cluster();
+    SA_STAMP(4);
+    if (C > 1) cl.sync(); else __syncthreads();
+    SA_STAMP(5);
+    for (int x = rank * blockDim.x + threadIdx.x; x < p.G * 16; x += C * blockDim.x) {
+        const int h = x >> 4, d0 = (x & 15) * 4;
+        float M = kNegInf;
+        for (int r = 0; r < C; ++r) {
+            const float *cr = C > 1 ? cl.map_shared_rank(cpart, r) : cpart;
+            M = fmaxf(M, cr[h * kSaPart + kAttnD]);
+        }
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        float l = 0.f;
+        if (M != kNegInf)
+            for (int r = 0; r < C; ++r) {
+                const float *cr = (C > 1 ? cl.map_shared_rank(cpart, r) : cpart) + h * kSaPart;
+                const float mr = cr[kAttnD];
+                const float f = mr == kNegInf ? 0.f : exp2f(mr - M);
+                l += cr[kAttnD + 1] * f;
+                const float4 v = *reinterpret_cast<const float4 *>(cr + d0);
+                acc.x += v.x * f; acc.y += v.y * f; acc.z += v.z * f; acc.w += v.w * f;
+            }
+        const size_t oh = (size_t)b * p.Hq + g * p.G + h;
+        const float inv = l > 0.f ? 1.f / l : 0.f;
+        *reinterpret_cast<float4 *>(p.o + oh * kAttnD + d0) =
+            make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+        if (p.lse && d0 == 0) p.lse[oh] = l > 0.f ? (M + log2f(l)) * kLn2 : kNegInf;
+    }
+    SA_STAMP(6);
+    if (C > 1) cl.sync();  // remote partials stay alive until every CTA has read them
+    if (p.ready && rank == 0 && threadIdx.x == 0) p.ready[row] = 0u;  // every CTA of the row is past its wait
+    SA_STAMP(7);
+}
+
+}  // namespace ts

@@ -37,6 +37,22 @@ if len(rows):
     r = (rows - t0) / 1e3
     print(f"row publish: n {len(r)} first {r.min():.2f} p10 {np.percentile(r,10):.2f} med {np.median(r):.2f} p90 {np.percentile(r,90):.2f} last {r.max():.2f} us")
 
+st = a[12288:16384].reshape(1024, 4).astype(np.float64)
+st[st == 0] = np.nan
+st = (st - t0) / 1e3
+ok = ~np.isnan(st[:, 0])
+if ok.any():
+    s = st[ok]
+    for e, nm in enumerate(["merge start", "chunk topk done", "cands loaded", "final topk done"]):
+        col = s[:, e]
+        if np.isfinite(col).any():
+            print(f"score item {nm:16s} min {np.nanmin(col):7.2f} med {np.nanmedian(col):7.2f} max {np.nanmax(col):7.2f} us")
+    d1 = s[:, 1] - s[:, 0]
+    print(f"chunk topk duration med {np.nanmedian(d1):.2f} max {np.nanmax(d1):.2f} us")
+    if np.isfinite(s[:, 3]).any():
+        d3 = s[:, 3] - s[:, 2]
+        d2 = s[:, 2] - s[:, 1]
+        print(f"ticket->cands loaded med {np.nanmedian(d2):.2f}; final topk med {np.nanmedian(d3):.2f} max {np.nanmax(d3):.2f} us")
 tr = a[16384:16384 + 4096].reshape(4, 512, 2)
 arr = a[16384 + 4096:16384 + 4096 + 1024].reshape(4, 256)
 for c in range(2):
