@@ -11,6 +11,7 @@
 #include "attn.cuh"
 #include "common.cuh"
 #include "decode_pipe.cuh"
+#include "fused_step.cuh"
 #include "meta.cuh"
 #include "score.cuh"
 #include "score_select.cuh"
@@ -188,6 +189,14 @@ StepWs step_ws_layout(const ts_layout *L, int kmax) {
     return w;
 }
 
+// Persistent score/select + attention pair (one CTA per row at a time, rows pipelined) when
+// the rows alone fill two CTAs per SM; cluster-per-row kernels otherwise.
+bool persist_rows(const ts_layout *L) {
+    static const int env = getenv("TS_PERSIST") ? atoi(getenv("TS_PERSIST")) : -1;
+    if (env == 0) return false;
+    return (L->batch * L->num_kv_heads >= 2 * device_sms() || env == 1) && L->max_pages <= 1024;
+}
+
 // K = floor(budget / S) clipped to [1, max_pages] (reading R4/R5; P_b <= max_pages)
 int kmax_of(const ts_layout *L, int budget) {
     const int k = budget / L->page_size > 1 ? budget / L->page_size : 1;
@@ -363,15 +372,17 @@ ts_status prepare_sa(size_t sm) {
 
 // C = CTAs per row: the largest C <= cdesired whose clusters all fit on the GPU at once
 template <int W, int DP>
-ts_status launch_sa(const AttnParams &p, int rows, int cdesired, bool pdl, cudaStream_t st) {
+ts_status launch_sa(const AttnParams &p, int rows, int cdesired, bool pdl, cudaStream_t st,
+                    int nclusters = 0) {
     auto kern = sparse_attn_kernel<W, DP>;
     const size_t sm = SaSmem<W>::bytes(p.sel_stride);
     ts_status s = prepare_sa<W, DP>(sm);
     if (s != TS_OK) return s;
     int C = std::max(1, cdesired);
     while (C > 1 && max_active_clusters(kern, W * 32, sm, C) < rows) --C;
+    if (nclusters <= 0) nclusters = rows;  // one row per cluster (else persistent over rows)
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(rows * C);
+    cfg.gridDim = dim3(nclusters * C);
     cfg.blockDim = dim3(W * 32);
     cfg.dynamicSmemBytes = sm;
     cfg.stream = st;
@@ -394,9 +405,73 @@ ts_status launch_sa(const AttnParams &p, int rows, int cdesired, bool pdl, cudaS
     return launch_status();
 }
 
-ts_status launch_sparse_attn(const ts_layout *L, const AttnParams &p, bool pdl, cudaStream_t st) {
+// TMA-ring attention (sparse_attn_tma_kernel), S % 16 == 0: one (row, split) per CTA.
+template <int W, int R>
+ts_status launch_sat(const ts_layout *L, const AttnParams &p, bool pdl, cudaStream_t st) {
+    auto kern = sparse_attn_tma_kernel<W, R>;
+    const int rows = L->batch * L->num_kv_heads;
+    const size_t sm = SatSmem<W, R>::bytes(p.sel_stride);
+    if (sm > 227 * 1024) return TS_ERR_UNSUPPORTED;
+    {
+        static std::mutex mu;
+        static size_t sm_set = 0;
+        static bool np_set = false;
+        std::lock_guard<std::mutex> g(mu);
+        if (sm > sm_set) {
+            if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) !=
+                cudaSuccess)
+                return TS_ERR_CUDA;
+            sm_set = sm;
+        }
+        if (!np_set) {
+            if (cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+                cudaSuccess)
+                return TS_ERR_CUDA;
+            np_set = true;
+        }
+    }
+    CUtensorMap tmK, tmV;
+    if (!make_pool_map(&tmK, p.k_pool, L, 16) || !make_pool_map(&tmV, p.v_pool, L, 16))
+        return TS_ERR_CUDA;
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (W + 1) * 32, sm);
+    static const int cmax_env = getenv("TS_SA_CMAX") ? atoi(getenv("TS_SA_CMAX")) : 16;
+    const int ntile = p.sel_stride * (L->page_size / 16);  // upper bound per row
+    // splits per row: fill one wave (rows x C <= CTAs resident), each warp >= 2 tiles
+    int C = std::max(1, std::min(cmax_env, device_sms() * std::max(1, per_sm) / std::max(1, rows)));
+    C = std::max(1, std::min(C, ntile / (2 * W)));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(rows * C);
+    cfg.blockDim = dim3((W + 1) * 32);
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    int na = 0;
+    if (pdl) {
+        at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    cfg.attrs = at;
+    cfg.numAttrs = na;
+    if (cudaLaunchKernelEx(&cfg, kern, tmK, tmV, p, C) != cudaSuccess) return TS_ERR_CUDA;
+    ++g_launches;
+    return launch_status();
+}
+
+ts_status launch_sparse_attn(const ts_layout *L, const AttnParams &p, bool pdl, cudaStream_t st,
+                             bool persist = false) {
     const int rows = L->batch * L->num_kv_heads;
     const int sms = device_sms();
+    static const int tma = getenv("TS_SA_TMA") ? atoi(getenv("TS_SA_TMA")) : 1;
+    if (tma && L->page_size % 16 == 0) {
+        static const int rr = getenv("TS_SA_R") ? atoi(getenv("TS_SA_R")) : 8;
+        if (rr == 12) return launch_sat<4, 12>(L, p, pdl, st);
+        if (rr == 16) return launch_sat<4, 16>(L, p, pdl, st);
+        return launch_sat<4, 8>(L, p, pdl, st);
+    }
+    if (persist)  // co-resident with the persistent selector: 2 CTAs of 4 warps per SM
+        return launch_sa<4, 3>(p, rows, 1, pdl, st, std::min(rows, 2 * sms));
     const int n_oct = p.sel_stride * (L->page_size / 8);  // upper bound per row
     static const int cmax_env = getenv("TS_SA_CMAX") ? atoi(getenv("TS_SA_CMAX")) : 16;
     int W = rows >= 2 * sms ? 4 : (rows * 16 < sms ? 16 : 8);
@@ -466,6 +541,78 @@ ts_status launch_ss_t(ScoreSelParams &p, int rows, int cdesired, cudaStream_t st
     return launch_status();
 }
 
+template <int W, int R, int KPL>
+ts_status launch_ssr_t(ScoreSelParams &p, int grid, bool pt_pref, cudaStream_t st) {
+    auto kern = score_select_rows_kernel<W, R, KPL>;
+    const size_t sm = SsrSmem<W, R>::bytes(p.max_pages, pt_pref);
+    if (sm > 227 * 1024) return TS_ERR_UNSUPPORTED;
+    {
+        static std::mutex mu;
+        static size_t sm_set = 0;
+        std::lock_guard<std::mutex> g(mu);
+        if (sm > sm_set) {
+            if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) !=
+                cudaSuccess)
+                return TS_ERR_CUDA;
+            sm_set = sm;
+        }
+    }
+    p.C = 1;
+    p.chunk = p.max_pages;
+    kern<<<grid, (W + 2) * 32, sm, st>>>(p, pt_pref ? 1 : 0);
+    ++g_launches;
+    return launch_status();
+}
+
+// One cooperative launch: NS selector CTAs + NA attention CTAs (fused_step.cuh).
+template <int W, int R1, int R2, int KPL>
+ts_status launch_fused_t(const ts_layout *L, ScoreSelParams &sp, const AttnParams &ap, bool pt_pref,
+                         cudaStream_t st) {
+    auto kern = decode_fused_kernel<W, R1, R2, KPL>;
+    const int rows = L->batch * L->num_kv_heads;
+    const size_t sm = 1024 + std::max(SsrSmem<W, R1>::bytes(L->max_pages, pt_pref),
+                                      AttnRoleSmem<W, R2>::bytes(ap.sel_stride));
+    if (sm > 227 * 1024) return TS_ERR_UNSUPPORTED;
+    {
+        static std::mutex mu;
+        static size_t sm_set = 0;
+        std::lock_guard<std::mutex> g(mu);
+        if (sm > sm_set) {
+            if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) !=
+                cudaSuccess)
+                return TS_ERR_CUDA;
+            sm_set = sm;
+        }
+    }
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (W + 2) * 32, sm) != cudaSuccess ||
+        per_sm < 2)
+        return TS_ERR_UNSUPPORTED;
+    const int cap = per_sm * device_sms();
+    static const int ns_env = getenv("TS_FUSED_NS") ? atoi(getenv("TS_FUSED_NS")) : 0;
+    const int ns = std::min(rows, ns_env > 0 ? std::min(ns_env, cap - 1) : cap / 2);
+    const int na = std::min(rows, cap - ns);
+    CUtensorMap tmK, tmV;
+    if (!make_pool_map(&tmK, ap.k_pool, L, 16) || !make_pool_map(&tmV, ap.v_pool, L, 16))
+        return TS_ERR_CUDA;
+    sp.C = 1;
+    sp.chunk = L->max_pages;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(ns + na);
+    cfg.blockDim = dim3((W + 2) * 32);
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident: the role spin-waits are safe
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, kern, tmK, tmV, sp, ap, pt_pref ? 1 : 0, ns) != cudaSuccess)
+        return TS_ERR_CUDA;
+    ++g_launches;
+    return launch_status();
+}
+
 ts_status launch_score_select(const ts_layout *L, const void *q, const void *meta, const int *pt,
                               const int *sl, int *ids, int *blk, int *cnt, int kmax, unsigned *ready,
                               cudaStream_t st) {
@@ -493,6 +640,13 @@ ts_status launch_score_select(const ts_layout *L, const void *q, const void *met
     const int max_c = std::max(1, std::min(cmax, (L->max_pages + 63) / 64));  // >= 64 pages per CTA
     const int C = std::max(1, std::min(max_c, (target + rows - 1) / rows));
     p.ready = ready;
+    if (persist_rows(L) && ready) {  // many rows: persistent CTAs, selection hidden behind the stream
+        const bool pt_pref = (L->max_pages & 3) == 0;
+        const int grid = std::min(rows, 2 * device_sms());
+        if (L->max_pages <= 256) return launch_ssr_t<4, 4, 8>(p, grid, pt_pref, st);
+        if (L->max_pages <= 512) return launch_ssr_t<4, 4, 16>(p, grid, pt_pref, st);
+        return launch_ssr_t<4, 4, 32>(p, grid, pt_pref, st);
+    }
     return launch_ss_t<4, 4>(p, rows, C, st);
 }
 
@@ -724,6 +878,48 @@ ts_status ts_decode_step(const ts_layout *L, const void *q, const void *k_pool, 
         phase_mark(3, st);
         return TS_OK;
     }
+    static const bool fused_ok = getenv("TS_FUSED") && atoi(getenv("TS_FUSED"));
+    if (L->kv_dtype == TS_BF16 && group_of(L) <= 8 && L->head_dim == 64 && fused_ok &&
+        persist_rows(L) && L->page_size % 16 == 0 && rows > 0) {
+        // one cooperative launch: selector CTAs + attention CTAs (fused_step.cuh)
+        ScoreSelParams sp{};
+        sp.q = static_cast<const uint16_t *>(q);
+        sp.meta = static_cast<const uint16_t *>(meta);
+        sp.page_table = page_table;
+        sp.seq_lens = seq_lens;
+        sp.sel_ids = ids;
+        sp.sel_blk = reinterpret_cast<int *>(wb + w.sel_blk);
+        sp.sel_count = cnt;
+        sp.B = L->batch;
+        sp.Hq = L->num_q_heads;
+        sp.Hkv = L->num_kv_heads;
+        sp.G = group_of(L);
+        sp.S = L->page_size;
+        sp.max_pages = L->max_pages;
+        sp.kmax = kmax;
+        sp.ready = reinterpret_cast<unsigned *>(wb + w.ready);
+        sp.dbg = g_dbg_ss;
+        AttnParams ap = attn_params(L, q, k_pool, v_pool, page_table, seq_lens, ids, cnt, kmax, scale,
+                                    o, lse, ws);
+        ap.sel_blk = sp.sel_blk;
+        ap.ready = sp.ready;
+        const bool pt_pref = (L->max_pages & 3) == 0;
+        phase_mark(0, st);
+        static const int r2 = getenv("TS_FUSED_R2") ? atoi(getenv("TS_FUSED_R2")) : 16;
+        if (L->max_pages <= 256)
+            s = r2 == 8 ? launch_fused_t<4, 4, 8, 8>(L, sp, ap, pt_pref, st)
+                        : (r2 == 24 ? launch_fused_t<4, 4, 24, 8>(L, sp, ap, pt_pref, st)
+                                    : launch_fused_t<4, 4, 16, 8>(L, sp, ap, pt_pref, st));
+        else if (L->max_pages <= 512)
+            s = launch_fused_t<4, 4, 16, 16>(L, sp, ap, pt_pref, st);
+        else
+            s = launch_fused_t<4, 4, 16, 32>(L, sp, ap, pt_pref, st);
+        phase_mark(3, st);
+        if (s != TS_ERR_UNSUPPORTED) {
+            g_launches = 1;
+            return s;
+        }
+    }
     if (L->kv_dtype == TS_BF16 && group_of(L) <= 8 && L->head_dim == 64) {
         // score + select (cluster per row) -> sparse attention (PDL, blocks pre-resolved)
         int *blk = reinterpret_cast<int *>(wb + w.sel_blk);
@@ -741,7 +937,7 @@ ts_status ts_decode_step(const ts_layout *L, const void *q, const void *k_pool, 
             p.sel_blk = blk;
             p.ready = ready;
             static const bool pdl = !getenv("TS_NO_PDL");
-            if ((s = launch_sparse_attn(L, p, pdl, st)) != TS_OK) return s;
+            if ((s = launch_sparse_attn(L, p, pdl, st, persist_rows(L) && ready)) != TS_OK) return s;
         }
         phase_mark(3, st);
         g_launches = rows > 0 ? 2 : 1;

@@ -83,6 +83,11 @@ TS_DEV void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
                  : "memory");
 }
+// expect `bytes` more transaction bytes in the current phase, WITHOUT an arrive
+TS_DEV void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(bytes)
+                 : "memory");
+}
 TS_DEV void mbar_wait(uint32_t bar, uint32_t parity) {
     asm volatile(
         "{\n"

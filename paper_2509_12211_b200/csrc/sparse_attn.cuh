@@ -55,8 +55,12 @@ __global__ void __launch_bounds__(W * 32, 512 / (W * 32)) sparse_attn_kernel(Att
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int gid = lane >> 2, t = lane & 3;
-    const int row = blockIdx.x / C, rank = blockIdx.x % C;
-    unsigned long long *dts = p.dbg && blockIdx.x < 2048 ? p.dbg + blockIdx.x * 8 : nullptr;
+    const int rank = blockIdx.x % C, ncl = gridDim.x / C;
+    const int rows = p.B * p.Hkv;
+    // persistent over rows: cluster x handles rows x, x + clusters, ... (row order = the
+    // selector's order, so the first rows it releases are the first ones attended)
+    for (int row = blockIdx.x / C; row < rows; row += ncl) {
+    unsigned long long *dts = p.dbg && blockIdx.x < 2048 && row < ncl ? p.dbg + blockIdx.x * 8 : nullptr;
 #define SA_STAMP(e) \
     if (dts && threadIdx.x == 0) dts[e] = globaltimer();
     SA_STAMP(0);
@@ -275,9 +279,325 @@ __global__ void __launch_bounds__(W * 32, 512 / (W * 32)) sparse_attn_kernel(Att
         if (p.lse && d0 == 0) p.lse[oh] = l > 0.f ? (M + log2f(l)) * kLn2 : kNegInf;
     }
     SA_STAMP(6);
-    if (C > 1) cl.sync();  // remote partials stay alive until every CTA has read them
+    if (C > 1) cl.sync(); else __syncthreads();  // partials / page lists free for the next row
     if (p.ready && rank == 0 && threadIdx.x == 0) p.ready[row] = 0u;  // every CTA of the row is past its wait
     SA_STAMP(7);
+    }  // row loop
+}
+
+// ---------------------------------------------------------------------------------------
+// TMA variant (S a multiple of 16): one (row, split) per CTA.  A producer warp resolves the
+// CTA's pages and streams [16 x 64] K and V tiles (2-D tensor maps over the pools, 128-byte
+// swizzle, L2 evict-first) into an R-stage shared-memory ring; W consumer warps take tiles
+// round-robin (S^T = Q K^T on m16n8k16, online softmax, O += P V on m16n8k8 tf32) reading
+// the swizzled rows conflict-free; partials merge as in sparse_attn_kernel.  Bytes in
+// flight are bounded by shared memory (R x 4 KB per CTA), not by registers.
+template <int W, int R>
+struct SatSmem {
+    static constexpr int kTile = 16 * kRowBytes;                  // 2 KB
+    static constexpr int kStage = 2 * kTile;                      // K + V
+    static constexpr int kRing = 0;
+    static constexpr int kWarpPart = kRing + R * kStage;          // [W][8][kSaPart] fp32
+    static constexpr int kCtaPart = kWarpPart + W * 8 * kSaPart * 4;
+    static constexpr int kInfo = kCtaPart + 8 * kSaPart * 4;      // [R] int2 (token0, valid)
+    static constexpr int kBars = kInfo + R * 8;
+    static constexpr int kPages = kBars + 2 * R * 8;              // [sel_stride] int2 (row0, tok0)
+    static size_t bytes(int sel_stride) { return 1024 + kPages + (size_t)sel_stride * 8; }
+};
+
+template <int W, int R>
+__global__ void __launch_bounds__((W + 1) * 32, 4) sparse_attn_tma_kernel(
+    const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, AttnParams p,
+    int C) {
+    using SM = SatSmem<W, R>;
+    static_assert(R % W == 0, "stage -> consumer warp must be fixed");
+    extern __shared__ uint8_t sat_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(sat_raw) + 1023) &
+                                                ~uintptr_t(1023));
+    const uint32_t sb = smem_u32(smem);
+    const uint32_t full0 = sb + SM::kBars, empty0 = full0 + 8 * R;
+    float *wpart = reinterpret_cast<float *>(smem + SM::kWarpPart);
+    float *cpart = reinterpret_cast<float *>(smem + SM::kCtaPart);
+    int2 *info = reinterpret_cast<int2 *>(smem + SM::kInfo);
+    int2 *pages = reinterpret_cast<int2 *>(smem + SM::kPages);
+    __shared__ int s_nown;
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int row = blockIdx.x / C, rank = blockIdx.x % C;
+    const int b = row / p.Hkv, g = row % p.Hkv;
+    unsigned long long *dts = p.dbg && blockIdx.x < 2048 ? p.dbg + blockIdx.x * 8 : nullptr;
+    if (dts && threadIdx.x == 0) dts[0] = globaltimer();
+    if (threadIdx.x == 0) {
+        prefetch_tmap(&tmK);
+        prefetch_tmap(&tmV);
+        for (int i = 0; i < R; ++i) {
+            mbar_init(full0 + 8 * i, 1);
+            mbar_init(empty0 + 8 * i, 1);
+        }
+        fence_mbar_init();
+    }
+    const int L = p.seq_lens[b];
+    // ---- Q fragments (consumers; independent of the selection)
+    const int gid = lane >> 2, t = lane & 3;
+    uint32_t qa[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (warp < W && gid < p.G) {
+        const uint16_t *qr =
+            static_cast<const uint16_t *>(p.q) + ((size_t)b * p.Hq + g * p.G + gid) * kAttnD + 16 * t;
+        const uint4 x0 = ldg_nc_v4(qr), x1 = ldg_nc_v4(qr + 8);
+        qa[0] = x0.x; qa[1] = x0.y; qa[2] = x0.z; qa[3] = x0.w;
+        qa[4] = x1.x; qa[5] = x1.y; qa[6] = x1.z; qa[7] = x1.w;
+    }
+    // ---- wait for the selection, then the owned selected pages (producer warp)
+    if (p.ready) {
+        if (threadIdx.x == 0) {
+            while (ld_relaxed_u32(p.ready + row) == 0u) nanosleep_ns(64);
+            fence_acquire_gpu();
+        }
+    } else {
+        pdl_wait();
+    }
+    __syncthreads();
+    if (dts && threadIdx.x == 0) dts[1] = globaltimer();
+    if (p.stride == 1) {
+        // every selected page is owned: all threads resolve entries in parallel (one load
+        // round for the ids / blocks, one more for the page table when not pre-resolved)
+        const int cnt = __ldcg(p.sel_count + row);
+        const int *ids = p.sel_ids + (size_t)row * p.sel_stride;
+        const int *blks = p.sel_blk ? p.sel_blk + (size_t)row * p.sel_stride : nullptr;
+        for (int u = threadIdx.x; u < cnt; u += blockDim.x) {
+            const int j = __ldcg(ids + u);
+            const int blk = blks ? __ldcg(blks + u) : __ldg(p.page_table + (size_t)b * p.max_pages + j);
+            pages[u] = make_int2((blk * p.Hkv + g) * p.S, j * p.S);
+        }
+        if (threadIdx.x == 0) s_nown = cnt;
+    } else if (warp == W) {  // sequence sharding: owned pages, compacted in id order
+        const int cnt = __ldcg(p.sel_count + row);
+        const int *ids = p.sel_ids + (size_t)row * p.sel_stride;
+        int n = 0;
+        for (int u0 = 0; u0 < cnt; u0 += 32) {
+            const int u = u0 + lane;
+            const int j = u < cnt ? __ldcg(ids + u) : -1;
+            const bool own = j >= 0 && j % p.stride == p.offset;
+            const unsigned m = __ballot_sync(0xffffffffu, own);
+            if (own) {
+                const int blk = __ldg(p.page_table + (size_t)b * p.max_pages + j / p.stride);
+                pages[n + __popc(m & ((1u << lane) - 1u))] = make_int2((blk * p.Hkv + g) * p.S, j * p.S);
+            }
+            n += __popc(m);
+        }
+        if (lane == 0) s_nown = n;
+    }
+    __syncthreads();
+    if (p.ready && threadIdx.x == 0 && C == 1) p.ready[row] = 0u;
+    const int tpp = p.S >> 4;                 // tiles per page
+    const int ntile = s_nown * tpp;
+    const int t0 = (int)((long long)ntile * rank / C), t1 = (int)((long long)ntile * (rank + 1) / C);
+    if (dts && threadIdx.x == 0) dts[2] = globaltimer();
+
+    if (warp == W) {
+        // ================================ producer ================================
+        if (lane == 0) {
+            const uint64_t pol = l2_policy_evict_first();
+            for (int i = 0; i < t1 - t0; ++i) {
+                const int st = i % R;
+                mbar_wait(empty0 + 8 * st, ((i / R) & 1) ^ 1);
+                const int tl = t0 + i, u = tl / tpp, sub = tl - u * tpp;
+                const int2 pg = pages[u];
+                info[st] = make_int2(pg.y + 16 * sub, 0);
+                mbar_arrive_expect_tx(full0 + 8 * st, SM::kStage);
+                const uint32_t dst = sb + SM::kRing + st * SM::kStage;
+                tma_load_2d(dst, &tmK, 0, pg.x + 16 * sub, full0 + 8 * st, pol);
+                tma_load_2d(dst + SM::kTile, &tmV, 0, pg.x + 16 * sub, full0 + 8 * st, pol);
+            }
+        }
+    } else {
+        // ================================ consumers ===============================
+        const float sl2 = p.scale * kLog2e;
+        float m = kNegInf, lp = 0.f;
+        float oacc[8][4];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) oacc[j][0] = oacc[j][1] = oacc[j][2] = oacc[j][3] = 0.f;
+        for (int i = warp; i < t1 - t0; i += W) {
+            const int st = i % R;
+            mbar_wait(full0 + 8 * st, (i / R) & 1);
+            const int tok0 = info[st].x;
+            const uint32_t kb = sb + SM::kRing + st * SM::kStage, vb = kb + SM::kTile;
+            float sacc[2][4];
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) {
+                sacc[nt][0] = sacc[nt][1] = sacc[nt][2] = sacc[nt][3] = 0.f;
+                const int r = nt * 8 + gid;
+                const uint32_t ra = kb + r * kRowBytes;
+                const uint4 k0 = lds_v4(ra + (((2 * t) ^ (r & 7)) << 4));
+                const uint4 k1 = lds_v4(ra + (((2 * t + 1) ^ (r & 7)) << 4));
+                mma_bf16_16816(sacc[nt], qa[0], 0u, qa[1], 0u, k0.x, k0.y);
+                mma_bf16_16816(sacc[nt], qa[2], 0u, qa[3], 0u, k0.z, k0.w);
+                mma_bf16_16816(sacc[nt], qa[4], 0u, qa[5], 0u, k1.x, k1.y);
+                mma_bf16_16816(sacc[nt], qa[6], 0u, qa[7], 0u, k1.z, k1.w);
+            }
+            float x[2][2];
+            float tmax = kNegInf;
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                for (int q2 = 0; q2 < 2; ++q2) {
+                    const bool ok = tok0 + nt * 8 + 2 * t + q2 < L;
+                    x[nt][q2] = ok ? sacc[nt][q2] * sl2 : kNegInf;
+                    tmax = fmaxf(tmax, x[nt][q2]);
+                }
+            tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 1));
+            tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 2));
+            const float mnew = fmaxf(m, tmax);
+            const float mref = mnew == kNegInf ? 0.f : mnew;
+            const float corr = exp2f(m - mref);
+            m = mnew;
+            float pr[2][2];
+            float psum = 0.f;
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                for (int q2 = 0; q2 < 2; ++q2) {
+                    pr[nt][q2] = exp2f(x[nt][q2] - mref);
+                    psum += pr[nt][q2];
+                }
+            lp = lp * corr + psum;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                oacc[j][0] *= corr;
+                oacc[j][1] *= corr;
+            }
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) {
+                const int q0 = nt * 8 + 2 * t, q1 = q0 + 1;
+                uint4 v0 = lds_v4(vb + q0 * kRowBytes + ((gid ^ (q0 & 7)) << 4));
+                uint4 v1 = lds_v4(vb + q1 * kRowBytes + ((gid ^ (q1 & 7)) << 4));
+                if (tok0 + q0 >= L) v0 = make_uint4(0, 0, 0, 0);  // past seq_len: may be anything
+                if (tok0 + q1 >= L) v1 = make_uint4(0, 0, 0, 0);
+                const uint32_t a0 = f32_to_tf32(pr[nt][0]), a2 = f32_to_tf32(pr[nt][1]);
+                const uint32_t w0[4] = {v0.x, v0.y, v0.z, v0.w};
+                const uint32_t w1[4] = {v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const uint32_t b0 = (j & 1) ? (w0[j >> 1] & 0xffff0000u) : (w0[j >> 1] << 16);
+                    const uint32_t b1 = (j & 1) ? (w1[j >> 1] & 0xffff0000u) : (w1[j >> 1] << 16);
+                    mma_tf32_1688(oacc[j], a0, 0u, a2, 0u, b0, b1);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty0 + 8 * st);
+        }
+        // ---- warp partial: head gid, channels 16t + j (c0) and 16t + 8 + j (c1)
+        lp += __shfl_xor_sync(0xffffffffu, lp, 1);
+        lp += __shfl_xor_sync(0xffffffffu, lp, 2);
+        if (gid < p.G) {
+            float *wr = wpart + (warp * 8 + gid) * kSaPart;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                wr[16 * t + j] = oacc[j][0];
+                wr[16 * t + 8 + j] = oacc[j][1];
+            }
+            if (t == 0) {
+                wr[kAttnD] = m;
+                wr[kAttnD + 1] = lp;
+            }
+        }
+    }
+    __syncthreads();
+    if (dts && threadIdx.x == 0) dts[3] = globaltimer();
+    // ---- CTA merge of the W warp partials (C == 1: straight to o / lse)
+    for (int x = threadIdx.x; x < p.G * 16; x += blockDim.x) {
+        const int h = x >> 4, d0 = (x & 15) * 4;
+        float mw[W];
+#pragma unroll
+        for (int w = 0; w < W; ++w) mw[w] = wpart[(w * 8 + h) * kSaPart + kAttnD];
+        float M = kNegInf;
+#pragma unroll
+        for (int w = 0; w < W; ++w) M = fmaxf(M, mw[w]);
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        float l = 0.f;
+        if (M != kNegInf) {
+#pragma unroll
+            for (int w = 0; w < W; ++w) {
+                const float *wr = wpart + (w * 8 + h) * kSaPart;
+                const float f = mw[w] == kNegInf ? 0.f : exp2f(mw[w] - M);
+                l += wr[kAttnD + 1] * f;
+                const float4 v = *reinterpret_cast<const float4 *>(wr + d0);
+                acc.x += v.x * f; acc.y += v.y * f; acc.z += v.z * f; acc.w += v.w * f;
+            }
+        }
+        if (C == 1) {
+            const size_t oh = (size_t)b * p.Hq + g * p.G + h;
+            const float inv = l > 0.f ? 1.f / l : 0.f;
+            *reinterpret_cast<float4 *>(p.o + oh * kAttnD + d0) =
+                make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+            if (p.lse && d0 == 0) p.lse[oh] = l > 0.f ? (M + log2f(l)) * kLn2 : kNegInf;
+        } else {  // this CTA's partial -> global workspace [rows][C][8][kPS]
+            float *pr = p.part + (((size_t)row * C + rank) * 8 + h) * kPS;
+            *reinterpret_cast<float4 *>(pr + d0) = acc;
+            if (d0 == 0) {
+                pr[kAttnD] = M;
+                pr[kAttnD + 1] = l;
+            }
+        }
+    }
+    if (C > 1) {
+        // ---- split merge: the last CTA of the row (ticket) combines the C partials from L2
+        __shared__ int s_last;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            s_last = atomicAdd(p.tickets + row, 1u) == unsigned(C - 1);
+        }
+        __syncthreads();
+        if (s_last) {
+            __threadfence();
+            constexpr int kMaxC = 16;
+            const float *pb = p.part + (size_t)row * C * 8 * kPS;
+            for (int x = threadIdx.x; x < p.G * 16; x += blockDim.x) {
+                const int h = x >> 4, d0 = (x & 15) * 4;
+                float mr[kMaxC];
+#pragma unroll
+                for (int r = 0; r < kMaxC; ++r)
+                    mr[r] = r < C ? __ldcg(pb + (r * 8 + h) * kPS + kAttnD) : kNegInf;
+                float M = kNegInf;
+#pragma unroll
+                for (int r = 0; r < kMaxC; ++r) M = fmaxf(M, mr[r]);
+                float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+                float l = 0.f;
+                if (M != kNegInf) {
+#pragma unroll
+                    for (int r0 = 0; r0 < kMaxC; r0 += 4) {
+                        if (r0 >= C) break;
+                        float lq[4];
+                        float4 vq[4];
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const float *pr = pb + ((r0 + e) * 8 + h) * kPS;
+                            lq[e] = r0 + e < C ? __ldcg(pr + kAttnD + 1) : 0.f;
+                            vq[e] = r0 + e < C ? __ldcg(reinterpret_cast<const float4 *>(pr + d0))
+                                               : make_float4(0.f, 0.f, 0.f, 0.f);
+                        }
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const float f = mr[r0 + e] == kNegInf ? 0.f : exp2f(mr[r0 + e] - M);
+                            l += lq[e] * f;
+                            acc.x += vq[e].x * f; acc.y += vq[e].y * f; acc.z += vq[e].z * f; acc.w += vq[e].w * f;
+                        }
+                    }
+                }
+                const size_t oh = (size_t)b * p.Hq + g * p.G + h;
+                const float inv = l > 0.f ? 1.f / l : 0.f;
+                *reinterpret_cast<float4 *>(p.o + oh * kAttnD + d0) =
+                    make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+                if (p.lse && d0 == 0) p.lse[oh] = l > 0.f ? (M + log2f(l)) * kLn2 : kNegInf;
+            }
+            if (threadIdx.x == 0) {
+                p.tickets[row] = 0u;  // re-armed for the next launch
+                if (p.ready) p.ready[row] = 0u;
+            }
+        }
+    }
+    if (dts && threadIdx.x == 0) dts[7] = globaltimer();
 }
 
 }  // namespace ts

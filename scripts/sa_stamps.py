@@ -28,8 +28,10 @@ a = buf.cpu().numpy().reshape(2048, 8).astype(np.float64)
 a = a[a[:, 0] > 0]
 t0 = a[:, 0].min()
 rel = (a - t0) / 1e3
-names = ["start", "q", "pages", "loop_end", "cta_merged", "cl_sync1", "out", "cl_sync2"]
+names = (["start", "flag", "pages", "consumed", "-", "-", "-", "end"] if os.environ.get("TS_SA_TMA", "1") != "0" else ["start", "q", "pages", "loop_end", "cta_merged", "cl_sync1", "out", "cl_sync2"])
 print(name, "cnt1" if one else "", "CTAs", len(a))
 for i, n in enumerate(names):
     col = rel[:, i]
+    if n == "-" or not np.isfinite(col).any() or (a[:, i] == 0).all():
+        continue
     print(f"{n:10s} min {col.min():7.2f} p10 {np.percentile(col,10):7.2f} med {np.median(col):7.2f} p90 {np.percentile(col,90):7.2f} max {col.max():7.2f} us")
