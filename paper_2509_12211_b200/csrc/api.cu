@@ -12,6 +12,7 @@
 #include "common.cuh"
 #include "decode_pipe.cuh"
 #include "fused_step.cuh"
+#include "step_cluster.cuh"
 #include "meta.cuh"
 #include "score.cuh"
 #include "score_select.cuh"
@@ -529,13 +530,18 @@ ts_status launch_ss_t(ScoreSelParams &p, int rows, int cdesired, cudaStream_t st
     cfg.blockDim = dim3((W + 1) * 32);
     cfg.dynamicSmemBytes = sm;
     cfg.stream = st;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = p.C;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
+    // PDL: the prologue (barriers, histogram, cluster arrival) overlaps the previous kernel's
+    // tail; griddepcontrol.wait precedes every read of q / metadata / page table
+    static const bool pdl = !getenv("TS_NO_PDL");
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     if (cudaLaunchKernelEx(&cfg, kern, p) != cudaSuccess) return TS_ERR_CUDA;
     ++g_launches;
     return launch_status();
@@ -609,6 +615,73 @@ ts_status launch_fused_t(const ts_layout *L, ScoreSelParams &sp, const AttnParam
     cfg.numAttrs = 1;
     if (cudaLaunchKernelEx(&cfg, kern, tmK, tmV, sp, ap, pt_pref ? 1 : 0, ns) != cudaSuccess)
         return TS_ERR_CUDA;
+    ++g_launches;
+    return launch_status();
+}
+
+// The whole bf16 step as one cluster-per-row kernel (step_cluster.cuh).
+template <int W, int R>
+ts_status launch_step_cluster_t(const ts_layout *L, ScoreSelParams &sp, const AttnParams &ap,
+                                cudaStream_t st) {
+    auto kern = decode_cluster_kernel<W, R>;
+    const int rows = L->batch * L->num_kv_heads;
+    const size_t sm = 1024 + ScSmem<W, R>::bytes(sp.kmax, L->max_pages);
+    if (sm > 227 * 1024) return TS_ERR_UNSUPPORTED;
+    {
+        static std::mutex mu;
+        static size_t sm_set = 0;
+        static bool np_set = false;
+        std::lock_guard<std::mutex> g(mu);
+        if (sm > sm_set) {
+            if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) !=
+                cudaSuccess)
+                return TS_ERR_CUDA;
+            sm_set = sm;
+        }
+        if (!np_set) {
+            if (cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+                cudaSuccess)
+                return TS_ERR_CUDA;
+            np_set = true;
+        }
+    }
+    CUtensorMap tmK, tmV;
+    if (!make_pool_map(&tmK, ap.k_pool, L, 16) || !make_pool_map(&tmV, ap.v_pool, L, 16))
+        return TS_ERR_CUDA;
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (W + 1) * 32, sm);
+    static const int cmax = getenv("TS_SC_CMAX") ? atoi(getenv("TS_SC_CMAX")) : 16;
+    const int target = device_sms() * std::max(1, per_sm);
+    const int max_c = std::max(1, std::min(cmax, (L->max_pages + 63) / 64));  // >= 64 pages per CTA
+    int C = std::max(1, std::min(max_c, target / std::max(1, rows)));
+    int chunk = 0;
+    for (;; --C) {  // the largest C whose clusters are all co-resident (one wave)
+        chunk = (L->max_pages + C - 1) / C;
+        chunk = (chunk + kSsStagePages - 1) / kSsStagePages * kSsStagePages;
+        const int c = (L->max_pages + chunk - 1) / chunk;
+        if (C == 1 || max_active_clusters(kern, (W + 1) * 32, sm, c) >= rows) {
+            C = c;
+            break;
+        }
+    }
+    sp.C = C;
+    sp.chunk = chunk;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(rows * C);
+    cfg.blockDim = dim3((W + 1) * 32);
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = C;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    static const bool pdl = !getenv("TS_NO_PDL");
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    if (cudaLaunchKernelEx(&cfg, kern, tmK, tmV, sp, ap) != cudaSuccess) return TS_ERR_CUDA;
     ++g_launches;
     return launch_status();
 }
@@ -920,10 +993,43 @@ ts_status ts_decode_step(const ts_layout *L, const void *q, const void *k_pool, 
             return s;
         }
     }
+    static const int two_kernels = getenv("TS_TWO_KERNELS") ? atoi(getenv("TS_TWO_KERNELS")) : 0;
+    if (L->kv_dtype == TS_BF16 && group_of(L) <= 8 && L->head_dim == 64 && !two_kernels &&
+        L->page_size % 16 == 0 && rows > 0) {
+        // the whole step in one cluster-per-row kernel (step_cluster.cuh)
+        ScoreSelParams sp{};
+        sp.q = static_cast<const uint16_t *>(q);
+        sp.meta = static_cast<const uint16_t *>(meta);
+        sp.page_table = page_table;
+        sp.seq_lens = seq_lens;
+        sp.sel_ids = ids;
+        sp.sel_blk = nullptr;
+        sp.sel_count = cnt;
+        sp.B = L->batch;
+        sp.Hq = L->num_q_heads;
+        sp.Hkv = L->num_kv_heads;
+        sp.G = group_of(L);
+        sp.S = L->page_size;
+        sp.max_pages = L->max_pages;
+        sp.kmax = kmax;
+        sp.ready = nullptr;
+        sp.dbg = g_dbg_ss;
+        AttnParams ap = attn_params(L, q, k_pool, v_pool, page_table, seq_lens, ids, cnt, kmax, scale,
+                                    o, lse, ws);
+        phase_mark(0, st);
+        s = launch_step_cluster_t<4, 4>(L, sp, ap, st);
+        phase_mark(3, st);
+        if (s != TS_ERR_UNSUPPORTED) {
+            g_launches = 1;
+            return s;
+        }
+    }
     if (L->kv_dtype == TS_BF16 && group_of(L) <= 8 && L->head_dim == 64) {
         // score + select (cluster per row) -> sparse attention (PDL, blocks pre-resolved)
         int *blk = reinterpret_cast<int *>(wb + w.sel_blk);
-        static const bool flags = !getenv("TS_NO_FLAGS");
+        // per-row flags (attention starts on a row as soon as it is selected) measured slower
+        // than the plain PDL grid dependency on every config: opt-in only
+        static const bool flags = getenv("TS_FLAGS") && atoi(getenv("TS_FLAGS"));
         unsigned *ready = flags ? reinterpret_cast<unsigned *>(wb + w.ready) : nullptr;
         phase_mark(0, st);
         if ((s = launch_score_select(L, q, meta, page_table, seq_lens, ids, blk, cnt, kmax, ready,

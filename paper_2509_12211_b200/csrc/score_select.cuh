@@ -379,6 +379,7 @@ __global__ void __launch_bounds__((W + 1) * 32) score_select_kernel(ScoreSelPara
         for (int i = tid; i < kSsHist; i += NT) hist[i] = 0;
     __syncthreads();
     if (p.C > 1) cluster_arrive_relaxed();  // "this CTA is running" (before any DSMEM access)
+    pdl_wait();  // inputs may come from the previous kernel in the stream (PDL launch)
 
     const int L = p.seq_lens[b];
     const int P = (L + p.S - 1) / p.S;

@@ -327,6 +327,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) sparse_attn_tma_kernel(
     const int b = row / p.Hkv, g = row % p.Hkv;
     unsigned long long *dts = p.dbg && blockIdx.x < 2048 ? p.dbg + blockIdx.x * 8 : nullptr;
     if (dts && threadIdx.x == 0) dts[0] = globaltimer();
+    pdl_launch_dependents();  // the next step's selector may start its prologue
     if (threadIdx.x == 0) {
         prefetch_tmap(&tmK);
         prefetch_tmap(&tmV);

@@ -1,0 +1,471 @@
+// step_cluster.cuh — the bf16 decode step (Alg. 1; "integrates page
+// scoring, sparse memory access, and masked attention in a single pass") as ONE
+// kernel: a thread-block cluster of C CTAs per row (b, kv head g) does all four steps.
+//
+//  1. score (Eq. 2): each CTA streams a contiguous chunk of the row's metadata records with
+//     1-D bulk copies into an 8 KB-stage mbarrier ring; 4 consumer warps compute the
+//     [m | M] x [q^- ; q^+] products on mma.m16n8k16 and the group max (reading R9);
+//  2. select (TopK): the chunk scores go to the cluster leader's shared memory (DSMEM);
+//     the leader runs the exact CTA-wide top-K (cta_topk, score_select.cuh), writes the
+//     selection for the API and a (tile row, first token) list into its shared memory;
+//  3. gather: after a cluster barrier each CTA copies its share of that list (DSMEM) and
+//     its producer streams the selected pages' [16 x 64] K and V tiles with 2-D TMA
+//     (128-byte swizzle) into the SAME ring, now as 4 KB stages;
+//  4. attend: consumers run S = Q K^T (mma.m16n8k16), the fp32 online softmax and
+//     O += P V (mma.m16n8k8, tf32 P — R10) per tile, with the q fragments already in
+//     shared memory from step 1; warp partials merge in smem, the C CTA partials of a row
+//     through an L2 workspace (last CTA by atomic ticket).
+// No kernel boundary, no PDL gap, no second page-list lookup: the step is one launch.
+#pragma once
+#include "attn.cuh"
+#include "common.cuh"
+#include "score_select.cuh"
+#include "sparse_attn.cuh"
+
+namespace ts {
+
+template <int W, int R>
+struct ScSmem {
+    static constexpr int NT = (W + 1) * 32;
+    static constexpr int kRing = 0;                                 // R x 8 KB = 2R x 4 KB
+    static constexpr int kQ = kRing + R * kSsStageBytes;           // [8][64] bf16
+    static constexpr int kHist = kQ + 8 * kRowBytes;                // [2048] int
+    static constexpr int kRed = kHist + kSsHist * 4;                // [64] int
+    static constexpr int kWarpPart = kRed + 64 * 4;                 // [W][8][kSaPart] fp32
+    static constexpr int kInfo = kWarpPart + W * 8 * kSaPart * 4;   // [2R] int
+    static constexpr int kBars = (kInfo + 2 * R * 4 + 7) / 8 * 8;   // mfull,mempty[R]; afull,aempty[2R]; q; pt
+    static constexpr int kSel = (kBars + (6 * R + 2) * 8 + 15) / 16 * 16;  // [kmax] int2
+    __host__ __device__ static size_t scores_off(int kmax) { return ((size_t)kSel + (size_t)kmax * 8 + 127) / 128 * 128; }
+    static size_t bytes(int kmax, int max_pages) {
+        const size_t mp4 = (max_pages + 3) & ~3;
+        return scores_off(kmax) + mp4 * 4 + mp4 * 4 + 16;
+    }
+};
+
+template <int W, int R>
+__global__ void __launch_bounds__((W + 1) * 32) decode_cluster_kernel(
+    const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+    ScoreSelParams p, AttnParams ap) {
+    using SM = ScSmem<W, R>;
+    constexpr int NT = SM::NT;
+    constexpr int RA = 2 * R;  // attention stages (4 KB)
+    static_assert(R % W == 0 && RA % W == 0, "stage -> consumer warp must be fixed");
+    extern __shared__ uint8_t sc_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(sc_raw) + 1023) &
+                                                ~uintptr_t(1023));
+    const uint32_t sb = smem_u32(smem);
+    const uint32_t mfull0 = sb + SM::kBars, mempty0 = mfull0 + 8 * R;
+    const uint32_t afull0 = mempty0 + 8 * R, aempty0 = afull0 + 8 * RA;
+    const uint32_t qbar = aempty0 + 8 * RA, ptbar = qbar + 8;
+    const int mp4 = (p.max_pages + 3) & ~3;
+    float *sc = reinterpret_cast<float *>(smem + SM::scores_off(p.kmax));
+    int *pt_s = reinterpret_cast<int *>(sc) + mp4;
+    int *hist = reinterpret_cast<int *>(smem + SM::kHist);
+    int *red = reinterpret_cast<int *>(smem + SM::kRed);
+    float *wpart = reinterpret_cast<float *>(smem + SM::kWarpPart);
+    int *info = reinterpret_cast<int *>(smem + SM::kInfo);
+    int2 *sel = reinterpret_cast<int2 *>(smem + SM::kSel);
+    unsigned *s_kmin = reinterpret_cast<unsigned *>(red + 60), *s_kmax = s_kmin + 1;
+    __shared__ int s_cnt, s_last;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int C = p.C;
+    const int row = blockIdx.x / C, rank = blockIdx.x % C;
+    const int b = row / p.Hkv, g = row % p.Hkv;
+    unsigned long long *dts = p.dbg && blockIdx.x < 4096 ? p.dbg + blockIdx.x * 8 : nullptr;
+#define SC_STAMP(e) \
+    if (dts && tid == 0) dts[e] = globaltimer();
+    SC_STAMP(0);
+    if (tid == 0) {
+        prefetch_tmap(&tmK);
+        prefetch_tmap(&tmV);
+        for (int i = 0; i < R; ++i) {
+            mbar_init(mfull0 + 8 * i, 1);
+            mbar_init(mempty0 + 8 * i, 1);
+        }
+        for (int i = 0; i < RA; ++i) {
+            mbar_init(afull0 + 8 * i, 1);
+            mbar_init(aempty0 + 8 * i, 1);
+        }
+        mbar_init(qbar, 1);
+        mbar_init(ptbar, 1);
+        fence_mbar_init();
+        *s_kmin = 0xffffffffu;
+        *s_kmax = 0u;
+    }
+    if (rank == 0)
+        for (int i = tid; i < kSsHist; i += NT) hist[i] = 0;
+    __syncthreads();
+    if (C > 1) cluster_arrive_relaxed();  // "this CTA is running" (before any DSMEM access)
+    pdl_wait();  // inputs may come from the previous kernel in the stream
+
+    const int L = p.seq_lens[b];
+    const int P = (L + p.S - 1) / p.S;
+    const int j0 = rank * p.chunk;
+    const bool pt_bulk = (p.max_pages & 3) == 0;
+    const int nloc = max(0, min(P - j0, p.chunk));
+    const int nst = (nloc + kSsStagePages - 1) / kSsStagePages;
+    const int gid = lane >> 2, t = lane & 3;
+
+    // ===================================== 1. score =====================================
+    if (warp == W) {
+        if (lane == 0) {
+            const uint64_t pol = l2_policy_evict_first();
+            mbar_arrive_expect_tx(qbar, p.G * kRowBytes);
+            bulk_load(sb + SM::kQ, p.q + ((size_t)b * p.Hq + g * p.G) * kAttnD, p.G * kRowBytes, qbar);
+            if (rank == 0 && P > 0 && pt_bulk) {
+                const uint32_t ptb = min(((uint32_t)P * 4 + 15) & ~15u, (uint32_t)mp4 * 4);
+                mbar_arrive_expect_tx(ptbar, ptb);
+                bulk_load(smem_u32(pt_s), p.page_table + (size_t)b * p.max_pages, ptb, ptbar);
+            }
+            const uint16_t *mrow = p.meta + ((size_t)row * p.max_pages + j0) * 2 * kAttnD;
+            for (int i = 0; i < nst; ++i) {
+                const int st = i % R;
+                mbar_wait(mempty0 + 8 * st, ((i / R) & 1) ^ 1);
+                const int np = min(kSsStagePages, nloc - i * kSsStagePages);
+                const uint32_t bytes = np * 2 * kRowBytes;
+                mbar_arrive_expect_tx(mfull0 + 8 * st, bytes);
+                bulk_load_hint(sb + st * kSsStageBytes, mrow + (size_t)i * kSsStagePages * 2 * kAttnD,
+                               bytes, mfull0 + 8 * st, pol);
+            }
+        }
+    } else {
+        mbar_wait(qbar, 0);
+        uint32_t qa[8], qp[8];
+        {
+            const bool live = gid < p.G;
+            const uint32_t qrow = sb + SM::kQ + gid * kRowBytes;
+            const uint4 x0 = live ? lds_v4(qrow + 16 * t) : make_uint4(0, 0, 0, 0);
+            const uint4 x1 = live ? lds_v4(qrow + 16 * (t + 4)) : make_uint4(0, 0, 0, 0);
+            const uint32_t w0[4] = {x0.x, x0.y, x0.z, x0.w}, w1[4] = {x1.x, x1.y, x1.z, x1.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                qa[e] = bf16x2_min0(w0[e]);
+                qa[4 + e] = bf16x2_min0(w1[e]);
+                qp[e] = bf16x2_max0(w0[e]);
+                qp[4 + e] = bf16x2_max0(w1[e]);
+            }
+        }
+        const bool c0 = 2 * t < p.G, c1 = 2 * t + 1 < p.G;
+        uint32_t kmn = 0xffffffffu, kmx = 0u;
+        for (int i = warp; i < nst; i += W) {
+            const int st = i % R;
+            mbar_wait(mfull0 + 8 * st, (i / R) & 1);
+            const uint32_t kb = sb + st * kSsStageBytes;
+#pragma unroll
+            for (int tile = 0; tile < 2; ++tile) {
+                const uint32_t tb = kb + tile * 16 * 2 * kRowBytes;
+                float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                for (int ci = 0; ci < 4; ++ci) {
+                    const uint4 a = lds_v4(tb + gid * 2 * kRowBytes + 16 * (t + 4 * ci));
+                    const uint4 h = lds_v4(tb + (gid + 8) * 2 * kRowBytes + 16 * (t + 4 * ci));
+                    const uint32_t *cf = ci < 2 ? qa + 4 * ci : qp + 4 * (ci - 2);
+                    mma_bf16_16816(acc, a.x, h.x, a.y, h.y, cf[0], cf[1]);
+                    mma_bf16_16816(acc, a.z, h.z, a.w, h.w, cf[2], cf[3]);
+                }
+                float m0 = fmaxf(c0 ? acc[0] : kNegInf, c1 ? acc[1] : kNegInf);
+                float m1 = fmaxf(c0 ? acc[2] : kNegInf, c1 ? acc[3] : kNegInf);
+                m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, 1));
+                m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, 2));
+                m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, 1));
+                m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, 2));
+                if (t < 2) {
+                    const int pg = i * kSsStagePages + tile * 16 + gid + 8 * t;
+                    if (j0 + pg < p.max_pages) {
+                        const bool valid = pg < nloc;
+                        const float v = valid ? (t ? m1 : m0) + 0.0f : kNegInf;
+                        sc[j0 + pg] = v;
+                        if (valid) {
+                            const uint32_t key = score_key(v);
+                            kmn = min(kmn, key);
+                            kmx = max(kmx, key);
+                        }
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(mempty0 + 8 * st);
+        }
+        kmn = __reduce_min_sync(0xffffffffu, kmn);
+        kmx = __reduce_max_sync(0xffffffffu, kmx);
+        if (lane == 0 && kmn <= kmx) {
+            atomicMin(s_kmin, kmn);
+            atomicMax(s_kmax, kmx);
+        }
+    }
+    for (int pg = nst * kSsStagePages + tid; pg < p.chunk; pg += NT)
+        if (j0 + pg < p.max_pages) sc[j0 + pg] = kNegInf;
+    __syncthreads();
+    SC_STAMP(1);
+
+    // ===================================== 2. select =====================================
+    cg::cluster_group cl = cg::this_cluster();
+    if (C > 1) {
+        cluster_wait();  // every CTA of the cluster is running
+        if (rank != 0) {
+            float *dst = cl.map_shared_rank(sc, 0);
+            const int n = min(p.chunk, p.max_pages - j0);
+            for (int i = tid; i < n; i += NT) dst[j0 + i] = sc[j0 + i];
+            if (tid == 0 && *s_kmin <= *s_kmax) {
+                atomicMin(cl.map_shared_rank(s_kmin, 0), *s_kmin);
+                atomicMax(cl.map_shared_rank(s_kmax, 0), *s_kmax);
+            }
+        }
+        cluster_arrive_release();
+        cluster_wait();
+    }
+    if (rank == 0) {
+        uint32_t *keys = reinterpret_cast<uint32_t *>(sc);
+        for (int i = tid; i < ((P + 3) & ~3); i += NT) keys[i] = i < P ? score_key(sc[i]) : 0u;
+        if (P > 0 && pt_bulk) mbar_wait(ptbar, 0);
+        const int *ptrow = pt_bulk ? pt_s : p.page_table + (size_t)b * p.max_pages;
+        __syncthreads();
+        int *out_id = p.sel_ids + (size_t)row * p.kmax;
+        uint32_t *cand = reinterpret_cast<uint32_t *>(wpart);  // free until the attention ends
+        const int S = p.S;
+        const int kk = cta_topk<NT, 0>(keys, P, p.kmax, *s_kmin, *s_kmax, hist, red, cand,
+                                       [&](int pos, int i) {
+                                           out_id[pos] = i;
+                                           sel[pos] = make_int2((ptrow[i] * p.Hkv + g) * S, i * S);
+                                       });
+        for (int i = kk + tid; i < p.kmax; i += NT) out_id[i] = -1;
+        if (tid == 0) {
+            p.sel_count[row] = kk;
+            s_cnt = kk;
+        }
+        SC_STAMP(2);
+    }
+    // the selection list is in the leader's shared memory
+    if (C > 1) {
+        cluster_arrive_release();
+        cluster_wait();
+    } else {
+        __syncthreads();
+    }
+    const int cnt = C > 1 ? *cl.map_shared_rank(&s_cnt, 0) : s_cnt;
+    const int tpp = p.S >> 4;
+    const int ntile = cnt * tpp;
+    const int t0 = (int)((long long)ntile * rank / C), t1 = (int)((long long)ntile * (rank + 1) / C);
+    const int u0 = t0 / tpp, u1 = (t1 + tpp - 1) / tpp;  // pages touched by this CTA
+    if (C > 1) {
+        if (rank != 0) {
+            const int2 *src = cl.map_shared_rank(sel, 0);
+            for (int u = u0 + tid; u < u1; u += NT) sel[u] = src[u];
+        }
+        // the leader's list may be overwritten by nobody; other CTAs read it once: a
+        // second barrier keeps the leader alive (and its list valid) until they have
+        cluster_arrive_release();
+        cluster_wait();
+    }
+    __syncthreads();
+    SC_STAMP(3);
+
+    // ===================================== 3-4. gather + attend ==========================
+    const float sl2 = ap.scale * kLog2e;
+    if (warp == W) {
+        if (lane == 0) {
+            fence_proxy_async();  // the ring was last read by the generic proxy (scoring)
+            const uint64_t pol = l2_policy_evict_first();
+            for (int i = 0; i < t1 - t0; ++i) {
+                const int st = i % RA;
+                mbar_wait(aempty0 + 8 * st, ((i / RA) & 1) ^ 1);
+                const int tl = t0 + i, u = tl / tpp, sub = tl - u * tpp;
+                const int2 pg = sel[u];
+                info[st] = pg.y + 16 * sub;
+                mbar_arrive_expect_tx(afull0 + 8 * st, 2 * 16 * kRowBytes);
+                const uint32_t dst = sb + st * 2 * 16 * kRowBytes;
+                tma_load_2d(dst, &tmK, 0, pg.x + 16 * sub, afull0 + 8 * st, pol);
+                tma_load_2d(dst + 16 * kRowBytes, &tmV, 0, pg.x + 16 * sub, afull0 + 8 * st, pol);
+            }
+        }
+    } else {
+        uint32_t qa[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        if (gid < p.G) {
+            const uint32_t qrow = sb + SM::kQ + gid * kRowBytes + 32 * t;
+            const uint4 x0 = lds_v4(qrow), x1 = lds_v4(qrow + 16);
+            qa[0] = x0.x; qa[1] = x0.y; qa[2] = x0.z; qa[3] = x0.w;
+            qa[4] = x1.x; qa[5] = x1.y; qa[6] = x1.z; qa[7] = x1.w;
+        }
+        float m = kNegInf, lp = 0.f;
+        float oacc[8][4];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) oacc[j][0] = oacc[j][1] = oacc[j][2] = oacc[j][3] = 0.f;
+        for (int i = warp; i < t1 - t0; i += W) {
+            const int st = i % RA;
+            mbar_wait(afull0 + 8 * st, (i / RA) & 1);
+            const int tok0 = info[st];
+            const uint32_t kb = sb + st * 2 * 16 * kRowBytes, vb = kb + 16 * kRowBytes;
+            float sacc[2][4];
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) {
+                sacc[nt][0] = sacc[nt][1] = sacc[nt][2] = sacc[nt][3] = 0.f;
+                const int r = nt * 8 + gid;
+                const uint32_t ra = kb + r * kRowBytes;
+                const uint4 k0 = lds_v4(ra + (((2 * t) ^ (r & 7)) << 4));
+                const uint4 k1 = lds_v4(ra + (((2 * t + 1) ^ (r & 7)) << 4));
+                mma_bf16_16816(sacc[nt], qa[0], 0u, qa[1], 0u, k0.x, k0.y);
+                mma_bf16_16816(sacc[nt], qa[2], 0u, qa[3], 0u, k0.z, k0.w);
+                mma_bf16_16816(sacc[nt], qa[4], 0u, qa[5], 0u, k1.x, k1.y);
+                mma_bf16_16816(sacc[nt], qa[6], 0u, qa[7], 0u, k1.z, k1.w);
+            }
+            float x[2][2];
+            float tmax = kNegInf;
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                for (int q2 = 0; q2 < 2; ++q2) {
+                    const bool ok = tok0 + nt * 8 + 2 * t + q2 < L;
+                    x[nt][q2] = ok ? sacc[nt][q2] * sl2 : kNegInf;
+                    tmax = fmaxf(tmax, x[nt][q2]);
+                }
+            tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 1));
+            tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 2));
+            const float mnew = fmaxf(m, tmax);
+            const float mref = mnew == kNegInf ? 0.f : mnew;
+            const float corr = exp2f(m - mref);
+            m = mnew;
+            float pr[2][2];
+            float psum = 0.f;
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                for (int q2 = 0; q2 < 2; ++q2) {
+                    pr[nt][q2] = exp2f(x[nt][q2] - mref);
+                    psum += pr[nt][q2];
+                }
+            lp = lp * corr + psum;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                oacc[j][0] *= corr;
+                oacc[j][1] *= corr;
+            }
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) {
+                const int q0 = nt * 8 + 2 * t, q1 = q0 + 1;
+                uint4 v0 = lds_v4(vb + q0 * kRowBytes + ((gid ^ (q0 & 7)) << 4));
+                uint4 v1 = lds_v4(vb + q1 * kRowBytes + ((gid ^ (q1 & 7)) << 4));
+                if (tok0 + q0 >= L) v0 = make_uint4(0, 0, 0, 0);  // past seq_len: may be anything
+                if (tok0 + q1 >= L) v1 = make_uint4(0, 0, 0, 0);
+                const uint32_t a0 = f32_to_tf32(pr[nt][0]), a2 = f32_to_tf32(pr[nt][1]);
+                const uint32_t w0[4] = {v0.x, v0.y, v0.z, v0.w};
+                const uint32_t w1[4] = {v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const uint32_t b0 = (j & 1) ? (w0[j >> 1] & 0xffff0000u) : (w0[j >> 1] << 16);
+                    const uint32_t b1 = (j & 1) ? (w1[j >> 1] & 0xffff0000u) : (w1[j >> 1] << 16);
+                    mma_tf32_1688(oacc[j], a0, 0u, a2, 0u, b0, b1);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(aempty0 + 8 * st);
+        }
+        lp += __shfl_xor_sync(0xffffffffu, lp, 1);
+        lp += __shfl_xor_sync(0xffffffffu, lp, 2);
+        if (gid < p.G) {
+            float *wr = wpart + (warp * 8 + gid) * kSaPart;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                wr[16 * t + j] = oacc[j][0];
+                wr[16 * t + 8 + j] = oacc[j][1];
+            }
+            if (t == 0) {
+                wr[kAttnD] = m;
+                wr[kAttnD + 1] = lp;
+            }
+        }
+    }
+    __syncthreads();
+    SC_STAMP(4);
+    // ---- CTA merge of the W warp partials (C == 1: straight to o / lse)
+    for (int x = tid; x < p.G * 16; x += NT) {
+        const int h = x >> 4, d0 = (x & 15) * 4;
+        float mw[W];
+#pragma unroll
+        for (int w = 0; w < W; ++w) mw[w] = wpart[(w * 8 + h) * kSaPart + kAttnD];
+        float M = kNegInf;
+#pragma unroll
+        for (int w = 0; w < W; ++w) M = fmaxf(M, mw[w]);
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        float l = 0.f;
+        if (M != kNegInf) {
+#pragma unroll
+            for (int w = 0; w < W; ++w) {
+                const float *wr = wpart + (w * 8 + h) * kSaPart;
+                const float f = mw[w] == kNegInf ? 0.f : exp2f(mw[w] - M);
+                l += wr[kAttnD + 1] * f;
+                const float4 v = *reinterpret_cast<const float4 *>(wr + d0);
+                acc.x += v.x * f; acc.y += v.y * f; acc.z += v.z * f; acc.w += v.w * f;
+            }
+        }
+        if (C == 1) {
+            const size_t oh = (size_t)b * p.Hq + g * p.G + h;
+            const float inv = l > 0.f ? 1.f / l : 0.f;
+            *reinterpret_cast<float4 *>(ap.o + oh * kAttnD + d0) =
+                make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+            if (ap.lse && d0 == 0) ap.lse[oh] = l > 0.f ? (M + log2f(l)) * kLn2 : kNegInf;
+        } else {
+            float *pr = ap.part + (((size_t)row * C + rank) * 8 + h) * kPS;
+            *reinterpret_cast<float4 *>(pr + d0) = acc;
+            if (d0 == 0) {
+                pr[kAttnD] = M;
+                pr[kAttnD + 1] = l;
+            }
+        }
+    }
+    if (C > 1) {
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence();
+            s_last = atomicAdd(ap.tickets + row, 1u) == unsigned(C - 1);
+        }
+        __syncthreads();
+        if (s_last) {
+            __threadfence();
+            constexpr int kMaxC = 16;
+            const float *pb = ap.part + (size_t)row * C * 8 * kPS;
+            for (int x = tid; x < p.G * 16; x += NT) {
+                const int h = x >> 4, d0 = (x & 15) * 4;
+                float mr[kMaxC];
+#pragma unroll
+                for (int r = 0; r < kMaxC; ++r)
+                    mr[r] = r < C ? __ldcg(pb + (r * 8 + h) * kPS + kAttnD) : kNegInf;
+                float M = kNegInf;
+#pragma unroll
+                for (int r = 0; r < kMaxC; ++r) M = fmaxf(M, mr[r]);
+                float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+                float l = 0.f;
+                if (M != kNegInf) {
+#pragma unroll
+                    for (int r0 = 0; r0 < kMaxC; r0 += 4) {
+                        if (r0 >= C) break;
+                        float lq[4];
+                        float4 vq[4];
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const float *pr = pb + ((r0 + e) * 8 + h) * kPS;
+                            lq[e] = r0 + e < C ? __ldcg(pr + kAttnD + 1) : 0.f;
+                            vq[e] = r0 + e < C ? __ldcg(reinterpret_cast<const float4 *>(pr + d0))
+                                               : make_float4(0.f, 0.f, 0.f, 0.f);
+                        }
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const float f = mr[r0 + e] == kNegInf ? 0.f : exp2f(mr[r0 + e] - M);
+                            l += lq[e] * f;
+                            acc.x += vq[e].x * f; acc.y += vq[e].y * f; acc.z += vq[e].z * f; acc.w += vq[e].w * f;
+                        }
+                    }
+                }
+                const size_t oh = (size_t)b * p.Hq + g * p.G + h;
+                const float inv = l > 0.f ? 1.f / l : 0.f;
+                *reinterpret_cast<float4 *>(ap.o + oh * kAttnD + d0) =
+                    make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+                if (ap.lse && d0 == 0) ap.lse[oh] = l > 0.f ? (M + log2f(l)) * kLn2 : kNegInf;
+            }
+            if (tid == 0) ap.tickets[row] = 0u;  // re-armed for the next launch
+        }
+    }
+    SC_STAMP(7);
+}
+
+}  // namespace ts

@@ -32,9 +32,10 @@ t0 = a1[:, 0].min()
 def show(a, names, title):
     print(title, "CTAs", len(a))
     for i, n in enumerate(names):
+        if n == "-": continue
         col = a[:, i]; col = col[col > 0]
         if len(col) == 0: continue
         col = (col - t0) / 1e3
         print(f"  {n:11s} n {len(col):5d} min {col.min():7.2f} p10 {np.percentile(col,10):7.2f} med {np.median(col):7.2f} p90 {np.percentile(col,90):7.2f} max {col.max():7.2f} us")
 show(a1, ["start", "scored", "gathered", "selected", "keys", "pass0", "thresh", "compacted"], f"{name} K1 score_select")
-show(a2, ["start", "q", "pages", "loop_end", "cta_merged", "cl_sync1", "out", "cl_sync2"], f"{name} K2 sparse_attn")
+show(a2, ["start", "flag", "pages", "consumed", "-", "-", "-", "end"] if os.environ.get("TS_SA_TMA", "1") != "0" else ["start", "q", "pages", "loop_end", "cta_merged", "cl_sync1", "out", "cl_sync2"], f"{name} K2 sparse_attn")
