@@ -625,7 +625,12 @@ ts_status launch_step_cluster_t(const ts_layout *L, ScoreSelParams &sp, const At
                                 cudaStream_t st) {
     auto kern = decode_cluster_kernel<W, R>;
     const int rows = L->batch * L->num_kv_heads;
-    const size_t sm = 1024 + ScSmem<W, R>::bytes(sp.kmax, L->max_pages);
+    // flags: bit 0 page-table row prefetched to smem (rows up to 2048 pages); bit 1
+    // two-level select when rows are much longer than the candidates (set below with C)
+    sp.flags = ((L->max_pages & 3) == 0 && L->max_pages <= 2048) ? 1 : 0;
+    static const int two_env = getenv("TS_SC_TWO") ? atoi(getenv("TS_SC_TWO")) : -1;
+    const bool two_ok = two_env == 1 || (two_env != 0 && L->max_pages > 2048);  // long rows only
+    const size_t sm = 1024 + ScSmem<W, R>::bytes(sp.kmax, L->max_pages, sp.flags | (two_ok ? 2 : 0), 16);
     if (sm > 227 * 1024) return TS_ERR_UNSUPPORTED;
     {
         static std::mutex mu;
@@ -666,6 +671,8 @@ ts_status launch_step_cluster_t(const ts_layout *L, ScoreSelParams &sp, const At
     }
     sp.C = C;
     sp.chunk = chunk;
+    if (two_ok && C > 1 && (C * sp.kmax) % 4 == 0 && (two_env == 1 || L->max_pages >= 4 * C * sp.kmax))
+        sp.flags |= 2;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(rows * C);
     cfg.blockDim = dim3((W + 1) * 32);

@@ -38,6 +38,7 @@ struct ScoreSelParams {
     int *sel_count;           // [rows]
     int B, Hq, Hkv, G, S, max_pages, kmax;
     unsigned *ready;          // [rows] set to 1 once the row's selection is written (nullable)
+    int flags;                // step_cluster: bit 0 page-table prefetch, bit 1 two-level select
     int C;                    // CTAs per row (cluster size)
     int chunk;                // pages per CTA (multiple of 32)
     unsigned long long *dbg;  // development: per-CTA stamps (nullable)
@@ -147,13 +148,18 @@ TS_DEV int block_scan(int v, int *red, int *total) {
 #ifndef TS_TOPK_PROF
 #define TS_TOPK_PROF(i)
 #endif
-template <int NT, int BAR, typename Emit>
+template <int NT, int BAR, int HB = 11, typename Emit>
 TS_DEV int cta_topk(const uint32_t *keys, int n, int k, uint32_t kmin, uint32_t kmax, int *hist,
-                    int *red, uint32_t *cand, Emit emit, unsigned long long *dts = nullptr) {
+                    int *red, uint32_t *cand, Emit emit, unsigned long long *dts = nullptr,
+                    bool hist0_built = false, int nvalid = -1) {
+    // nvalid: number of live (non-zero) keys when keys[] holds zero padding (default n)
+    // hist0_built: the first pass histogram over [kmin, kmax] (shift as below) is already
+    // in hist (built in parallel by the CTAs of a cluster, score_select / step_cluster)
     // keys[] is 16-byte aligned and zero-padded to a multiple of 4 (0 < every valid key):
     // the scans below read it as uint4 for memory-level parallelism (smem latency ~30 cycles)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int kk = min(k, n);
+    const int nlive = nvalid < 0 ? n : nvalid;
+    const int kk = min(k, nlive);
     TS_TOPK_PROF(0);
     if (kk <= 0) return 0;
     const uint4 *k4 = reinterpret_cast<const uint4 *>(keys);
@@ -161,7 +167,7 @@ TS_DEV int cta_topk(const uint32_t *keys, int n, int k, uint32_t kmin, uint32_t 
     // selected = {key > tgt} + the first need_eq (lowest index) keys == teq
     uint32_t tgt = 0u, teq = 0xffffffffu;
     int need_eq = 0;
-    if (kk < n) {
+    if (kk < nlive) {
         int rem = kk;
 #pragma unroll 1
         for (int pass = 0;; ++pass) {
@@ -173,32 +179,35 @@ TS_DEV int cta_topk(const uint32_t *keys, int n, int k, uint32_t kmin, uint32_t 
             }
             const uint32_t span = kmax - kmin;
             const int bits = 32 - __clz(span);
-            const int shift = bits > 11 ? bits - 11 : 0;
+            const int shift = bits > HB ? bits - HB : 0;
             if (pass > 0) {
-                for (int i = tid; i < kSsHist; i += NT) hist[i] = 0;
+                for (int i = tid; i < (1 << HB); i += NT) hist[i] = 0;
                 sel_sync<NT, BAR>();
             }
+            if (pass > 0 || !hist0_built) {
 #pragma unroll 2
-            for (int i = tid; i < n4; i += NT) {
-                const uint4 v = k4[i];
-                const uint32_t e[4] = {v.x, v.y, v.z, v.w};
+                for (int i = tid; i < n4; i += NT) {
+                    const uint4 v = k4[i];
+                    const uint32_t e[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-                for (int j = 0; j < 4; ++j)
-                    if (e[j] >= kmin && e[j] <= kmax) atomicAdd(&hist[(e[j] - kmin) >> shift], 1);
+                    for (int j = 0; j < 4; ++j)
+                        if (e[j] >= kmin && e[j] <= kmax) atomicAdd(&hist[(e[j] - kmin) >> shift], 1);
+                }
+                sel_sync<NT, BAR>();
             }
-            sel_sync<NT, BAR>();
             TS_TOPK_PROF(1);
             if (warp == 0) {  // boundary bin: lane owns bins [64 lane, +64), scanned from the top
-                const int4 *h4 = reinterpret_cast<const int4 *>(hist) + lane * 16;
-                int c[64];
+                constexpr int PB = (1 << HB) / 32;  // bins per lane
+                const int4 *h4 = reinterpret_cast<const int4 *>(hist) + lane * (PB / 4);
+                int c[PB];
 #pragma unroll
-                for (int j = 0; j < 16; ++j) {
+                for (int j = 0; j < PB / 4; ++j) {
                     const int4 v = h4[j];
                     c[4 * j] = v.x; c[4 * j + 1] = v.y; c[4 * j + 2] = v.z; c[4 * j + 3] = v.w;
                 }
                 int s = 0;
 #pragma unroll
-                for (int j = 0; j < 64; ++j) s += c[j];
+                for (int j = 0; j < PB; ++j) s += c[j];
                 int suf = s;  // inclusive suffix over lanes >= lane
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
@@ -210,7 +219,7 @@ TS_DEV int cta_topk(const uint32_t *keys, int n, int k, uint32_t kmin, uint32_t 
                     int acc = above_run, bsel = 0, cb = 0, ab = 0;
                     bool done = false;
 #pragma unroll
-                    for (int j = 63; j >= 0; --j) {
+                    for (int j = PB - 1; j >= 0; --j) {
                         if (!done && acc + c[j] >= rem) {
                             bsel = j;
                             cb = c[j];
@@ -219,7 +228,7 @@ TS_DEV int cta_topk(const uint32_t *keys, int n, int k, uint32_t kmin, uint32_t 
                         }
                         acc += c[j];
                     }
-                    red[48] = lane * 64 + bsel;
+                    red[48] = lane * PB + bsel;
                     red[49] = ab;
                     red[50] = cb;
                 }
@@ -351,7 +360,7 @@ __global__ void __launch_bounds__((W + 1) * 32) score_select_kernel(ScoreSelPara
     const uint32_t full0 = sb + SM::kBars, empty0 = full0 + 8 * R;
     const uint32_t qbar = empty0 + 8 * R, ptbar = qbar + 8;
     float *sc = reinterpret_cast<float *>(smem + SM::kScores);
-    int *pt_s = reinterpret_cast<int *>(smem + SM::kScores) + ((p.max_pages + 3) & ~3);
+    int *pt_s = reinterpret_cast<int *>(smem + SM::kScores) + ((p.max_pages + 3) & ~3);  // (score_select_kernel)
     int *hist = reinterpret_cast<int *>(smem + SM::kHist);
     int *red = reinterpret_cast<int *>(smem + SM::kRed);
     unsigned *s_kmin = reinterpret_cast<unsigned *>(red + 60), *s_kmax = s_kmin + 1;

@@ -36,14 +36,17 @@ struct ScSmem {
     static constexpr int kBars = (kInfo + 2 * R * 4 + 7) / 8 * 8;   // mfull,mempty[R]; afull,aempty[2R]; q; pt
     static constexpr int kSel = (kBars + (6 * R + 2) * 8 + 15) / 16 * 16;  // [kmax] int2
     __host__ __device__ static size_t scores_off(int kmax) { return ((size_t)kSel + (size_t)kmax * 8 + 127) / 128 * 128; }
-    static size_t bytes(int kmax, int max_pages) {
+    // scores [mp4] fp32, then the page-table row [mp4] (flag bit 0), then the two-level
+    // candidates [C * kmax] keys + ids (flag bit 1)
+    static size_t bytes(int kmax, int max_pages, int flags, int C) {
         const size_t mp4 = (max_pages + 3) & ~3;
-        return scores_off(kmax) + mp4 * 4 + mp4 * 4 + 16;
+        return scores_off(kmax) + mp4 * 4 + ((flags & 1) ? mp4 * 4 : 0) +
+               ((flags & 2) ? (size_t)C * kmax * 8 : 0) + 16;
     }
 };
 
 template <int W, int R>
-__global__ void __launch_bounds__((W + 1) * 32) decode_cluster_kernel(
+__global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
     const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
     ScoreSelParams p, AttnParams ap) {
     using SM = ScSmem<W, R>;
@@ -59,7 +62,10 @@ __global__ void __launch_bounds__((W + 1) * 32) decode_cluster_kernel(
     const uint32_t qbar = aempty0 + 8 * RA, ptbar = qbar + 8;
     const int mp4 = (p.max_pages + 3) & ~3;
     float *sc = reinterpret_cast<float *>(smem + SM::scores_off(p.kmax));
+    const bool pt_bulk = p.flags & 1, two = (p.flags & 2) && p.C > 1;
     int *pt_s = reinterpret_cast<int *>(sc) + mp4;
+    uint32_t *ckey = reinterpret_cast<uint32_t *>(pt_s + (pt_bulk ? mp4 : 0));  // [C * kmax]
+    int *cid = reinterpret_cast<int *>(ckey) + p.C * p.kmax;
     int *hist = reinterpret_cast<int *>(smem + SM::kHist);
     int *red = reinterpret_cast<int *>(smem + SM::kRed);
     float *wpart = reinterpret_cast<float *>(smem + SM::kWarpPart);
@@ -92,17 +98,19 @@ __global__ void __launch_bounds__((W + 1) * 32) decode_cluster_kernel(
         fence_mbar_init();
         *s_kmin = 0xffffffffu;
         *s_kmax = 0u;
+        s_cnt = 0;
     }
-    if (rank == 0)
+    if (rank == 0 || two)
         for (int i = tid; i < kSsHist; i += NT) hist[i] = 0;
     __syncthreads();
-    if (C > 1) cluster_arrive_relaxed();  // "this CTA is running" (before any DSMEM access)
+    // "this CTA is running" (before any DSMEM access); release: its initialised counters
+    // and histogram are visible to the remote updates that follow the matching wait
+    if (C > 1) cluster_arrive_release();
     pdl_wait();  // inputs may come from the previous kernel in the stream
 
     const int L = p.seq_lens[b];
     const int P = (L + p.S - 1) / p.S;
     const int j0 = rank * p.chunk;
-    const bool pt_bulk = (p.max_pages & 3) == 0;
     const int nloc = max(0, min(P - j0, p.chunk));
     const int nst = (nloc + kSsStagePages - 1) / kSsStagePages;
     const int gid = lane >> 2, t = lane & 3;
@@ -200,8 +208,37 @@ __global__ void __launch_bounds__((W + 1) * 32) decode_cluster_kernel(
     SC_STAMP(1);
 
     // ===================================== 2. select =====================================
+    // one-level: the chunk scores go to the leader, which runs the exact CTA-wide top-K.
+    // two-level (rows much longer than C x K): every CTA selects its chunk's top-K (in
+    // parallel) and sends those candidates; the leader selects from the C x K candidates.
+    // Exact: a page of the row's top-K is beaten by fewer than K pages of its own chunk
+    // (same order: score, then lower id), so it is among its chunk's candidates.  (A
+    // cluster-parallel radix pass through DSMEM atomics was measured slower.)
     cg::cluster_group cl = cg::this_cluster();
-    if (C > 1) {
+    if (two) {
+        cluster_wait();  // every CTA of the cluster is running
+        uint32_t *lkeys = reinterpret_cast<uint32_t *>(sc) + j0;
+        for (int i = tid; i < ((nloc + 3) & ~3); i += NT) lkeys[i] = i < nloc ? score_key(sc[j0 + i]) : 0u;
+        __syncthreads();
+        uint32_t *rk = cl.map_shared_rank(ckey, 0) + rank * p.kmax;
+        int *ri = cl.map_shared_rank(cid, 0) + rank * p.kmax;
+        uint32_t *cand = reinterpret_cast<uint32_t *>(wpart);
+        auto emit_c = [&](int pos, int i) {
+            rk[pos] = lkeys[i];
+            ri[pos] = j0 + i;
+        };
+        const int kl = nloc <= 512
+                           ? cta_topk<NT, 0, 9>(lkeys, nloc, p.kmax, *s_kmin, *s_kmax, hist, red, cand, emit_c)
+                           : cta_topk<NT, 0, 11>(lkeys, nloc, p.kmax, *s_kmin, *s_kmax, hist, red, cand, emit_c);
+        for (int i = kl + tid; i < p.kmax; i += NT) rk[i] = 0u;  // absent
+        if (tid == 0) atomicAdd(cl.map_shared_rank(&s_cnt, 0), kl);
+        if (rank == 0) {  // the leader's candidate range for its select (all CTAs' keys)
+            __syncthreads();
+            for (int i = tid; i < kSsHist; i += NT) hist[i] = 0;
+        }
+        cluster_arrive_release();
+        cluster_wait();
+    } else if (C > 1) {
         cluster_wait();  // every CTA of the cluster is running
         if (rank != 0) {
             float *dst = cl.map_shared_rank(sc, 0);
@@ -215,21 +252,47 @@ __global__ void __launch_bounds__((W + 1) * 32) decode_cluster_kernel(
         cluster_arrive_release();
         cluster_wait();
     }
+    SC_STAMP(5);
     if (rank == 0) {
-        uint32_t *keys = reinterpret_cast<uint32_t *>(sc);
-        for (int i = tid; i < ((P + 3) & ~3); i += NT) keys[i] = i < P ? score_key(sc[i]) : 0u;
-        if (P > 0 && pt_bulk) mbar_wait(ptbar, 0);
         const int *ptrow = pt_bulk ? pt_s : p.page_table + (size_t)b * p.max_pages;
-        __syncthreads();
         int *out_id = p.sel_ids + (size_t)row * p.kmax;
         uint32_t *cand = reinterpret_cast<uint32_t *>(wpart);  // free until the attention ends
         const int S = p.S;
-        const int kk = cta_topk<NT, 0>(keys, P, p.kmax, *s_kmin, *s_kmax, hist, red, cand,
-                                       [&](int pos, int i) {
-                                           out_id[pos] = i;
-                                           sel[pos] = make_int2((ptrow[i] * p.Hkv + g) * S, i * S);
-                                       });
+        int kk;
+        if (two) {
+            const int nc = C * p.kmax, nlive = s_cnt;
+            uint32_t mn = 0xffffffffu, mx = 0u;
+            for (int i = tid; i < nc; i += NT)
+                if (ckey[i]) {
+                    mn = min(mn, ckey[i]);
+                    mx = max(mx, ckey[i]);
+                }
+            if (P > 0 && pt_bulk) mbar_wait(ptbar, 0);
+            block_minmax<NT, 0>(mn, mx, red);
+            SC_STAMP(6);
+            auto emit = [&](int pos, int i) {
+                const int pg = cid[i];
+                out_id[pos] = pg;
+                sel[pos] = make_int2((ptrow[pg] * p.Hkv + g) * S, pg * S);
+            };
+            // candidates are chunk-major, ids ascending inside a chunk: entry order == id order
+            kk = cta_topk<NT, 0, 11>(ckey, nc, p.kmax, mn, mx, hist, red, cand, emit, nullptr, false, nlive);
+        } else {
+            uint32_t *keys = reinterpret_cast<uint32_t *>(sc);
+            for (int i = tid; i < ((P + 3) & ~3); i += NT) keys[i] = i < P ? score_key(sc[i]) : 0u;
+            if (P > 0 && pt_bulk) mbar_wait(ptbar, 0);
+            __syncthreads();
+            SC_STAMP(6);
+            auto emit = [&](int pos, int i) {
+                out_id[pos] = i;
+                sel[pos] = make_int2((ptrow[i] * p.Hkv + g) * S, i * S);
+            };
+            // radix width by row length: ~1 key per bin on the first pass
+            kk = P <= 512 ? cta_topk<NT, 0, 9>(keys, P, p.kmax, *s_kmin, *s_kmax, hist, red, cand, emit)
+                          : cta_topk<NT, 0, 11>(keys, P, p.kmax, *s_kmin, *s_kmax, hist, red, cand, emit);
+        }
         for (int i = kk + tid; i < p.kmax; i += NT) out_id[i] = -1;
+        __syncthreads();
         if (tid == 0) {
             p.sel_count[row] = kk;
             s_cnt = kk;

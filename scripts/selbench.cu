@@ -29,7 +29,7 @@ __global__ void __launch_bounds__(NT) bench(const float *scores, int n, int k, i
     block_minmax<NT>(mn, mx, red);
     long long t1 = clock64();
     int *o = out + (size_t)blockIdx.x * k;
-    const int kk = cta_topk<NT, 0>(keys, n, k, mn, mx, hist, red, cand, [&](int pos, int i) { o[pos] = i; });
+    const int kk = (n <= 512 ? cta_topk<NT, 0, 9>(keys, n, k, mn, mx, hist, red, cand, [&](int pos, int i) { o[pos] = i; }) : cta_topk<NT, 0, 11>(keys, n, k, mn, mx, hist, red, cand, [&](int pos, int i) { o[pos] = i; }));
     __syncthreads();
     long long t2 = clock64();
     if (threadIdx.x == 0 && blockIdx.x == 0) { cyc[0] = t1 - t0; cyc[1] = t2 - t1; cyc[2] = kk; }

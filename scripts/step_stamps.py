@@ -37,5 +37,8 @@ def show(a, names, title):
         if len(col) == 0: continue
         col = (col - t0) / 1e3
         print(f"  {n:11s} n {len(col):5d} min {col.min():7.2f} p10 {np.percentile(col,10):7.2f} med {np.median(col):7.2f} p90 {np.percentile(col,90):7.2f} max {col.max():7.2f} us")
+if os.environ.get("TS_TWO_KERNELS", "0") == "0":
+    show(a1, ["start", "scored", "selected", "listed", "consumed", "gathered", "keys", "end"], f"{name} decode_cluster_kernel")
+    sys.exit(0)
 show(a1, ["start", "scored", "gathered", "selected", "keys", "pass0", "thresh", "compacted"], f"{name} K1 score_select")
 show(a2, ["start", "flag", "pages", "consumed", "-", "-", "-", "end"] if os.environ.get("TS_SA_TMA", "1") != "0" else ["start", "q", "pages", "loop_end", "cta_merged", "cl_sync1", "out", "cl_sync2"], f"{name} K2 sparse_attn")
