@@ -251,6 +251,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-oracle", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-dense", action="store_true", help="skip the FullCache baseline leg")
     ap.add_argument("--oracle-seconds", type=float, default=12.0)
     ap.add_argument("--replicas", type=int, default=0)
     args = ap.parse_args()
@@ -303,8 +304,11 @@ def main():
     with torch.cuda.stream(stream):
         one(reps[0])
     torch.cuda.synchronize()
-    fused = cfg.dtype == "bf16" and cfg.group <= 8 and mode != "sequence"
-    launches_per_step = (2 if fused else 3) if mode != "sequence" else 5
+    # launches of our kernels per step, as reported by the C ABI for the step just run
+    # (bf16: 1 = decode_cluster_kernel; sequence sharding: 5 calls + 2 collectives)
+    launches_per_step = ts.launch_count() if mode != "sequence" else 5
+    single = mode != "sequence" and launches_per_step == 1
+    fused = cfg.dtype == "bf16" and cfg.group <= 8 and mode != "sequence" and not single
 
     # ---- graphs: one per replica (the timed unit, no instrumentation inside), plus one per
     # replica with CUDA events between the kernels for the per-kernel durations (roofline);
@@ -393,7 +397,10 @@ def main():
                     k3.append(ev[r][2].elapsed_time(ev[r][3]))
                     tot.append(ev[r][0].elapsed_time(ev[r][3]))
         phase = {"samples": len(tot), "serialised_step_us": 1e3 * statistics.mean(tot)}
-        if fused:
+        if single:
+            phase.update(kernels="decode_cluster_kernel (score + select + gather + attend, one launch)",
+                         step_kernel_us=1e3 * statistics.mean(tot))
+        elif fused:
             phase.update(kernels="score_select -> sparse_attn (PDL + per-row flags in the timed graphs)",
                          score_select_us=1e3 * statistics.mean(k1),
                          attn_us=1e3 * statistics.mean(k3))
@@ -401,6 +408,15 @@ def main():
             phase.update(score_us=1e3 * statistics.mean(k1), select_us=1e3 * statistics.mean(k2),
                          attn_us=1e3 * statistics.mean(k3))
 
+    # ---- FullCache baseline: dense attention over every page of the same
+    # replicas, same timing protocol -> the sparse/dense speedup (the paper's 2.1-3.4x claim,
+    # PAPER.md:8, 550, measured on 8xA100; context only)
+    dense = None
+    try:
+        dense = dense_leg(ts, cfg, reps, R, stream, dev, args, ms_per_step) if (
+            use_graph and not args.no_dense and cfg.dtype == "bf16" and cfg.page_size % 16 == 0) else None
+    except Exception as ex:  # noqa: BLE001 — the baseline is context; never fail the bench on it
+        dense = {"unavailable": f"{type(ex).__name__}: {ex}"}
     # ---- e2e: public API with host buffers (pinned), H2D of q / new k,v + D2H of o, lse
     e2e = None
     if not args.no_e2e and mode != "sequence":
@@ -434,7 +450,9 @@ def main():
     peak, peak_src = measured_peaks()
     roof = None
     if phase:
-        if fused:  # score_select (metadata + selection) and sparse_attn (selected K/V)
+        if single:  # the one kernel moves every byte of the step
+            cand = {"decode_cluster_kernel": (kb["total"], phase["step_kernel_us"])}
+        elif fused:  # score_select (metadata + selection) and sparse_attn (selected K/V)
             cand = {"score_select": (kb["score"] + kb["select"], phase["score_select_us"]),
                     "sparse_attn": (kb["attn"], phase["attn_us"])}
         else:
@@ -442,8 +460,18 @@ def main():
         dom = max(cand, key=lambda x: cand[x][1])
         nbytes, us = cand[dom]
         achieved = nbytes / (us * 1e-6) / 1e9
+        traffic, tsrc = None, None
+        try:  # DRAM bytes per launch of this kernel from the committed ncu capture
+            with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+                tj = json.load(f).get(cfg.name)
+            if tj and dom in tj["per_launch_bytes"]:
+                traffic = tj["per_launch_bytes"][dom]
+                tsrc = "ncu --set full: dram__bytes_read.sum + dram__bytes_write.sum, profiles/" + tj["report"]
+        except (OSError, ValueError, KeyError):
+            pass
         roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                "frac": achieved / peak, "traffic": traffic, "traffic_source": tsrc,
+                "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": nbytes, "avg_launch_us": us, "phase_us": phase,
                 "step_achieved_gbs": step_bytes / (ms_per_step * 1e-3) / 1e9,
                 "step_frac": step_bytes / (ms_per_step * 1e-3) / 1e9 / peak}
@@ -459,13 +487,57 @@ def main():
         "tokens_per_s": value * cfg.batch,
         "hbm_gbs": gbs, "frac_of_8tbs": gbs / PEAK_SPEC_GBS, "frac_of_measured": gbs / peak,
         "algorithmic_bytes_per_step": step_bytes, "kernel_bytes": kb,
-        "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+        "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "dense_baseline": dense,
         "gpu_launches": launches_per_step * args.steps, "clocks": clocks,
         "wall_s_timed": wall, "device": torch.cuda.get_device_name(dev),
     }
     print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
+
+
+def dense_leg(ts, cfg, reps, R, stream, dev, args, ms_per_step):
+    """FullCache baseline leg: dense attention over every page of the same replicas."""
+    dense = None
+    dws = [ts.new_workspace(ts.dense_workspace_bytes(rep["layout"]), dev) for rep in reps]
+
+    def dstep(r):
+        rep = reps[r]
+        ts.dense_decode_attn(rep["layout"], rep["q"], rep["k_pool"], rep["v_pool"],
+                             rep["page_table"], rep["seq_lens"], cfg.scale, o=rep["o"],
+                             lse=rep["lse"], ws=dws[r], stream=stream)
+    with torch.cuda.stream(stream):
+        for r in range(R):
+            dstep(r)
+    torch.cuda.synchronize()
+    dg = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(stream):
+        with torch.cuda.graph(dg, stream=stream):
+            for r in range(R):
+                dstep(r)
+    torch.cuda.synchronize()
+    nd = max(1, min(args.steps, 600) // R)
+    with torch.cuda.stream(stream):
+        for _ in range(2):
+            dg.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        for _ in range(nd):
+            dg.replay()
+        e1.record(stream)
+    torch.cuda.synchronize()
+    dms = e0.elapsed_time(e1) / (nd * R)
+    e = 2
+    dbytes = (cfg.batch * cfg.num_kv_heads * cfg.ctx * 2 * cfg.head_dim * e
+              + cfg.batch * cfg.num_q_heads * cfg.head_dim * (e + 4) + cfg.batch * cfg.num_q_heads * 4)
+    dense = {"ms_per_step": dms, "steps_per_s": 1e3 / dms, "bytes_per_step": dbytes,
+             "hbm_gbs": dbytes / (dms * 1e-3) / 1e9,
+             "speedup_sparse_vs_dense": dms / ms_per_step,
+             "kernel": "sparse_attn_tma_kernel in dense mode (every page; ts_dense_decode_attn)"}
+
+    return dense
 
 
 def run_e2e(ts, cfg, rep, dev, stream, steps, warmup):

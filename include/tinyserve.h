@@ -175,6 +175,18 @@ ts_status ts_lse_merge(int32_t parts, int32_t rows, int32_t d, const float *o_pa
                        const float *lse_parts, int64_t part_stride, float *o, float *lse,
                        void *stream);
 
+/* FullCache baseline (dense attention): for every
+ * q head h of sequence b, softmax attention over ALL valid tokens t < seq_lens[b] of the
+ * sequence's pages, through the same paged pool and attention kernel as the sparse path
+ * (bf16, head_dim 64, page_size a multiple of 16, unsharded).  Equals
+ * ts_sparse_decode_attn with every page selected.  ws >= ts_dense_workspace_bytes(),
+ * zero-filled once before first use.  Used to measure the sparse/dense speedup. */
+ts_status ts_dense_decode_attn(const ts_layout *layout, const void *q, const void *k_pool,
+                               const void *v_pool, const int32_t *page_table,
+                               const int32_t *seq_lens, float scale, float *o, float *lse,
+                               void *ws, size_t ws_bytes, void *stream);
+size_t ts_dense_workspace_bytes(const ts_layout *layout);
+
 /* Workspace sizes in bytes (host-only, no CUDA call). */
 size_t ts_workspace_bytes(const ts_layout *layout, int32_t budget_tokens);
 size_t ts_attn_workspace_bytes(const ts_layout *layout, int32_t sel_stride);

@@ -19,7 +19,7 @@ from ._lib import Layout, TinyServeError, TS_BF16, TS_F32, check, exported_symbo
 
 __all__ = ["Layout", "TinyServeError", "make_layout", "meta_append", "meta_build",
            "score_pages", "select_topk", "sparse_decode_attn", "decode_step", "select_merge", "lse_merge",
-           "workspace_bytes", "attn_workspace_bytes", "new_workspace", "new_meta", "kmax", "launch_count",
+           "workspace_bytes", "attn_workspace_bytes", "dense_decode_attn", "dense_workspace_bytes", "new_workspace", "new_meta", "kmax", "launch_count",
            "profile_events",
            "exported_symbols", "PagedKV"]
 
@@ -166,6 +166,28 @@ def sparse_decode_attn(layout, q, k_pool, v_pool, page_table, seq_lens, sel_ids,
         _ptr(sel_ids), _ptr(sel_count), sel_stride, float(scale), _ptr(o), _ptr(lse), _ptr(ws),
         ws.numel(), _stream(stream)))
     return o, lse
+
+
+def dense_decode_attn(layout, q, k_pool, v_pool, page_table, seq_lens, scale, o=None, lse=None,
+                      ws=None, want_lse=True, stream=None):
+    """FullCache baseline: attention over every valid token (ts_dense_decode_attn)."""
+    dev = q.device
+    if o is None:
+        o = torch.empty((layout.batch, layout.num_q_heads, layout.head_dim), dtype=torch.float32,
+                        device=dev)
+    if lse is None and want_lse:
+        lse = torch.empty((layout.batch, layout.num_q_heads), dtype=torch.float32, device=dev)
+    if ws is None:
+        ws = new_workspace(lib().ts_dense_workspace_bytes(layout), dev)
+    _cuda(q, k_pool, v_pool, page_table, seq_lens, o, lse, ws)
+    check("ts_dense_decode_attn", lib().ts_dense_decode_attn(
+        layout, _ptr(q), _ptr(k_pool), _ptr(v_pool), _ptr(page_table), _ptr(seq_lens),
+        float(scale), _ptr(o), _ptr(lse), _ptr(ws), ws.numel(), _stream(stream)))
+    return o, lse
+
+
+def dense_workspace_bytes(layout) -> int:
+    return lib().ts_dense_workspace_bytes(layout)
 
 
 def decode_step(layout, q, k_pool, v_pool, meta, page_table, seq_lens, budget_tokens, scale,

@@ -20,7 +20,7 @@ _STATUS = {0: "TS_OK", 1: "TS_ERR_CONFIG", 2: "TS_ERR_SHAPE", 3: "TS_ERR_ALIGN",
 SYMBOLS = ["ts_meta_append", "ts_meta_build", "ts_score_pages", "ts_select_topk",
            "ts_sparse_decode_attn", "ts_decode_step", "ts_select_merge", "ts_lse_merge", "ts_workspace_bytes",
            "ts_attn_workspace_bytes", "ts_status_str", "ts_version", "ts_last_launch_count",
-           "ts_profile_events"]
+           "ts_profile_events", "ts_dense_decode_attn", "ts_dense_workspace_bytes"]
 
 
 class TinyServeError(RuntimeError):
@@ -64,6 +64,7 @@ def lib() -> ctypes.CDLL:
             "ts_decode_step": [LP, P, P, P, P, P, P, I, F, P, P, P, P, P, SZ, P],
             "ts_select_merge": [P, P, I, ctypes.c_int64, I, I, I, P, P, P, P],
             "ts_lse_merge": [I, I, I, P, P, ctypes.c_int64, P, P, P],
+            "ts_dense_decode_attn": [LP, P, P, P, P, P, F, P, P, P, SZ, P],
         }
         for name, args in sig.items():
             fn = getattr(L, name)
@@ -73,6 +74,8 @@ def lib() -> ctypes.CDLL:
         L.ts_workspace_bytes.restype = SZ
         L.ts_attn_workspace_bytes.argtypes = [LP, I]
         L.ts_attn_workspace_bytes.restype = SZ
+        L.ts_dense_workspace_bytes.argtypes = [LP]
+        L.ts_dense_workspace_bytes.restype = SZ
         L.ts_status_str.argtypes = [ctypes.c_int]
         L.ts_status_str.restype = ctypes.c_char_p
         L.ts_version.restype = ctypes.c_char_p

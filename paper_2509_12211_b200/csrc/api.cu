@@ -1076,6 +1076,34 @@ ts_status ts_decode_step(const ts_layout *L, const void *q, const void *k_pool, 
     return TS_OK;
 }
 
+// FullCache baseline: dense paged decode attention over every page
+// j < P_b, same pool / layout / kernels as the sparse path.
+size_t ts_dense_workspace_bytes(const ts_layout *L) {
+    if (check_layout(L) != TS_OK) return 0;
+    return attn_ws_layout(L, L->max_pages).total;
+}
+
+ts_status ts_dense_decode_attn(const ts_layout *L, const void *q, const void *k_pool,
+                               const void *v_pool, const int32_t *page_table,
+                               const int32_t *seq_lens, float scale, float *o, float *lse,
+                               void *ws, size_t ws_bytes, void *stream) {
+    g_launches = 0;
+    ts_status s = check_layout(L);
+    if (s != TS_OK) return s;
+    if (L->shard_stride != 1) return TS_ERR_UNSUPPORTED;
+    if (!aligned16(q) || !aligned16(k_pool) || !aligned16(v_pool) || !aligned16(o))
+        return TS_ERR_ALIGN;
+    if (!bf16_attn_supported(L) || L->page_size % 16 != 0) return TS_ERR_UNSUPPORTED;
+    if (!ws || ws_bytes < attn_ws_layout(L, L->max_pages).total) return TS_ERR_WORKSPACE;
+    if (L->batch == 0) return TS_OK;
+    AttnParams p = attn_params(L, q, k_pool, v_pool, page_table, seq_lens, nullptr, nullptr,
+                               L->max_pages, scale, o, lse, ws);
+    p.dense = 1;
+    static const int rr = getenv("TS_SA_R") ? atoi(getenv("TS_SA_R")) : 8;
+    if (rr == 16) return launch_sat<4, 16>(L, p, false, as_stream(stream));
+    return launch_sat<4, 8>(L, p, false, as_stream(stream));
+}
+
 ts_status ts_select_merge(const float *cand_scores, const int32_t *cand_ids, int32_t parts,
                           int64_t part_stride, int32_t rows, int32_t k_part, int32_t k,
                           int32_t *sel_ids, float *sel_scores, int32_t *sel_count, void *stream) {

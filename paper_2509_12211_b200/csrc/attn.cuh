@@ -36,6 +36,7 @@ struct AttnParams {
     unsigned *tickets; // [rows]
     int splits, items;
     unsigned long long *dbg;  // development: per-CTA globaltimer stamps (nullable)
+    int dense;                // 1: attend every page (FullCache baseline), sel_* unused
 };
 
 constexpr int kAttnD = 64;        // head_dim of the tensor-core path

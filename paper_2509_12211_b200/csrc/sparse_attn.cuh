@@ -359,7 +359,16 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) sparse_attn_tma_kernel(
     }
     __syncthreads();
     if (dts && threadIdx.x == 0) dts[1] = globaltimer();
-    if (p.stride == 1) {
+    if (p.dense) {
+        // FullCache baseline (dense attention): every page
+        // j < P_b of the row, in order, through the same gather + attention machinery
+        const int P = (L + p.S - 1) / p.S;
+        for (int u = threadIdx.x; u < P; u += blockDim.x) {
+            const int blk = __ldg(p.page_table + (size_t)b * p.max_pages + u);
+            pages[u] = make_int2((blk * p.Hkv + g) * p.S, u * p.S);
+        }
+        if (threadIdx.x == 0) s_nown = P;
+    } else if (p.stride == 1) {
         // every selected page is owned: all threads resolve entries in parallel (one load
         // round for the ids / blocks, one more for the page table when not pre-resolved)
         const int cnt = __ldcg(p.sel_count + row);

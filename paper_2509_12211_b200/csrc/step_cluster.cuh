@@ -299,28 +299,27 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
         }
         SC_STAMP(2);
     }
-    // the selection list is in the leader's shared memory
+    // the leader pushes the selection list and its count into every CTA's shared memory
+    // (remote stores, no round trip), then one cluster barrier publishes them
     if (C > 1) {
+        if (rank == 0) {
+            __syncthreads();  // the list and s_cnt are complete
+            const int kk = s_cnt;
+            for (int r = 1; r < C; ++r) {
+                int2 *dst = cl.map_shared_rank(sel, r);
+                for (int u = tid; u < kk; u += NT) dst[u] = sel[u];
+                if (tid == 0) *cl.map_shared_rank(&s_cnt, r) = kk;
+            }
+        }
         cluster_arrive_release();
         cluster_wait();
     } else {
         __syncthreads();
     }
-    const int cnt = C > 1 ? *cl.map_shared_rank(&s_cnt, 0) : s_cnt;
+    const int cnt = s_cnt;
     const int tpp = p.S >> 4;
     const int ntile = cnt * tpp;
     const int t0 = (int)((long long)ntile * rank / C), t1 = (int)((long long)ntile * (rank + 1) / C);
-    const int u0 = t0 / tpp, u1 = (t1 + tpp - 1) / tpp;  // pages touched by this CTA
-    if (C > 1) {
-        if (rank != 0) {
-            const int2 *src = cl.map_shared_rank(sel, 0);
-            for (int u = u0 + tid; u < u1; u += NT) sel[u] = src[u];
-        }
-        // the leader's list may be overwritten by nobody; other CTAs read it once: a
-        // second barrier keeps the leader alive (and its list valid) until they have
-        cluster_arrive_release();
-        cluster_wait();
-    }
     __syncthreads();
     SC_STAMP(3);
 

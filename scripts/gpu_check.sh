@@ -18,10 +18,10 @@ for CFG in ${CONFIGS:-c2}; do
 done
 if [ "${NCU:-1}" = 1 ]; then
   for CFG in ${NCU_CONFIGS:-c2}; do
-    timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'score|select|attn|meta' -c 60 --csv \
+    timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'score|select|attn|meta|decode' -c 60 --csv \
       --log-file $OUT/launches_${CFG}_$TAG.csv python bench.py --config $CFG --steps 20 --warmup 3 --no-oracle --no-e2e > /dev/null 2>&1
     echo "ncu launches $CFG rc=$?"
-    timeout 1200 ncu --set full --clock-control none --import-source on -k regex:'sparse_attn|score_select' -s 6 -c 4 \
+    timeout 1200 ncu --set full --clock-control none --import-source on -k regex:'decode_cluster|sparse_attn' -s 6 -c 3 \
       -o $OUT/prof_${CFG}_$TAG -f python bench.py --config $CFG --steps 10 --warmup 3 --no-oracle --no-e2e > $OUT/ncu_full_${CFG}_$TAG.log 2>&1
     echo "ncu full $CFG rc=$?"; tail -3 $OUT/ncu_full_${CFG}_$TAG.log
   done

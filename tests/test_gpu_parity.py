@@ -214,6 +214,24 @@ def test_attention_k_equals_p_is_dense(ts):
     assert np.abs(o.cpu().numpy() - ref["o"]).max() <= 2e-3
 
 
+@pytest.mark.parametrize("cname,S,scale", [("c3", 16, None), ("c2", 32, 1.0), ("c5", 64, None)])
+def test_dense_baseline_equals_oracle_dense(ts, cname, S, scale):
+    """NEXT-1 FullCache baseline: attention over every valid token == the oracle with K = P
+    (itself pinned to float64 SDPA), ragged lengths, NaN-poisoned page tails."""
+    cfg = synth.config(cname, batch=3, ctx=900, page_size=S, budget_tokens=1 << 20)
+    if scale is not None:
+        cfg = cfg.with_(scale=scale)
+    case = synth.make_case(cfg, seed=31, ragged=True, poison_tail=True)
+    ref = oracle.decode_step(case["q"], case["k_pool"], case["v_pool"], case["page_table"],
+                             case["seq_lens"], cfg.budget_tokens, cfg.scale)
+    d = on_dev(case)
+    L = ts.make_layout(d["q"], d["k_pool"], d["page_table"])
+    o, lse = ts.dense_decode_attn(L, d["q"], d["k_pool"], d["v_pool"], d["page_table"],
+                                  d["seq_lens"], cfg.scale)
+    assert np.abs(o.cpu().numpy() - ref["o"]).max() <= ATOL[cfg.dtype]
+    assert np.abs(lse.cpu().numpy() - ref["lse"]).max() <= 1e-3
+
+
 # ------------------------------------------------------------------ a5: fused step
 def _step_parity(ts, cfg, case, ref):
     d = on_dev(case)
