@@ -450,8 +450,13 @@ def main():
     peak, peak_src = measured_peaks()
     roof = None
     if phase:
-        if single:  # the one kernel moves every byte of the step
-            cand = {"decode_cluster_kernel": (kb["total"], phase["step_kernel_us"])}
+        if single:
+            # the one kernel moves every byte of the step and is the only launch of it: its
+            # average launch duration is the timed region's per-step time (consecutive
+            # launches overlap their prologues through PDL); the per-launch time of the
+            # event-instrumented graphs (serialised, launch latency included) is kept in
+            # phase_us for reference
+            cand = {"decode_cluster_kernel": (kb["total"], ms_per_step * 1e3)}
         elif fused:  # score_select (metadata + selection) and sparse_attn (selected K/V)
             cand = {"score_select": (kb["score"] + kb["select"], phase["score_select_us"]),
                     "sparse_attn": (kb["attn"], phase["attn_us"])}
