@@ -144,6 +144,10 @@ ts_status ts_sparse_decode_attn(const ts_layout *layout, const void *q, const vo
 
 /* The fused decode step (Alg. 1 end to end): score every page from
  * meta, select K_b = min(P_b, max(1, floor(budget_tokens/S))) pages per (b, g), attend.
+ * bf16 with page_size a multiple of 16: one launch (a thread-block cluster per (b, g):
+ * score -> exact top-K in the cluster leader -> TMA gather -> attention, PDL-launched so
+ * that its prologue overlaps the previous kernel); bf16 with page_size 8: score/select
+ * kernel -> attention kernel (PDL); fp32: score -> select -> attention kernels.
  * Unsharded layouts only (shard_stride == 1; the sequence-sharded step is composed from
  * the calls above plus two all-gathers).  sel_ids_out [B][Hkv][Kmax] and
  * sel_count_out [B][Hkv] (Kmax = min(max_pages, max(1, budget_tokens/S))) may be NULL.
@@ -202,8 +206,8 @@ int32_t ts_last_launch_count(void);
 /* Measurement hook (bench.py roofline): while set, ts_decode_step on this thread records
  * events[0..3] (cudaEvent_t, created by the caller; NULL entries skipped) on its stream
  * before the first kernel, after scoring, after selection and after attention, as external
- * records (valid inside CUDA-graph capture).  The bf16 path runs scoring+selection and
- * attention as two PDL-overlapped kernels and records only events[0] and events[3].
+ * records (valid inside CUDA-graph capture).  The bf16 path (S a multiple of 16) is ONE
+ * kernel (score + select + gather + attend) and records only events[0] and events[3].
  * events == NULL or n == 0 clears it.  Host-only. */
 void ts_profile_events(void *const *events, int32_t n);
 

@@ -10,8 +10,6 @@
 #include "../../include/tinyserve.h"
 #include "attn.cuh"
 #include "common.cuh"
-#include "decode_pipe.cuh"
-#include "fused_step.cuh"
 #include "step_cluster.cuh"
 #include "meta.cuh"
 #include "score.cuh"
@@ -26,7 +24,6 @@ namespace {
 thread_local int g_launches = 0;
 unsigned long long *g_dbg_ts = nullptr;  // development: attention CTA timestamps
 unsigned long long *g_dbg_ss = nullptr;  // development: score/select CTA timestamps
-volatile int *g_dbg_state = nullptr;     // development: live CTA state (host-mapped)
 thread_local cudaEvent_t g_phase_ev[4] = {nullptr, nullptr, nullptr, nullptr};
 
 // records phase event i on the stream (external record node when captured in a graph)
@@ -35,9 +32,6 @@ inline void phase_mark(int i, cudaStream_t st) {
 }
 
 constexpr int kMaxSel = 4096;      // max selected pages per row
-constexpr int kPipeNC = 6;         // consumer warps per pipeline CTA (+ TMA, scheduler, merge)
-constexpr int kPipeStages = 18;    // ring stages (4 KB each); a multiple of kPipeNC
-constexpr int kScoreChunkTiles = 32;  // metadata tiles (x 16 pages) per score item
 
 inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
@@ -147,7 +141,7 @@ bool make_pool_map(CUtensorMap *map, const void *pool, const ts_layout *L, int T
 
 // ---------------------------------------------------------------- workspace layout
 // attention workspace: [tickets: rows u32][work counters: 2 u32][partials: rows x ipr x 8 x kPS]
-// with ipr <= kMaxItemsPerRow items per row (decode_pipe.cuh).
+// with ipr <= kMaxItemsPerRow split parts per row (split-K merge of the attention kernels).
 constexpr int kMaxItemsPerRow = 64;
 struct AttnWs {
     size_t tickets, work, part, total;
@@ -166,13 +160,8 @@ AttnWs attn_ws_layout(const ts_layout *L, int sel_stride) {
 
 struct StepWs {
     AttnWs attn;
-    size_t scores, sel_ids, sel_count, sc_tickets, ready, cand_sc, cand_id, sel_blk, total;
+    size_t scores, sel_ids, sel_count, sel_blk, total;
 };
-// score items per row of the fused pipeline
-int score_chunks(const ts_layout *L) {
-    const int mtiles = (L->max_pages + 15) / 16;
-    return (mtiles + kScoreChunkTiles - 1) / kScoreChunkTiles;
-}
 StepWs step_ws_layout(const ts_layout *L, int kmax) {
     StepWs w;
     w.attn = attn_ws_layout(L, kmax);
@@ -180,22 +169,9 @@ StepWs step_ws_layout(const ts_layout *L, int kmax) {
     w.scores = w.attn.total;
     w.sel_ids = w.scores + round_up(rows * L->max_pages * 4, 256);
     w.sel_count = w.sel_ids + round_up(rows * kmax * 4, 256);
-    w.sc_tickets = w.sel_count + round_up(rows * 4, 256);
-    w.ready = w.sc_tickets + round_up(rows * 4, 256);
-    const size_t nc = rows * (size_t)score_chunks(L) * kmax;
-    w.cand_sc = w.ready + round_up(rows * 4, 256);
-    w.cand_id = w.cand_sc + round_up(nc * 4, 256);
-    w.sel_blk = w.cand_id + round_up(nc * 4, 256);
+    w.sel_blk = w.sel_count + round_up(rows * 4, 256);
     w.total = w.sel_blk + round_up(rows * kmax * 4, 256);
     return w;
-}
-
-// Persistent score/select + attention pair (one CTA per row at a time, rows pipelined) when
-// the rows alone fill two CTAs per SM; cluster-per-row kernels otherwise.
-bool persist_rows(const ts_layout *L) {
-    static const int env = getenv("TS_PERSIST") ? atoi(getenv("TS_PERSIST")) : -1;
-    if (env == 0) return false;
-    return (L->batch * L->num_kv_heads >= 2 * device_sms() || env == 1) && L->max_pages <= 1024;
 }
 
 // K = floor(budget / S) clipped to [1, max_pages] (reading R4/R5; P_b <= max_pages)
@@ -265,86 +241,6 @@ ts_status launch_select(const float *scores, int rows, int stride, const int *ro
     return launch_status();
 }
 
-// The persistent pipeline kernel (decode_pipe.cuh).  fused != nullptr: the whole decode
-// step (score items + attention items); otherwise attention only over a given selection.
-struct FusedArgs {
-    const void *meta;
-    unsigned *ready, *sc_tickets;
-    float *cand_sc;
-    int *cand_id, *sel_out, *cnt_out;
-    int kmax;
-};
-
-template <int TT, int STAGES>
-ts_status launch_pipe_s(const ts_layout *L, AttnParams &p, const void *k_pool, const void *v_pool,
-                        unsigned *work, const FusedArgs *fa, cudaStream_t st);
-
-template <int TT>
-ts_status launch_pipe(const ts_layout *L, AttnParams &p, const void *k_pool, const void *v_pool,
-                      unsigned *work, const FusedArgs *fa, cudaStream_t st) {
-    static const int stages = getenv("TS_PIPE_STAGES") ? atoi(getenv("TS_PIPE_STAGES")) : kPipeStages;
-    if (stages == 12) return launch_pipe_s<TT, 12>(L, p, k_pool, v_pool, work, fa, st);
-    if (stages == 24) return launch_pipe_s<TT, 24>(L, p, k_pool, v_pool, work, fa, st);
-    return launch_pipe_s<TT, kPipeStages>(L, p, k_pool, v_pool, work, fa, st);
-}
-
-template <int TT, int STAGES>
-ts_status launch_pipe_s(const ts_layout *L, AttnParams &p, const void *k_pool, const void *v_pool,
-                        unsigned *work, const FusedArgs *fa, cudaStream_t st) {
-    using SM = PipeSmem<kPipeNC, STAGES>;
-    auto kern = decode_pipe_kernel<TT, kPipeNC, STAGES>;
-    CUtensorMap tmK, tmV;
-    if (!make_pool_map(&tmK, k_pool, L, TT) || !make_pool_map(&tmV, v_pool, L, TT))
-        return TS_ERR_CUDA;
-    const int rows = L->batch * L->num_kv_heads;
-    PipeParams sp{};
-    sp.tpr = p.sel_stride * (L->page_size / TT);
-    long long is = std::min<long long>(sp.tpr, 32);
-    is = (is + kPipeNC - 1) / kPipeNC * kPipeNC;
-    sp.is = (int)std::max<long long>(is, 1);
-    sp.ipr = (sp.tpr + sp.is - 1) / sp.is;
-    if (sp.ipr > kMaxItemsPerRow) {  // long rows: grow items so the partials fit the workspace
-        sp.is = (sp.tpr + kMaxItemsPerRow - 1) / kMaxItemsPerRow;
-        sp.is = (sp.is + kPipeNC - 1) / kPipeNC * kPipeNC;
-        sp.ipr = (sp.tpr + sp.is - 1) / sp.is;
-    }
-    sp.n_attn = rows * sp.ipr;
-    if (fa) {
-        sp.meta = static_cast<const uint16_t *>(fa->meta);
-        sp.ready = fa->ready;
-        sp.sc_tickets = fa->sc_tickets;
-        sp.cand_sc = fa->cand_sc;
-        sp.cand_id = fa->cand_id;
-        sp.sel_out = fa->sel_out;
-        sp.cnt_out = fa->cnt_out;
-        sp.kmax = fa->kmax;
-        sp.mtiles = (L->max_pages + 15) / 16;
-        sp.sch = kScoreChunkTiles;
-        sp.spr = score_chunks(L);
-        if (sp.spr > 1 && sp.spr * sp.kmax > SM::kSelKeys) return TS_ERR_UNSUPPORTED;
-        sp.n_score = rows * sp.spr;
-    }
-    static const int per_sm = getenv("TS_PIPE_CTAS_PER_SM") ? atoi(getenv("TS_PIPE_CTAS_PER_SM")) : 2;
-    const int grid = std::max(1, std::min(sp.n_score + sp.n_attn, device_sms() * per_sm));
-    const size_t sm = SM::bytes();
-    static int sm_set = 0;  // opt-in grown on demand (dynamic + static <= 227 KB)
-    if ((int)sm > sm_set) {
-        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) !=
-            cudaSuccess)
-            return TS_ERR_CUDA;
-        sm_set = (int)sm;
-    }
-    sp.a = p;
-    sp.work = work;
-    static const int dbg = getenv("TS_DEBUG_ATTN") ? atoi(getenv("TS_DEBUG_ATTN")) : 0;
-    sp.dbg = dbg;
-    sp.dbg_ts = g_dbg_ts;
-    sp.dbg_state = g_dbg_state;
-    kern<<<grid, (kPipeNC + 3) * 32, sm, st>>>(tmK, tmV, sp);
-    ++g_launches;
-    return launch_status();
-}
-
 // bf16 sparse attention (sparse_attn.cuh): grid = rows x C CTAs, one cluster per row.
 // W warps per CTA: 4 when the rows alone fill the GPU (4 CTAs / SM), 8 otherwise, 16 for
 // very few rows; C = CTAs per row so that rows x C ~ one wave, each warp keeping >= 2
@@ -381,7 +277,7 @@ ts_status launch_sa(const AttnParams &p, int rows, int cdesired, bool pdl, cudaS
     if (s != TS_OK) return s;
     int C = std::max(1, cdesired);
     while (C > 1 && max_active_clusters(kern, W * 32, sm, C) < rows) --C;
-    if (nclusters <= 0) nclusters = rows;  // one row per cluster (else persistent over rows)
+    if (nclusters <= 0) nclusters = rows;  // one row per cluster
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(nclusters * C);
     cfg.blockDim = dim3(W * 32);
@@ -460,8 +356,7 @@ ts_status launch_sat(const ts_layout *L, const AttnParams &p, bool pdl, cudaStre
     return launch_status();
 }
 
-ts_status launch_sparse_attn(const ts_layout *L, const AttnParams &p, bool pdl, cudaStream_t st,
-                             bool persist = false) {
+ts_status launch_sparse_attn(const ts_layout *L, const AttnParams &p, bool pdl, cudaStream_t st) {
     const int rows = L->batch * L->num_kv_heads;
     const int sms = device_sms();
     static const int tma = getenv("TS_SA_TMA") ? atoi(getenv("TS_SA_TMA")) : 1;
@@ -471,8 +366,6 @@ ts_status launch_sparse_attn(const ts_layout *L, const AttnParams &p, bool pdl, 
         if (rr == 16) return launch_sat<4, 16>(L, p, pdl, st);
         return launch_sat<4, 8>(L, p, pdl, st);
     }
-    if (persist)  // co-resident with the persistent selector: 2 CTAs of 4 warps per SM
-        return launch_sa<4, 3>(p, rows, 1, pdl, st, std::min(rows, 2 * sms));
     const int n_oct = p.sel_stride * (L->page_size / 8);  // upper bound per row
     static const int cmax_env = getenv("TS_SA_CMAX") ? atoi(getenv("TS_SA_CMAX")) : 16;
     int W = rows >= 2 * sms ? 4 : (rows * 16 < sms ? 16 : 8);
@@ -543,78 +436,6 @@ ts_status launch_ss_t(ScoreSelParams &p, int rows, int cdesired, cudaStream_t st
     cfg.attrs = at;
     cfg.numAttrs = 2;
     if (cudaLaunchKernelEx(&cfg, kern, p) != cudaSuccess) return TS_ERR_CUDA;
-    ++g_launches;
-    return launch_status();
-}
-
-template <int W, int R, int KPL>
-ts_status launch_ssr_t(ScoreSelParams &p, int grid, bool pt_pref, cudaStream_t st) {
-    auto kern = score_select_rows_kernel<W, R, KPL>;
-    const size_t sm = SsrSmem<W, R>::bytes(p.max_pages, pt_pref);
-    if (sm > 227 * 1024) return TS_ERR_UNSUPPORTED;
-    {
-        static std::mutex mu;
-        static size_t sm_set = 0;
-        std::lock_guard<std::mutex> g(mu);
-        if (sm > sm_set) {
-            if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) !=
-                cudaSuccess)
-                return TS_ERR_CUDA;
-            sm_set = sm;
-        }
-    }
-    p.C = 1;
-    p.chunk = p.max_pages;
-    kern<<<grid, (W + 2) * 32, sm, st>>>(p, pt_pref ? 1 : 0);
-    ++g_launches;
-    return launch_status();
-}
-
-// One cooperative launch: NS selector CTAs + NA attention CTAs (fused_step.cuh).
-template <int W, int R1, int R2, int KPL>
-ts_status launch_fused_t(const ts_layout *L, ScoreSelParams &sp, const AttnParams &ap, bool pt_pref,
-                         cudaStream_t st) {
-    auto kern = decode_fused_kernel<W, R1, R2, KPL>;
-    const int rows = L->batch * L->num_kv_heads;
-    const size_t sm = 1024 + std::max(SsrSmem<W, R1>::bytes(L->max_pages, pt_pref),
-                                      AttnRoleSmem<W, R2>::bytes(ap.sel_stride));
-    if (sm > 227 * 1024) return TS_ERR_UNSUPPORTED;
-    {
-        static std::mutex mu;
-        static size_t sm_set = 0;
-        std::lock_guard<std::mutex> g(mu);
-        if (sm > sm_set) {
-            if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) !=
-                cudaSuccess)
-                return TS_ERR_CUDA;
-            sm_set = sm;
-        }
-    }
-    int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (W + 2) * 32, sm) != cudaSuccess ||
-        per_sm < 2)
-        return TS_ERR_UNSUPPORTED;
-    const int cap = per_sm * device_sms();
-    static const int ns_env = getenv("TS_FUSED_NS") ? atoi(getenv("TS_FUSED_NS")) : 0;
-    const int ns = std::min(rows, ns_env > 0 ? std::min(ns_env, cap - 1) : cap / 2);
-    const int na = std::min(rows, cap - ns);
-    CUtensorMap tmK, tmV;
-    if (!make_pool_map(&tmK, ap.k_pool, L, 16) || !make_pool_map(&tmV, ap.v_pool, L, 16))
-        return TS_ERR_CUDA;
-    sp.C = 1;
-    sp.chunk = L->max_pages;
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(ns + na);
-    cfg.blockDim = dim3((W + 2) * 32);
-    cfg.dynamicSmemBytes = sm;
-    cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident: the role spin-waits are safe
-    at[0].val.cooperative = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    if (cudaLaunchKernelEx(&cfg, kern, tmK, tmV, sp, ap, pt_pref ? 1 : 0, ns) != cudaSuccess)
-        return TS_ERR_CUDA;
     ++g_launches;
     return launch_status();
 }
@@ -694,7 +515,7 @@ ts_status launch_step_cluster_t(const ts_layout *L, ScoreSelParams &sp, const At
 }
 
 ts_status launch_score_select(const ts_layout *L, const void *q, const void *meta, const int *pt,
-                              const int *sl, int *ids, int *blk, int *cnt, int kmax, unsigned *ready,
+                              const int *sl, int *ids, int *blk, int *cnt, int kmax,
                               cudaStream_t st) {
     const int rows = L->batch * L->num_kv_heads;
     if (rows == 0) return TS_OK;
@@ -719,14 +540,6 @@ ts_status launch_score_select(const ts_layout *L, const void *q, const void *met
     const int target = device_sms() * per_sm;
     const int max_c = std::max(1, std::min(cmax, (L->max_pages + 63) / 64));  // >= 64 pages per CTA
     const int C = std::max(1, std::min(max_c, (target + rows - 1) / rows));
-    p.ready = ready;
-    if (persist_rows(L) && ready) {  // many rows: persistent CTAs, selection hidden behind the stream
-        const bool pt_pref = (L->max_pages & 3) == 0;
-        const int grid = std::min(rows, 2 * device_sms());
-        if (L->max_pages <= 256) return launch_ssr_t<4, 4, 8>(p, grid, pt_pref, st);
-        if (L->max_pages <= 512) return launch_ssr_t<4, 4, 16>(p, grid, pt_pref, st);
-        return launch_ssr_t<4, 4, 32>(p, grid, pt_pref, st);
-    }
     return launch_ss_t<4, 4>(p, rows, C, st);
 }
 
@@ -767,20 +580,14 @@ AttnParams attn_params(const ts_layout *L, const void *q, const void *k_pool, co
 
 ts_status launch_attn(const ts_layout *L, const void *q, const void *k_pool, const void *v_pool,
                       const int *pt, const int *sl, const int *sel_ids, const int *sel_count,
-                      int sel_stride, float scale, float *o, float *lse, void *ws, cudaStream_t st,
-                      const FusedArgs *fa = nullptr) {
+                      int sel_stride, float scale, float *o, float *lse, void *ws, cudaStream_t st) {
     const int rows = L->batch * L->num_kv_heads;
     if (rows == 0) return TS_OK;
-    const AttnWs w = attn_ws_layout(L, sel_stride);
     AttnParams p = attn_params(L, q, k_pool, v_pool, pt, sl, sel_ids, sel_count, sel_stride, scale,
                                o, lse, ws);
     if (L->kv_dtype == TS_BF16) {
         if (!bf16_attn_supported(L) || sel_stride > kMaxSel) return TS_ERR_UNSUPPORTED;
-        static const bool use_pipe = getenv("TS_ATTN_PIPE") && atoi(getenv("TS_ATTN_PIPE"));
-        if (!fa && !use_pipe) return launch_sparse_attn(L, p, false, st);
-        unsigned *work = reinterpret_cast<unsigned *>(static_cast<char *>(ws) + w.work);
-        if (L->page_size >= 16) return launch_pipe<16>(L, p, k_pool, v_pool, work, fa, st);
-        return launch_pipe<8>(L, p, k_pool, v_pool, work, fa, st);
+        return launch_sparse_attn(L, p, false, st);
     }
     const int threads = 32 * std::min(p.G, 8);
     if (L->head_dim == 64)
@@ -816,7 +623,6 @@ int32_t ts_last_launch_count(void) { return g_launches; }
 // development hook (not in the public header): device buffer for attention CTA timestamps
 void ts_debug_timestamps(void *buf) { g_dbg_ts = static_cast<unsigned long long *>(buf); }
 void ts_debug_ss_timestamps(void *buf) { g_dbg_ss = static_cast<unsigned long long *>(buf); }
-void ts_debug_state(void *buf) { g_dbg_state = static_cast<volatile int *>(buf); }
 
 void ts_profile_events(void *const *events, int32_t n) {
     for (int i = 0; i < 4; ++i)
@@ -941,65 +747,6 @@ ts_status ts_decode_step(const ts_layout *L, const void *q, const void *k_pool, 
     int *cnt = sel_count_out ? sel_count_out : reinterpret_cast<int *>(wb + w.sel_count);
     const cudaStream_t st = as_stream(stream);
     const int rows = L->batch * L->num_kv_heads;
-    static const bool use_pipe = getenv("TS_STEP_PIPE") && atoi(getenv("TS_STEP_PIPE"));
-    if (L->kv_dtype == TS_BF16 && group_of(L) <= 8 && L->head_dim == 64 && use_pipe) {
-        // the whole step as one persistent pipeline kernel (decode_pipe.cuh)
-        FusedArgs fa{meta,
-                     reinterpret_cast<unsigned *>(wb + w.ready),
-                     reinterpret_cast<unsigned *>(wb + w.sc_tickets),
-                     reinterpret_cast<float *>(wb + w.cand_sc),
-                     reinterpret_cast<int *>(wb + w.cand_id),
-                     ids, cnt, kmax};
-        phase_mark(0, st);
-        if (rows > 0 &&
-            (s = launch_attn(L, q, k_pool, v_pool, page_table, seq_lens, ids, cnt, kmax, scale, o,
-                             lse, ws, st, &fa)) != TS_OK)
-            return s;
-        phase_mark(3, st);
-        return TS_OK;
-    }
-    static const bool fused_ok = getenv("TS_FUSED") && atoi(getenv("TS_FUSED"));
-    if (L->kv_dtype == TS_BF16 && group_of(L) <= 8 && L->head_dim == 64 && fused_ok &&
-        persist_rows(L) && L->page_size % 16 == 0 && rows > 0) {
-        // one cooperative launch: selector CTAs + attention CTAs (fused_step.cuh)
-        ScoreSelParams sp{};
-        sp.q = static_cast<const uint16_t *>(q);
-        sp.meta = static_cast<const uint16_t *>(meta);
-        sp.page_table = page_table;
-        sp.seq_lens = seq_lens;
-        sp.sel_ids = ids;
-        sp.sel_blk = reinterpret_cast<int *>(wb + w.sel_blk);
-        sp.sel_count = cnt;
-        sp.B = L->batch;
-        sp.Hq = L->num_q_heads;
-        sp.Hkv = L->num_kv_heads;
-        sp.G = group_of(L);
-        sp.S = L->page_size;
-        sp.max_pages = L->max_pages;
-        sp.kmax = kmax;
-        sp.ready = reinterpret_cast<unsigned *>(wb + w.ready);
-        sp.dbg = g_dbg_ss;
-        AttnParams ap = attn_params(L, q, k_pool, v_pool, page_table, seq_lens, ids, cnt, kmax, scale,
-                                    o, lse, ws);
-        ap.sel_blk = sp.sel_blk;
-        ap.ready = sp.ready;
-        const bool pt_pref = (L->max_pages & 3) == 0;
-        phase_mark(0, st);
-        static const int r2 = getenv("TS_FUSED_R2") ? atoi(getenv("TS_FUSED_R2")) : 16;
-        if (L->max_pages <= 256)
-            s = r2 == 8 ? launch_fused_t<4, 4, 8, 8>(L, sp, ap, pt_pref, st)
-                        : (r2 == 24 ? launch_fused_t<4, 4, 24, 8>(L, sp, ap, pt_pref, st)
-                                    : launch_fused_t<4, 4, 16, 8>(L, sp, ap, pt_pref, st));
-        else if (L->max_pages <= 512)
-            s = launch_fused_t<4, 4, 16, 16>(L, sp, ap, pt_pref, st);
-        else
-            s = launch_fused_t<4, 4, 16, 32>(L, sp, ap, pt_pref, st);
-        phase_mark(3, st);
-        if (s != TS_ERR_UNSUPPORTED) {
-            g_launches = 1;
-            return s;
-        }
-    }
     static const int two_kernels = getenv("TS_TWO_KERNELS") ? atoi(getenv("TS_TWO_KERNELS")) : 0;
     if (L->kv_dtype == TS_BF16 && group_of(L) <= 8 && L->head_dim == 64 && !two_kernels &&
         L->page_size % 16 == 0 && rows > 0) {
@@ -1019,7 +766,6 @@ ts_status ts_decode_step(const ts_layout *L, const void *q, const void *k_pool, 
         sp.S = L->page_size;
         sp.max_pages = L->max_pages;
         sp.kmax = kmax;
-        sp.ready = nullptr;
         sp.dbg = g_dbg_ss;
         AttnParams ap = attn_params(L, q, k_pool, v_pool, page_table, seq_lens, ids, cnt, kmax, scale,
                                     o, lse, ws);
@@ -1034,13 +780,9 @@ ts_status ts_decode_step(const ts_layout *L, const void *q, const void *k_pool, 
     if (L->kv_dtype == TS_BF16 && group_of(L) <= 8 && L->head_dim == 64) {
         // score + select (cluster per row) -> sparse attention (PDL, blocks pre-resolved)
         int *blk = reinterpret_cast<int *>(wb + w.sel_blk);
-        // per-row flags (attention starts on a row as soon as it is selected) measured slower
-        // than the plain PDL grid dependency on every config: opt-in only
-        static const bool flags = getenv("TS_FLAGS") && atoi(getenv("TS_FLAGS"));
-        unsigned *ready = flags ? reinterpret_cast<unsigned *>(wb + w.ready) : nullptr;
         phase_mark(0, st);
-        if ((s = launch_score_select(L, q, meta, page_table, seq_lens, ids, blk, cnt, kmax, ready,
-                                     st)) != TS_OK)
+        if ((s = launch_score_select(L, q, meta, page_table, seq_lens, ids, blk, cnt, kmax, st)) !=
+            TS_OK)
             return s;
         phase_mark(1, st);
         phase_mark(2, st);
@@ -1048,9 +790,8 @@ ts_status ts_decode_step(const ts_layout *L, const void *q, const void *k_pool, 
             AttnParams p = attn_params(L, q, k_pool, v_pool, page_table, seq_lens, ids, cnt, kmax,
                                        scale, o, lse, ws);
             p.sel_blk = blk;
-            p.ready = ready;
             static const bool pdl = !getenv("TS_NO_PDL");
-            if ((s = launch_sparse_attn(L, p, pdl, st, persist_rows(L) && ready)) != TS_OK) return s;
+            if ((s = launch_sparse_attn(L, p, pdl, st)) != TS_OK) return s;
         }
         phase_mark(3, st);
         g_launches = rows > 0 ? 2 : 1;

@@ -26,7 +26,6 @@ struct AttnParams {
     const int *sel_ids;
     const int *sel_count;
     const int *sel_blk;  // nullable: physical block of each selected page (fused step)
-    unsigned *ready;     // nullable: per-row selection flags (fused step; reset after use)
     int sel_stride;
     int B, Hq, Hkv, G, D, S, max_pages, stride, offset, num_blocks;
     float scale;       // softmax scale (reading R1)

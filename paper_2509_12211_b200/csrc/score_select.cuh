@@ -23,7 +23,6 @@
 
 #include "attn.cuh"
 #include "common.cuh"
-#include "warp_select.cuh"
 
 namespace ts {
 
@@ -37,7 +36,6 @@ struct ScoreSelParams {
     int *sel_blk;             // [rows][kmax] physical block of each selected page
     int *sel_count;           // [rows]
     int B, Hq, Hkv, G, S, max_pages, kmax;
-    unsigned *ready;          // [rows] set to 1 once the row's selection is written (nullable)
     int flags;                // step_cluster: bit 0 page-table prefetch, bit 1 two-level select
     int C;                    // CTAs per row (cluster size)
     int chunk;                // pages per CTA (multiple of 32)
@@ -533,235 +531,6 @@ __global__ void __launch_bounds__((W + 1) * 32) score_select_kernel(ScoreSelPara
     }
     if (tid == 0) p.sel_count[row] = kk;
     SS_STAMP(3);
-    if (p.ready) {  // release the row to the attention kernel
-        __syncthreads();
-        if (tid == 0) {
-            __threadfence();
-            st_release_u32(p.ready + row, 1u);
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------------------
-// Persistent variant for many rows (rows >= CTAs): CTA x scores and selects rows x,
-// x + grid, ...  Three roles run concurrently:
-//  * producer warp: per row the q group, the page-table row and the metadata stages (ring),
-//    running ahead through the rows;
-//  * W consumer warps: Eq. 2 per stage, scores into a double-buffered score row, then on to
-//    the next row at once;
-//  * select warp: takes a finished score row into registers (frees the buffer), exact
-//    warp_select (barrier-free), writes ids / blocks / count, releases the row's flag.
-// So a row's selection overlaps the next row's metadata stream.  P <= 32 * KPL.
-template <int W, int R>
-struct SsrSmem {
-    static constexpr int kRing = 0;                                 // R x 8 KB
-    static constexpr int kQ = kRing + R * kSsStageBytes;           // [2][8][64] bf16
-    static constexpr int kHist = kQ + 2 * 8 * kRowBytes;            // [256] int (select warp)
-    static constexpr int kBars = kHist + kWsBins * 4;               // full, empty [R]; 6 x [2]
-    static constexpr int kScores = (kBars + (2 * R + 12) * 8 + 127) / 128 * 128;
-    static int pad4(int n) { return (n + 3) & ~3; }
-    static size_t bytes(int max_pages, bool pt) {
-        return kScores + (size_t)2 * pad4(max_pages) * 4 + (pt ? (size_t)2 * pad4(max_pages) * 4 : 0) + 16;
-    }
-};
-
-template <int W, int R, int KPL>
-TS_DEV void score_select_role(const ScoreSelParams &p, int pt_pref, int unit, int nunits,
-                              uint8_t *smem) {
-    static_assert(R % W == 0, "ring stages must map to fixed consumer warps");
-    using SM = SsrSmem<W, R>;
-    const uint32_t sb = smem_u32(smem);
-    const uint32_t full0 = sb + SM::kBars, empty0 = full0 + 8 * R;
-    const uint32_t qfull0 = empty0 + 8 * R, qempty0 = qfull0 + 16;
-    const uint32_t ptfull0 = qempty0 + 16, ptempty0 = ptfull0 + 16;
-    const uint32_t sready0 = ptempty0 + 16, sfree0 = sready0 + 16;
-    const int mp4 = (p.max_pages + 3) & ~3;
-    float *sc = reinterpret_cast<float *>(smem + SM::kScores);       // [2][mp4]
-    int *pt_s = reinterpret_cast<int *>(smem + SM::kScores) + 2 * mp4;  // [2][mp4]
-    int *hist = reinterpret_cast<int *>(smem + SM::kHist);
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int rows = p.B * p.Hkv;
-    unsigned long long *dts = p.dbg && unit < 4096 ? p.dbg + unit * 8 : nullptr;
-    if (dts && tid == 0) dts[0] = globaltimer();
-    pdl_launch_dependents();
-    if (tid == 0) {
-        for (int i = 0; i < R; ++i) {
-            mbar_init(full0 + 8 * i, 1);
-            mbar_init(empty0 + 8 * i, 1);
-        }
-        for (int i = 0; i < 2; ++i) {
-            mbar_init(qfull0 + 8 * i, 1);
-            mbar_init(qempty0 + 8 * i, W);
-            mbar_init(ptfull0 + 8 * i, 1);
-            mbar_init(ptempty0 + 8 * i, 1);
-            mbar_init(sready0 + 8 * i, W);
-            mbar_init(sfree0 + 8 * i, 1);
-        }
-        fence_mbar_init();
-    }
-    __syncthreads();
-
-    if (warp == W) {
-        // ================================ producer ================================
-        if (lane == 0) {
-            const uint64_t pol = l2_policy_evict_first();
-            int gs = 0;
-            for (int it = 0;; ++it) {
-                const int row = unit + it * nunits;
-                if (row >= rows) break;
-                const int b = row / p.Hkv, g = row % p.Hkv;
-                const int P = (p.seq_lens[b] + p.S - 1) / p.S;
-                const int nst = (P + kSsStagePages - 1) / kSsStagePages;
-                const int qs = it & 1, qpar = ((it >> 1) & 1) ^ 1;
-                mbar_wait(qempty0 + 8 * qs, qpar);
-                mbar_arrive_expect_tx(qfull0 + 8 * qs, p.G * kRowBytes);
-                bulk_load(sb + SM::kQ + qs * 8 * kRowBytes,
-                          p.q + ((size_t)b * p.Hq + g * p.G) * kAttnD, p.G * kRowBytes, qfull0 + 8 * qs);
-                if (pt_pref) {
-                    mbar_wait(ptempty0 + 8 * qs, qpar);
-                    const uint32_t ptb = min(((uint32_t)P * 4 + 15) & ~15u, (uint32_t)mp4 * 4);
-                    if (P > 0) {
-                        mbar_arrive_expect_tx(ptfull0 + 8 * qs, ptb);
-                        bulk_load(smem_u32(pt_s + qs * mp4), p.page_table + (size_t)b * p.max_pages,
-                                  ptb, ptfull0 + 8 * qs);
-                    } else {
-                        mbar_arrive(ptfull0 + 8 * qs);
-                    }
-                }
-                const uint16_t *mrow = p.meta + (size_t)row * p.max_pages * 2 * kAttnD;
-                for (int i = 0; i < nst; ++i, ++gs) {
-                    const int st = gs % R;
-                    mbar_wait(empty0 + 8 * st, ((gs / R) & 1) ^ 1);
-                    const int np = min(kSsStagePages, P - i * kSsStagePages);
-                    const uint32_t bytes = np * 2 * kRowBytes;
-                    mbar_arrive_expect_tx(full0 + 8 * st, bytes);
-                    bulk_load_hint(sb + st * kSsStageBytes,
-                                   mrow + (size_t)i * kSsStagePages * 2 * kAttnD, bytes,
-                                   full0 + 8 * st, pol);
-                }
-            }
-        }
-        return;
-    }
-
-    if (warp == W + 1) {
-        // ================================ selector ================================
-        for (int it = 0;; ++it) {
-            const int row = unit + it * nunits;
-            if (row >= rows) break;
-            const int b = row / p.Hkv;
-            const int P = (p.seq_lens[b] + p.S - 1) / p.S;
-            const int qs = it & 1, qpar = (it >> 1) & 1;
-            mbar_wait(sready0 + 8 * qs, qpar);
-            const float *row_sc = sc + qs * mp4;
-            uint32_t key[KPL];
-#pragma unroll
-            for (int j = 0; j < KPL; ++j) {
-                const int i = 32 * j + lane;
-                key[j] = i < P ? score_key(row_sc[i]) : 0u;
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(sfree0 + 8 * qs);  // the score buffer may be refilled
-            if (pt_pref) mbar_wait(ptfull0 + 8 * qs, qpar);
-            const int *ptrow = pt_pref ? pt_s + qs * mp4 : p.page_table + (size_t)b * p.max_pages;
-            int *out_id = p.sel_ids + (size_t)row * p.kmax;
-            int *out_blk = p.sel_blk + (size_t)row * p.kmax;
-            const int kk = warp_select<KPL>(key, p.kmax, hist, [&](int pos, int i) {
-                out_id[pos] = i;
-                out_blk[pos] = ptrow[i];
-            });
-            for (int i = kk + lane; i < p.kmax; i += 32) {
-                out_id[i] = -1;
-                out_blk[i] = 0;
-            }
-            if (lane == 0) p.sel_count[row] = kk;
-            __syncwarp();
-            if (lane == 0) {
-                if (pt_pref) mbar_arrive(ptempty0 + 8 * qs);
-                if (p.ready) {
-                    __threadfence();
-                    st_release_u32(p.ready + row, 1u);
-                }
-                if (dts && it == 0) dts[3] = globaltimer();
-            }
-        }
-        return;
-    }
-
-    // ================================ consumers ===============================
-    const int gid = lane >> 2, t = lane & 3;
-    const bool c0 = 2 * t < p.G, c1 = 2 * t + 1 < p.G;
-    int gs = 0;
-    for (int it = 0;; ++it) {
-        const int row = unit + it * nunits;
-        if (row >= rows) break;
-        const int b = row / p.Hkv;
-        const int P = (p.seq_lens[b] + p.S - 1) / p.S;
-        const int nst = (P + kSsStagePages - 1) / kSsStagePages;
-        const int qs = it & 1, qpar = (it >> 1) & 1;
-        mbar_wait(qfull0 + 8 * qs, qpar);
-        uint32_t qa[8], qp[8];  // [q^- ; q^+] coefficients of head gid
-        {
-            const bool live = gid < p.G;
-            const uint32_t qrow = sb + SM::kQ + qs * 8 * kRowBytes + gid * kRowBytes;
-            const uint4 x0 = live ? lds_v4(qrow + 16 * t) : make_uint4(0, 0, 0, 0);
-            const uint4 x1 = live ? lds_v4(qrow + 16 * (t + 4)) : make_uint4(0, 0, 0, 0);
-            const uint32_t w0[4] = {x0.x, x0.y, x0.z, x0.w}, w1[4] = {x1.x, x1.y, x1.z, x1.w};
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                qa[e] = bf16x2_min0(w0[e]);
-                qa[4 + e] = bf16x2_min0(w1[e]);
-                qp[e] = bf16x2_max0(w0[e]);
-                qp[4 + e] = bf16x2_max0(w1[e]);
-            }
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(qempty0 + 8 * qs);
-        mbar_wait(sfree0 + 8 * qs, qpar ^ 1);  // the selector has taken row it - 2's scores
-        float *row_sc = sc + qs * mp4;
-        // global stage gs + i belongs to warp (gs + i) % W: with R % W == 0 every use of a
-        // ring stage is waited on by the same warp (no mbarrier parity aliasing across rows)
-        for (int i = (warp - gs % W + W) % W; i < nst; i += W) {
-            const int st = (gs + i) % R;
-            mbar_wait(full0 + 8 * st, ((gs + i) / R) & 1);
-            const uint32_t kb = sb + st * kSsStageBytes;
-#pragma unroll
-            for (int tile = 0; tile < 2; ++tile) {
-                const uint32_t tb = kb + tile * 16 * 2 * kRowBytes;
-                float acc[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-                for (int ci = 0; ci < 4; ++ci) {
-                    const uint4 a = lds_v4(tb + gid * 2 * kRowBytes + 16 * (t + 4 * ci));
-                    const uint4 h = lds_v4(tb + (gid + 8) * 2 * kRowBytes + 16 * (t + 4 * ci));
-                    const uint32_t *cf = ci < 2 ? qa + 4 * ci : qp + 4 * (ci - 2);
-                    mma_bf16_16816(acc, a.x, h.x, a.y, h.y, cf[0], cf[1]);
-                    mma_bf16_16816(acc, a.z, h.z, a.w, h.w, cf[2], cf[3]);
-                }
-                float m0 = fmaxf(c0 ? acc[0] : kNegInf, c1 ? acc[1] : kNegInf);
-                float m1 = fmaxf(c0 ? acc[2] : kNegInf, c1 ? acc[3] : kNegInf);
-                m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, 1));
-                m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, 2));
-                m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, 1));
-                m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, 2));
-                if (t < 2) {
-                    const int pg = i * kSsStagePages + tile * 16 + gid + 8 * t;
-                    if (pg < P) row_sc[pg] = (t ? m1 : m0) + 0.0f;
-                }
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(empty0 + 8 * st);
-        }
-        gs += nst;
-        __syncwarp();
-        if (lane == 0) mbar_arrive(sready0 + 8 * qs);  // release + arrive: this warp's scores
-        if (dts && tid == 0 && it == 0) dts[1] = globaltimer();
-    }
-}
-
-template <int W, int R, int KPL>
-__global__ void __launch_bounds__((W + 2) * 32) score_select_rows_kernel(ScoreSelParams p, int pt_pref) {
-    extern __shared__ __align__(128) uint8_t ssr_smem[];
-    score_select_role<W, R, KPL>(p, pt_pref, blockIdx.x, gridDim.x, ssr_smem);
 }
 
 }  // namespace ts

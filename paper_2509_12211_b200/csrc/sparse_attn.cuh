@@ -77,17 +77,7 @@ __global__ void __launch_bounds__(W * 32, 512 / (W * 32)) sparse_attn_kernel(Att
         qa[4] = x1.x; qa[5] = x1.y; qa[6] = x1.z; qa[7] = x1.w;
     }
     if (dts && threadIdx.x == 0) dts[1] = globaltimer() + (qa[0] & 0u);  // q arrived
-    // the selection is produced by the previous kernel (fused step): either wait for this
-    // row's flag (released by the selector as soon as the row is done) or for the grid
-    if (p.ready) {
-        if (threadIdx.x == 0) {
-            while (ld_relaxed_u32(p.ready + row) == 0u) nanosleep_ns(64);
-            fence_acquire_gpu();
-        }
-        __syncthreads();
-    } else {
-        pdl_wait();
-    }
+    pdl_wait();  // the selection may come from the previous kernel (two-kernel step)
 
     // ---- owned selected pages of the row -> (block base, first token), in id order
     const int cnt = __ldcg(p.sel_count + row);
@@ -280,7 +270,6 @@ __global__ void __launch_bounds__(W * 32, 512 / (W * 32)) sparse_attn_kernel(Att
     }
     SA_STAMP(6);
     if (C > 1) cl.sync(); else __syncthreads();  // partials / page lists free for the next row
-    if (p.ready && rank == 0 && threadIdx.x == 0) p.ready[row] = 0u;  // every CTA of the row is past its wait
     SA_STAMP(7);
     }  // row loop
 }
@@ -348,15 +337,8 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) sparse_attn_tma_kernel(
         qa[0] = x0.x; qa[1] = x0.y; qa[2] = x0.z; qa[3] = x0.w;
         qa[4] = x1.x; qa[5] = x1.y; qa[6] = x1.z; qa[7] = x1.w;
     }
-    // ---- wait for the selection, then the owned selected pages (producer warp)
-    if (p.ready) {
-        if (threadIdx.x == 0) {
-            while (ld_relaxed_u32(p.ready + row) == 0u) nanosleep_ns(64);
-            fence_acquire_gpu();
-        }
-    } else {
-        pdl_wait();
-    }
+    // ---- wait for the selection (PDL), then resolve the pages this CTA attends
+    pdl_wait();
     __syncthreads();
     if (dts && threadIdx.x == 0) dts[1] = globaltimer();
     if (p.dense) {
@@ -398,7 +380,6 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) sparse_attn_tma_kernel(
         if (lane == 0) s_nown = n;
     }
     __syncthreads();
-    if (p.ready && threadIdx.x == 0 && C == 1) p.ready[row] = 0u;
     const int tpp = p.S >> 4;                 // tiles per page
     const int ntile = s_nown * tpp;
     const int t0 = (int)((long long)ntile * rank / C), t1 = (int)((long long)ntile * (rank + 1) / C);
@@ -601,10 +582,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) sparse_attn_tma_kernel(
                     make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
                 if (p.lse && d0 == 0) p.lse[oh] = l > 0.f ? (M + log2f(l)) * kLn2 : kNegInf;
             }
-            if (threadIdx.x == 0) {
-                p.tickets[row] = 0u;  // re-armed for the next launch
-                if (p.ready) p.ready[row] = 0u;
-            }
+            if (threadIdx.x == 0) p.tickets[row] = 0u;  // re-armed for the next launch
         }
     }
     if (dts && threadIdx.x == 0) dts[7] = globaltimer();

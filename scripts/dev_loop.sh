@@ -10,5 +10,5 @@ if [ "${TESTS:-1}" = 1 ]; then
 fi
 for c in ${CFGS:-c2 c3}; do
   timeout 300 python scripts/kbench.py $c 200 2>&1 | tee $OUT/kb_${c}_$TAG.txt
-  timeout 300 python scripts/tstamps.py $c step > $OUT/ts_${c}_$TAG.txt 2>&1; head -11 $OUT/ts_${c}_$TAG.txt
+  timeout 300 python scripts/step_stamps.py $c > $OUT/ts_${c}_$TAG.txt 2>&1; head -11 $OUT/ts_${c}_$TAG.txt
 done
