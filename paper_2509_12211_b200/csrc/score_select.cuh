@@ -194,43 +194,54 @@ TS_DEV int cta_topk(const uint32_t *keys, int n, int k, uint32_t kmin, uint32_t 
                 sel_sync<NT, BAR>();
             }
             TS_TOPK_PROF(1);
-            if (warp == 0) {  // boundary bin: lane owns bins [64 lane, +64), scanned from the top
-                constexpr int PB = (1 << HB) / 32;  // bins per lane
-                const int4 *h4 = reinterpret_cast<const int4 *>(hist) + lane * (PB / 4);
-                int c[PB];
+            {  // boundary bin: thread t < TT owns bins [16 t, 16 t + 16); block suffix scan
+                constexpr int PB = 16, TT = (1 << HB) / PB, TW = (TT + 31) / 32;
+                static_assert(TT <= NT, "bin search needs (1 << HB) / 16 threads");
+                int c[PB], sm = 0, suf = 0;
+                if (warp < TW) {
+                    if (tid < TT) {
+                        const int4 *h4 = reinterpret_cast<const int4 *>(hist) + tid * (PB / 4);
 #pragma unroll
-                for (int j = 0; j < PB / 4; ++j) {
-                    const int4 v = h4[j];
-                    c[4 * j] = v.x; c[4 * j + 1] = v.y; c[4 * j + 2] = v.z; c[4 * j + 3] = v.w;
-                }
-                int s = 0;
-#pragma unroll
-                for (int j = 0; j < PB; ++j) s += c[j];
-                int suf = s;  // inclusive suffix over lanes >= lane
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int y = __shfl_down_sync(0xffffffffu, suf, o);
-                    if (lane + o < 32) suf += y;
-                }
-                const int above_run = suf - s;
-                if (above_run < rem && suf >= rem) {  // exactly one lane
-                    int acc = above_run, bsel = 0, cb = 0, ab = 0;
-                    bool done = false;
-#pragma unroll
-                    for (int j = PB - 1; j >= 0; --j) {
-                        if (!done && acc + c[j] >= rem) {
-                            bsel = j;
-                            cb = c[j];
-                            ab = acc;
-                            done = true;
+                        for (int j = 0; j < PB / 4; ++j) {
+                            const int4 v = h4[j];
+                            c[4 * j] = v.x; c[4 * j + 1] = v.y; c[4 * j + 2] = v.z; c[4 * j + 3] = v.w;
                         }
-                        acc += c[j];
+                        sm = ((c[0] + c[1]) + (c[2] + c[3])) + ((c[4] + c[5]) + (c[6] + c[7])) +
+                             ((c[8] + c[9]) + (c[10] + c[11])) + ((c[12] + c[13]) + (c[14] + c[15]));
                     }
-                    red[48] = lane * PB + bsel;
-                    red[49] = ab;
-                    red[50] = cb;
+                    suf = sm;  // inclusive suffix over the lanes >= lane of this warp
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int y = __shfl_down_sync(0xffffffffu, suf, o);
+                        if (lane + o < 32) suf += y;
+                    }
+                    if (lane == 0) red[40 + warp] = suf;  // warp total
                 }
-                if (lane == 0) red[51] = 0;  // candidate counter
+                sel_sync<NT, BAR>();
+                if (tid < TT) {
+#pragma unroll
+                    for (int w = 0; w < TW; ++w)
+                        if (w > warp) suf += red[40 + w];
+                    const int above_run = suf - sm;
+                    if (above_run < rem && suf >= rem) {  // exactly one thread
+                        int acc = above_run, bsel = 0, cb = 0, ab = 0;
+                        bool done = false;
+#pragma unroll
+                        for (int j = PB - 1; j >= 0; --j) {
+                            if (!done && acc + c[j] >= rem) {
+                                bsel = j;
+                                cb = c[j];
+                                ab = acc;
+                                done = true;
+                            }
+                            acc += c[j];
+                        }
+                        red[48] = tid * PB + bsel;
+                        red[49] = ab;
+                        red[50] = cb;
+                    }
+                }
+                if (tid == 0) red[51] = 0;  // candidate counter
             }
             sel_sync<NT, BAR>();
             if (dts && tid == 0 && pass == 0) dts[5] = globaltimer();
