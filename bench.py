@@ -267,11 +267,18 @@ def main():
         return
 
     import paper_2509_12211_b200 as ts
+    # TS_BENCH_BACKEND=gloo (testing only): exercise the multi-rank path with several ranks
+    # sharing the visible GPUs; the driver's runs use NCCL, one rank per GPU
+    backend = os.environ.get("TS_BENCH_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count()) if backend != "nccl" else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     props = torch.cuda.get_device_properties(dev)
     l2 = getattr(props, "L2_cache_size", 126 * 2**20) or 126 * 2**20
