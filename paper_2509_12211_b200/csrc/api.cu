@@ -494,6 +494,10 @@ ts_status launch_step_cluster_t(const ts_layout *L, ScoreSelParams &sp, const At
     sp.chunk = chunk;
     if (two_ok && C > 1 && (C * sp.kmax) % 4 == 0 && (two_env == 1 || L->max_pages >= 4 * C * sp.kmax))
         sp.flags |= 2;
+    // early PDL trigger (the next kernel's prologue overlaps our tail): measured faster with
+    // clusters of <= 8 CTAs (C2 / C3 / C4), slower with C5's 13-CTA clusters
+    static const int trig_env = getenv("TS_SC_TRIGGER") ? atoi(getenv("TS_SC_TRIGGER")) : -1;
+    if (trig_env == 1 || (trig_env != 0 && C <= 8)) sp.flags |= 8;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(rows * C);
     cfg.blockDim = dim3((W + 1) * 32);

@@ -82,6 +82,9 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
 #define SC_STAMP(e) \
     if (dts && tid == 0) dts[e] = globaltimer();
     SC_STAMP(0);
+    // the next kernel in the stream (the next layer / step) may be scheduled as our CTAs
+    // retire: its prologue overlaps our tail; it waits for our completion before any read
+    if (p.flags & 8) pdl_launch_dependents();  // (host: measured faster up to 8-CTA clusters)
     if (tid == 0) {
         prefetch_tmap(&tmK);
         prefetch_tmap(&tmV);
