@@ -451,49 +451,69 @@ ts_status launch_step_cluster_t(const ts_layout *L, ScoreSelParams &sp, const At
     sp.flags = ((L->max_pages & 3) == 0 && L->max_pages <= 2048) ? 1 : 0;
     static const int two_env = getenv("TS_SC_TWO") ? atoi(getenv("TS_SC_TWO")) : -1;
     const bool two_ok = two_env == 1 || (two_env != 0 && L->max_pages > 2048);  // long rows only
-    const size_t sm = 1024 + ScSmem<W, R>::bytes(sp.kmax, L->max_pages, sp.flags | (two_ok ? 2 : 0), 16);
-    if (sm > 227 * 1024) return TS_ERR_UNSUPPORTED;
-    {
-        static std::mutex mu;
-        static size_t sm_set = 0;
-        static bool np_set = false;
+    static std::mutex mu;
+    static size_t sm_set = 0;
+    static bool np_set = false;
+    auto allow = [&](size_t smb) -> bool {  // grow the opt-in shared memory on demand
         std::lock_guard<std::mutex> g(mu);
-        if (sm > sm_set) {
-            if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) !=
-                cudaSuccess)
-                return TS_ERR_CUDA;
-            sm_set = sm;
-        }
         if (!np_set) {
             if (cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
                 cudaSuccess)
-                return TS_ERR_CUDA;
+                return false;
             np_set = true;
+        }
+        if (smb > sm_set) {
+            if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb) !=
+                cudaSuccess)
+                return false;
+            sm_set = smb;
+        }
+        return true;
+    };
+    static const int cmax = getenv("TS_SC_CMAX") ? atoi(getenv("TS_SC_CMAX")) : 16;
+    const int max_c = std::max(1, std::min(cmax, (L->max_pages + 63) / 64));  // >= 64 pages per CTA
+    auto chunk_of = [&](int c) {
+        int ch = (L->max_pages + c - 1) / c;
+        return (ch + kSsStagePages - 1) / kSsStagePages * kSsStagePages;
+    };
+    int C = 0, chunk = 0;
+    size_t sm = 0;
+    if (two_ok) {  // two-level select: every CTA keeps only its chunk's scores
+        for (int c = max_c; c >= 2; --c) {
+            const int ch = chunk_of(c), cc = (L->max_pages + ch - 1) / ch;
+            if ((cc * sp.kmax) % 4 != 0 || (two_env != 1 && L->max_pages < 4 * cc * sp.kmax)) continue;
+            const size_t smc = 1024 + ScSmem<W, R>::bytes(sp.kmax, L->max_pages, sp.flags | 2, cc, ch);
+            if (smc > 227 * 1024 || !allow(smc)) continue;
+            if (max_active_clusters(kern, (W + 1) * 32, smc, cc) >= rows) {
+                C = cc;
+                chunk = ch;
+                sm = smc;
+                sp.flags |= 2;
+                break;
+            }
+        }
+    }
+    if (C == 0) {  // one-level select: the leader gathers the whole row's scores
+        sm = 1024 + ScSmem<W, R>::bytes(sp.kmax, L->max_pages, sp.flags, 1, 0);
+        if (sm > 227 * 1024 || !allow(sm)) return TS_ERR_UNSUPPORTED;
+        int per_sm = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (W + 1) * 32, sm);
+        const int target = device_sms() * std::max(1, per_sm);
+        C = std::max(1, std::min(max_c, target / std::max(1, rows)));
+        for (;; --C) {  // the largest C whose clusters are all co-resident (one wave)
+            chunk = chunk_of(C);
+            const int c = (L->max_pages + chunk - 1) / chunk;
+            if (C == 1 || max_active_clusters(kern, (W + 1) * 32, sm, c) >= rows) {
+                C = c;
+                break;
+            }
         }
     }
     CUtensorMap tmK, tmV;
     if (!make_pool_map(&tmK, ap.k_pool, L, 16) || !make_pool_map(&tmV, ap.v_pool, L, 16))
         return TS_ERR_CUDA;
-    int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (W + 1) * 32, sm);
-    static const int cmax = getenv("TS_SC_CMAX") ? atoi(getenv("TS_SC_CMAX")) : 16;
-    const int target = device_sms() * std::max(1, per_sm);
-    const int max_c = std::max(1, std::min(cmax, (L->max_pages + 63) / 64));  // >= 64 pages per CTA
-    int C = std::max(1, std::min(max_c, target / std::max(1, rows)));
-    int chunk = 0;
-    for (;; --C) {  // the largest C whose clusters are all co-resident (one wave)
-        chunk = (L->max_pages + C - 1) / C;
-        chunk = (chunk + kSsStagePages - 1) / kSsStagePages * kSsStagePages;
-        const int c = (L->max_pages + chunk - 1) / chunk;
-        if (C == 1 || max_active_clusters(kern, (W + 1) * 32, sm, c) >= rows) {
-            C = c;
-            break;
-        }
-    }
     sp.C = C;
     sp.chunk = chunk;
-    if (two_ok && C > 1 && (C * sp.kmax) % 4 == 0 && (two_env == 1 || L->max_pages >= 4 * C * sp.kmax))
-        sp.flags |= 2;
     // early PDL trigger (the next kernel's prologue overlaps our tail): measured faster with
     // clusters of <= 8 CTAs (C2 / C3 / C4), slower with C5's 13-CTA clusters
     static const int trig_env = getenv("TS_SC_TRIGGER") ? atoi(getenv("TS_SC_TRIGGER")) : -1;

@@ -36,12 +36,16 @@ struct ScSmem {
     static constexpr int kBars = (kInfo + 2 * R * 4 + 7) / 8 * 8;   // mfull,mempty[R]; afull,aempty[2R]; q; pt
     static constexpr int kSel = (kBars + (6 * R + 2) * 8 + 15) / 16 * 16;  // [kmax] int2
     __host__ __device__ static size_t scores_off(int kmax) { return ((size_t)kSel + (size_t)kmax * 8 + 127) / 128 * 128; }
-    // scores [mp4] fp32, then the page-table row [mp4] (flag bit 0), then the two-level
-    // candidates [C * kmax] keys + ids (flag bit 1)
-    static size_t bytes(int kmax, int max_pages, int flags, int C) {
+    // scores [cap] fp32 (cap = the row, or only this CTA's chunk for the two-level select,
+    // flag bit 1), then the page-table row [mp4] (flag bit 0), then the two-level candidates
+    // [C * kmax] keys + ids (flag bit 1)
+    __host__ __device__ static int score_cap(int max_pages, int flags, int chunk) {
+        return (flags & 2) ? ((chunk + 3) & ~3) : ((max_pages + 3) & ~3);
+    }
+    static size_t bytes(int kmax, int max_pages, int flags, int C, int chunk) {
         const size_t mp4 = (max_pages + 3) & ~3;
-        return scores_off(kmax) + mp4 * 4 + ((flags & 1) ? mp4 * 4 : 0) +
-               ((flags & 2) ? (size_t)C * kmax * 8 : 0) + 16;
+        return scores_off(kmax) + (size_t)score_cap(max_pages, flags, chunk) * 4 +
+               ((flags & 1) ? mp4 * 4 : 0) + ((flags & 2) ? (size_t)C * kmax * 8 : 0) + 16;
     }
 };
 
@@ -63,7 +67,8 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
     const int mp4 = (p.max_pages + 3) & ~3;
     float *sc = reinterpret_cast<float *>(smem + SM::scores_off(p.kmax));
     const bool pt_bulk = p.flags & 1, two = (p.flags & 2) && p.C > 1;
-    int *pt_s = reinterpret_cast<int *>(sc) + mp4;
+    const int scap = SM::score_cap(p.max_pages, p.flags, p.chunk);
+    int *pt_s = reinterpret_cast<int *>(sc) + scap;
     uint32_t *ckey = reinterpret_cast<uint32_t *>(pt_s + (pt_bulk ? mp4 : 0));  // [C * kmax]
     int *cid = reinterpret_cast<int *>(ckey) + p.C * p.kmax;
     int *hist = reinterpret_cast<int *>(smem + SM::kHist);
@@ -115,6 +120,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
     const int P = (L + p.S - 1) / p.S;
     const int j0 = rank * p.chunk;
     const int nloc = max(0, min(P - j0, p.chunk));
+    const int sb0 = two ? 0 : j0;  // index of this CTA's first page in sc[]
     const int nst = (nloc + kSsStagePages - 1) / kSsStagePages;
     const int gid = lane >> 2, t = lane & 3;
 
@@ -183,10 +189,10 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
                 m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, 2));
                 if (t < 2) {
                     const int pg = i * kSsStagePages + tile * 16 + gid + 8 * t;
-                    if (j0 + pg < p.max_pages) {
+                    if (j0 + pg < p.max_pages && pg < p.chunk) {
                         const bool valid = pg < nloc;
                         const float v = valid ? (t ? m1 : m0) + 0.0f : kNegInf;
-                        sc[j0 + pg] = v;
+                        sc[sb0 + pg] = v;
                         if (valid) {
                             const uint32_t key = score_key(v);
                             kmn = min(kmn, key);
@@ -206,7 +212,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
         }
     }
     for (int pg = nst * kSsStagePages + tid; pg < p.chunk; pg += NT)
-        if (j0 + pg < p.max_pages) sc[j0 + pg] = kNegInf;
+        if (j0 + pg < p.max_pages) sc[sb0 + pg] = kNegInf;
     __syncthreads();
     SC_STAMP(1);
 
@@ -220,8 +226,8 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
     cg::cluster_group cl = cg::this_cluster();
     if (two) {
         cluster_wait();  // every CTA of the cluster is running
-        uint32_t *lkeys = reinterpret_cast<uint32_t *>(sc) + j0;
-        for (int i = tid; i < ((nloc + 3) & ~3); i += NT) lkeys[i] = i < nloc ? score_key(sc[j0 + i]) : 0u;
+        uint32_t *lkeys = reinterpret_cast<uint32_t *>(sc);  // chunk-local scores
+        for (int i = tid; i < ((nloc + 3) & ~3); i += NT) lkeys[i] = i < nloc ? score_key(sc[i]) : 0u;
         __syncthreads();
         uint32_t *rk = cl.map_shared_rank(ckey, 0) + rank * p.kmax;
         int *ri = cl.map_shared_rank(cid, 0) + rank * p.kmax;
@@ -308,10 +314,13 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
         if (rank == 0) {
             __syncthreads();  // the list and s_cnt are complete
             const int kk = s_cnt;
-            for (int r = 1; r < C; ++r) {
-                int2 *dst = cl.map_shared_rank(sel, r);
-                for (int u = tid; u < kk; u += NT) dst[u] = sel[u];
-                if (tid == 0) *cl.map_shared_rank(&s_cnt, r) = kk;
+            // (C - 1) x kk independent remote stores spread over all threads, plus the count
+            for (int x = tid; x < (C - 1) * (kk + 1); x += NT) {
+                const int r = 1 + x / (kk + 1), u = x % (kk + 1);
+                if (u < kk)
+                    cl.map_shared_rank(sel, r)[u] = sel[u];
+                else
+                    *cl.map_shared_rank(&s_cnt, r) = kk;
             }
         }
         cluster_arrive_release();
