@@ -227,7 +227,7 @@ ts_status launch_select(const float *scores, int rows, int stride, const int *ro
                         long long part_stride = 0) {
     if (rows == 0) return TS_OK;
     const size_t n = (size_t)stride * parts;
-    const size_t sm = n * 4 * (ids_in ? 3 : 1);
+    const size_t sm = ids_in ? n * 4 * 3 : ((n + 3) & ~(size_t)3) * 4;  // affine keys padded to 4
     if (sm > 200 * 1024) return TS_ERR_UNSUPPORTED;
     if (ids_in && n > 16 * kSelThreads) return TS_ERR_UNSUPPORTED;
     static std::once_flag once;

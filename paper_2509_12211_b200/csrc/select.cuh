@@ -14,6 +14,7 @@
 // Exact: only integer comparisons.  Deterministic.
 #pragma once
 #include "common.cuh"
+#include "score_select.cuh"  // cta_topk
 
 namespace ts {
 
@@ -39,6 +40,8 @@ struct SelectSmem {
     int hist[kHistBins];
     int wsum[NT / 32 + 1];
     int bc[4];
+    int red[64];        // cta_topk scratch
+    uint32_t cand[128];  // cta_topk candidate slots
 };
 
 // Block-wide exclusive scan of one int per thread (NT threads); returns the exclusive
@@ -142,13 +145,23 @@ TS_DEV void select_row(const SelectParams &p, int r, uint32_t *keys, SelectSmem<
     const int len = p.row_len ? min(p.row_len[r], p.stride) : p.stride;
 
     int nvalid = 0;
-    for (int i = tid; i < len; i += NT) {
+    uint32_t kmin = 0xffffffffu, kmax = 0u;
+    const int lenp = p.ids_in ? len : ((len + 3) & ~3);  // affine: zero-padded to 4 (uint4 scans)
+    for (int i = tid; i < lenp; i += NT) {
         // entry i of row r = element (part i / kp, row r, column i % kp)
-        const size_t at = (size_t)(i / p.kp) * p.part_stride + (size_t)r * p.kp + (i % p.kp);
-        const uint32_t key = score_key(__ldcg(p.scores + at));
-        keys[i] = key;
-        if (p.ids_in) ids[i] = p.ids_in[at];
-        nvalid += key != kKeyNegInf;
+        uint32_t key = 0u;
+        if (i < len) {
+            const size_t at = (size_t)(i / p.kp) * p.part_stride + (size_t)r * p.kp + (i % p.kp);
+            key = score_key(__ldcg(p.scores + at));
+            if (p.ids_in) ids[i] = p.ids_in[at];
+            if (key != kKeyNegInf) {
+                ++nvalid;
+                kmin = min(kmin, key);
+                kmax = max(kmax, key);
+            }
+        }
+        // affine ids: -inf ("no page") -> 0, below every live key (cta_topk convention)
+        keys[i] = (!p.ids_in && key == kKeyNegInf) ? 0u : key;
     }
     int tot;
     block_excl_scan<NT>(nvalid, S.wsum, &tot);
@@ -162,35 +175,25 @@ TS_DEV void select_row(const SelectParams &p, int r, uint32_t *keys, SelectSmem<
     if (tid == 0) p.sel_count[r] = kk;
     if (kk == 0) return;
 
+    if (!p.ids_in) {
+        // ---- affine ids (ascending id == ascending index): the adaptive radix top-K of the
+        // fused kernels (score_select.cuh)
+        block_minmax<NT, 0>(kmin, kmax, S.red);
+        for (int i = tid; i < kHistBins; i += NT) S.hist[i] = 0;
+        __syncthreads();
+        cta_topk<NT, 0, 11>(keys, len, p.k, kmin, kmax, S.hist, S.red, S.cand,
+                            [&](int pos, int i) {
+                                out_ids[pos] = i * p.id_stride + p.id_offset;
+                                if (out_sc) out_sc[pos] = key_score(keys[i]);
+                            },
+                            nullptr, false, tot);
+        return;
+    }
     uint32_t T = kKeyNegInf, pmask = 0xffffffffu;
     int need_eq = 0;  // kk == tot: every candidate (key > key(-inf)) is selected
     if (kk < tot) radix_threshold<NT>(keys, len, kk, S, T, pmask, need_eq);
 
-    if (!p.ids_in) {
-        // ---- affine ids: ascending id == ascending index.  Contiguous segment per thread.
-        const int per = (len + NT - 1) / NT;
-        const int lo = tid * per, hi = min(len, lo + per);
-        int n_gt = 0, n_eq = 0;
-        for (int i = lo; i < hi; ++i) {
-            const uint32_t key = keys[i] & pmask;
-            n_gt += key > T;
-            n_eq += key == T;
-        }
-        const int eq_before = block_excl_scan<NT>(n_eq, S.wsum, &tot);
-        const int take_eq = max(0, min(n_eq, need_eq - eq_before));
-        int pos = block_excl_scan<NT>(n_gt + take_eq, S.wsum, &tot);
-        int eq_seen = 0;
-        for (int i = lo; i < hi; ++i) {
-            const uint32_t key = keys[i] & pmask;
-            bool sel = key > T;
-            if (key == T) { sel = eq_seen < take_eq; ++eq_seen; }
-            if (sel) {
-                out_ids[pos] = i * p.id_stride + p.id_offset;
-                if (out_sc) out_sc[pos] = key_score(keys[i]);
-                ++pos;
-            }
-        }
-    } else {
+    {
         // ---- explicit ids: compact candidates (masked key >= T) then rank by id.  Requires
         // per-thread segments of <= 16 entries (stride <= 16 * NT, host-checked).
         int *flg = ids + p.stride;
