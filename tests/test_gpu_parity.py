@@ -64,6 +64,11 @@ CASES = {
     "f32_gqa": ("c1", dict(batch=2, num_q_heads=8, num_kv_heads=2, ctx=700, page_size=16,
                            budget_tokens=160), True),
     "bf16_d128_score": ("c3", dict(batch=2, head_dim=128, ctx=900, budget_tokens=128), True),
+    # cluster-kernel paths: odd / non-power-of-two groups, S = 64 one-level split rows, and
+    # rows longer than 2048 pages (two-level select: chunk top-K, then candidate top-K)
+    "g3_s16": ("c3", dict(batch=3, num_q_heads=12, ctx=1300, budget_tokens=160), True),
+    "g6_s64": ("c3", dict(batch=2, num_q_heads=24, ctx=6000, page_size=64, budget_tokens=1024), True),
+    "two_level": ("c3", dict(batch=1, ctx=36000, budget_tokens=512), True),
 }
 
 
