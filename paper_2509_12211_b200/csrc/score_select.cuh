@@ -144,8 +144,21 @@ TS_DEV int block_scan(int v, int *red, int *total) {
 // pass plus the ranking is the common case.  The final compaction is one block scan of
 // packed (greater, equal) counts over contiguous per-thread segments (ascending output).
 #ifndef TS_TOPK_PROF
+#ifdef TS_SEL_PROF  // development build (TS_NVCC_EXTRA=-DTS_SEL_PROF): phase stamps in dts[0..4]
+#define TS_TOPK_PROF(i) \
+    if (dts && threadIdx.x == 0) dts[i] = globaltimer();
+#else
 #define TS_TOPK_PROF(i)
 #endif
+#endif
+#ifndef TS_TOPK_PROF2
+#define TS_TOPK_PROF2(i)
+#endif
+// Histogram bin b lives at int index hsw(b): the 16-bin runs read as 4 x int4 by one thread
+// of the bin search are XOR-rotated by (run >> 1) & 3, so 8 consecutive lanes hit 8
+// different 16-byte bank groups (no bank conflicts); a bijection on every 64-bin block.
+TS_DEV int hsw(int b) { return b ^ ((b >> 3) & 12); }
+
 template <int NT, int BAR, int HB = 11, typename Emit>
 TS_DEV int cta_topk(const uint32_t *keys, int n, int k, uint32_t kmin, uint32_t kmax, int *hist,
                     int *red, uint32_t *cand, Emit emit, unsigned long long *dts = nullptr,
@@ -188,8 +201,11 @@ TS_DEV int cta_topk(const uint32_t *keys, int n, int k, uint32_t kmin, uint32_t 
                     const uint4 v = k4[i];
                     const uint32_t e[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-                    for (int j = 0; j < 4; ++j)
-                        if (e[j] >= kmin && e[j] <= kmax) atomicAdd(&hist[(e[j] - kmin) >> shift], 1);
+                    for (int j = 0; j < 4; ++j) {  // branch-free: a key out of range adds 0
+                        const bool in = e[j] >= kmin && e[j] <= kmax;
+                        const int bn = in ? (int)((e[j] - kmin) >> shift) : lane;
+                        atomicAdd(&hist[hsw(bn)], in ? 1 : 0);
+                    }
                 }
                 sel_sync<NT, BAR>();
             }
@@ -198,12 +214,13 @@ TS_DEV int cta_topk(const uint32_t *keys, int n, int k, uint32_t kmin, uint32_t 
                 constexpr int PB = 16, TT = (1 << HB) / PB, TW = (TT + 31) / 32;
                 static_assert(TT <= NT, "bin search needs (1 << HB) / 16 threads");
                 int c[PB], sm = 0, suf = 0;
+                TS_TOPK_PROF2(8);
                 if (warp < TW) {
                     if (tid < TT) {
                         const int4 *h4 = reinterpret_cast<const int4 *>(hist) + tid * (PB / 4);
 #pragma unroll
                         for (int j = 0; j < PB / 4; ++j) {
-                            const int4 v = h4[j];
+                            const int4 v = h4[j ^ ((tid >> 1) & 3)];  // hsw layout
                             c[4 * j] = v.x; c[4 * j + 1] = v.y; c[4 * j + 2] = v.z; c[4 * j + 3] = v.w;
                         }
                         sm = ((c[0] + c[1]) + (c[2] + c[3])) + ((c[4] + c[5]) + (c[6] + c[7])) +
@@ -217,7 +234,9 @@ TS_DEV int cta_topk(const uint32_t *keys, int n, int k, uint32_t kmin, uint32_t 
                     }
                     if (lane == 0) red[40 + warp] = suf;  // warp total
                 }
+                TS_TOPK_PROF2(9);
                 sel_sync<NT, BAR>();
+                TS_TOPK_PROF2(10);
                 if (tid < TT) {
 #pragma unroll
                     for (int w = 0; w < TW; ++w)
@@ -242,6 +261,7 @@ TS_DEV int cta_topk(const uint32_t *keys, int n, int k, uint32_t kmin, uint32_t 
                     }
                 }
                 if (tid == 0) red[51] = 0;  // candidate counter
+                TS_TOPK_PROF2(11);
             }
             sel_sync<NT, BAR>();
             if (dts && tid == 0 && pass == 0) dts[5] = globaltimer();
@@ -320,33 +340,67 @@ TS_DEV int cta_topk(const uint32_t *keys, int n, int k, uint32_t kmin, uint32_t 
     if (dts && tid == 0) dts[6] = globaltimer();
     TS_TOPK_PROF(4);
     // compaction in index order: thread owns the contiguous run of uint4 [tid*per4, +per4);
-    // one scan of packed (greater, equal) counts: before me, min(need_eq, eq_before) ties
+    // one scan of packed (greater, equal) counts: before me, min(need_eq, eq_before) ties.
+    // Runs of <= 64 keys keep (greater, equal) bit masks, so the emit visits only the
+    // selected keys (about k / NT per thread) without re-reading shared memory.
     const int per4 = (n4 + NT - 1) / NT;
     const int i0 = tid * per4, i1 = min(n4, i0 + per4);
-    int n_gt = 0, n_eq = 0;
+    if (per4 <= 16) {
+        uint64_t gm = 0, em = 0;
 #pragma unroll 4
-    for (int i = i0; i < i1; ++i) {
-        const uint4 v = k4[i];
-        n_gt += (v.x > tgt) + (v.y > tgt) + (v.z > tgt) + (v.w > tgt);
-        n_eq += (v.x == teq) + (v.y == teq) + (v.z == teq) + (v.w == teq);
-    }
-    int tot;
-    const int before = block_scan<NT, BAR>((n_gt << 16) | n_eq, red, &tot);
-    const int eq_before = before & 0xffff, gt_before = before >> 16;
-    TS_TOPK_PROF(5);
-    int pos = gt_before + min(need_eq, eq_before);
-    int taken = eq_before;
-    if (n_gt + n_eq > 0)
         for (int i = i0; i < i1; ++i) {
             const uint4 v = k4[i];
             const uint32_t e[4] = {v.x, v.y, v.z, v.w};
+            uint32_t g4 = 0, e4 = 0;
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-                bool sel = e[j] > tgt;
-                if (e[j] == teq) sel = taken++ < need_eq;
-                if (sel) emit(pos++, 4 * i + j);
+                g4 |= (uint32_t)(e[j] > tgt && e[j] != teq) << j;
+                e4 |= (uint32_t)(e[j] == teq) << j;
             }
+            gm |= (uint64_t)g4 << (4 * (i - i0));
+            em |= (uint64_t)e4 << (4 * (i - i0));
         }
+        const int n_gt = __popcll(gm), n_eq = __popcll(em);
+        int tot;
+        const int before = block_scan<NT, BAR>((n_gt << 16) | n_eq, red, &tot);
+        const int eq_before = before & 0xffff, gt_before = before >> 16;
+        TS_TOPK_PROF(5);
+        int pos = gt_before + min(need_eq, eq_before);
+        uint64_t sm = gm;
+        for (int t = max(0, min(need_eq - eq_before, n_eq)); t > 0; --t) {  // lowest-index ties
+            sm |= em & (~em + 1);
+            em &= em - 1;
+        }
+        while (sm) {
+            emit(pos++, 4 * i0 + __ffsll((long long)sm) - 1);
+            sm &= sm - 1;
+        }
+    } else {
+        int n_gt = 0, n_eq = 0;
+#pragma unroll 4
+        for (int i = i0; i < i1; ++i) {
+            const uint4 v = k4[i];
+            n_gt += (v.x > tgt) + (v.y > tgt) + (v.z > tgt) + (v.w > tgt);
+            n_eq += (v.x == teq) + (v.y == teq) + (v.z == teq) + (v.w == teq);
+        }
+        int tot;
+        const int before = block_scan<NT, BAR>((n_gt << 16) | n_eq, red, &tot);
+        const int eq_before = before & 0xffff, gt_before = before >> 16;
+        TS_TOPK_PROF(5);
+        int pos = gt_before + min(need_eq, eq_before);
+        int taken = eq_before;
+        if (n_gt + n_eq > 0)
+            for (int i = i0; i < i1; ++i) {
+                const uint4 v = k4[i];
+                const uint32_t e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    bool sel = e[j] > tgt;
+                    if (e[j] == teq) sel = taken++ < need_eq;
+                    if (sel) emit(pos++, 4 * i + j);
+                }
+            }
+    }
     TS_TOPK_PROF(6);
     return kk;
 }

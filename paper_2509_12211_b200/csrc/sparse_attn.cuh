@@ -301,8 +301,9 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) sparse_attn_tma_kernel(
     using SM = SatSmem<W, R>;
     static_assert(R % W == 0, "stage -> consumer warp must be fixed");
     extern __shared__ uint8_t sat_raw[];
-    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(sat_raw) + 1023) &
-                                                ~uintptr_t(1023));
+    // 1024-byte aligned (TMA swizzle atoms) by pointer arithmetic on the __shared__ array
+    // itself, so the compiler keeps the shared state space (LDS / ATOMS, not generic LD / ATOM)
+    uint8_t *smem = sat_raw + ((1024u - (smem_u32(sat_raw) & 1023u)) & 1023u);
     const uint32_t sb = smem_u32(smem);
     const uint32_t full0 = sb + SM::kBars, empty0 = full0 + 8 * R;
     float *wpart = reinterpret_cast<float *>(smem + SM::kWarpPart);

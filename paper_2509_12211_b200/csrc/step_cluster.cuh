@@ -5,11 +5,11 @@
 //  1. score (Eq. 2): each CTA streams a contiguous chunk of the row's metadata records with
 //     1-D bulk copies into an 8 KB-stage mbarrier ring; 4 consumer warps compute the
 //     [m | M] x [q^- ; q^+] products on mma.m16n8k16 and the group max (reading R9);
-//  2. select (TopK): the chunk scores go to the cluster leader's shared memory (DSMEM);
-//     the leader runs the exact CTA-wide top-K (cta_topk, score_select.cuh), writes the
-//     selection for the API and a (tile row, first token) list into its shared memory;
-//  3. gather: after a cluster barrier each CTA copies its share of that list (DSMEM) and
-//     its producer streams the selected pages' [16 x 64] K and V tiles with 2-D TMA
+//  2. select (TopK): the chunk keys are all-gathered into every CTA's shared memory (DSMEM
+//     remote stores, one cluster barrier); every CTA runs the same exact CTA-wide top-K
+//     (cta_topk, score_select.cuh) and keeps only the (tile row, first token) entries of
+//     its own share of the ascending selection — no list broadcast, no second barrier;
+//  3. gather: each CTA's producer streams its share's [16 x 64] K and V tiles with 2-D TMA
 //     (128-byte swizzle) into the SAME ring, now as 4 KB stages;
 //  4. attend: consumers run S = Q K^T (mma.m16n8k16), the fp32 online softmax and
 //     O += P V (mma.m16n8k8, tf32 P — R10) per tile, with the q fragments already in
@@ -58,8 +58,9 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
     constexpr int RA = 2 * R;  // attention stages (4 KB)
     static_assert(R % W == 0 && RA % W == 0, "stage -> consumer warp must be fixed");
     extern __shared__ uint8_t sc_raw[];
-    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(sc_raw) + 1023) &
-                                                ~uintptr_t(1023));
+    // 1024-byte aligned (TMA swizzle atoms) by pointer arithmetic on the __shared__ array
+    // itself, so the compiler keeps the shared state space (LDS / ATOMS, not generic LD / ATOM)
+    uint8_t *smem = sc_raw + ((1024u - (smem_u32(sc_raw) & 1023u)) & 1023u);
     const uint32_t sb = smem_u32(smem);
     const uint32_t mfull0 = sb + SM::kBars, mempty0 = mfull0 + 8 * R;
     const uint32_t afull0 = mempty0 + 8 * R, aempty0 = afull0 + 8 * RA;
@@ -77,13 +78,18 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
     int *info = reinterpret_cast<int *>(smem + SM::kInfo);
     int2 *sel = reinterpret_cast<int2 *>(smem + SM::kSel);
     unsigned *s_kmin = reinterpret_cast<unsigned *>(red + 60), *s_kmax = s_kmin + 1;
-    __shared__ int s_cnt, s_last;
+    __shared__ int s_last;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int C = p.C;
     const int row = blockIdx.x / C, rank = blockIdx.x % C;
     const int b = row / p.Hkv, g = row % p.Hkv;
     unsigned long long *dts = p.dbg && blockIdx.x < 4096 ? p.dbg + blockIdx.x * 8 : nullptr;
+#ifdef TS_SEL_PROF  // select-internal stamps: leader's select at +4096*8, chunk selects at +8192*8
+    unsigned long long *dsel = dts ? dts + 4096 * 8 : nullptr, *dchk = dts ? dts + 8192 * 8 : nullptr;
+#else
+    unsigned long long *dsel = nullptr, *dchk = nullptr;
+#endif
 #define SC_STAMP(e) \
     if (dts && tid == 0) dts[e] = globaltimer();
     SC_STAMP(0);
@@ -106,10 +112,8 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
         fence_mbar_init();
         *s_kmin = 0xffffffffu;
         *s_kmax = 0u;
-        s_cnt = 0;
     }
-    if (rank == 0 || two)
-        for (int i = tid; i < kSsHist; i += NT) hist[i] = 0;
+    for (int i = tid; i < kSsHist; i += NT) hist[i] = 0;
     __syncthreads();
     // "this CTA is running" (before any DSMEM access); release: its initialised counters
     // and histogram are visible to the remote updates that follow the matching wait
@@ -130,7 +134,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
             const uint64_t pol = l2_policy_evict_first();
             mbar_arrive_expect_tx(qbar, p.G * kRowBytes);
             bulk_load(sb + SM::kQ, p.q + ((size_t)b * p.Hq + g * p.G) * kAttnD, p.G * kRowBytes, qbar);
-            if (rank == 0 && P > 0 && pt_bulk) {
+            if (P > 0 && pt_bulk) {  // every CTA: it maps its own share of the selection
                 const uint32_t ptb = min(((uint32_t)P * 4 + 15) & ~15u, (uint32_t)mp4 * 4);
                 mbar_arrive_expect_tx(ptbar, ptb);
                 bulk_load(smem_u32(pt_s), p.page_table + (size_t)b * p.max_pages, ptb, ptbar);
@@ -217,59 +221,83 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
     SC_STAMP(1);
 
     // ===================================== 2. select =====================================
-    // one-level: the chunk scores go to the leader, which runs the exact CTA-wide top-K.
-    // two-level (rows much longer than C x K): every CTA selects its chunk's top-K (in
-    // parallel) and sends those candidates; the leader selects from the C x K candidates.
-    // Exact: a page of the row's top-K is beaten by fewer than K pages of its own chunk
-    // (same order: score, then lower id), so it is among its chunk's candidates.  (A
-    // cluster-parallel radix pass through DSMEM atomics was measured slower.)
+    // Every CTA of the cluster ends up with the whole row's keys (one-level) or all C x K
+    // chunk candidates (two-level) in its own shared memory — an all-gather through DSMEM
+    // remote stores and ONE cluster barrier — and runs the same exact top-K redundantly.
+    // Each CTA then keeps only its share of the ascending selection (the pages covering its
+    // tiles [t0, t1)), so no selection list is broadcast and no second barrier is needed.
+    // Two-level (rows much longer than C x K): every CTA first selects its chunk's top-K;
+    // exact, as a page of the row's top-K is beaten by fewer than K pages of its own chunk
+    // (same order: score, then lower id), so it is among its chunk's candidates.
     cg::cluster_group cl = cg::this_cluster();
+    const int S = p.S, tpp = S >> 4;
+    const int kk = min(p.kmax, P);  // the selection size is known before the select
+    const int ntile = kk * tpp;
+    const int t0 = (int)((long long)ntile * rank / C), t1 = (int)((long long)ntile * (rank + 1) / C);
+    const int u0 = t0 / tpp, u1 = (t1 + tpp - 1) / tpp;     // pages of this CTA's tiles
+    const int w0 = kk * rank / C, w1 = kk * (rank + 1) / C;  // sel_ids entries this CTA writes
+    const int *ptrow = pt_bulk ? pt_s : p.page_table + (size_t)b * p.max_pages;
+    int *out_id = p.sel_ids + (size_t)row * p.kmax;
+    uint32_t *cand = reinterpret_cast<uint32_t *>(wpart);  // free until the attention ends
+    auto emit_pg = [&](int pos, int pg) {
+        if (pos >= u0 && pos < u1) sel[pos - u0] = make_int2((ptrow[pg] * p.Hkv + g) * S, pg * S);
+        if (pos >= w0 && pos < w1) out_id[pos] = pg;
+    };
     if (two) {
-        cluster_wait();  // every CTA of the cluster is running
-        uint32_t *lkeys = reinterpret_cast<uint32_t *>(sc);  // chunk-local scores
+        uint32_t *lkeys = reinterpret_cast<uint32_t *>(sc);  // chunk-local scores -> keys
         for (int i = tid; i < ((nloc + 3) & ~3); i += NT) lkeys[i] = i < nloc ? score_key(sc[i]) : 0u;
         __syncthreads();
-        uint32_t *rk = cl.map_shared_rank(ckey, 0) + rank * p.kmax;
-        int *ri = cl.map_shared_rank(cid, 0) + rank * p.kmax;
-        uint32_t *cand = reinterpret_cast<uint32_t *>(wpart);
+        uint32_t *myk = ckey + rank * p.kmax;
+        int *myi = cid + rank * p.kmax;
         auto emit_c = [&](int pos, int i) {
-            rk[pos] = lkeys[i];
-            ri[pos] = j0 + i;
+            myk[pos] = lkeys[i];
+            myi[pos] = j0 + i;
         };
         const int kl = nloc <= 512
-                           ? cta_topk<NT, 0, 9>(lkeys, nloc, p.kmax, *s_kmin, *s_kmax, hist, red, cand, emit_c)
-                           : cta_topk<NT, 0, 11>(lkeys, nloc, p.kmax, *s_kmin, *s_kmax, hist, red, cand, emit_c);
-        for (int i = kl + tid; i < p.kmax; i += NT) rk[i] = 0u;  // absent
-        if (tid == 0) atomicAdd(cl.map_shared_rank(&s_cnt, 0), kl);
-        if (rank == 0) {  // the leader's candidate range for its select (all CTAs' keys)
-            __syncthreads();
-            for (int i = tid; i < kSsHist; i += NT) hist[i] = 0;
-        }
-        cluster_arrive_release();
-        cluster_wait();
-    } else if (C > 1) {
+                           ? cta_topk<NT, 0, 9>(lkeys, nloc, p.kmax, *s_kmin, *s_kmax, hist, red, cand, emit_c, dchk)
+                           : cta_topk<NT, 0, 11>(lkeys, nloc, p.kmax, *s_kmin, *s_kmax, hist, red, cand, emit_c, dchk);
+        for (int i = kl + tid; i < p.kmax; i += NT) myk[i] = 0u;  // absent
+        __syncthreads();
         cluster_wait();  // every CTA of the cluster is running
-        if (rank != 0) {
-            float *dst = cl.map_shared_rank(sc, 0);
-            const int n = min(p.chunk, p.max_pages - j0);
-            for (int i = tid; i < n; i += NT) dst[j0 + i] = sc[j0 + i];
-            if (tid == 0 && *s_kmin <= *s_kmax) {
-                atomicMin(cl.map_shared_rank(s_kmin, 0), *s_kmin);
-                atomicMax(cl.map_shared_rank(s_kmax, 0), *s_kmax);
-            }
+        // push this chunk's K candidates into every other CTA; reset the histogram meanwhile
+        for (int x = tid; x < (C - 1) * p.kmax; x += NT) {
+            const int r = rank + 1 + x / p.kmax, u = x % p.kmax;
+            const int peer = r < C ? r : r - C;
+            cl.map_shared_rank(ckey, peer)[rank * p.kmax + u] = myk[u];
+            cl.map_shared_rank(cid, peer)[rank * p.kmax + u] = myi[u];
         }
+        for (int i = tid; i < kSsHist; i += NT) hist[i] = 0;
         cluster_arrive_release();
         cluster_wait();
+    } else {
+        // this CTA's slice of the row as keys (0 = no page, up to the 4-padded row length)
+        const int e1 = min(j0 + p.chunk, (P + 3) & ~3);
+        uint32_t *keys = reinterpret_cast<uint32_t *>(sc);
+        for (int i = j0 + tid; i < e1; i += NT) keys[i] = i < P ? score_key(sc[i]) : 0u;
+        if (C > 1) {
+            __syncthreads();
+            cluster_wait();  // every CTA of the cluster is running
+            const int n = max(0, e1 - j0);
+            for (int x = tid; x < (C - 1) * n; x += NT) {
+                const int r = rank + 1 + x / n, i = j0 + x % n;
+                cl.map_shared_rank(keys, r < C ? r : r - C)[i] = keys[i];
+            }
+            if (tid >= 1 && tid < C && *s_kmin <= *s_kmax) {  // thread r: peer rank + r
+                const int r = rank + tid, peer = r < C ? r : r - C;
+                atomicMin(cl.map_shared_rank(s_kmin, peer), *s_kmin);
+                atomicMax(cl.map_shared_rank(s_kmax, peer), *s_kmax);
+            }
+            cluster_arrive_release();
+            cluster_wait();
+        }
     }
     SC_STAMP(5);
-    if (rank == 0) {
-        const int *ptrow = pt_bulk ? pt_s : p.page_table + (size_t)b * p.max_pages;
-        int *out_id = p.sel_ids + (size_t)row * p.kmax;
-        uint32_t *cand = reinterpret_cast<uint32_t *>(wpart);  // free until the attention ends
-        const int S = p.S;
-        int kk;
+    {
+        int kd;
         if (two) {
-            const int nc = C * p.kmax, nlive = s_cnt;
+            const int nc = C * p.kmax;
+            int nlive = 0;  // live candidates: sum over chunks of min(K, chunk pages)
+            for (int r = 0; r < C; ++r) nlive += min(p.kmax, max(0, min(P - r * p.chunk, p.chunk)));
             uint32_t mn = 0xffffffffu, mx = 0u;
             for (int i = tid; i < nc; i += NT)
                 if (ckey[i]) {
@@ -279,60 +307,28 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
             if (P > 0 && pt_bulk) mbar_wait(ptbar, 0);
             block_minmax<NT, 0>(mn, mx, red);
             SC_STAMP(6);
-            auto emit = [&](int pos, int i) {
-                const int pg = cid[i];
-                out_id[pos] = pg;
-                sel[pos] = make_int2((ptrow[pg] * p.Hkv + g) * S, pg * S);
-            };
+            auto emit = [&](int pos, int i) { emit_pg(pos, cid[i]); };
             // candidates are chunk-major, ids ascending inside a chunk: entry order == id order
-            kk = cta_topk<NT, 0, 11>(ckey, nc, p.kmax, mn, mx, hist, red, cand, emit, nullptr, false, nlive);
+            kd = cta_topk<NT, 0, 11>(ckey, nc, p.kmax, mn, mx, hist, red, cand, emit, dsel, false, nlive);
         } else {
-            uint32_t *keys = reinterpret_cast<uint32_t *>(sc);
-            for (int i = tid; i < ((P + 3) & ~3); i += NT) keys[i] = i < P ? score_key(sc[i]) : 0u;
+            const uint32_t *keys = reinterpret_cast<const uint32_t *>(sc);
             if (P > 0 && pt_bulk) mbar_wait(ptbar, 0);
             __syncthreads();
             SC_STAMP(6);
-            auto emit = [&](int pos, int i) {
-                out_id[pos] = i;
-                sel[pos] = make_int2((ptrow[i] * p.Hkv + g) * S, i * S);
-            };
+            auto emit = [&](int pos, int i) { emit_pg(pos, i); };
             // radix width by row length: ~1 key per bin on the first pass
-            kk = P <= 512 ? cta_topk<NT, 0, 9>(keys, P, p.kmax, *s_kmin, *s_kmax, hist, red, cand, emit)
-                          : cta_topk<NT, 0, 11>(keys, P, p.kmax, *s_kmin, *s_kmax, hist, red, cand, emit);
+            kd = P <= 512 ? cta_topk<NT, 0, 9>(keys, P, p.kmax, *s_kmin, *s_kmax, hist, red, cand, emit, dsel)
+                          : cta_topk<NT, 0, 11>(keys, P, p.kmax, *s_kmin, *s_kmax, hist, red, cand, emit, dsel);
         }
-        for (int i = kk + tid; i < p.kmax; i += NT) out_id[i] = -1;
+        (void)kd;  // == kk
+        if (rank == 0) {
+            for (int i = kk + tid; i < p.kmax; i += NT) out_id[i] = -1;
+            if (tid == 0) p.sel_count[row] = kk;
+        }
         __syncthreads();
-        if (tid == 0) {
-            p.sel_count[row] = kk;
-            s_cnt = kk;
-        }
+        if (dsel && tid == 0) dsel[7] = globaltimer();
         SC_STAMP(2);
     }
-    // the leader pushes the selection list and its count into every CTA's shared memory
-    // (remote stores, no round trip), then one cluster barrier publishes them
-    if (C > 1) {
-        if (rank == 0) {
-            __syncthreads();  // the list and s_cnt are complete
-            const int kk = s_cnt;
-            // (C - 1) x kk independent remote stores spread over all threads, plus the count
-            for (int x = tid; x < (C - 1) * (kk + 1); x += NT) {
-                const int r = 1 + x / (kk + 1), u = x % (kk + 1);
-                if (u < kk)
-                    cl.map_shared_rank(sel, r)[u] = sel[u];
-                else
-                    *cl.map_shared_rank(&s_cnt, r) = kk;
-            }
-        }
-        cluster_arrive_release();
-        cluster_wait();
-    } else {
-        __syncthreads();
-    }
-    const int cnt = s_cnt;
-    const int tpp = p.S >> 4;
-    const int ntile = cnt * tpp;
-    const int t0 = (int)((long long)ntile * rank / C), t1 = (int)((long long)ntile * (rank + 1) / C);
-    __syncthreads();
     SC_STAMP(3);
 
     // ===================================== 3-4. gather + attend ==========================
@@ -345,7 +341,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
                 const int st = i % RA;
                 mbar_wait(aempty0 + 8 * st, ((i / RA) & 1) ^ 1);
                 const int tl = t0 + i, u = tl / tpp, sub = tl - u * tpp;
-                const int2 pg = sel[u];
+                const int2 pg = sel[u - u0];
                 info[st] = pg.y + 16 * sub;
                 mbar_arrive_expect_tx(afull0 + 8 * st, 2 * 16 * kRowBytes);
                 const uint32_t dst = sb + st * 2 * 16 * kRowBytes;
