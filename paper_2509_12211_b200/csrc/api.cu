@@ -481,7 +481,7 @@ ts_status launch_step_cluster_t(const ts_layout *L, ScoreSelParams &sp, const At
     if (two_ok) {  // two-level select: every CTA keeps only its chunk's scores
         for (int c = max_c; c >= 2; --c) {
             const int ch = chunk_of(c), cc = (L->max_pages + ch - 1) / ch;
-            if ((cc * sp.kmax) % 4 != 0 || (two_env != 1 && L->max_pages < 4 * cc * sp.kmax)) continue;
+            if (sp.kmax % 4 != 0 || (two_env != 1 && L->max_pages < 4 * cc * sp.kmax)) continue;
             const size_t smc = 1024 + ScSmem<W, R>::bytes(sp.kmax, L->max_pages, sp.flags | 2, cc, ch);
             if (smc > 227 * 1024 || !allow(smc)) continue;
             if (max_active_clusters(kern, (W + 1) * 32, smc, cc) >= rows) {

@@ -260,11 +260,14 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
         __syncthreads();
         cluster_wait();  // every CTA of the cluster is running
         // push this chunk's K candidates into every other CTA; reset the histogram meanwhile
-        for (int x = tid; x < (C - 1) * p.kmax; x += NT) {
-            const int r = rank + 1 + x / p.kmax, u = x % p.kmax;
+        const int k4n = p.kmax >> 2;  // 16-byte remote stores (host: kmax % 4 == 0)
+        for (int x = tid; x < (C - 1) * k4n; x += NT) {
+            const int r = rank + 1 + x / k4n, u = x % k4n;
             const int peer = r < C ? r : r - C;
-            cl.map_shared_rank(ckey, peer)[rank * p.kmax + u] = myk[u];
-            cl.map_shared_rank(cid, peer)[rank * p.kmax + u] = myi[u];
+            reinterpret_cast<uint4 *>(cl.map_shared_rank(ckey, peer) + rank * p.kmax)[u] =
+                reinterpret_cast<const uint4 *>(myk)[u];
+            reinterpret_cast<int4 *>(cl.map_shared_rank(cid, peer) + rank * p.kmax)[u] =
+                reinterpret_cast<const int4 *>(myi)[u];
         }
         for (int i = tid; i < kSsHist; i += NT) hist[i] = 0;
         cluster_arrive_release();
@@ -277,10 +280,11 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
         if (C > 1) {
             __syncthreads();
             cluster_wait();  // every CTA of the cluster is running
-            const int n = max(0, e1 - j0);
-            for (int x = tid; x < (C - 1) * n; x += NT) {
-                const int r = rank + 1 + x / n, i = j0 + x % n;
-                cl.map_shared_rank(keys, r < C ? r : r - C)[i] = keys[i];
+            const int n4 = max(0, e1 - j0) >> 2;  // j0 and e1 are multiples of 4: 16-byte stores
+            const uint4 *src = reinterpret_cast<const uint4 *>(keys + j0);
+            for (int x = tid; x < (C - 1) * n4; x += NT) {
+                const int r = rank + 1 + x / n4, i = x % n4;
+                reinterpret_cast<uint4 *>(cl.map_shared_rank(keys, r < C ? r : r - C) + j0)[i] = src[i];
             }
             if (tid >= 1 && tid < C && *s_kmin <= *s_kmax) {  // thread r: peer rank + r
                 const int r = rank + tid, peer = r < C ? r : r - C;
