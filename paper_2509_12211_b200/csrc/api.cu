@@ -794,7 +794,11 @@ ts_status ts_decode_step(const ts_layout *L, const void *q, const void *k_pool, 
         AttnParams ap = attn_params(L, q, k_pool, v_pool, page_table, seq_lens, ids, cnt, kmax, scale,
                                     o, lse, ws);
         phase_mark(0, st);
-        s = launch_step_cluster_t<4, 4>(L, sp, ap, st);
+        // ring depth: 8 stages (64 KB in flight per CTA) when the rows leave SMs for wide
+        // clusters (measured: C3 / C5 faster); 4 stages when many rows need >= 3 CTAs per SM
+        static const int ring_env = getenv("TS_SC_R") ? atoi(getenv("TS_SC_R")) : 0;  // dev knob
+        const int ring = ring_env ? ring_env : (L->batch * L->num_kv_heads <= device_sms() ? 8 : 4);
+        s = ring == 8 ? launch_step_cluster_t<4, 8>(L, sp, ap, st) : launch_step_cluster_t<4, 4>(L, sp, ap, st);
         phase_mark(3, st);
         if (s != TS_ERR_UNSUPPORTED) {
             g_launches = 1;
