@@ -169,6 +169,9 @@ TS_DEV int cta_topk(const uint32_t *keys, int n, int k, uint32_t kmin, uint32_t 
     // keys[] is 16-byte aligned and zero-padded to a multiple of 4 (0 < every valid key):
     // the scans below read it as uint4 for memory-level parallelism (smem latency ~30 cycles)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // HB = 0: radix width by length at run time (~1 key per bin on the first pass), one
+    // instantiation instead of two (instruction-cache footprint of the fused kernel)
+    const int hb = HB ? HB : (n <= 512 ? 9 : 11);
     const int nlive = nvalid < 0 ? n : nvalid;
     const int kk = min(k, nlive);
     TS_TOPK_PROF(0);
@@ -190,9 +193,9 @@ TS_DEV int cta_topk(const uint32_t *keys, int n, int k, uint32_t kmin, uint32_t 
             }
             const uint32_t span = kmax - kmin;
             const int bits = 32 - __clz(span);
-            const int shift = bits > HB ? bits - HB : 0;
+            const int shift = bits > hb ? bits - hb : 0;
             if (pass > 0) {
-                for (int i = tid; i < (1 << HB); i += NT) hist[i] = 0;
+                for (int i = tid; i < (1 << hb); i += NT) hist[i] = 0;
                 sel_sync<NT, BAR>();
             }
             if (pass > 0 || !hist0_built) {
@@ -211,8 +214,9 @@ TS_DEV int cta_topk(const uint32_t *keys, int n, int k, uint32_t kmin, uint32_t 
             }
             TS_TOPK_PROF(1);
             {  // boundary bin: thread t < TT owns bins [16 t, 16 t + 16); block suffix scan
-                constexpr int PB = 16, TT = (1 << HB) / PB, TW = (TT + 31) / 32;
-                static_assert(TT <= NT, "bin search needs (1 << HB) / 16 threads");
+                constexpr int PB = 16;
+                static_assert((1 << 11) / PB <= NT, "bin search needs (1 << hb) / 16 threads");
+                const int TT = (1 << hb) / PB, TW = (TT + 31) / 32;
                 int c[PB], sm = 0, suf = 0;
                 TS_TOPK_PROF2(8);
                 if (warp < TW) {

@@ -253,9 +253,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
             myk[pos] = lkeys[i];
             myi[pos] = j0 + i;
         };
-        const int kl = nloc <= 512
-                           ? cta_topk<NT, 0, 9>(lkeys, nloc, p.kmax, *s_kmin, *s_kmax, hist, red, cand, emit_c, dchk)
-                           : cta_topk<NT, 0, 11>(lkeys, nloc, p.kmax, *s_kmin, *s_kmax, hist, red, cand, emit_c, dchk);
+        const int kl = cta_topk<NT, 0, 0>(lkeys, nloc, p.kmax, *s_kmin, *s_kmax, hist, red, cand, emit_c, dchk);
         for (int i = kl + tid; i < p.kmax; i += NT) myk[i] = 0u;  // absent
         __syncthreads();
         cluster_wait();  // every CTA of the cluster is running
@@ -320,9 +318,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
             __syncthreads();
             SC_STAMP(6);
             auto emit = [&](int pos, int i) { emit_pg(pos, i); };
-            // radix width by row length: ~1 key per bin on the first pass
-            kd = P <= 512 ? cta_topk<NT, 0, 9>(keys, P, p.kmax, *s_kmin, *s_kmax, hist, red, cand, emit, dsel)
-                          : cta_topk<NT, 0, 11>(keys, P, p.kmax, *s_kmin, *s_kmax, hist, red, cand, emit, dsel);
+            kd = cta_topk<NT, 0, 0>(keys, P, p.kmax, *s_kmin, *s_kmax, hist, red, cand, emit, dsel);
         }
         (void)kd;  // == kk
         if (rank == 0) {
