@@ -440,15 +440,25 @@ ts_status launch_ss_t(ScoreSelParams &p, int rows, int cdesired, cudaStream_t st
     return launch_status();
 }
 
-// The whole bf16 step as one cluster-per-row kernel (step_cluster.cuh).
-template <int W, int R>
-ts_status launch_step_cluster_t(const ts_layout *L, ScoreSelParams &sp, const AttnParams &ap,
-                                cudaStream_t st) {
-    auto kern = decode_cluster_kernel<W, R>;
+// The whole bf16 step as one cluster-per-row kernel (step_cluster.cuh): plan (cluster width
+// C, chunk, shared memory, flags) and launch.  DSM: the CTA partials merge in the cluster
+// leader's shared memory (a separate instantiation, so the other configurations keep the
+// leaner kernel).
+struct StepPlan {
+    bool ok = false;
+    int C = 0, chunk = 0, flags = 0;
+    size_t sm = 0;
+};
+
+template <int W, int R, bool DSM>
+StepPlan plan_step(const ts_layout *L, int kmax) {
+    auto kern = decode_cluster_kernel<W, R, DSM>;
+    StepPlan pl;
     const int rows = L->batch * L->num_kv_heads;
     // flags: bit 0 page-table row prefetched to smem (rows up to 2048 pages); bit 1
-    // two-level select when rows are much longer than the candidates (set below with C)
-    sp.flags = ((L->max_pages & 3) == 0 && L->max_pages <= 2048) ? 1 : 0;
+    // two-level select when rows are much longer than the candidates; bit 2 DSMEM merge
+    // area (DSM); bit 3 early PDL trigger (set at launch)
+    int fl = (((L->max_pages & 3) == 0 && L->max_pages <= 2048) ? 1 : 0) | (DSM ? 4 : 0);
     static const int two_env = getenv("TS_SC_TWO") ? atoi(getenv("TS_SC_TWO")) : -1;
     const bool two_ok = two_env == 1 || (two_env != 0 && L->max_pages > 2048);  // long rows only
     static std::mutex mu;
@@ -476,56 +486,68 @@ ts_status launch_step_cluster_t(const ts_layout *L, ScoreSelParams &sp, const At
         int ch = (L->max_pages + c - 1) / c;
         return (ch + kSsStagePages - 1) / kSsStagePages * kSsStagePages;
     };
-    int C = 0, chunk = 0;
-    size_t sm = 0;
     if (two_ok) {  // two-level select: every CTA keeps only its chunk's scores
         for (int c = max_c; c >= 2; --c) {
             const int ch = chunk_of(c), cc = (L->max_pages + ch - 1) / ch;
-            if (sp.kmax % 4 != 0 || (two_env != 1 && L->max_pages < 4 * cc * sp.kmax)) continue;
-            const size_t smc = 1024 + ScSmem<W, R>::bytes(sp.kmax, L->max_pages, sp.flags | 2, cc, ch);
+            if (kmax % 4 != 0 || (two_env != 1 && L->max_pages < 4 * cc * kmax)) continue;
+            const size_t smc = 1024 + ScSmem<W, R>::bytes(kmax, L->max_pages, fl | 2, cc, ch);
             if (smc > 227 * 1024 || !allow(smc)) continue;
             if (max_active_clusters(kern, (W + 1) * 32, smc, cc) >= rows) {
-                C = cc;
-                chunk = ch;
-                sm = smc;
-                sp.flags |= 2;
-                break;
+                pl.ok = true;
+                pl.C = cc;
+                pl.chunk = ch;
+                pl.sm = smc;
+                pl.flags = fl | 2;
+                return pl;
             }
         }
     }
-    if (C == 0) {  // one-level select: the leader gathers the whole row's scores
-        sm = 1024 + ScSmem<W, R>::bytes(sp.kmax, L->max_pages, sp.flags, 1, 0);
-        if (sm > 227 * 1024 || !allow(sm)) return TS_ERR_UNSUPPORTED;
-        int per_sm = 1;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (W + 1) * 32, sm);
-        const int target = device_sms() * std::max(1, per_sm);
-        C = std::max(1, std::min(max_c, target / std::max(1, rows)));
-        for (;; --C) {  // the largest C whose clusters are all co-resident (one wave)
-            chunk = chunk_of(C);
-            const int c = (L->max_pages + chunk - 1) / chunk;
-            if (C == 1 || max_active_clusters(kern, (W + 1) * 32, sm, c) >= rows) {
-                C = c;
-                break;
-            }
+    // one-level select: every CTA selects over the whole row's keys; the largest C whose
+    // clusters are all co-resident (one wave)
+    size_t sm = 1024 + ScSmem<W, R>::bytes(kmax, L->max_pages, fl, 1, 0);
+    if (sm > 227 * 1024 || !allow(sm)) return pl;
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (W + 1) * 32, sm);
+    const int target = device_sms() * std::max(1, per_sm);
+    for (int C = std::max(1, std::min(max_c, target / std::max(1, rows)));; --C) {
+        const int chunk = chunk_of(C);
+        const int c = (L->max_pages + chunk - 1) / chunk;
+        const size_t smc = c == 1 ? sm : 1024 + ScSmem<W, R>::bytes(kmax, L->max_pages, fl, c, chunk);
+        if (c == 1 || (smc <= 227 * 1024 && allow(smc) &&
+                       max_active_clusters(kern, (W + 1) * 32, smc, c) >= rows)) {
+            pl.ok = true;
+            pl.C = c;
+            pl.chunk = chunk;
+            pl.sm = smc;
+            pl.flags = fl;
+            return pl;
         }
     }
+}
+
+template <int W, int R, bool DSM>
+ts_status launch_step(const ts_layout *L, ScoreSelParams &sp, const AttnParams &ap,
+                      const StepPlan &pl, cudaStream_t st) {
+    auto kern = decode_cluster_kernel<W, R, DSM>;
+    const int rows = L->batch * L->num_kv_heads;
     CUtensorMap tmK, tmV;
     if (!make_pool_map(&tmK, ap.k_pool, L, 16) || !make_pool_map(&tmV, ap.v_pool, L, 16))
         return TS_ERR_CUDA;
-    sp.C = C;
-    sp.chunk = chunk;
+    sp.C = pl.C;
+    sp.chunk = pl.chunk;
+    sp.flags = pl.flags;
     // early PDL trigger (the next kernel's prologue overlaps our tail): measured faster with
     // clusters of <= 8 CTAs (C2 / C3 / C4), slower with C5's 13-CTA clusters
     static const int trig_env = getenv("TS_SC_TRIGGER") ? atoi(getenv("TS_SC_TRIGGER")) : -1;
-    if (trig_env == 1 || (trig_env != 0 && C <= 8)) sp.flags |= 8;
+    if (trig_env == 1 || (trig_env != 0 && pl.C <= 8)) sp.flags |= 8;
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(rows * C);
+    cfg.gridDim = dim3(rows * pl.C);
     cfg.blockDim = dim3((W + 1) * 32);
-    cfg.dynamicSmemBytes = sm;
+    cfg.dynamicSmemBytes = pl.sm;
     cfg.stream = st;
     cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = C;
+    at[0].val.clusterDim.x = pl.C;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     static const bool pdl = !getenv("TS_NO_PDL");
@@ -536,6 +558,22 @@ ts_status launch_step_cluster_t(const ts_layout *L, ScoreSelParams &sp, const At
     if (cudaLaunchKernelEx(&cfg, kern, tmK, tmV, sp, ap) != cudaSuccess) return TS_ERR_CUDA;
     ++g_launches;
     return launch_status();
+}
+
+template <int W, int R>
+ts_status launch_step_cluster_t(const ts_layout *L, ScoreSelParams &sp, const AttnParams &ap,
+                                cudaStream_t st) {
+    // DSMEM merge when its merge area costs no cluster width and C <= 8 (measured: faster at
+    // C = 4 (C3); at C = 13 (C5) one SM receiving 13 partials loses to the L2 ticket merge)
+    static const int dsm_env = getenv("TS_SC_DSM") ? atoi(getenv("TS_SC_DSM")) : -1;  // dev knob
+    const StepPlan b = plan_step<W, R, false>(L, sp.kmax);
+    if constexpr (R == 8) {
+        const StepPlan a = plan_step<W, R, true>(L, sp.kmax);
+        if (dsm_env != 0 && a.ok && a.C > 1 && (dsm_env == 1 || !b.ok || (a.C >= b.C && a.C <= 8)))
+            return launch_step<W, R, true>(L, sp, ap, a, st);
+    }
+    if (!b.ok) return TS_ERR_UNSUPPORTED;
+    return launch_step<W, R, false>(L, sp, ap, b, st);
 }
 
 ts_status launch_score_select(const ts_layout *L, const void *q, const void *meta, const int *pt,

@@ -14,7 +14,8 @@
 //  4. attend: consumers run S = Q K^T (mma.m16n8k16), the fp32 online softmax and
 //     O += P V (mma.m16n8k8, tf32 P — R10) per tile, with the q fragments already in
 //     shared memory from step 1; warp partials merge in smem, the C CTA partials of a row
-//     through an L2 workspace (last CTA by atomic ticket).
+//     in the cluster leader's shared memory (DSM instantiation: DSMEM stores, one cluster
+//     arrive / wait) or through an L2 workspace (last CTA by atomic ticket).
 // No kernel boundary, no PDL gap, no second page-list lookup: the step is one launch.
 #pragma once
 #include "attn.cuh"
@@ -42,14 +43,16 @@ struct ScSmem {
     __host__ __device__ static int score_cap(int max_pages, int flags, int chunk) {
         return (flags & 2) ? ((chunk + 3) & ~3) : ((max_pages + 3) & ~3);
     }
+    // ... then the leader's merge area for the C CTA partials [C][8][kPS] fp32 (flag bit 2)
     static size_t bytes(int kmax, int max_pages, int flags, int C, int chunk) {
         const size_t mp4 = (max_pages + 3) & ~3;
         return scores_off(kmax) + (size_t)score_cap(max_pages, flags, chunk) * 4 +
-               ((flags & 1) ? mp4 * 4 : 0) + ((flags & 2) ? (size_t)C * kmax * 8 : 0) + 16;
+               ((flags & 1) ? mp4 * 4 : 0) + ((flags & 2) ? (size_t)C * kmax * 8 : 0) +
+               ((flags & 4) && C > 1 ? (size_t)C * 8 * kPS * 4 : 0) + 16;
     }
 };
 
-template <int W, int R>
+template <int W, int R, bool DSM>
 __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
     const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
     ScoreSelParams p, AttnParams ap) {
@@ -72,6 +75,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
     int *pt_s = reinterpret_cast<int *>(sc) + scap;
     uint32_t *ckey = reinterpret_cast<uint32_t *>(pt_s + (pt_bulk ? mp4 : 0));  // [C * kmax]
     int *cid = reinterpret_cast<int *>(ckey) + p.C * p.kmax;
+    float *mrg = reinterpret_cast<float *>(ckey + ((p.flags & 2) ? 2 * p.C * p.kmax : 0));  // DSM: [C][8][kPS]
     int *hist = reinterpret_cast<int *>(smem + SM::kHist);
     int *red = reinterpret_cast<int *>(smem + SM::kRed);
     float *wpart = reinterpret_cast<float *>(smem + SM::kWarpPart);
@@ -474,6 +478,10 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
             *reinterpret_cast<float4 *>(ap.o + oh * kAttnD + d0) =
                 make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
             if (ap.lse && d0 == 0) ap.lse[oh] = l > 0.f ? (M + log2f(l)) * kLn2 : kNegInf;
+        } else if constexpr (DSM) {  // into the leader's merge area (DSMEM stores)
+            float *pr = cl.map_shared_rank(mrg, 0) + (rank * 8 + h) * kPS;
+            *reinterpret_cast<float4 *>(pr + d0) = acc;
+            if (d0 == 0) *reinterpret_cast<float2 *>(pr + kAttnD) = make_float2(M, l);
         } else {
             float *pr = ap.part + (((size_t)row * C + rank) * 8 + h) * kPS;
             *reinterpret_cast<float4 *>(pr + d0) = acc;
@@ -483,7 +491,36 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
             }
         }
     }
-    if (C > 1) {
+    if constexpr (DSM) {
+        // one cluster arrive (release) publishes this CTA's partial; the leader alone waits
+        // and merges the C partials from its own shared memory (no L2 round trips)
+        if (C > 1) {
+            cluster_arrive_release();
+            if (rank == 0) {
+                cluster_wait();
+                for (int x = tid; x < p.G * 16; x += NT) {
+                    const int h = x >> 4, d0 = (x & 15) * 4;
+                    float M = kNegInf;
+                    for (int r = 0; r < C; ++r) M = fmaxf(M, mrg[(r * 8 + h) * kPS + kAttnD]);
+                    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+                    float l = 0.f;
+                    if (M != kNegInf)
+                        for (int r = 0; r < C; ++r) {
+                            const float *pr = mrg + (r * 8 + h) * kPS;
+                            const float f = pr[kAttnD] == kNegInf ? 0.f : exp2f(pr[kAttnD] - M);
+                            l += pr[kAttnD + 1] * f;
+                            const float4 v = *reinterpret_cast<const float4 *>(pr + d0);
+                            acc.x += v.x * f; acc.y += v.y * f; acc.z += v.z * f; acc.w += v.w * f;
+                        }
+                    const size_t oh = (size_t)b * p.Hq + g * p.G + h;
+                    const float inv = l > 0.f ? 1.f / l : 0.f;
+                    *reinterpret_cast<float4 *>(ap.o + oh * kAttnD + d0) =
+                        make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+                    if (ap.lse && d0 == 0) ap.lse[oh] = l > 0.f ? (M + log2f(l)) * kLn2 : kNegInf;
+                }
+            }
+        }
+    } else if (C > 1) {
         __syncthreads();
         if (tid == 0) {
             __threadfence();
