@@ -118,6 +118,13 @@ TS_DEV uint32_t ld_relaxed_u32(const unsigned *p) {
     asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+// ticket: atomic add with acquire-release semantics at GPU scope (after a CTA barrier, the
+// release is cumulative over the CTA's prior writes; no separate membar round trip)
+TS_DEV uint32_t atom_add_acq_rel_gpu(unsigned *p, unsigned v) {
+    uint32_t old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
 TS_DEV void fence_acquire_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 TS_DEV void st_release_u32(unsigned *p, uint32_t v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");

@@ -522,13 +522,9 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
         }
     } else if (C > 1) {
         __syncthreads();
-        if (tid == 0) {
-            __threadfence();
-            s_last = atomicAdd(ap.tickets + row, 1u) == unsigned(C - 1);
-        }
+        if (tid == 0) s_last = atom_add_acq_rel_gpu(ap.tickets + row, 1u) == unsigned(C - 1);
         __syncthreads();
         if (s_last) {
-            __threadfence();
             constexpr int kMaxC = 16;
             const float *pb = ap.part + (size_t)row * C * 8 * kPS;
             for (int x = tid; x < p.G * 16; x += NT) {
