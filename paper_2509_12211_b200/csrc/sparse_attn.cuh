@@ -536,13 +536,9 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) sparse_attn_tma_kernel(
         // ---- split merge: the last CTA of the row (ticket) combines the C partials from L2
         __shared__ int s_last;
         __syncthreads();
-        if (threadIdx.x == 0) {
-            __threadfence();
-            s_last = atomicAdd(p.tickets + row, 1u) == unsigned(C - 1);
-        }
+        if (threadIdx.x == 0) s_last = atom_add_acq_rel_gpu(p.tickets + row, 1u) == unsigned(C - 1);
         __syncthreads();
         if (s_last) {
-            __threadfence();
             constexpr int kMaxC = 16;
             const float *pb = p.part + (size_t)row * C * 8 * kPS;
             for (int x = threadIdx.x; x < p.G * 16; x += blockDim.x) {

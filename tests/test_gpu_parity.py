@@ -290,7 +290,7 @@ def test_decode_step_integer_ties(ts):
     _step_parity(ts, cfg, case, ref)
 
 
-@pytest.mark.parametrize("cname", ["c2", "c3"])
+@pytest.mark.parametrize("cname", ["c2", "c3", "c4"])
 def test_decode_step_full_size(ts, cname):
     """BASELINE configs at full size, in bench.py's launch configuration."""
     cfg = synth.config(cname)
@@ -299,9 +299,11 @@ def test_decode_step_full_size(ts, cname):
     _step_parity(ts, cfg, case, ref)
 
 
-def test_decode_step_c5_full_context(ts):
-    """C5 shape (512k ctx, S = 64, budget 4096) at batch 1."""
-    cfg = synth.config("c5", batch=1)
+@pytest.mark.parametrize("batch", [1, 4])
+def test_decode_step_c5_full_context(ts, batch):
+    """C5 shape (512k ctx, S = 64, budget 4096); batch 4 = bench.py's launch configuration
+    (two-level select, 13-CTA clusters, L2-ticket merge)."""
+    cfg = synth.config("c5", batch=batch)
     case = synth.make_case(cfg, seed=42, ragged=True)
     ref = oracle.margin.enforce(case, cfg.budget_tokens)
     _step_parity(ts, cfg, case, ref)
