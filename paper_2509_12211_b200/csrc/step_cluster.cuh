@@ -134,26 +134,33 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
 
     // ===================================== 1. score =====================================
     if (warp == W) {
-        if (lane == 0) {
-            const uint64_t pol = l2_policy_evict_first();
+        // the first min(R, stages) ring stages are free: one lane each issues its bulk copy
+        // in parallel (TMA issue is ~100 cycles); lane 0 then refills stages as they drain
+        const uint64_t pol = l2_policy_evict_first();
+        const uint16_t *mrow = p.meta + ((size_t)row * p.max_pages + j0) * 2 * kAttnD;
+        auto issue = [&](int i) {
+            const int st = i % R;
+            const int np = min(kSsStagePages, nloc - i * kSsStagePages);
+            const uint32_t bytes = np * 2 * kRowBytes;
+            mbar_arrive_expect_tx(mfull0 + 8 * st, bytes);
+            bulk_load_hint(sb + st * kSsStageBytes, mrow + (size_t)i * kSsStagePages * 2 * kAttnD, bytes,
+                           mfull0 + 8 * st, pol);
+        };
+        if (lane < R && lane < nst) issue(lane);
+        if (lane == R) {
             mbar_arrive_expect_tx(qbar, p.G * kRowBytes);
             bulk_load(sb + SM::kQ, p.q + ((size_t)b * p.Hq + g * p.G) * kAttnD, p.G * kRowBytes, qbar);
-            if (P > 0 && pt_bulk) {  // every CTA: it maps its own share of the selection
-                const uint32_t ptb = min(((uint32_t)P * 4 + 15) & ~15u, (uint32_t)mp4 * 4);
-                mbar_arrive_expect_tx(ptbar, ptb);
-                bulk_load(smem_u32(pt_s), p.page_table + (size_t)b * p.max_pages, ptb, ptbar);
-            }
-            const uint16_t *mrow = p.meta + ((size_t)row * p.max_pages + j0) * 2 * kAttnD;
-            for (int i = 0; i < nst; ++i) {
-                const int st = i % R;
-                mbar_wait(mempty0 + 8 * st, ((i / R) & 1) ^ 1);
-                const int np = min(kSsStagePages, nloc - i * kSsStagePages);
-                const uint32_t bytes = np * 2 * kRowBytes;
-                mbar_arrive_expect_tx(mfull0 + 8 * st, bytes);
-                bulk_load_hint(sb + st * kSsStageBytes, mrow + (size_t)i * kSsStagePages * 2 * kAttnD,
-                               bytes, mfull0 + 8 * st, pol);
-            }
         }
+        if (lane == R + 1 && P > 0 && pt_bulk) {  // every CTA: it maps its own share of the selection
+            const uint32_t ptb = min(((uint32_t)P * 4 + 15) & ~15u, (uint32_t)mp4 * 4);
+            mbar_arrive_expect_tx(ptbar, ptb);
+            bulk_load(smem_u32(pt_s), p.page_table + (size_t)b * p.max_pages, ptb, ptbar);
+        }
+        if (lane == 0)
+            for (int i = R; i < nst; ++i) {
+                mbar_wait(mempty0 + 8 * (i % R), ((i / R) & 1) ^ 1);
+                issue(i);
+            }
     } else {
         mbar_wait(qbar, 0);
         uint32_t qa[8], qp[8];
@@ -338,21 +345,25 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
     // ===================================== 3-4. gather + attend ==========================
     const float sl2 = ap.scale * kLog2e;
     if (warp == W) {
-        if (lane == 0) {
-            fence_proxy_async();  // the ring was last read by the generic proxy (scoring)
-            const uint64_t pol = l2_policy_evict_first();
-            for (int i = 0; i < t1 - t0; ++i) {
-                const int st = i % RA;
-                mbar_wait(aempty0 + 8 * st, ((i / RA) & 1) ^ 1);
-                const int tl = t0 + i, u = tl / tpp, sub = tl - u * tpp;
-                const int2 pg = sel[u - u0];
-                info[st] = pg.y + 16 * sub;
-                mbar_arrive_expect_tx(afull0 + 8 * st, 2 * 16 * kRowBytes);
-                const uint32_t dst = sb + st * 2 * 16 * kRowBytes;
-                tma_load_2d(dst, &tmK, 0, pg.x + 16 * sub, afull0 + 8 * st, pol);
-                tma_load_2d(dst + 16 * kRowBytes, &tmV, 0, pg.x + 16 * sub, afull0 + 8 * st, pol);
+        fence_proxy_async();  // the ring was last read by the generic proxy (scoring)
+        const uint64_t pol = l2_policy_evict_first();
+        auto issue = [&](int i) {
+            const int st = i % RA;
+            const int tl = t0 + i, u = tl / tpp, sub = tl - u * tpp;
+            const int2 pg = sel[u - u0];
+            info[st] = pg.y + 16 * sub;
+            mbar_arrive_expect_tx(afull0 + 8 * st, 2 * 16 * kRowBytes);
+            const uint32_t dst = sb + st * 2 * 16 * kRowBytes;
+            tma_load_2d(dst, &tmK, 0, pg.x + 16 * sub, afull0 + 8 * st, pol);
+            tma_load_2d(dst + 16 * kRowBytes, &tmV, 0, pg.x + 16 * sub, afull0 + 8 * st, pol);
+        };
+        const int nt = t1 - t0;
+        if (lane < RA && lane < nt) issue(lane);  // the free stages: lane-parallel issue
+        if (lane == 0)
+            for (int i = RA; i < nt; ++i) {  // refills in order, as the consumers drain
+                mbar_wait(aempty0 + 8 * (i % RA), ((i / RA) & 1) ^ 1);
+                issue(i);
             }
-        }
     } else {
         uint32_t qa[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         if (gid < p.G) {
