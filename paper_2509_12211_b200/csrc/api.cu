@@ -539,7 +539,8 @@ ts_status launch_step(const ts_layout *L, ScoreSelParams &sp, const AttnParams &
     // early PDL trigger (the next kernel's prologue overlaps our tail): measured faster with
     // clusters of <= 8 CTAs (C2 / C3 / C4), slower with C5's 13-CTA clusters
     static const int trig_env = getenv("TS_SC_TRIGGER") ? atoi(getenv("TS_SC_TRIGGER")) : -1;
-    if (trig_env == 1 || (trig_env != 0 && pl.C <= 8)) sp.flags |= 8;
+    if (trig_env == 1 || (trig_env < 0 && pl.C <= 8)) sp.flags |= 8;
+    if (trig_env == 2) sp.flags |= 16;  // late trigger (after the attention loop)
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(rows * pl.C);
     cfg.blockDim = dim3((W + 1) * 32);

@@ -100,24 +100,17 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
     // the next kernel in the stream (the next layer / step) may be scheduled as our CTAs
     // retire: its prologue overlaps our tail; it waits for our completion before any read
     if (p.flags & 8) pdl_launch_dependents();  // (host: measured faster up to 8-CTA clusters)
-    if (tid == 0) {
-        prefetch_tmap(&tmK);
-        prefetch_tmap(&tmV);
-        for (int i = 0; i < R; ++i) {
-            mbar_init(mfull0 + 8 * i, 1);
-            mbar_init(mempty0 + 8 * i, 1);
-        }
-        for (int i = 0; i < RA; ++i) {
-            mbar_init(afull0 + 8 * i, 1);
-            mbar_init(aempty0 + 8 * i, 1);
-        }
-        mbar_init(qbar, 1);
-        mbar_init(ptbar, 1);
+    if (warp == 0) {  // the 6R + 2 consecutive mbarriers (all count 1), one per lane
+        for (int i = lane; i < 6 * R + 2; i += 32) mbar_init(mfull0 + 8 * i, 1);
         fence_mbar_init();
-        *s_kmin = 0xffffffffu;
-        *s_kmax = 0u;
+        if (lane == 0) {
+            *s_kmin = 0xffffffffu;
+            *s_kmax = 0u;
+        }
+    } else if (warp == 1 && lane < 2) {
+        prefetch_tmap(lane ? &tmV : &tmK);
     }
-    for (int i = tid; i < kSsHist; i += NT) hist[i] = 0;
+    for (int i = tid; i < kSsHist / 4; i += NT) reinterpret_cast<int4 *>(hist)[i] = make_int4(0, 0, 0, 0);
     __syncthreads();
     // "this CTA is running" (before any DSMEM access); release: its initialised counters
     // and histogram are visible to the remote updates that follow the matching wait
@@ -278,7 +271,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
             reinterpret_cast<int4 *>(cl.map_shared_rank(cid, peer) + rank * p.kmax)[u] =
                 reinterpret_cast<const int4 *>(myi)[u];
         }
-        for (int i = tid; i < kSsHist; i += NT) hist[i] = 0;
+        for (int i = tid; i < kSsHist / 4; i += NT) reinterpret_cast<int4 *>(hist)[i] = make_int4(0, 0, 0, 0);
         cluster_arrive_release();
         cluster_wait();
     } else {
@@ -462,6 +455,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
     }
     __syncthreads();
     SC_STAMP(4);
+    if (p.flags & 16) pdl_launch_dependents();  // late trigger: only the merge / tail remains
     // ---- CTA merge of the W warp partials (C == 1: straight to o / lse)
     for (int x = tid; x < p.G * 16; x += NT) {
         const int h = x >> 4, d0 = (x & 15) * 4;
