@@ -554,8 +554,8 @@ def dense_leg(ts, cfg, reps, R, stream, dev, args, ms_per_step):
 
 def run_e2e(ts, cfg, reps, dev, stream, steps, warmup):
     """Same metric through the public API with host buffers.  Every step: its inputs q,
-    k_new, v_new (one pinned buffer) go H2D, ts_meta_append rewrites the newest token of
-    every sequence (length kept, so the workload stays the config's), ts_decode_step runs,
+    k_new, v_new (one pinned buffer) go H2D, ts_decode_step_append rewrites the newest token
+    of every sequence (length kept, so the workload stays the config's) and runs the step,
     and its o and lse (one buffer) come back D2H into pinned memory.  The copies run on a
     second stream with double-buffered staging, so step i's H2D / D2H overlap the kernels of
     steps i -/+ 1 (a step's inputs do not depend on the previous step's outputs here); each
@@ -568,7 +568,6 @@ def run_e2e(ts, cfg, reps, dev, stream, steps, warmup):
     hout = [torch.empty(no, dtype=torch.float32).pin_memory() for _ in range(2)]
     din = [torch.empty_like(hin[0], device=dev) for _ in range(2)]
     dout = [torch.empty(no, dtype=torch.float32, device=dev) for _ in range(2)]
-    pos = [(rep["seq_lens"] - 1).contiguous() for rep in reps]  # append at the last token
     h2d_s = torch.cuda.Stream(device=dev)  # separate copy streams: an H2D never queues
     d2h_s = torch.cuda.Stream(device=dev)  # behind a D2H that waits for the previous step
     R = len(reps)
@@ -597,12 +596,13 @@ def run_e2e(ts, cfg, reps, dev, stream, steps, warmup):
             dk = x[nq:nq + nk].view(B, Hkv, d)
             dv = x[nq + nk:].view(B, Hkv, d)
             y = dout[sl]
-            ts.meta_append(rep["layout"], dk, dv, pos[i % R], rep["page_table"], rep["k_pool"],
-                           rep["v_pool"], rep["meta"], advance=False, stream=stream)
-            ts.decode_step(rep["layout"], dq, rep["k_pool"], rep["v_pool"], rep["meta"],
-                           rep["page_table"], rep["seq_lens"], cfg.budget_tokens, cfg.scale,
-                           o=y[:B * Hq * d].view(B, Hq, d), lse=y[B * Hq * d:].view(B, Hq),
-                           sel_ids=rep["ids"], sel_count=rep["cnt"], ws=rep["ws"], stream=stream)
+            # append the step's token (slot seq_len - 1: the length is kept, so the workload
+            # stays the config's) and run the step: one launch (ts_decode_step_append)
+            ts.decode_step_append(rep["layout"], dq, dk, dv, rep["k_pool"], rep["v_pool"],
+                                  rep["meta"], rep["page_table"], rep["seq_lens"],
+                                  cfg.budget_tokens, cfg.scale, o=y[:B * Hq * d].view(B, Hq, d),
+                                  lse=y[B * Hq * d:].view(B, Hq), sel_ids=rep["ids"],
+                                  sel_count=rep["cnt"], ws=rep["ws"], stream=stream)
             ev_done[i].record(stream)
             with torch.cuda.stream(d2h_s):  # D2H of step i
                 d2h_s.wait_event(ev_done[i])
@@ -637,9 +637,10 @@ def run_e2e(ts, cfg, reps, dev, stream, steps, warmup):
     d2h = hout[0].numel() * 4
     return {"value": 1e3 / ms, "unit": "steps/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "ms_per_step": ms, "steps": n * n_chain,
-            "api": "paper_2509_12211_b200.meta_append + decode_step (ctypes -> C ABI); per step one "
-                   "pinned H2D of [q|k_new|v_new] and one D2H of [o|lse] on two copy streams, double-"
-                   "buffered and overlapped with the neighbouring steps' kernels; CUDA graphs"}
+            "api": "paper_2509_12211_b200.decode_step_append (ctypes -> C ABI: ts_decode_step_append, "
+                   "the token append fused into the step's one launch); per step one pinned H2D of "
+                   "[q|k_new|v_new] and one D2H of [o|lse] on two copy streams, double-buffered and "
+                   "overlapped with the neighbouring steps' kernels; CUDA graphs"}
 
 
 if __name__ == "__main__":

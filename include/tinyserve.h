@@ -10,6 +10,7 @@
  *   ts_select_topk        top-K pages per (sequence, kv head)    PAPER.md:162-167; Alg. 1 Step 2
  *   ts_sparse_decode_attn softmax attention over selected pages  PAPER.md:169-172; Alg. 1 Steps 3-4
  *   ts_decode_step        score -> select -> attend in one call  Alg. 1, PAPER.md:209-249 ("single pass")
+ *   ts_decode_step_append append the new token, then the step     Eq. 1 + Alg. 1 (one launch, bf16)
  *   ts_lse_merge          merge of partial attentions (split-K / multi-GPU)
  *
  * Conventions (apply to every entry point):
@@ -157,6 +158,25 @@ ts_status ts_decode_step(const ts_layout *layout, const void *q, const void *k_p
                          const int32_t *seq_lens, int32_t budget_tokens, float scale, float *o,
                          float *lse, int32_t *sel_ids_out, int32_t *sel_count_out, void *ws,
                          size_t ws_bytes, void *stream);
+
+/* ts_decode_step_append — one decode step of a serving loop: append the newest token, then
+ * Alg. 1.  For every sequence b with seq_lens[b] = t + 1 > 0 (seq_lens
+ * ALREADY counts the new token), k_new[b] / v_new[b] ([batch][num_kv_heads][head_dim],
+ * kv_dtype, device) are written to slot t % page_size of the block holding logical page
+ * t / page_size, the (m, M) record of that page is updated as ts_meta_append does (Eq. 1,
+ * PAPER.md:177-178; m = M = k for the first key of a page), and then the step runs exactly
+ * as ts_decode_step with the same arguments — in ONE launch for the bf16 cluster path (the
+ * page's scorer patches its staged record and persists it; the K/V row is published to the
+ * attention phase by the cluster barrier).  Other layouts fall back to ts_meta_append's
+ * kernel followed by ts_decode_step.  k_pool, v_pool and meta are modified in place; the
+ * results equal ts_meta_append(seq_lens - 1) followed by ts_decode_step bit for bit in the
+ * metadata and the page sets.  Unsharded layouts only (TS_ERR_UNSUPPORTED otherwise). */
+ts_status ts_decode_step_append(const ts_layout *layout, const void *q, const void *k_new,
+                                const void *v_new, void *k_pool, void *v_pool, void *meta,
+                                const int32_t *page_table, const int32_t *seq_lens,
+                                int32_t budget_tokens, float scale, float *o, float *lse,
+                                int32_t *sel_ids, int32_t *sel_count, void *ws, size_t ws_bytes,
+                                void *stream);
 
 /* Candidate merge — the exchange step of sequence sharding: the global
  * top-k over the union of per-rank candidate lists.  Part p (< parts) of row r holds k_part

@@ -18,7 +18,7 @@ import torch
 from ._lib import Layout, TinyServeError, TS_BF16, TS_F32, check, exported_symbols, lib
 
 __all__ = ["Layout", "TinyServeError", "make_layout", "meta_append", "meta_build",
-           "score_pages", "select_topk", "sparse_decode_attn", "decode_step", "select_merge", "lse_merge",
+           "score_pages", "select_topk", "sparse_decode_attn", "decode_step", "decode_step_append", "select_merge", "lse_merge",
            "workspace_bytes", "attn_workspace_bytes", "dense_decode_attn", "dense_workspace_bytes", "new_workspace", "new_meta", "kmax", "launch_count",
            "profile_events",
            "exported_symbols", "PagedKV"]
@@ -214,6 +214,34 @@ def decode_step(layout, q, k_pool, v_pool, meta, page_table, seq_lens, budget_to
         layout, _ptr(q), _ptr(k_pool), _ptr(v_pool), _ptr(meta), _ptr(page_table), _ptr(seq_lens),
         int(budget_tokens), float(scale), _ptr(o), _ptr(lse), _ptr(sel_ids), _ptr(sel_count),
         _ptr(ws), ws.numel(), _stream(stream)))
+    return o, lse, sel_ids, sel_count
+
+
+def decode_step_append(layout, q, k_new, v_new, k_pool, v_pool, meta, page_table, seq_lens,
+                       budget_tokens, scale, o=None, lse=None, sel_ids=None, sel_count=None, ws=None,
+                       want_lse=True, want_selection=True, stream=None):
+    """Serving-loop step: append the newest token (slot seq_lens - 1: seq_lens already counts
+    it) into k_pool / v_pool / meta, then Alg. 1 — one launch on the bf16 cluster path.
+    Returns (o, lse, sel_ids, sel_count)."""
+    dev = q.device
+    K = kmax(layout, budget_tokens)
+    if o is None:
+        o = torch.empty((layout.batch, layout.num_q_heads, layout.head_dim), dtype=torch.float32,
+                        device=dev)
+    if lse is None and want_lse:
+        lse = torch.empty((layout.batch, layout.num_q_heads), dtype=torch.float32, device=dev)
+    if want_selection:
+        if sel_ids is None:
+            sel_ids = torch.empty((layout.batch, layout.num_kv_heads, K), dtype=torch.int32, device=dev)
+        if sel_count is None:
+            sel_count = torch.empty((layout.batch, layout.num_kv_heads), dtype=torch.int32, device=dev)
+    if ws is None:
+        ws = new_workspace(workspace_bytes(layout, budget_tokens), dev)
+    _cuda(q, k_new, v_new, k_pool, v_pool, meta, page_table, seq_lens, o, lse, sel_ids, sel_count, ws)
+    check("ts_decode_step_append", lib().ts_decode_step_append(
+        layout, _ptr(q), _ptr(k_new), _ptr(v_new), _ptr(k_pool), _ptr(v_pool), _ptr(meta),
+        _ptr(page_table), _ptr(seq_lens), int(budget_tokens), float(scale), _ptr(o), _ptr(lse),
+        _ptr(sel_ids), _ptr(sel_count), _ptr(ws), ws.numel(), _stream(stream)))
     return o, lse, sel_ids, sel_count
 
 

@@ -450,9 +450,9 @@ struct StepPlan {
     size_t sm = 0;
 };
 
-template <int W, int R, bool DSM>
+template <int W, int R, bool DSM, bool APP>
 StepPlan plan_step(const ts_layout *L, int kmax) {
-    auto kern = decode_cluster_kernel<W, R, DSM>;
+    auto kern = decode_cluster_kernel<W, R, DSM, APP>;
     StepPlan pl;
     const int rows = L->batch * L->num_kv_heads;
     // flags: bit 0 page-table row prefetched to smem (rows up to 2048 pages); bit 1
@@ -525,10 +525,10 @@ StepPlan plan_step(const ts_layout *L, int kmax) {
     }
 }
 
-template <int W, int R, bool DSM>
+template <int W, int R, bool DSM, bool APP>
 ts_status launch_step(const ts_layout *L, ScoreSelParams &sp, const AttnParams &ap,
                       const StepPlan &pl, cudaStream_t st) {
-    auto kern = decode_cluster_kernel<W, R, DSM>;
+    auto kern = decode_cluster_kernel<W, R, DSM, APP>;
     const int rows = L->batch * L->num_kv_heads;
     CUtensorMap tmK, tmV;
     if (!make_pool_map(&tmK, ap.k_pool, L, 16) || !make_pool_map(&tmV, ap.v_pool, L, 16))
@@ -561,20 +561,29 @@ ts_status launch_step(const ts_layout *L, ScoreSelParams &sp, const AttnParams &
     return launch_status();
 }
 
-template <int W, int R>
-ts_status launch_step_cluster_t(const ts_layout *L, ScoreSelParams &sp, const AttnParams &ap,
-                                cudaStream_t st) {
+template <int W, int R, bool APP>
+ts_status launch_step_cluster_app(const ts_layout *L, ScoreSelParams &sp, const AttnParams &ap,
+                                 cudaStream_t st) {
     // DSMEM merge when its merge area costs no cluster width and C <= 8 (measured: faster at
     // C = 4 (C3); at C = 13 (C5) one SM receiving 13 partials loses to the L2 ticket merge)
     static const int dsm_env = getenv("TS_SC_DSM") ? atoi(getenv("TS_SC_DSM")) : -1;  // dev knob
-    const StepPlan b = plan_step<W, R, false>(L, sp.kmax);
+    const StepPlan b = plan_step<W, R, false, APP>(L, sp.kmax);
     if constexpr (R == 8) {
-        const StepPlan a = plan_step<W, R, true>(L, sp.kmax);
+        const StepPlan a = plan_step<W, R, true, APP>(L, sp.kmax);
         if (dsm_env != 0 && a.ok && a.C > 1 && (dsm_env == 1 || !b.ok || (a.C >= b.C && a.C <= 8)))
-            return launch_step<W, R, true>(L, sp, ap, a, st);
+            return launch_step<W, R, true, APP>(L, sp, ap, a, st);
     }
     if (!b.ok) return TS_ERR_UNSUPPORTED;
-    return launch_step<W, R, false>(L, sp, ap, b, st);
+    return launch_step<W, R, false, APP>(L, sp, ap, b, st);
+}
+
+// the fused-append instantiation (APP) only when the call appends: the plain step keeps the
+// leaner kernel (measured ~3 % on every config)
+template <int W, int R>
+ts_status launch_step_cluster_t(const ts_layout *L, ScoreSelParams &sp, const AttnParams &ap,
+                                cudaStream_t st) {
+    return sp.k_new ? launch_step_cluster_app<W, R, true>(L, sp, ap, st)
+                    : launch_step_cluster_app<W, R, false>(L, sp, ap, st);
 }
 
 ts_status launch_score_select(const ts_layout *L, const void *q, const void *meta, const int *pt,
@@ -702,10 +711,21 @@ size_t ts_workspace_bytes(const ts_layout *L, int32_t budget_tokens) {
     return step_ws_layout(L, kmax_of(L, budget_tokens)).total;
 }
 
+static ts_status meta_append_impl(const ts_layout *L, const void *k_new, const void *v_new,
+                                  int32_t *seq_lens, int32_t advance, const int32_t *page_table,
+                                  void *k_pool, void *v_pool, void *meta, void *stream);
+
 ts_status ts_meta_append(const ts_layout *L, const void *k_new, const void *v_new,
                          int32_t *seq_lens, int32_t advance, const int32_t *page_table,
                          void *k_pool, void *v_pool, void *meta, void *stream) {
     g_launches = 0;
+    return meta_append_impl(L, k_new, v_new, seq_lens, advance != 0 ? 1 : 0, page_table, k_pool,
+                            v_pool, meta, stream);
+}
+
+static ts_status meta_append_impl(const ts_layout *L, const void *k_new, const void *v_new,
+                                  int32_t *seq_lens, int32_t advance, const int32_t *page_table,
+                                  void *k_pool, void *v_pool, void *meta, void *stream) {
     ts_status s = check_layout(L);
     if (s != TS_OK) return s;
     if (!aligned16(k_new) || !aligned16(v_new) || !aligned16(k_pool) || !aligned16(v_pool) ||
@@ -786,12 +806,44 @@ ts_status ts_sparse_decode_attn(const ts_layout *L, const void *q, const void *k
                        scale, o, lse, ws, as_stream(stream));
 }
 
+static ts_status decode_step_impl(const ts_layout *L, const void *q, const void *k_new,
+                                  const void *v_new, const void *k_pool, const void *v_pool,
+                                  const void *meta, const int32_t *page_table,
+                                  const int32_t *seq_lens, int32_t budget_tokens, float scale,
+                                  float *o, float *lse, int32_t *sel_ids_out,
+                                  int32_t *sel_count_out, void *ws, size_t ws_bytes, void *stream);
+
 ts_status ts_decode_step(const ts_layout *L, const void *q, const void *k_pool, const void *v_pool,
                          const void *meta, const int32_t *page_table, const int32_t *seq_lens,
                          int32_t budget_tokens, float scale, float *o, float *lse,
                          int32_t *sel_ids_out, int32_t *sel_count_out, void *ws, size_t ws_bytes,
                          void *stream) {
     g_launches = 0;
+    return decode_step_impl(L, q, nullptr, nullptr, k_pool, v_pool, meta, page_table, seq_lens,
+                            budget_tokens, scale, o, lse, sel_ids_out, sel_count_out, ws, ws_bytes,
+                            stream);
+}
+
+ts_status ts_decode_step_append(const ts_layout *L, const void *q, const void *k_new,
+                                const void *v_new, void *k_pool, void *v_pool, void *meta,
+                                const int32_t *page_table, const int32_t *seq_lens,
+                                int32_t budget_tokens, float scale, float *o, float *lse,
+                                int32_t *sel_ids_out, int32_t *sel_count_out, void *ws,
+                                size_t ws_bytes, void *stream) {
+    g_launches = 0;
+    if (!k_new || !v_new) return TS_ERR_CONFIG;
+    if (!aligned16(k_new) || !aligned16(v_new)) return TS_ERR_ALIGN;
+    return decode_step_impl(L, q, k_new, v_new, k_pool, v_pool, meta, page_table, seq_lens,
+                            budget_tokens, scale, o, lse, sel_ids_out, sel_count_out, ws, ws_bytes,
+                            stream);
+}
+
+static ts_status decode_step_impl(const ts_layout *L, const void *q, const void *k_new,
+                                  const void *v_new, const void *k_pool, const void *v_pool,
+                                  const void *meta, const int32_t *page_table,
+                                  const int32_t *seq_lens, int32_t budget_tokens, float scale,
+                                  float *o, float *lse, int32_t *sel_ids_out,
+                                  int32_t *sel_count_out, void *ws, size_t ws_bytes, void *stream) {
     ts_status s = check_layout(L);
     if (s != TS_OK) return s;
     if (budget_tokens < 1) return TS_ERR_CONFIG;
@@ -830,6 +882,8 @@ ts_status ts_decode_step(const ts_layout *L, const void *q, const void *k_pool, 
         sp.max_pages = L->max_pages;
         sp.kmax = kmax;
         sp.dbg = g_dbg_ss;
+        sp.k_new = static_cast<const uint16_t *>(k_new);  // fused append (nullable)
+        sp.v_new = static_cast<const uint16_t *>(v_new);
         AttnParams ap = attn_params(L, q, k_pool, v_pool, page_table, seq_lens, ids, cnt, kmax, scale,
                                     o, lse, ws);
         phase_mark(0, st);
@@ -844,6 +898,13 @@ ts_status ts_decode_step(const ts_layout *L, const void *q, const void *k_pool, 
             return s;
         }
     }
+    if (k_new) {  // not fused here: append first (slot seq_len - 1), then the plain step
+        if ((s = meta_append_impl(L, k_new, v_new, const_cast<int32_t *>(seq_lens), -1, page_table,
+                                  const_cast<void *>(k_pool), const_cast<void *>(v_pool),
+                                  const_cast<void *>(meta), stream)) != TS_OK)
+            return s;
+    }
+    const int pre = k_new ? 1 : 0;  // launches so far
     if (L->kv_dtype == TS_BF16 && group_of(L) <= 8 && L->head_dim == 64) {
         // score + select (cluster per row) -> sparse attention (PDL, blocks pre-resolved)
         int *blk = reinterpret_cast<int *>(wb + w.sel_blk);
@@ -861,10 +922,11 @@ ts_status ts_decode_step(const ts_layout *L, const void *q, const void *k_pool, 
             if ((s = launch_sparse_attn(L, p, pdl, st)) != TS_OK) return s;
         }
         phase_mark(3, st);
-        g_launches = rows > 0 ? 2 : 1;
+        g_launches = pre + (rows > 0 ? 2 : 1);
         return TS_OK;
     }
-    int launches = 0;
+    int launches = pre;
+    g_launches = 0;
     phase_mark(0, st);
     if ((s = launch_score(L, q, meta, page_table, seq_lens, scores, st)) != TS_OK) return s;
     phase_mark(1, st);

@@ -79,6 +79,9 @@ TS_DEV void mbar_init(uint32_t bar, uint32_t count) {
 }
 TS_DEV void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 TS_DEV void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+// generic-proxy writes (shared or global) ordered before this thread's later async-proxy
+// (TMA / bulk copy) accesses
+TS_DEV void fence_proxy_async_all() { asm volatile("fence.proxy.async;" ::: "memory"); }
 TS_DEV void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
                  : "memory");

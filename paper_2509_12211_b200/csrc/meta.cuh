@@ -56,12 +56,14 @@ __global__ void meta_append_kernel(MetaParams p, const T *__restrict__ k_new,
     const int cpr = p.D / V::kElems;
     const int b = blockIdx.x;
     const int h = threadIdx.x / cpr, c = threadIdx.x % cpr;
-    const int t = seq_lens[b];
-    if (advance) {  // every thread has read t; then one thread publishes t + 1
+    // advance < 0 (internal, ts_decode_step_append fallback): seq_lens already counts the
+    // new token, which goes to slot t = seq_len - 1
+    const int t = seq_lens[b] + (advance < 0 ? -1 : 0);
+    if (advance > 0) {  // every thread has read t; then one thread publishes t + 1
         __syncthreads();
         if (threadIdx.x == 0) seq_lens[b] = t + 1;
     }
-    if (h >= p.Hkv) return;
+    if (h >= p.Hkv || t < 0) return;
     const int j = t / p.S, slot = t % p.S;
     if (j % p.stride != p.offset) return;  // page owned by another rank
     const int jl = j / p.stride;

@@ -40,6 +40,10 @@ struct ScoreSelParams {
     int C;                    // CTAs per row (cluster size)
     int chunk;                // pages per CTA (multiple of 32)
     unsigned long long *dbg;  // development: per-CTA stamps (nullable)
+    // step_cluster, ts_decode_step_append: the newest token of every row (t = seq_len - 1)
+    // to append before scoring (nullable: plain decode step)
+    const uint16_t *k_new;    // [B][Hkv][64]
+    const uint16_t *v_new;    // [B][Hkv][64]
 };
 
 constexpr int kSsStagePages = 32;                         // pages per ring stage

@@ -52,7 +52,7 @@ struct ScSmem {
     }
 };
 
-template <int W, int R, bool DSM>
+template <int W, int R, bool DSM, bool APP>
 __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
     const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
     ScoreSelParams p, AttnParams ap) {
@@ -122,6 +122,12 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
     const int j0 = rank * p.chunk;
     const int nloc = max(0, min(P - j0, p.chunk));
     const int sb0 = two ? 0 : j0;  // index of this CTA's first page in sc[]
+    // fused append (ts_decode_step_append, Eq. 1 / SPEC.md:56-59): the row's newest token
+    // t = L - 1 goes into its K/V slot and into the min/max record of its page before that
+    // page is scored; the CTA whose chunk holds the page does both
+    const bool app = APP && L > 0;  // APP instantiation: p.k_new / p.v_new are set
+    const int ja = app ? (L - 1) / p.S : -1, aslot = app ? (L - 1) - ja * p.S : 0;
+    const bool own = app && ja >= j0 && ja < j0 + nloc;
     const int nst = (nloc + kSsStagePages - 1) / kSsStagePages;
     const int gid = lane >> 2, t = lane & 3;
 
@@ -149,6 +155,17 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
             mbar_arrive_expect_tx(ptbar, ptb);
             bulk_load(smem_u32(pt_s), p.page_table + (size_t)b * p.max_pages, ptb, ptbar);
         }
+        if (own && lane >= 16 && lane < 24) {  // the new token's K and V rows (16 B per lane)
+            const int c = lane - 16;
+            const int blk = p.page_table[(size_t)b * p.max_pages + ja];
+            const size_t src = ((size_t)b * p.Hkv + g) * kAttnD + c * 8;
+            const size_t dst = (((size_t)blk * p.Hkv + g) * p.S + aslot) * kAttnD + c * 8;
+            uint16_t *kp = const_cast<uint16_t *>(static_cast<const uint16_t *>(ap.k_pool));
+            uint16_t *vp = const_cast<uint16_t *>(static_cast<const uint16_t *>(ap.v_pool));
+            *reinterpret_cast<uint4 *>(kp + dst) = *reinterpret_cast<const uint4 *>(p.k_new + src);
+            *reinterpret_cast<uint4 *>(vp + dst) = *reinterpret_cast<const uint4 *>(p.v_new + src);
+            fence_proxy_async_all();  // before the attention phase's TMA reads of this page
+        }
         if (lane == 0)
             for (int i = R; i < nst; ++i) {
                 mbar_wait(mempty0 + 8 * (i % R), ((i / R) & 1) ^ 1);
@@ -173,10 +190,36 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
         }
         const bool c0 = 2 * t < p.G, c1 = 2 * t + 1 < p.G;
         uint32_t kmn = 0xffffffffu, kmx = 0u;
+        const int apl = own ? ja - j0 : -1;  // the appended page, chunk-local
+        uint4 kn = make_uint4(0, 0, 0, 0);
+        if (own && lane < 16 && (apl / kSsStagePages) % W == warp)
+            kn = *reinterpret_cast<const uint4 *>(p.k_new + ((size_t)b * p.Hkv + g) * kAttnD + (lane & 7) * 8);
         for (int i = warp; i < nst; i += W) {
             const int st = i % R;
             mbar_wait(mfull0 + 8 * st, (i / R) & 1);
             const uint32_t kb = sb + st * kSsStageBytes;
+            if (apl >= i * kSsStagePages && apl < (i + 1) * kSsStagePages) {  // warp-uniform
+                if (lane < 16) {  // lanes 0-7: the m row, 8-15: the M row (16 B each)
+                    const uint32_t a = kb + (apl - i * kSsStagePages) * 2 * kRowBytes + (lane >> 3) * kRowBytes +
+                                       (lane & 7) * 16;
+                    uint4 v = lds_v4(a);
+                    if (aslot == 0) {  // first key of the page: m = M = k
+                        v = kn;
+                    } else if (lane < 8) {
+                        v = make_uint4(bf16x2_min(v.x, kn.x), bf16x2_min(v.y, kn.y), bf16x2_min(v.z, kn.z),
+                                       bf16x2_min(v.w, kn.w));
+                    } else {
+                        v = make_uint4(bf16x2_max(v.x, kn.x), bf16x2_max(v.y, kn.y), bf16x2_max(v.z, kn.z),
+                                       bf16x2_max(v.w, kn.w));
+                    }
+                    sts_v4(a, v);
+                    uint16_t *mrec = const_cast<uint16_t *>(p.meta) + ((size_t)row * p.max_pages + ja) * 2 * kAttnD +
+                                     (lane >> 3) * kAttnD + (lane & 7) * 8;
+                    *reinterpret_cast<uint4 *>(mrec) = v;  // the cache's record (logical layout)
+                    fence_proxy_async();  // generic smem write before the stage's next TMA fill
+                }
+                __syncwarp();
+            }
 #pragma unroll
             for (int tile = 0; tile < 2; ++tile) {
                 const uint32_t tb = kb + tile * 16 * 2 * kRowBytes;
@@ -234,7 +277,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
     // exact, as a page of the row's top-K is beaten by fewer than K pages of its own chunk
     // (same order: score, then lower id), so it is among its chunk's candidates.
     cg::cluster_group cl = cg::this_cluster();
-    const int S = p.S, tpp = S >> 4;
+    const int S = p.S, tpp = S >> 4, tps = __ffs(tpp) - 1;  // tiles per page (power of 2), log2
     const int kk = min(p.kmax, P);  // the selection size is known before the select
     const int ntile = kk * tpp;
     const int t0 = (int)((long long)ntile * rank / C), t1 = (int)((long long)ntile * (rank + 1) / C);
@@ -338,13 +381,17 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
     // ===================================== 3-4. gather + attend ==========================
     const float sl2 = ap.scale * kLog2e;
     if (warp == W) {
-        fence_proxy_async();  // the ring was last read by the generic proxy (scoring)
+        // the ring was last accessed by the generic proxy (scoring); APP: the appended K/V
+        // row (another CTA's generic stores, published by the cluster barrier) is read by TMA
+        if constexpr (APP)
+            fence_proxy_async_all();
+        else
+            fence_proxy_async();
         const uint64_t pol = l2_policy_evict_first();
         auto issue = [&](int i) {
             const int st = i % RA;
-            const int tl = t0 + i, u = tl / tpp, sub = tl - u * tpp;
+            const int tl = t0 + i, u = tl >> tps, sub = tl & (tpp - 1);
             const int2 pg = sel[u - u0];
-            info[st] = pg.y + 16 * sub;
             mbar_arrive_expect_tx(afull0 + 8 * st, 2 * 16 * kRowBytes);
             const uint32_t dst = sb + st * 2 * 16 * kRowBytes;
             tma_load_2d(dst, &tmK, 0, pg.x + 16 * sub, afull0 + 8 * st, pol);
@@ -371,8 +418,10 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
         for (int j = 0; j < 8; ++j) oacc[j][0] = oacc[j][1] = oacc[j][2] = oacc[j][3] = 0.f;
         for (int i = warp; i < t1 - t0; i += W) {
             const int st = i % RA;
+            // the tile's first token, from sel[] (complete before the barrier), ahead of the wait
+            const int tl = t0 + i, tu = tl >> tps;
+            const int tok0 = sel[tu - u0].y + 16 * (tl & (tpp - 1));
             mbar_wait(afull0 + 8 * st, (i / RA) & 1);
-            const int tok0 = info[st];
             const uint32_t kb = sb + st * 2 * 16 * kRowBytes, vb = kb + 16 * kRowBytes;
             float sacc[2][4];
 #pragma unroll

@@ -261,6 +261,43 @@ def test_decode_step(ts, name):
     _step_parity(ts, cfg, case, ref)
 
 
+@pytest.mark.parametrize("name", ["c3_small", "c2_small", "two_level", "g4_s32", "g6_s64", "g3_s16"])
+def test_decode_step_append(ts, name):
+    """ts_decode_step_append == ts_meta_append then the step: the newest
+    token of every row is taken out of the cache (its slot garbage, the metadata built
+    without it), handed in as k_new / v_new, and the call must restore the cache exactly
+    (pools and the oracle's batch metadata bit for bit) and produce the oracle's step."""
+    cfg, case = make(name, seed=23)
+    ref = oracle.margin.enforce(case, cfg.budget_tokens)  # the step on the FULL cache
+    S = cfg.page_size
+    pt = case["page_table"].numpy()
+    lens = case["seq_lens"]
+    B, Hkv, d = cfg.batch, cfg.num_kv_heads, cfg.head_dim
+    kp, vp = case["k_pool"].clone(), case["v_pool"].clone()
+    k_new = torch.zeros(B, Hkv, d, dtype=kp.dtype)
+    v_new = torch.zeros_like(k_new)
+    for b, L in enumerate(lens.tolist()):
+        if L > 0:
+            blk, sl = pt[b, (L - 1) // S], (L - 1) % S
+            k_new[b], v_new[b] = kp[blk, :, sl], vp[blk, :, sl]
+            kp[blk, :, sl], vp[blk, :, sl] = 7.0, -3.0  # stale slot content
+    dq, dpt, dl = case["q"].to(DEV), case["page_table"].to(DEV), lens.to(DEV)
+    dkp, dvp = kp.to(DEV), vp.to(DEV)
+    L_ = ts.make_layout(dq, dkp, dpt)
+    meta = ts.meta_build(L_, dkp, dpt, torch.clamp(dl - 1, min=0).to(torch.int32))
+    o, lse, ids, cnt = ts.decode_step_append(L_, dq, k_new.to(DEV), v_new.to(DEV), dkp, dvp, meta,
+                                             dpt, dl, cfg.budget_tokens, cfg.scale)
+    same = lambda a, b: torch.equal(a.contiguous().view(torch.uint8), b.contiguous().view(torch.uint8))
+    assert same(dkp.cpu(), case["k_pool"]) and same(dvp.cpu(), case["v_pool"])  # NaN tails: bytes
+    gmin, gmax = logical_meta(meta, case["page_table"], lens, S)
+    omin, omax = oracle.meta_build(case["k_pool"], case["page_table"], lens)
+    assert np.array_equal(gmin, omin) and np.array_equal(gmax, omax)
+    assert np.array_equal(cnt.cpu().numpy(), ref["sel_count"])
+    K = ids.shape[2]
+    assert np.array_equal(ids.cpu().numpy(), ref["sel_ids"][:, :, :K])
+    assert np.abs(o.cpu().numpy() - ref["o"]).max() <= ATOL[cfg.dtype]
+
+
 @pytest.mark.parametrize("lens", [[0, 5, 16, 17], [1, 1, 1, 1], [0, 0, 0, 0], [31, 64, 2, 48]])
 def test_decode_step_edge_lengths(ts, lens):
     """seq_len 0 (o = 0, lse = -inf), seq_len < S, exact page multiples, K >= P."""
