@@ -33,8 +33,7 @@ struct ScSmem {
     static constexpr int kHist = kQ + 8 * kRowBytes;                // [2048] int
     static constexpr int kRed = kHist + kSsHist * 4;                // [64] int
     static constexpr int kWarpPart = kRed + 64 * 4;                 // [W][8][kSaPart] fp32
-    static constexpr int kInfo = kWarpPart + W * 8 * kSaPart * 4;   // [2R] int
-    static constexpr int kBars = (kInfo + 2 * R * 4 + 7) / 8 * 8;   // mfull,mempty[R]; afull,aempty[2R]; q; pt
+    static constexpr int kBars = (kWarpPart + W * 8 * kSaPart * 4 + 7) / 8 * 8;  // mfull,mempty[R]; afull,aempty[2R]; q; pt
     static constexpr int kSel = (kBars + (6 * R + 2) * 8 + 15) / 16 * 16;  // [kmax] int2
     __host__ __device__ static size_t scores_off(int kmax) { return ((size_t)kSel + (size_t)kmax * 8 + 127) / 128 * 128; }
     // scores [cap] fp32 (cap = the row, or only this CTA's chunk for the two-level select,
@@ -79,7 +78,6 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
     int *hist = reinterpret_cast<int *>(smem + SM::kHist);
     int *red = reinterpret_cast<int *>(smem + SM::kRed);
     float *wpart = reinterpret_cast<float *>(smem + SM::kWarpPart);
-    int *info = reinterpret_cast<int *>(smem + SM::kInfo);
     int2 *sel = reinterpret_cast<int2 *>(smem + SM::kSel);
     unsigned *s_kmin = reinterpret_cast<unsigned *>(red + 60), *s_kmax = s_kmin + 1;
     __shared__ int s_last;
@@ -157,7 +155,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
         }
         if (own && lane >= 16 && lane < 24) {  // the new token's K and V rows (16 B per lane)
             const int c = lane - 16;
-            const int blk = p.page_table[(size_t)b * p.max_pages + ja];
+            const int blk = p.page_table[(size_t)b * p.max_pages + max(ja, 0)];  // (ja >= 0 when own)
             const size_t src = ((size_t)b * p.Hkv + g) * kAttnD + c * 8;
             const size_t dst = (((size_t)blk * p.Hkv + g) * p.S + aslot) * kAttnD + c * 8;
             uint16_t *kp = const_cast<uint16_t *>(static_cast<const uint16_t *>(ap.k_pool));
@@ -213,7 +211,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
                                        bf16x2_max(v.w, kn.w));
                     }
                     sts_v4(a, v);
-                    uint16_t *mrec = const_cast<uint16_t *>(p.meta) + ((size_t)row * p.max_pages + ja) * 2 * kAttnD +
+                    uint16_t *mrec = const_cast<uint16_t *>(p.meta) + ((size_t)row * p.max_pages + max(ja, 0)) * 2 * kAttnD +
                                      (lane >> 3) * kAttnD + (lane & 7) * 8;
                     *reinterpret_cast<uint4 *>(mrec) = v;  // the cache's record (logical layout)
                     fence_proxy_async();  // generic smem write before the stage's next TMA fill
