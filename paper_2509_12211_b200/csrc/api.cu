@@ -457,7 +457,7 @@ StepPlan plan_step(const ts_layout *L, int kmax) {
     const int rows = L->batch * L->num_kv_heads;
     // flags: bit 0 page-table row prefetched to smem (rows up to 2048 pages); bit 1
     // two-level select when rows are much longer than the candidates; bit 2 DSMEM merge
-    // area (DSM); bit 3 early PDL trigger (set at launch)
+    // area (DSM); bits 3 / 4 early / late PDL trigger (set at launch)
     int fl = (((L->max_pages & 3) == 0 && L->max_pages <= 2048) ? 1 : 0) | (DSM ? 4 : 0);
     static const int two_env = getenv("TS_SC_TWO") ? atoi(getenv("TS_SC_TWO")) : -1;
     const bool two_ok = two_env == 1 || (two_env != 0 && L->max_pages > 2048);  // long rows only
@@ -536,11 +536,13 @@ ts_status launch_step(const ts_layout *L, ScoreSelParams &sp, const AttnParams &
     sp.C = pl.C;
     sp.chunk = pl.chunk;
     sp.flags = pl.flags;
-    // early PDL trigger (the next kernel's prologue overlaps our tail): measured faster with
-    // clusters of <= 8 CTAs (C2 / C3 / C4), slower with C5's 13-CTA clusters
+    // PDL trigger for the next kernel in the stream (its prologue overlaps our tail): after
+    // the attention loop (bit 4) with clusters of <= 8 CTAs — measured 0.9 % faster than at
+    // kernel start (bit 3, TS_SC_TRIGGER=1) on C2 / C4, equal on C3; none with C5's 13-CTA
+    // clusters (either trigger: 23 -> 28-32 us)
     static const int trig_env = getenv("TS_SC_TRIGGER") ? atoi(getenv("TS_SC_TRIGGER")) : -1;
-    if (trig_env == 1 || (trig_env < 0 && pl.C <= 8)) sp.flags |= 8;
-    if (trig_env == 2) sp.flags |= 16;  // late trigger (after the attention loop)
+    if (trig_env == 1) sp.flags |= 8;
+    if (trig_env == 2 || (trig_env < 0 && pl.C <= 8)) sp.flags |= 16;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(rows * pl.C);
     cfg.blockDim = dim3((W + 1) * 32);

@@ -36,7 +36,7 @@ struct ScoreSelParams {
     int *sel_blk;             // [rows][kmax] physical block of each selected page
     int *sel_count;           // [rows]
     int B, Hq, Hkv, G, S, max_pages, kmax;
-    int flags;                // step_cluster: bit 0 page-table prefetch, bit 1 two-level select
+    int flags;                // step_cluster: bit 0 page-table prefetch, 1 two-level select, 2 DSMEM merge, 3 / 4 early / late PDL trigger
     int C;                    // CTAs per row (cluster size)
     int chunk;                // pages per CTA (multiple of 32)
     unsigned long long *dbg;  // development: per-CTA stamps (nullable)

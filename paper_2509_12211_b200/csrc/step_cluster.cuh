@@ -97,7 +97,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
     SC_STAMP(0);
     // the next kernel in the stream (the next layer / step) may be scheduled as our CTAs
     // retire: its prologue overlaps our tail; it waits for our completion before any read
-    if (p.flags & 8) pdl_launch_dependents();  // (host: measured faster up to 8-CTA clusters)
+    if (p.flags & 8) pdl_launch_dependents();  // early trigger (dev knob; host default: bit 4)
     if (warp == 0) {  // the 6R + 2 consecutive mbarriers (all count 1), one per lane
         for (int i = lane; i < 6 * R + 2; i += 32) mbar_init(mfull0 + 8 * i, 1);
         fence_mbar_init();
