@@ -110,6 +110,30 @@ int max_active_clusters(K kern, int threads, size_t smem, int cluster) {
     return n;
 }
 
+// Opt-in shared memory / non-portable cluster size for a kernel, per DEVICE (a process may
+// drive several GPUs: cudaFuncSetAttribute applies to the current device only).  Grows the
+// opt-in size on demand; cached per (device, kernel).
+bool ensure_func_attrs(const void *kern, size_t smem, bool nonportable) {
+    static std::mutex mu;
+    static std::unordered_map<unsigned long long, size_t> set_smem;
+    static std::unordered_map<unsigned long long, bool> set_np;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const unsigned long long key = (unsigned long long)reinterpret_cast<uintptr_t>(kern) ^ ((unsigned long long)dev << 56);
+    std::lock_guard<std::mutex> g(mu);
+    if (nonportable && !set_np[key]) {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+            return false;
+        set_np[key] = true;
+    }
+    if (smem > set_smem[key]) {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+            return false;
+        set_smem[key] = smem;
+    }
+    return true;
+}
+
 // ---------------------------------------------------------------- TMA descriptors
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -143,13 +167,16 @@ bool make_pool_map(CUtensorMap *map, const void *pool, const ts_layout *L, int T
 // attention workspace: [tickets: rows u32][work counters: 2 u32][partials: rows x ipr x 8 x kPS]
 // with ipr <= kMaxItemsPerRow split parts per row (split-K merge of the attention kernels).
 constexpr int kMaxItemsPerRow = 64;
+constexpr int kMaxClusterC = 16;  // widest cluster the step planner may choose (partials per row)
 struct AttnWs {
     size_t tickets, work, part, total;
 };
-AttnWs attn_ws_layout(const ts_layout *L, int sel_stride) {
+AttnWs attn_ws_layout(const ts_layout *L, int sel_stride, int min_parts = 1) {
     const size_t rows = (size_t)L->batch * L->num_kv_heads;
     const int tpr = sel_stride * std::max(1, L->page_size / 16);
-    const int ipr = std::min(kMaxItemsPerRow, std::max(1, tpr));
+    // split parts per row: the attention kernels split a row at most into its tiles; the
+    // fused step's cluster may be wider than the selection (min_parts = its largest C)
+    const int ipr = std::max(min_parts, std::min(kMaxItemsPerRow, std::max(1, tpr)));
     AttnWs w;
     w.tickets = 0;
     w.work = round_up(rows * 4, 256);
@@ -164,7 +191,7 @@ struct StepWs {
 };
 StepWs step_ws_layout(const ts_layout *L, int kmax) {
     StepWs w;
-    w.attn = attn_ws_layout(L, kmax);
+    w.attn = attn_ws_layout(L, kmax, kMaxClusterC);
     const size_t rows = (size_t)L->batch * L->num_kv_heads;
     w.scores = w.attn.total;
     w.sel_ids = w.scores + round_up(rows * L->max_pages * 4, 256);
@@ -201,18 +228,18 @@ ts_status launch_score(const ts_layout *L, const void *q, const void *meta, cons
         if (sm > 200 * 1024) return TS_ERR_UNSUPPORTED;
         if (L->kv_dtype == TS_BF16) {
             if (L->head_dim == 64) {
-                cudaFuncSetAttribute(score_simt_kernel<uint16_t, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+                if (!ensure_func_attrs((const void *)score_simt_kernel<uint16_t, 64>, sm, false)) return TS_ERR_CUDA;
                 score_simt_kernel<uint16_t, 64><<<grid, kSimtWarps * 32, sm, st>>>(p, (const uint16_t *)q, (const uint16_t *)meta, pt, sl, scores);
             } else {
-                cudaFuncSetAttribute(score_simt_kernel<uint16_t, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+                if (!ensure_func_attrs((const void *)score_simt_kernel<uint16_t, 128>, sm, false)) return TS_ERR_CUDA;
                 score_simt_kernel<uint16_t, 128><<<grid, kSimtWarps * 32, sm, st>>>(p, (const uint16_t *)q, (const uint16_t *)meta, pt, sl, scores);
             }
         } else {
             if (L->head_dim == 64) {
-                cudaFuncSetAttribute(score_simt_kernel<float, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+                if (!ensure_func_attrs((const void *)score_simt_kernel<float, 64>, sm, false)) return TS_ERR_CUDA;
                 score_simt_kernel<float, 64><<<grid, kSimtWarps * 32, sm, st>>>(p, (const float *)q, (const float *)meta, pt, sl, scores);
             } else {
-                cudaFuncSetAttribute(score_simt_kernel<float, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+                if (!ensure_func_attrs((const void *)score_simt_kernel<float, 128>, sm, false)) return TS_ERR_CUDA;
                 score_simt_kernel<float, 128><<<grid, kSimtWarps * 32, sm, st>>>(p, (const float *)q, (const float *)meta, pt, sl, scores);
             }
         }
@@ -230,10 +257,7 @@ ts_status launch_select(const float *scores, int rows, int stride, const int *ro
     const size_t sm = ids_in ? n * 4 * 3 : ((n + 3) & ~(size_t)3) * 4;  // affine keys padded to 4
     if (sm > 200 * 1024) return TS_ERR_UNSUPPORTED;
     if (ids_in && n > 16 * kSelThreads) return TS_ERR_UNSUPPORTED;
-    static std::once_flag once;
-    std::call_once(once, [] {
-        cudaFuncSetAttribute(select_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    });
+    if (!ensure_func_attrs((const void *)select_topk_kernel, 200 * 1024, false)) return TS_ERR_CUDA;
     SelectParams p{scores, rows, stride * parts, row_len, ids_in, id_stride, id_offset, k,
                    stride, part_stride, sel_ids, sel_scores, sel_count};
     select_topk_kernel<<<rows, kSelThreads, sm, st>>>(p);
@@ -248,23 +272,7 @@ ts_status launch_select(const float *scores, int rows, int stride, const int *ro
 template <int W, int DP>
 ts_status prepare_sa(size_t sm) {
     auto kern = sparse_attn_kernel<W, DP>;
-    static std::mutex mu;
-    static size_t sm_set = 0;
-    static bool np_set = false;
-    std::lock_guard<std::mutex> g(mu);
-    if (sm > sm_set) {
-        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) !=
-            cudaSuccess)
-            return TS_ERR_CUDA;
-        sm_set = sm;
-    }
-    if (!np_set) {
-        if (cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
-            cudaSuccess)
-            return TS_ERR_CUDA;
-        np_set = true;
-    }
-    return TS_OK;
+    return ensure_func_attrs((const void *)kern, sm, true) ? TS_OK : TS_ERR_CUDA;
 }
 
 // C = CTAs per row: the largest C <= cdesired whose clusters all fit on the GPU at once
@@ -309,30 +317,13 @@ ts_status launch_sat(const ts_layout *L, const AttnParams &p, bool pdl, cudaStre
     const int rows = L->batch * L->num_kv_heads;
     const size_t sm = SatSmem<W, R>::bytes(p.sel_stride);
     if (sm > 227 * 1024) return TS_ERR_UNSUPPORTED;
-    {
-        static std::mutex mu;
-        static size_t sm_set = 0;
-        static bool np_set = false;
-        std::lock_guard<std::mutex> g(mu);
-        if (sm > sm_set) {
-            if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) !=
-                cudaSuccess)
-                return TS_ERR_CUDA;
-            sm_set = sm;
-        }
-        if (!np_set) {
-            if (cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
-                cudaSuccess)
-                return TS_ERR_CUDA;
-            np_set = true;
-        }
-    }
+    if (!ensure_func_attrs((const void *)kern, sm, true)) return TS_ERR_CUDA;
     CUtensorMap tmK, tmV;
     if (!make_pool_map(&tmK, p.k_pool, L, 16) || !make_pool_map(&tmV, p.v_pool, L, 16))
         return TS_ERR_CUDA;
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (W + 1) * 32, sm);
-    static const int cmax_env = getenv("TS_SA_CMAX") ? atoi(getenv("TS_SA_CMAX")) : 16;
+    static const int cmax_env = std::min(kMaxClusterC, getenv("TS_SA_CMAX") ? std::max(1, atoi(getenv("TS_SA_CMAX"))) : 16);
     const int ntile = p.sel_stride * (L->page_size / 16);  // upper bound per row
     // splits per row: fill one wave (rows x C <= CTAs resident), each warp >= 2 tiles
     int C = std::max(1, std::min(cmax_env, device_sms() * std::max(1, per_sm) / std::max(1, rows)));
@@ -367,7 +358,7 @@ ts_status launch_sparse_attn(const ts_layout *L, const AttnParams &p, bool pdl, 
         return launch_sat<4, 8>(L, p, pdl, st);
     }
     const int n_oct = p.sel_stride * (L->page_size / 8);  // upper bound per row
-    static const int cmax_env = getenv("TS_SA_CMAX") ? atoi(getenv("TS_SA_CMAX")) : 16;
+    static const int cmax_env = std::min(kMaxClusterC, getenv("TS_SA_CMAX") ? std::max(1, atoi(getenv("TS_SA_CMAX"))) : 16);
     int W = rows >= 2 * sms ? 4 : (rows * 16 < sms ? 16 : 8);
     static const int w_env = getenv("TS_SA_W") ? atoi(getenv("TS_SA_W")) : 0;
     if (w_env == 4 || w_env == 8 || w_env == 16) W = w_env;
@@ -386,24 +377,7 @@ ts_status launch_ss_t(ScoreSelParams &p, int rows, int cdesired, cudaStream_t st
     auto kern = score_select_kernel<W, R>;
     const size_t sm = SsSmem<W, R>::bytes(p.max_pages);
     if (sm > 227 * 1024) return TS_ERR_UNSUPPORTED;
-    {
-        static std::mutex mu;
-        static size_t sm_set = 0;
-        static bool np_set = false;
-        std::lock_guard<std::mutex> g(mu);
-        if (sm > sm_set) {
-            if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) !=
-                cudaSuccess)
-                return TS_ERR_CUDA;
-            sm_set = sm;
-        }
-        if (!np_set) {
-            if (cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
-                cudaSuccess)
-                return TS_ERR_CUDA;
-            np_set = true;
-        }
-    }
+    if (!ensure_func_attrs((const void *)kern, sm, true)) return TS_ERR_CUDA;
     // chunk per CTA (a multiple of the stage), C = CTAs per row; the largest C <= cdesired
     // whose clusters all fit at once (one wave: no row waits for another row's CTAs)
     int C = std::max(1, cdesired), chunk = 0;
@@ -461,26 +435,10 @@ StepPlan plan_step(const ts_layout *L, int kmax) {
     int fl = (((L->max_pages & 3) == 0 && L->max_pages <= 2048) ? 1 : 0) | (DSM ? 4 : 0);
     static const int two_env = getenv("TS_SC_TWO") ? atoi(getenv("TS_SC_TWO")) : -1;
     const bool two_ok = two_env == 1 || (two_env != 0 && L->max_pages > 2048);  // long rows only
-    static std::mutex mu;
-    static size_t sm_set = 0;
-    static bool np_set = false;
     auto allow = [&](size_t smb) -> bool {  // grow the opt-in shared memory on demand
-        std::lock_guard<std::mutex> g(mu);
-        if (!np_set) {
-            if (cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
-                cudaSuccess)
-                return false;
-            np_set = true;
-        }
-        if (smb > sm_set) {
-            if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb) !=
-                cudaSuccess)
-                return false;
-            sm_set = smb;
-        }
-        return true;
+        return ensure_func_attrs((const void *)kern, smb, true);
     };
-    static const int cmax = getenv("TS_SC_CMAX") ? atoi(getenv("TS_SC_CMAX")) : 16;
+    static const int cmax = std::min(kMaxClusterC, getenv("TS_SC_CMAX") ? std::max(1, atoi(getenv("TS_SC_CMAX"))) : 16);
     const int max_c = std::max(1, std::min(cmax, (L->max_pages + 63) / 64));  // >= 64 pages per CTA
     auto chunk_of = [&](int c) {
         int ch = (L->max_pages + c - 1) / c;
@@ -610,7 +568,7 @@ ts_status launch_score_select(const ts_layout *L, const void *q, const void *met
     p.kmax = kmax;
     p.dbg = g_dbg_ss;
     static const int per_sm = getenv("TS_SS_PER_SM") ? atoi(getenv("TS_SS_PER_SM")) : 3;
-    static const int cmax = getenv("TS_SS_CMAX") ? atoi(getenv("TS_SS_CMAX")) : 16;
+    static const int cmax = std::min(kMaxClusterC, getenv("TS_SS_CMAX") ? std::max(1, atoi(getenv("TS_SS_CMAX"))) : 16);
     const int target = device_sms() * per_sm;
     const int max_c = std::max(1, std::min(cmax, (L->max_pages + 63) / 64));  // >= 64 pages per CTA
     const int C = std::max(1, std::min(max_c, (target + rows - 1) / rows));

@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(256) attn_simt_kernel(AttnParams p, const floa
     const int row = blockIdx.x;
     const int b = row / p.Hkv, g = row % p.Hkv;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-    const int L = p.seq_lens[b];
+    const int L = clamp_len(p.seq_lens[b], p.max_pages, p.stride, p.S);
     const int cnt = p.sel_count[row];
     const int *ids = p.sel_ids + (size_t)row * p.sel_stride;
     const float *q = static_cast<const float *>(p.q);

@@ -222,6 +222,14 @@ TS_DEV float warp_sum(float v) {
     return v;
 }
 
+// Sequence length as the kernels see it: at most the capacity of the page-table row
+// (global pages < max_pages * stride).  seq_len beyond it is a caller error (undefined per
+// include/tinyserve.h); clamping keeps every read inside the row and the pools' pages.
+TS_DEV int clamp_len(int L, int max_pages, int stride, int S) {
+    const long long cap = (long long)max_pages * stride * S;
+    return L < cap ? L : (int)cap;
+}
+
 // Orderable key of an fp32 score: larger score <-> larger unsigned key; -0.0 == +0.0.
 TS_DEV uint32_t score_key(float s) {
     uint32_t u = __float_as_uint(s + 0.0f);  // -0.0 + 0.0 = +0.0 (round-to-nearest)

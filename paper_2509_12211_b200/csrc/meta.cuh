@@ -59,11 +59,16 @@ __global__ void meta_append_kernel(MetaParams p, const T *__restrict__ k_new,
     // advance < 0 (internal, ts_decode_step_append fallback): seq_lens already counts the
     // new token, which goes to slot t = seq_len - 1
     const int t = seq_lens[b] + (advance < 0 ? -1 : 0);
+    // capacity of the sequence: global pages j < max_pages * stride (the last rank's local
+    // row may be one page short; that page has no slot and is rejected below).  A token past
+    // the capacity is dropped AND the length is not advanced, so no later step sees a
+    // P_b beyond the page-table row (the oracle's or_meta_append reports a shape error here).
+    const long long cap = (long long)p.max_pages * p.stride * p.S;
     if (advance > 0) {  // every thread has read t; then one thread publishes t + 1
         __syncthreads();
-        if (threadIdx.x == 0) seq_lens[b] = t + 1;
+        if (threadIdx.x == 0 && t + 1LL <= cap) seq_lens[b] = t + 1;
     }
-    if (h >= p.Hkv || t < 0) return;
+    if (h >= p.Hkv || t < 0 || t >= cap) return;
     const int j = t / p.S, slot = t % p.S;
     if (j % p.stride != p.offset) return;  // page owned by another rank
     const int jl = j / p.stride;

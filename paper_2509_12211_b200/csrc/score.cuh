@@ -51,7 +51,7 @@ TS_DEV void score_mma_block(const ScoreParams &p, const uint16_t *__restrict__ q
     const int b = row / p.Hkv, g = row % p.Hkv;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int gid = lane >> 2, t = lane & 3;
-    const int P = local_pages(seq_lens[b], p.S, p.stride, p.offset);
+    const int P = local_pages(clamp_len(seq_lens[b], p.max_pages, p.stride, p.S), p.S, p.stride, p.offset);
     const int cta_base = chunk * kScorePagesPerCta;
     float *srow = scores + (size_t)row * p.max_pages;
 
@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(kSimtWarps * 32)
     const int row = blockIdx.y;
     const int b = row / p.Hkv, g = row % p.Hkv;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int P = local_pages(seq_lens[b], p.S, p.stride, p.offset);
+    const int P = local_pages(clamp_len(seq_lens[b], p.max_pages, p.stride, p.S), p.S, p.stride, p.offset);
     float *srow = scores + (size_t)row * p.max_pages;
     const int base = blockIdx.x * kSimtPagesPerCta;
     // coefficient rows [G][2D]: [q^- | q^+]

@@ -461,7 +461,7 @@ __global__ void __launch_bounds__((W + 1) * 32) score_select_kernel(ScoreSelPara
     if (p.C > 1) cluster_arrive_relaxed();  // "this CTA is running" (before any DSMEM access)
     pdl_wait();  // inputs may come from the previous kernel in the stream (PDL launch)
 
-    const int L = p.seq_lens[b];
+    const int L = clamp_len(p.seq_lens[b], p.max_pages, 1, p.S);
     const int P = (L + p.S - 1) / p.S;
     const int j0 = rank * p.chunk;
     const bool pt_bulk = (p.max_pages & 3) == 0;  // row start 16-byte aligned

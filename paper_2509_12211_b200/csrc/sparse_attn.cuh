@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(W * 32, 512 / (W * 32)) sparse_attn_kernel(Att
     if (dts && threadIdx.x == 0) dts[e] = globaltimer();
     SA_STAMP(0);
     const int b = row / p.Hkv, g = row % p.Hkv;
-    const int L = p.seq_lens[b];
+    const int L = clamp_len(p.seq_lens[b], p.max_pages, p.stride, p.S);
 
     // ---- Q fragments (independent of the selection): q heads g*G + gid, channels [16t, +16)
     uint32_t qa[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -327,7 +327,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) sparse_attn_tma_kernel(
         }
         fence_mbar_init();
     }
-    const int L = p.seq_lens[b];
+    const int L = clamp_len(p.seq_lens[b], p.max_pages, p.stride, p.S);
     // ---- Q fragments (consumers; independent of the selection)
     const int gid = lane >> 2, t = lane & 3;
     uint32_t qa[8] = {0, 0, 0, 0, 0, 0, 0, 0};

@@ -115,7 +115,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
     if (C > 1) cluster_arrive_release();
     pdl_wait();  // inputs may come from the previous kernel in the stream
 
-    const int L = p.seq_lens[b];
+    const int L = clamp_len(p.seq_lens[b], p.max_pages, 1, p.S);
     const int P = (L + p.S - 1) / p.S;
     const int j0 = rank * p.chunk;
     const int nloc = max(0, min(P - j0, p.chunk));

@@ -28,7 +28,8 @@ class ShardStep:
     def __init__(self, ops, layout, world: int, rank: int, budget_tokens: int, device):
         assert layout.shard_stride == world and layout.shard_offset == rank
         self.ops, self.L, self.G, self.r = ops, layout, world, rank
-        self.K = max(1, budget_tokens // layout.page_size)
+        # K = floor(budget / S) clipped to the GLOBAL page count (as ts.kmax unsharded)
+        self.K = min(layout.max_pages * world, max(1, budget_tokens // layout.page_size))
         B, Hkv, Hq, d = layout.batch, layout.num_kv_heads, layout.num_q_heads, layout.head_dim
         self.rows = B * Hkv
         self.nq = B * Hq * d

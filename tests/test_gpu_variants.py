@@ -15,7 +15,7 @@ import torch
 pytestmark = pytest.mark.gpu
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-CASES = "test_decode_step and (c3_small or g4_s32 or g6_s64 or two_level or c1_ragged or g3_s16)"
+CASES = "test_decode_step and (c3_small or g4_s32 or g6_s64 or two_level or c1_ragged or g3_s16 or small_budget_long)"
 
 
 @pytest.mark.skipif(os.environ.get("TS_VARIANT_CHILD") == "1", reason="child process")
