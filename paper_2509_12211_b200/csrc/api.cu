@@ -11,6 +11,7 @@
 #include "attn.cuh"
 #include "common.cuh"
 #include "step_cluster.cuh"
+#include "step_pipe.cuh"
 #include "meta.cuh"
 #include "score.cuh"
 #include "score_select.cuh"
@@ -546,6 +547,123 @@ ts_status launch_step_cluster_t(const ts_layout *L, ScoreSelParams &sp, const At
                     : launch_step_cluster_app<W, R, false>(L, sp, ap, st);
 }
 
+
+// ---------------------------------------------------------------- pipelined step (step_pipe.cuh)
+// Plan: NR rows per cluster, C CTAs per cluster (chunks of each row), R ring stages.  The
+// model behind the choice: the step moves `total` bytes; a CTA moves its
+// share `cta` and, latency-bound, streams at most ring / ~1.5 us; HBM caps the whole grid at
+// ~6.5 TB/s.  Estimated time = max(total / HBM, cta / (ring / lat)) + per-row exchange and
+// merge latencies (C > 1) + the exposed select of the single-row (NR = 1) schedule.
+struct PipePlan {
+    bool ok = false;
+    int NR = 0, C = 0, chunk = 0, R = 0, two = 0, share = 0, pt_smem = 0;
+    size_t sm = 0;
+    double est_us = 1e30;
+};
+
+int env_int(const char *name, int dflt) {  // development A/B knobs (read once per call site)
+    const char *v = getenv(name);
+    return v ? atoi(v) : dflt;
+}
+
+template <bool APP>
+PipePlan plan_pipe(const ts_layout *L, int kmax) {
+    auto kern = decode_pipe_kernel<APP>;
+    PipePlan best;
+    const int rows = L->batch * L->num_kv_heads;
+    const int sms = device_sms();
+    const int S = L->page_size, tpp = S / 16, G = group_of(L);
+    const double e = 2.0, d = 64.0;
+    // bytes of one row: metadata of every page + the selected K/V (upper bound: full pages)
+    const double P = L->max_pages, K = std::min(kmax, L->max_pages);
+    const double row_bytes = P * 2 * d * e + K * S * 2 * d * e + G * d * (e + 4);
+    const double total = rows * row_bytes;
+    static const int nr_env = env_int("TS_PIPE_NR", 0), c_env = env_int("TS_PIPE_C", 0),
+                     r_env = env_int("TS_PIPE_R", 0);
+    for (int NR = 2; NR >= 1; --NR) {
+        if (nr_env && NR != nr_env) continue;
+        const int ncl = (rows + NR - 1) / NR;
+        for (int Cd = 1; Cd <= kMaxClusterC; ++Cd) {
+            int chunk = (L->max_pages + Cd - 1) / Cd;
+            chunk = (chunk + kSsStagePages - 1) / kSsStagePages * kSsStagePages;
+            const int C = (L->max_pages + chunk - 1) / chunk;
+            if (C != Cd) continue;  // the same split as a smaller Cd
+            if (c_env && C != c_env) continue;
+            if (C > 1 && chunk < 64 && !c_env) continue;  // >= 64 pages per CTA
+            const int two = (C > 1 && kmax % 4 == 0 && L->max_pages > 2048 &&
+                             L->max_pages >= 4 * C * kmax) ? 1 : 0;
+            const int share = ((kmax * tpp + C - 1) / C + tpp - 1) / tpp + 1;
+            const int T = ncl * C;
+            for (int m = 1; m <= 4; ++m) {  // CTAs per SM the shared memory is sized for
+                if ((long long)m * sms < std::min(T, 2 * sms) && m < 4) continue;  // one wave (or two SM-loads)
+                const int pt_smem = ((L->max_pages & 3) == 0 && L->max_pages <= 2048) ? 1 : 0;
+                const PipeLayout l0 = PipeLayout::make(0, NR, C, L->max_pages, kmax, chunk, two, share, pt_smem);
+                const long long budget = std::min<long long>(227 * 1024, 228 * 1024 / m - 1024) - 1024;
+                int R = (int)std::min<long long>(24, (budget - l0.total - 128) / kPipeStage);
+                if (r_env) R = std::min(R, r_env);
+                if (R < 4) continue;
+                const PipeLayout l = PipeLayout::make(R, NR, C, L->max_pages, kmax, chunk, two, share, pt_smem);
+                const size_t sm = 1024 + (size_t)l.total;
+                const double ring = (double)R * kPipeStage;
+                const double cta = NR * row_bytes / C;
+                const double lat_us = 1.5;
+                const double t_bw = total / 6.5e6;               // us at 6.5 TB/s
+                const double waves = std::ceil((double)T / ((double)m * sms));
+                const double t_cta = waves * cta / (ring / lat_us);
+                double est = std::max(t_bw, t_cta) + 2.0;         // launch ramp + tail
+                if (C > 1) est += 1.0 + (two ? 1.0 : 0.0);        // exchange + ticket merge
+                if (NR == 1) est += two ? 4.0 : 2.0;              // the exposed select(s)
+                if (est < best.est_us) {
+                    if (!ensure_func_attrs((const void *)kern, sm, true)) continue;
+                    if (max_active_clusters(kern, kPipeNT, sm, C) < std::min(ncl, (int)(m * sms / C))) continue;
+                    best.ok = true;
+                    best.NR = NR; best.C = C; best.chunk = chunk; best.R = R; best.two = two;
+                    best.share = share; best.pt_smem = pt_smem; best.sm = sm; best.est_us = est;
+                }
+                break;  // larger m only shrinks the ring
+            }
+        }
+    }
+    return best;
+}
+
+template <bool APP>
+ts_status launch_pipe(const ts_layout *L, PipeParams &pp, cudaStream_t st) {
+    auto kern = decode_pipe_kernel<APP>;
+    const PipePlan pl = plan_pipe<APP>(L, pp.kmax);
+    if (!pl.ok) return TS_ERR_UNSUPPORTED;
+    CUtensorMap tmK, tmV;
+    if (!make_pool_map(&tmK, pp.k_pool, L, 16) || !make_pool_map(&tmV, pp.v_pool, L, 16))
+        return TS_ERR_CUDA;
+    pp.NR = pl.NR;
+    pp.C = pl.C;
+    pp.chunk = pl.chunk;
+    pp.R = pl.R;
+    pp.two = pl.two;
+    pp.share = pl.share;
+    pp.pt_smem = pl.pt_smem;
+    static const int trig = env_int("TS_PIPE_TRIGGER", 1);
+    pp.flags = trig ? 16 : 0;
+    const int ncl = (pp.rows + pl.NR - 1) / pl.NR;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(ncl * pl.C);
+    cfg.blockDim = dim3(kPipeNT);
+    cfg.dynamicSmemBytes = pl.sm;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = pl.C;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    if (cudaLaunchKernelEx(&cfg, kern, tmK, tmV, pp) != cudaSuccess) return TS_ERR_CUDA;
+    ++g_launches;
+    return launch_status();
+}
+
 ts_status launch_score_select(const ts_layout *L, const void *q, const void *meta, const int *pt,
                               const int *sl, int *ids, int *blk, int *cnt, int kmax,
                               cudaStream_t st) {
@@ -823,6 +941,43 @@ static ts_status decode_step_impl(const ts_layout *L, const void *q, const void 
     const cudaStream_t st = as_stream(stream);
     const int rows = L->batch * L->num_kv_heads;
     static const int two_kernels = getenv("TS_TWO_KERNELS") ? atoi(getenv("TS_TWO_KERNELS")) : 0;
+    static const int pipe = env_int("TS_PIPE", 1);
+    if (L->kv_dtype == TS_BF16 && group_of(L) <= 8 && L->head_dim == 64 && !two_kernels && pipe &&
+        L->page_size % 16 == 0 && rows > 0) {
+        // the whole step in one pipelined kernel (step_pipe.cuh)
+        const AttnWs aw = attn_ws_layout(L, kmax, kMaxClusterC);
+        PipeParams pp{};
+        pp.q = static_cast<const uint16_t *>(q);
+        pp.meta = static_cast<const uint16_t *>(meta);
+        pp.page_table = page_table;
+        pp.seq_lens = seq_lens;
+        pp.sel_ids = ids;
+        pp.sel_count = cnt;
+        pp.k_new = static_cast<const uint16_t *>(k_new);
+        pp.v_new = static_cast<const uint16_t *>(v_new);
+        pp.k_pool = static_cast<uint16_t *>(const_cast<void *>(k_pool));
+        pp.v_pool = static_cast<uint16_t *>(const_cast<void *>(v_pool));
+        pp.o = o;
+        pp.lse = lse;
+        pp.part = reinterpret_cast<float *>(wb + aw.part);
+        pp.tickets = reinterpret_cast<unsigned *>(wb + aw.tickets);
+        pp.scale = scale;
+        pp.B = L->batch;
+        pp.Hq = L->num_q_heads;
+        pp.Hkv = L->num_kv_heads;
+        pp.G = group_of(L);
+        pp.S = L->page_size;
+        pp.max_pages = L->max_pages;
+        pp.kmax = kmax;
+        pp.rows = rows;
+        phase_mark(0, st);
+        s = k_new ? launch_pipe<true>(L, pp, st) : launch_pipe<false>(L, pp, st);
+        phase_mark(3, st);
+        if (s != TS_ERR_UNSUPPORTED) {
+            g_launches = 1;
+            return s;
+        }
+    }
     if (L->kv_dtype == TS_BF16 && group_of(L) <= 8 && L->head_dim == 64 && !two_kernels &&
         L->page_size % 16 == 0 && rows > 0) {
         // the whole step in one cluster-per-row kernel (step_cluster.cuh)

@@ -1,0 +1,737 @@
+// step_pipe.cuh — the bf16 decode step (Alg. 1; "integrates page scoring,
+// sparse memory access, and masked attention in a single pass") as ONE kernel in
+// which a CTA (or a thread-block cluster of C CTAs) carries NR = 1 or 2 rows (b, kv head g)
+// through the four steps as a software pipeline over one shared TMA ring:
+//
+//   producer warp : meta(A) meta(B) | K/V(A) once A is selected | K/V(B) once B is selected
+//   4 consumer warps: score A, select A, score B, select B, attend A (+ merge), attend B (+ merge)
+//
+// so the exact top-K of row A (latency-bound: smem round trips and barriers, HBM idle) runs
+// while row B's metadata streams into the ring, and the top-K of row B while row A's K/V
+// streams.  With every CTA of the grid in the same phase at the same time (one wave), a
+// one-row-per-CTA kernel leaves HBM idle during the select; here the HBM stream of every CTA
+// continues through it.
+//
+//  1. score (Eq. 2; Alg. 1 Step 1): the CTA's contiguous chunk of the row's
+//     metadata records (logical layout: one run per row) is bulk-copied (cp.async.bulk,
+//     L2 evict-first) in 8 KB stages of 32 pages; consumers compute [m | M] x [q^- ; q^+] on
+//     mma.m16n8k16 (exact bf16 products, fp32 sums) and the max over the GQA group (R9);
+//  2. select (TopK; Alg. 1 Step 2): C > 1 — the chunk keys (one-level) or
+//     the chunk's own top-K candidates (two-level, rows >> C K) are pushed into every peer's
+//     shared memory (DSMEM stores) and announced by remote mbarrier arrives (release.cluster;
+//     no cluster-wide barrier, so the producer warp and the other row never wait for it);
+//     every CTA then runs the same exact CTA-wide radix top-K (cta_topk, lowest page id
+//     wins ties, R6) and keeps its share of the ascending selection;
+//  3. gather: the producer streams the share's [16 x 64] K and V tiles (2 tiles per 8 KB
+//     stage) with 2-D TMA (128-byte swizzle, L2 evict-first), 4 lanes issuing in parallel;
+//  4. attend (SparseAttn): S = Q K^T (mma.m16n8k16), fp32 online softmax
+//     in exp2, O += P V (mma.m16n8k8, tf32 P — R10), tokens >= seq_len masked (R7); warp
+//     partials merge in smem; a split row's C CTA partials through an L2 workspace, the last
+//     CTA of the row (acq_rel ticket) combining them.
+#pragma once
+#include "attn.cuh"
+#include "common.cuh"
+#include "score_select.cuh"
+#include "sparse_attn.cuh"
+
+namespace ts {
+
+constexpr int kPipeW = 4;                    // consumer warps
+constexpr int kPipeCT = kPipeW * 32;         // consumer threads (warps 0 .. 3)
+constexpr int kPipeNT = kPipeCT + 32;        // + the producer warp (warp 4)
+constexpr int kPipeMaxNR = 2;                // rows per CTA
+constexpr int kPipeStage = 8192;             // ring stage: 32 metadata records or 2 K/V tiles
+constexpr int kPipeBar = 1;                  // named barrier of the consumer warps
+
+struct PipeParams {
+    const uint16_t *q;        // [B][Hq][64]
+    const uint16_t *meta;     // [B][Hkv][max_pages][2][64]  (APP: patched in place)
+    const int *page_table;    // [B][max_pages]
+    const int *seq_lens;      // [B]
+    int *sel_ids;             // [rows][kmax] ascending, -1 padding
+    int *sel_count;           // [rows]
+    const uint16_t *k_new;    // APP: [B][Hkv][64] the newest token (slot seq_len - 1)
+    const uint16_t *v_new;
+    uint16_t *k_pool;         // APP: [NB][Hkv][S][64]
+    uint16_t *v_pool;
+    float *o;                 // [B][Hq][64]
+    float *lse;               // [B][Hq] (nullable)
+    float *part;              // [rows][C][8][kPS] split partials (C > 1)
+    unsigned *tickets;        // [rows] zero on entry, re-armed by the kernel
+    float scale;
+    int B, Hq, Hkv, G, S, max_pages, kmax, rows;
+    int NR;                   // rows per cluster (1 or 2)
+    int C;                    // CTAs per cluster (chunks per row)
+    int chunk;                // pages per CTA chunk (multiple of 32)
+    int R;                    // ring stages
+    int two;                  // two-level select (chunk top-K, then top-K of C * kmax candidates)
+    int share;                // sel entries per row kept by a CTA (>= its pages of the selection)
+    int pt_smem;              // page-table rows prefetched into shared memory
+    int flags;                // bit 4: PDL trigger after the attention loop
+};
+
+// Byte offsets of the shared-memory regions (from the 1024-aligned base); host and device.
+struct PipeLayout {
+    int ring, q, hist, red, wpart, bars, kmm, sel, sc, pt, cand, total;
+    int scap, ptcap, candcap;  // per row: score entries, page-table entries, candidate words
+    __host__ __device__ static int up(int x, int a) { return (x + a - 1) / a * a; }
+    __host__ __device__ static PipeLayout make(int R, int NR, int C, int max_pages, int kmax, int chunk,
+                                               int two, int share, int pt_smem) {
+        PipeLayout l;
+        const int mp4 = up(max_pages, 4);
+        l.scap = two ? up(chunk, 4) : mp4;
+        l.ptcap = pt_smem ? mp4 : 0;
+        l.candcap = two ? 2 * C * kmax : 0;
+        l.ring = 0;
+        l.q = R * kPipeStage;                              // [NR][8][64] bf16
+        l.hist = l.q + NR * 8 * kRowBytes;                 // [2048] int
+        l.red = l.hist + kSsHist * 4;                      // [64] int
+        l.wpart = l.red + 64 * 4;                          // [W][8][kSaPart] fp32 (select scratch before)
+        l.bars = up(l.wpart + kPipeW * 8 * kSaPart * 4, 8);  // full[R] empty[R] q pt[NR] sel[NR] keys[NR]
+        l.kmm = l.bars + (2 * R + 1 + 3 * NR) * 8;         // [NR][2] key range
+        l.sel = up(l.kmm + NR * 8, 16);                    // [NR][share] int2 (block row, first token)
+        l.sc = up(l.sel + NR * share * 8, 16);             // [NR][scap] fp32 scores -> keys
+        l.pt = l.sc + NR * l.scap * 4;                     // [NR][ptcap] int
+        l.cand = l.pt + NR * l.ptcap * 4;                  // [NR][C][kmax] keys, then [NR][C][kmax] ids
+        l.total = l.cand + NR * l.candcap * 4;
+        return l;
+    }
+};
+
+TS_DEV void fence_acq_rel_cluster() { asm volatile("fence.acq_rel.cluster;" ::: "memory"); }
+// arrive (release, cluster scope) on the mbarrier at the same offset in CTA `peer`'s smem
+TS_DEV void mbar_arrive_remote(uint32_t bar, uint32_t peer) {
+    uint32_t rb;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(bar), "r"(peer));
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(rb) : "memory");
+}
+TS_DEV void mbar_wait_cluster(uint32_t bar, uint32_t parity) {  // acquire at cluster scope
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAITC_%=:\n"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAITC_%=;\n"
+        "}\n" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+
+// What every thread of a CTA knows about row slot r of its cluster (from seq_lens only, so
+// every CTA of the cluster and both warp roles agree on every stage count).
+struct PipeRow {
+    int row, b, g, L, P;
+    int nloc, nst;     // this CTA's valid pages of the row, metadata stages
+    int kk, t0, t1;    // selection size; this CTA's K/V tiles [t0, t1)
+    int u0, w0, w1;    // first selected page of its tiles; its sel_ids entries [w0, w1)
+    int nkv;           // K/V stages (2 tiles each)
+    bool valid;
+};
+
+TS_DEV PipeRow pipe_row(const PipeParams &p, int cluster, int r, int rank) {
+    PipeRow x;
+    x.row = cluster * p.NR + r;
+    x.valid = r < p.NR && x.row < p.rows;
+    const int row = x.valid ? x.row : 0;
+    x.b = row / p.Hkv;
+    x.g = row % p.Hkv;
+    x.L = x.valid ? clamp_len(p.seq_lens[x.b], p.max_pages, 1, p.S) : 0;
+    x.P = (x.L + p.S - 1) / p.S;
+    const int j0 = rank * p.chunk;
+    x.nloc = max(0, min(x.P - j0, p.chunk));
+    x.nst = (x.nloc + kSsStagePages - 1) / kSsStagePages;
+    x.kk = min(p.kmax, x.P);
+    const int tpp = p.S >> 4, tps = __ffs(tpp) - 1;
+    const int ntile = x.kk * tpp;
+    x.t0 = (int)((long long)ntile * rank / p.C);
+    x.t1 = (int)((long long)ntile * (rank + 1) / p.C);
+    x.u0 = x.t0 >> tps;
+    x.w0 = x.kk * rank / p.C;
+    x.w1 = x.kk * (rank + 1) / p.C;
+    x.nkv = (x.t1 - x.t0 + 1) >> 1;
+    return x;
+}
+
+template <bool APP>
+__global__ void __launch_bounds__(kPipeNT, 2) decode_pipe_kernel(
+    const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, PipeParams p) {
+    constexpr int W = kPipeW, CT = kPipeCT;
+    extern __shared__ uint8_t pp_raw[];
+    // 1024-byte aligned (TMA swizzle atoms) by pointer arithmetic on the __shared__ array
+    // itself, so the compiler keeps the shared state space (LDS / ATOMS, not generic LD / ATOM)
+    uint8_t *smem = pp_raw + ((1024u - (smem_u32(pp_raw) & 1023u)) & 1023u);
+    const uint32_t sb = smem_u32(smem);
+    const PipeLayout LY = PipeLayout::make(p.R, p.NR, p.C, p.max_pages, p.kmax, p.chunk, p.two,
+                                           p.share, p.pt_smem);
+    const int R = p.R, NR = p.NR, C = p.C;
+    const uint32_t full0 = sb + LY.bars, empty0 = full0 + 8 * R, qbar = empty0 + 8 * R;
+    const uint32_t ptbar0 = qbar + 8, selbar0 = ptbar0 + 8 * NR, keybar0 = selbar0 + 8 * NR;
+    int *hist = reinterpret_cast<int *>(smem + LY.hist);
+    int *red = reinterpret_cast<int *>(smem + LY.red);
+    float *wpart = reinterpret_cast<float *>(smem + LY.wpart);
+    unsigned *kmm = reinterpret_cast<unsigned *>(smem + LY.kmm);
+    __shared__ int s_last;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int cluster = blockIdx.x / C, rank = blockIdx.x % C;
+    const int j0 = rank * p.chunk;
+    const int S = p.S, tpp = S >> 4, tps = __ffs(tpp) - 1;
+    cg::cluster_group cl = cg::this_cluster();
+
+    if (warp == 0) {  // full[R] empty[R] q pt[NR] sel[NR]: count 1; keys[NR]: the C - 1 peers
+        for (int i = lane; i < 2 * R + 1 + 2 * NR; i += 32) mbar_init(full0 + 8 * i, 1);
+        if (lane < NR) mbar_init(keybar0 + 8 * lane, C > 1 ? C - 1 : 1);
+        if (lane < NR) {
+            kmm[2 * lane] = 0xffffffffu;
+            kmm[2 * lane + 1] = 0u;
+        }
+        fence_mbar_init();
+    } else if (warp == 1 && lane < 2) {
+        prefetch_tmap(lane ? &tmV : &tmK);
+    }
+    for (int i = tid; i < kSsHist / 4; i += kPipeNT) reinterpret_cast<int4 *>(hist)[i] = make_int4(0, 0, 0, 0);
+    __syncthreads();
+    // "this CTA is running and initialised" (before any DSMEM access by a peer); only the
+    // consumers wait for the peers, right before their first remote store
+    if (C > 1) cluster_arrive_release();
+    pdl_wait();  // inputs may come from the previous kernel in the stream
+
+    // stage bases: meta(row 0), meta(row 1), K/V(row 0), K/V(row 1)
+    PipeRow rw[kPipeMaxNR];
+#pragma unroll
+    for (int r = 0; r < kPipeMaxNR; ++r) rw[r] = pipe_row(p, cluster, r, rank);
+    int mbase[kPipeMaxNR], kbase[kPipeMaxNR];
+    {
+        int n = 0;
+#pragma unroll
+        for (int r = 0; r < kPipeMaxNR; ++r) {
+            mbase[r] = n;
+            n += rw[r].valid ? rw[r].nst : 0;
+        }
+#pragma unroll
+        for (int r = 0; r < kPipeMaxNR; ++r) {
+            kbase[r] = n;
+            n += rw[r].valid ? rw[r].nkv : 0;
+        }
+    }
+    auto sel_of = [&](int r) { return reinterpret_cast<int2 *>(smem + LY.sel) + r * p.share; };
+    auto sc_of = [&](int r) { return reinterpret_cast<float *>(smem + LY.sc) + r * LY.scap; };
+    auto pt_of = [&](int r) { return reinterpret_cast<int *>(smem + LY.pt) + r * LY.ptcap; };
+
+    if (warp == W) {
+        // ===================================== producer =====================================
+        const uint64_t pol = l2_policy_evict_first();
+        if (lane == 31) {  // the rows' q groups (G x 128 B each)
+            uint32_t bytes = 0;
+            for (int r = 0; r < NR; ++r) bytes += rw[r].valid ? p.G * kRowBytes : 0;
+            mbar_arrive_expect_tx(qbar, bytes);
+            for (int r = 0; r < NR; ++r)
+                if (rw[r].valid)
+                    bulk_load(sb + LY.q + r * 8 * kRowBytes,
+                              p.q + ((size_t)rw[r].b * p.Hq + rw[r].g * p.G) * kAttnD, p.G * kRowBytes, qbar);
+        }
+        if (lane >= 28 && lane - 28 < NR) {  // page-table row -> smem (page -> block map)
+            const int r = lane - 28;
+            const PipeRow &x = rw[r];
+            if (p.pt_smem && x.valid && x.P > 0) {
+                const uint32_t ptb = min(((uint32_t)x.P * 4 + 15) & ~15u, (uint32_t)LY.ptcap * 4);
+                mbar_arrive_expect_tx(ptbar0 + 8 * r, ptb);
+                bulk_load(smem_u32(pt_of(r)), p.page_table + (size_t)x.b * p.max_pages, ptb, ptbar0 + 8 * r);
+            } else {
+                mbar_arrive(ptbar0 + 8 * r);
+            }
+        }
+        const int nmeta = kbase[0];
+        auto issue_meta = [&](int n) {
+            const int r = (NR > 1 && n >= mbase[1]) ? 1 : 0;
+            const int i = n - mbase[r], st = n % R;
+            const int np = min(kSsStagePages, rw[r].nloc - i * kSsStagePages);
+            const uint32_t bytes = np * 2 * kRowBytes;
+            const uint16_t *src = p.meta + ((size_t)rw[r].row * p.max_pages + j0 + i * kSsStagePages) * 2 * kAttnD;
+            mbar_arrive_expect_tx(full0 + 8 * st, bytes);
+            bulk_load_hint(sb + st * kPipeStage, src, bytes, full0 + 8 * st, pol);
+        };
+        // the ring starts empty: its first stages are issued lane-parallel (TMA issue ~100
+        // cycles each); lane 0 refills in order as the consumers release stages
+        if (lane < min(R, nmeta)) issue_meta(lane);
+        if (lane == 0)
+            for (int n = R; n < nmeta; ++n) {
+                mbar_wait(empty0 + 8 * (n % R), ((n / R) & 1) ^ 1);
+                issue_meta(n);
+            }
+        __syncwarp();
+        for (int r = 0; r < NR; ++r) {
+            const PipeRow &x = rw[r];
+            if (!x.valid || x.nkv == 0) continue;
+            mbar_wait(selbar0 + 8 * r, 0);  // the row's selection (this CTA's share) is in sel[r]
+            // the ring was last read by the generic proxy; APP: the appended K/V row (generic
+            // stores of some CTA of the cluster, published through the key exchange) is read
+            // by TMA below
+            if constexpr (APP)
+                fence_proxy_async_all();
+            else
+                fence_proxy_async();
+            const int2 *sel = sel_of(r);
+            for (int i = 0; i < x.nkv; ++i) {
+                const int n = kbase[r] + i, st = n % R;
+                const int nt = min(2, x.t1 - x.t0 - 2 * i);
+                if (lane == 0) {
+                    if (n >= R) mbar_wait(empty0 + 8 * st, ((n / R) & 1) ^ 1);
+                    mbar_arrive_expect_tx(full0 + 8 * st, nt * 2 * 16 * kRowBytes);
+                }
+                __syncwarp();
+                if (lane < 2 * nt) {  // lane = 2 * tile + (0: K, 1: V)
+                    const int e = lane >> 1, kv = lane & 1;
+                    const int tl = x.t0 + 2 * i + e;
+                    const int2 pg = sel[(tl >> tps) - x.u0];
+                    tma_load_2d(sb + st * kPipeStage + e * 2 * 16 * kRowBytes + kv * 16 * kRowBytes,
+                                kv ? &tmV : &tmK, 0, pg.x + 16 * (tl & (tpp - 1)), full0 + 8 * st, pol);
+                }
+            }
+        }
+        return;
+    }
+
+    // ======================================= consumers ======================================
+    const int gid = lane >> 2, t = lane & 3;
+    mbar_wait(qbar, 0);
+    if constexpr (APP) {
+        // fused append (ts_decode_step_append; Eq. 1): the CTA whose chunk holds
+        // the newest token's page writes its K / V row (16 B per lane of warp 0); the consumer
+        // barrier + release of the key exchange publish it to every CTA's attention TMA
+        if (warp == 0 && lane < 16)
+            for (int r = 0; r < NR; ++r) {
+                const PipeRow &x = rw[r];
+                if (!x.valid || x.L == 0) continue;
+                const int ja = (x.L - 1) / S, aslot = (x.L - 1) - ja * S;
+                if (ja < j0 || ja >= j0 + x.nloc) continue;
+                const int c = lane & 7;
+                const int blk = p.page_table[(size_t)x.b * p.max_pages + ja];
+                const size_t src = ((size_t)x.b * p.Hkv + x.g) * kAttnD + c * 8;
+                const size_t dst = (((size_t)blk * p.Hkv + x.g) * S + aslot) * kAttnD + c * 8;
+                uint16_t *pool = lane < 8 ? p.k_pool : p.v_pool;
+                const uint16_t *nw = lane < 8 ? p.k_new : p.v_new;
+                *reinterpret_cast<uint4 *>(pool + dst) = *reinterpret_cast<const uint4 *>(nw + src);
+            }
+        fence_proxy_async_all();  // before any TMA read of that page
+    }
+
+    bool cluster_ready = false;  // the start cluster barrier was waited for
+    for (int r = 0; r < NR; ++r) {
+        const PipeRow &x = rw[r];
+        if (!x.valid) continue;  // uniform across the cluster (row index only)
+        float *sc = sc_of(r);
+        const int sb0 = p.two ? 0 : j0;  // index of this CTA's first page in sc[]
+        // ------------------------------------------------------------- 1. score
+        uint32_t qa[8], qp[8];
+        {
+            const bool live = gid < p.G;
+            const uint32_t qrow = sb + LY.q + (r * 8 + gid) * kRowBytes;
+            const uint4 x0 = live ? lds_v4(qrow + 16 * t) : make_uint4(0, 0, 0, 0);
+            const uint4 x1 = live ? lds_v4(qrow + 16 * (t + 4)) : make_uint4(0, 0, 0, 0);
+            const uint32_t u0w[4] = {x0.x, x0.y, x0.z, x0.w}, u1w[4] = {x1.x, x1.y, x1.z, x1.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                qa[e] = bf16x2_min0(u0w[e]);
+                qa[4 + e] = bf16x2_min0(u1w[e]);
+                qp[e] = bf16x2_max0(u0w[e]);
+                qp[4 + e] = bf16x2_max0(u1w[e]);
+            }
+        }
+        const bool c0 = 2 * t < p.G, c1 = 2 * t + 1 < p.G;
+        uint32_t kmn = 0xffffffffu, kmx = 0u;
+        int apl = -1, aslot = 0, ja = 0;  // APP: the appended page, chunk-local
+        uint4 kn = make_uint4(0, 0, 0, 0);
+        if constexpr (APP) {
+            if (x.L > 0) {
+                ja = (x.L - 1) / S;
+                aslot = (x.L - 1) - ja * S;
+                if (ja >= j0 && ja < j0 + x.nloc) apl = ja - j0;
+            }
+            if (apl >= 0 && lane < 16 && (apl / kSsStagePages) % W == warp)
+                kn = *reinterpret_cast<const uint4 *>(p.k_new + ((size_t)x.b * p.Hkv + x.g) * kAttnD + (lane & 7) * 8);
+        }
+        for (int i = warp; i < x.nst; i += W) {
+            const int n = mbase[r] + i, st = n % R;
+            mbar_wait(full0 + 8 * st, (n / R) & 1);
+            const uint32_t kb = sb + st * kPipeStage;
+            if (APP && apl >= i * kSsStagePages && apl < (i + 1) * kSsStagePages) {  // warp-uniform
+                if (lane < 16) {  // lanes 0-7: the m row, 8-15: the M row (16 B each)
+                    const uint32_t a = kb + (apl - i * kSsStagePages) * 2 * kRowBytes + (lane >> 3) * kRowBytes +
+                                       (lane & 7) * 16;
+                    uint4 v = lds_v4(a);
+                    if (aslot == 0) {  // first key of the page: m = M = k
+                        v = kn;
+                    } else if (lane < 8) {
+                        v = make_uint4(bf16x2_min(v.x, kn.x), bf16x2_min(v.y, kn.y), bf16x2_min(v.z, kn.z),
+                                       bf16x2_min(v.w, kn.w));
+                    } else {
+                        v = make_uint4(bf16x2_max(v.x, kn.x), bf16x2_max(v.y, kn.y), bf16x2_max(v.z, kn.z),
+                                       bf16x2_max(v.w, kn.w));
+                    }
+                    sts_v4(a, v);
+                    uint16_t *mrec = const_cast<uint16_t *>(p.meta) + ((size_t)x.row * p.max_pages + ja) * 2 * kAttnD +
+                                     (lane >> 3) * kAttnD + (lane & 7) * 8;
+                    *reinterpret_cast<uint4 *>(mrec) = v;  // the cache's record (logical layout)
+                    fence_proxy_async();  // generic smem write before the stage's next TMA fill
+                }
+                __syncwarp();
+            }
+#pragma unroll
+            for (int tile = 0; tile < 2; ++tile) {
+                const uint32_t tb = kb + tile * 16 * 2 * kRowBytes;
+                float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                for (int ci = 0; ci < 4; ++ci) {
+                    const uint4 a = lds_v4(tb + gid * 2 * kRowBytes + 16 * (t + 4 * ci));
+                    const uint4 h = lds_v4(tb + (gid + 8) * 2 * kRowBytes + 16 * (t + 4 * ci));
+                    const uint32_t *cf = ci < 2 ? qa + 4 * ci : qp + 4 * (ci - 2);
+                    mma_bf16_16816(acc, a.x, h.x, a.y, h.y, cf[0], cf[1]);
+                    mma_bf16_16816(acc, a.z, h.z, a.w, h.w, cf[2], cf[3]);
+                }
+                float m0 = fmaxf(c0 ? acc[0] : kNegInf, c1 ? acc[1] : kNegInf);
+                float m1 = fmaxf(c0 ? acc[2] : kNegInf, c1 ? acc[3] : kNegInf);
+                m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, 1));
+                m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, 2));
+                m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, 1));
+                m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, 2));
+                if (t < 2) {
+                    const int pg = i * kSsStagePages + tile * 16 + gid + 8 * t;
+                    if (j0 + pg < p.max_pages && pg < p.chunk) {
+                        const bool valid = pg < x.nloc;
+                        const float v = valid ? (t ? m1 : m0) + 0.0f : kNegInf;
+                        sc[sb0 + pg] = v;
+                        if (valid) {
+                            const uint32_t key = score_key(v);
+                            kmn = min(kmn, key);
+                            kmx = max(kmx, key);
+                        }
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty0 + 8 * st);
+        }
+        kmn = __reduce_min_sync(0xffffffffu, kmn);
+        kmx = __reduce_max_sync(0xffffffffu, kmx);
+        if (lane == 0 && kmn <= kmx) {
+            atomicMin(&kmm[2 * r], kmn);
+            atomicMax(&kmm[2 * r + 1], kmx);
+        }
+        for (int pg = x.nst * kSsStagePages + tid; pg < p.chunk; pg += CT)  // chunk pages past P_b
+            if (j0 + pg < p.max_pages) sc[sb0 + pg] = kNegInf;
+        named_bar_sync(kPipeBar, CT);
+
+        // ------------------------------------------------------------- 2. select
+        const int *ptrow = p.pt_smem ? pt_of(r) : p.page_table + (size_t)x.b * p.max_pages;
+        int2 *sel = sel_of(r);
+        int *out_id = p.sel_ids + (size_t)x.row * p.kmax;
+        uint32_t *cand = reinterpret_cast<uint32_t *>(wpart);  // select scratch (attention later)
+        auto emit_pg = [&](int pos, int pg) {
+            const int u = pos - x.u0;
+            if (u >= 0 && u < p.share) sel[u] = make_int2((ptrow[pg] * p.Hkv + x.g) * S, pg * S);
+            if (pos >= x.w0 && pos < x.w1) out_id[pos] = pg;
+        };
+        auto exchange = [&](const uint32_t *src, uint32_t *dst_local, int n4, bool key_range) {
+            // push n4 x 16 B from src into every peer's dst_local (same offset), then announce
+            if (!cluster_ready) {
+                cluster_wait();  // every CTA of the cluster has initialised its barriers
+                cluster_ready = true;
+            }
+            for (int e = tid; e < (C - 1) * n4; e += CT) {
+                const int rr = rank + 1 + e / n4, u = e % n4;
+                const int peer = rr < C ? rr : rr - C;
+                reinterpret_cast<uint4 *>(cl.map_shared_rank(dst_local, peer))[u] =
+                    reinterpret_cast<const uint4 *>(src)[u];
+            }
+            if (key_range && tid >= 1 && tid < C && kmm[2 * r] <= kmm[2 * r + 1]) {
+                const int rr = rank + tid, peer = rr < C ? rr : rr - C;
+                atomicMin(cl.map_shared_rank(&kmm[2 * r], peer), kmm[2 * r]);
+                atomicMax(cl.map_shared_rank(&kmm[2 * r + 1], peer), kmm[2 * r + 1]);
+            }
+            named_bar_sync(kPipeBar, CT);
+            if (tid == 0) {
+                fence_acq_rel_cluster();
+                for (int q = 1; q < C; ++q) mbar_arrive_remote(keybar0 + 8 * r, (rank + q) % C);
+            }
+            mbar_wait_cluster(keybar0 + 8 * r, 0);
+        };
+        if (p.two && C > 1) {
+            // two-level: this chunk's top-K (exact: a page of the row's top-K is beaten by
+            // fewer than K pages of its own chunk, same order), pushed to every peer
+            uint32_t *lkeys = reinterpret_cast<uint32_t *>(sc);
+            for (int i = tid; i < ((x.nloc + 3) & ~3); i += CT) lkeys[i] = i < x.nloc ? score_key(sc[i]) : 0u;
+            uint32_t *ckey = reinterpret_cast<uint32_t *>(smem + LY.cand) + r * LY.candcap;
+            int *cid = reinterpret_cast<int *>(ckey) + C * p.kmax;
+            uint32_t *myk = ckey + rank * p.kmax;
+            int *myi = cid + rank * p.kmax;
+            named_bar_sync(kPipeBar, CT);
+            const int kl = cta_topk<CT, kPipeBar, 0>(lkeys, x.nloc, p.kmax, kmm[2 * r], kmm[2 * r + 1], hist, red,
+                                                     cand, [&](int pos, int i) {
+                                                         myk[pos] = lkeys[i];
+                                                         myi[pos] = j0 + i;
+                                                     });
+            for (int i = kl + tid; i < p.kmax; i += CT) myk[i] = 0u;  // absent
+            for (int i = tid; i < kSsHist / 4; i += CT) reinterpret_cast<int4 *>(hist)[i] = make_int4(0, 0, 0, 0);
+            named_bar_sync(kPipeBar, CT);
+            // keys and ids of this chunk (host: kmax % 4 == 0): two pushes, one announcement
+            {
+                if (!cluster_ready) {
+                    cluster_wait();
+                    cluster_ready = true;
+                }
+                const int k4n = p.kmax >> 2;
+                for (int e = tid; e < (C - 1) * 2 * k4n; e += CT) {
+                    const int which = e / ((C - 1) * k4n), f = e % ((C - 1) * k4n);
+                    const int rr = rank + 1 + f / k4n, u = f % k4n;
+                    const int peer = rr < C ? rr : rr - C;
+                    uint32_t *base = which ? reinterpret_cast<uint32_t *>(myi) : myk;
+                    reinterpret_cast<uint4 *>(cl.map_shared_rank(base, peer))[u] = reinterpret_cast<const uint4 *>(base)[u];
+                }
+                named_bar_sync(kPipeBar, CT);
+                if (tid == 0) {
+                    fence_acq_rel_cluster();
+                    for (int q = 1; q < C; ++q) mbar_arrive_remote(keybar0 + 8 * r, (rank + q) % C);
+                }
+                mbar_wait_cluster(keybar0 + 8 * r, 0);
+            }
+            const int nc = C * p.kmax;
+            int nlive = 0;  // live candidates: sum over chunks of min(K, chunk pages)
+            for (int c = 0; c < C; ++c) nlive += min(p.kmax, max(0, min(x.P - c * p.chunk, p.chunk)));
+            uint32_t mn = 0xffffffffu, mx = 0u;
+            for (int i = tid; i < nc; i += CT)
+                if (ckey[i]) {
+                    mn = min(mn, ckey[i]);
+                    mx = max(mx, ckey[i]);
+                }
+            mbar_wait(ptbar0 + 8 * r, 0);
+            block_minmax<CT, kPipeBar>(mn, mx, red);
+            // candidates are chunk-major, ids ascending inside a chunk: entry order == id order
+            cta_topk<CT, kPipeBar, 11>(ckey, nc, p.kmax, mn, mx, hist, red, cand,
+                                       [&](int pos, int i) { emit_pg(pos, cid[i]); }, nullptr, false, nlive);
+        } else {
+            uint32_t *keys = reinterpret_cast<uint32_t *>(sc);
+            const int e1 = min(j0 + p.chunk, (x.P + 3) & ~3);
+            for (int i = j0 + tid; i < e1; i += CT) keys[i] = i < x.P ? score_key(sc[i]) : 0u;
+            if (C > 1) {
+                named_bar_sync(kPipeBar, CT);
+                exchange(keys + j0, keys + j0, max(0, e1 - j0) >> 2, true);
+            }
+            mbar_wait(ptbar0 + 8 * r, 0);
+            named_bar_sync(kPipeBar, CT);
+            cta_topk<CT, kPipeBar, 0>(keys, x.P, p.kmax, kmm[2 * r], kmm[2 * r + 1], hist, red, cand,
+                                      [&](int pos, int i) { emit_pg(pos, i); });
+        }
+        if (rank == 0) {
+            for (int i = x.kk + tid; i < p.kmax; i += CT) out_id[i] = -1;
+            if (tid == 0) p.sel_count[x.row] = x.kk;
+        }
+        for (int i = tid; i < kSsHist / 4; i += CT) reinterpret_cast<int4 *>(hist)[i] = make_int4(0, 0, 0, 0);
+        named_bar_sync(kPipeBar, CT);
+        if (tid == 0) mbar_arrive(selbar0 + 8 * r);  // release: sel[r] complete -> producer
+    }
+
+    // ------------------------------------------------------------- 3-4. attend + merge
+    const float sl2 = p.scale * kLog2e;
+    int last = -1;
+    for (int r = 0; r < NR; ++r)
+        if (rw[r].valid) last = r;
+    for (int r = 0; r < NR; ++r) {
+        const PipeRow &x = rw[r];
+        if (!x.valid) continue;
+        const int2 *sel = sel_of(r);
+        uint32_t qa[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        if (gid < p.G) {
+            const uint32_t qrow = sb + LY.q + (r * 8 + gid) * kRowBytes + 32 * t;
+            const uint4 x0 = lds_v4(qrow), x1 = lds_v4(qrow + 16);
+            qa[0] = x0.x; qa[1] = x0.y; qa[2] = x0.z; qa[3] = x0.w;
+            qa[4] = x1.x; qa[5] = x1.y; qa[6] = x1.z; qa[7] = x1.w;
+        }
+        float m = kNegInf, lp = 0.f;
+        float oacc[8][4];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) oacc[j][0] = oacc[j][1] = oacc[j][2] = oacc[j][3] = 0.f;
+        for (int i = warp; i < x.nkv; i += W) {
+            const int n = kbase[r] + i, st = n % R;
+            const int nt = min(2, x.t1 - x.t0 - 2 * i);
+            int tok0[2];
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {  // first tokens, from sel[] (complete), ahead of the wait
+                const int tl = x.t0 + 2 * i + min(e, nt - 1);
+                tok0[e] = sel[(tl >> tps) - x.u0].y + 16 * (tl & (tpp - 1));
+            }
+            mbar_wait(full0 + 8 * st, (n / R) & 1);
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                if (e >= nt) break;
+                const uint32_t kb = sb + st * kPipeStage + e * 2 * 16 * kRowBytes, vb = kb + 16 * kRowBytes;
+                float sacc[2][4];
+#pragma unroll
+                for (int ntl = 0; ntl < 2; ++ntl) {
+                    sacc[ntl][0] = sacc[ntl][1] = sacc[ntl][2] = sacc[ntl][3] = 0.f;
+                    const int rr = ntl * 8 + gid;
+                    const uint32_t ra = kb + rr * kRowBytes;
+                    const uint4 k0 = lds_v4(ra + (((2 * t) ^ (rr & 7)) << 4));
+                    const uint4 k1 = lds_v4(ra + (((2 * t + 1) ^ (rr & 7)) << 4));
+                    mma_bf16_16816(sacc[ntl], qa[0], 0u, qa[1], 0u, k0.x, k0.y);
+                    mma_bf16_16816(sacc[ntl], qa[2], 0u, qa[3], 0u, k0.z, k0.w);
+                    mma_bf16_16816(sacc[ntl], qa[4], 0u, qa[5], 0u, k1.x, k1.y);
+                    mma_bf16_16816(sacc[ntl], qa[6], 0u, qa[7], 0u, k1.z, k1.w);
+                }
+                float xs[2][2];
+                float tmax = kNegInf;
+#pragma unroll
+                for (int ntl = 0; ntl < 2; ++ntl)
+#pragma unroll
+                    for (int q2 = 0; q2 < 2; ++q2) {
+                        const bool ok = tok0[e] + ntl * 8 + 2 * t + q2 < x.L;
+                        xs[ntl][q2] = ok ? sacc[ntl][q2] * sl2 : kNegInf;
+                        tmax = fmaxf(tmax, xs[ntl][q2]);
+                    }
+                tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 1));
+                tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 2));
+                const float mnew = fmaxf(m, tmax);
+                const float mref = mnew == kNegInf ? 0.f : mnew;
+                const float corr = exp2f(m - mref);
+                m = mnew;
+                float pr[2][2];
+                float psum = 0.f;
+#pragma unroll
+                for (int ntl = 0; ntl < 2; ++ntl)
+#pragma unroll
+                    for (int q2 = 0; q2 < 2; ++q2) {
+                        pr[ntl][q2] = exp2f(xs[ntl][q2] - mref);
+                        psum += pr[ntl][q2];
+                    }
+                lp = lp * corr + psum;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    oacc[j][0] *= corr;
+                    oacc[j][1] *= corr;
+                }
+#pragma unroll
+                for (int ntl = 0; ntl < 2; ++ntl) {
+                    const int q0 = ntl * 8 + 2 * t, q1 = q0 + 1;
+                    uint4 v0 = lds_v4(vb + q0 * kRowBytes + ((gid ^ (q0 & 7)) << 4));
+                    uint4 v1 = lds_v4(vb + q1 * kRowBytes + ((gid ^ (q1 & 7)) << 4));
+                    if (tok0[e] + q0 >= x.L) v0 = make_uint4(0, 0, 0, 0);  // past seq_len: may be anything
+                    if (tok0[e] + q1 >= x.L) v1 = make_uint4(0, 0, 0, 0);
+                    const uint32_t a0 = f32_to_tf32(pr[ntl][0]), a2 = f32_to_tf32(pr[ntl][1]);
+                    const uint32_t w0v[4] = {v0.x, v0.y, v0.z, v0.w};
+                    const uint32_t w1v[4] = {v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const uint32_t b0 = (j & 1) ? (w0v[j >> 1] & 0xffff0000u) : (w0v[j >> 1] << 16);
+                        const uint32_t b1 = (j & 1) ? (w1v[j >> 1] & 0xffff0000u) : (w1v[j >> 1] << 16);
+                        mma_tf32_1688(oacc[j], a0, 0u, a2, 0u, b0, b1);
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty0 + 8 * st);
+        }
+        lp += __shfl_xor_sync(0xffffffffu, lp, 1);
+        lp += __shfl_xor_sync(0xffffffffu, lp, 2);
+        if (gid < p.G) {
+            float *wr = wpart + (warp * 8 + gid) * kSaPart;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                wr[16 * t + j] = oacc[j][0];
+                wr[16 * t + 8 + j] = oacc[j][1];
+            }
+            if (t == 0) {
+                wr[kAttnD] = m;
+                wr[kAttnD + 1] = lp;
+            }
+        }
+        named_bar_sync(kPipeBar, CT);
+        if (r == last && (p.flags & 16)) pdl_launch_dependents();  // only the merge / tail remains
+        // ---- CTA merge of the W warp partials (C == 1: straight to o / lse)
+        for (int xi = tid; xi < p.G * 16; xi += CT) {
+            const int h = xi >> 4, d0 = (xi & 15) * 4;
+            float mw[W];
+#pragma unroll
+            for (int w = 0; w < W; ++w) mw[w] = wpart[(w * 8 + h) * kSaPart + kAttnD];
+            float M = kNegInf;
+#pragma unroll
+            for (int w = 0; w < W; ++w) M = fmaxf(M, mw[w]);
+            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+            float l = 0.f;
+            if (M != kNegInf) {
+#pragma unroll
+                for (int w = 0; w < W; ++w) {
+                    const float *wr = wpart + (w * 8 + h) * kSaPart;
+                    const float f = mw[w] == kNegInf ? 0.f : exp2f(mw[w] - M);
+                    l += wr[kAttnD + 1] * f;
+                    const float4 v = *reinterpret_cast<const float4 *>(wr + d0);
+                    acc.x += v.x * f; acc.y += v.y * f; acc.z += v.z * f; acc.w += v.w * f;
+                }
+            }
+            if (C == 1) {
+                const size_t oh = (size_t)x.b * p.Hq + x.g * p.G + h;
+                const float inv = l > 0.f ? 1.f / l : 0.f;
+                *reinterpret_cast<float4 *>(p.o + oh * kAttnD + d0) =
+                    make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+                if (p.lse && d0 == 0) p.lse[oh] = l > 0.f ? (M + log2f(l)) * kLn2 : kNegInf;
+            } else {
+                float *pr = p.part + (((size_t)x.row * C + rank) * 8 + h) * kPS;
+                *reinterpret_cast<float4 *>(pr + d0) = acc;
+                if (d0 == 0) {
+                    pr[kAttnD] = M;
+                    pr[kAttnD + 1] = l;
+                }
+            }
+        }
+        if (C > 1) {  // the last CTA of the row (acq_rel ticket) merges the C partials
+            named_bar_sync(kPipeBar, CT);
+            if (tid == 0) s_last = atom_add_acq_rel_gpu(p.tickets + x.row, 1u) == unsigned(C - 1);
+            named_bar_sync(kPipeBar, CT);
+            if (s_last) {
+                constexpr int kMaxC = 16;
+                const float *pb = p.part + (size_t)x.row * C * 8 * kPS;
+                for (int xi = tid; xi < p.G * 16; xi += CT) {
+                    const int h = xi >> 4, d0 = (xi & 15) * 4;
+                    float mr[kMaxC];
+#pragma unroll
+                    for (int c = 0; c < kMaxC; ++c)
+                        mr[c] = c < C ? __ldcg(pb + (c * 8 + h) * kPS + kAttnD) : kNegInf;
+                    float M = kNegInf;
+#pragma unroll
+                    for (int c = 0; c < kMaxC; ++c) M = fmaxf(M, mr[c]);
+                    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+                    float l = 0.f;
+                    if (M != kNegInf) {
+#pragma unroll
+                        for (int c0i = 0; c0i < kMaxC; c0i += 4) {
+                            if (c0i >= C) break;
+                            float lq[4];
+                            float4 vq[4];
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                const float *pr = pb + ((c0i + e) * 8 + h) * kPS;
+                                lq[e] = c0i + e < C ? __ldcg(pr + kAttnD + 1) : 0.f;
+                                vq[e] = c0i + e < C ? __ldcg(reinterpret_cast<const float4 *>(pr + d0))
+                                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+                            }
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                const float f = mr[c0i + e] == kNegInf ? 0.f : exp2f(mr[c0i + e] - M);
+                                l += lq[e] * f;
+                                acc.x += vq[e].x * f; acc.y += vq[e].y * f; acc.z += vq[e].z * f; acc.w += vq[e].w * f;
+                            }
+                        }
+                    }
+                    const size_t oh = (size_t)x.b * p.Hq + x.g * p.G + h;
+                    const float inv = l > 0.f ? 1.f / l : 0.f;
+                    *reinterpret_cast<float4 *>(p.o + oh * kAttnD + d0) =
+                        make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+                    if (p.lse && d0 == 0) p.lse[oh] = l > 0.f ? (M + log2f(l)) * kLn2 : kNegInf;
+                }
+                if (tid == 0) p.tickets[x.row] = 0u;  // re-armed for the next launch
+            }
+        }
+        named_bar_sync(kPipeBar, CT);  // wpart / s_last reused by the next row
+    }
+}
+
+}  // namespace ts
