@@ -3,6 +3,7 @@
 // on the caller's stream; nothing here allocates device memory or synchronises.
 #include <cudaTypedefs.h>
 
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 #include <unordered_map>
@@ -568,62 +569,47 @@ int env_int(const char *name, int dflt) {  // development A/B knobs (read once p
 
 template <bool APP>
 PipePlan plan_pipe(const ts_layout *L, int kmax) {
+    // NR = 2 rows per cluster (two consumer groups per CTA); C = the widest split of a row
+    // that keeps the grid within one wave at 2 CTAs per SM (every CTA of a cluster does
+    // the same work, so the CTAs finish together) and >= 64 pages per CTA; the ring takes
+    // the shared memory left at ceil(CTAs / SMs) CTAs per SM
     auto kern = decode_pipe_kernel<APP>;
     PipePlan best;
     const int rows = L->batch * L->num_kv_heads;
     const int sms = device_sms();
-    const int S = L->page_size, tpp = S / 16, G = group_of(L);
-    const double e = 2.0, d = 64.0;
-    // bytes of one row: metadata of every page + the selected K/V (upper bound: full pages)
-    const double P = L->max_pages, K = std::min(kmax, L->max_pages);
-    const double row_bytes = P * 2 * d * e + K * S * 2 * d * e + G * d * (e + 4);
-    const double total = rows * row_bytes;
+    const int tpp = L->page_size / 16;
     static const int nr_env = env_int("TS_PIPE_NR", 0), c_env = env_int("TS_PIPE_C", 0),
                      r_env = env_int("TS_PIPE_R", 0);
-    for (int NR = 2; NR >= 1; --NR) {
-        if (nr_env && NR != nr_env) continue;
-        const int ncl = (rows + NR - 1) / NR;
-        for (int Cd = 1; Cd <= kMaxClusterC; ++Cd) {
-            int chunk = (L->max_pages + Cd - 1) / Cd;
-            chunk = (chunk + kSsStagePages - 1) / kSsStagePages * kSsStagePages;
-            const int C = (L->max_pages + chunk - 1) / chunk;
-            if (C != Cd) continue;  // the same split as a smaller Cd
-            if (c_env && C != c_env) continue;
-            if (C > 1 && chunk < 64 && !c_env) continue;  // >= 64 pages per CTA
-            const int two = (C > 1 && kmax % 4 == 0 && L->max_pages > 2048 &&
-                             L->max_pages >= 4 * C * kmax) ? 1 : 0;
-            const int share = ((kmax * tpp + C - 1) / C + tpp - 1) / tpp + 1;
-            const int T = ncl * C;
-            for (int m = 1; m <= 4; ++m) {  // CTAs per SM the shared memory is sized for
-                if ((long long)m * sms < std::min(T, 2 * sms) && m < 4) continue;  // one wave (or two SM-loads)
-                const int pt_smem = ((L->max_pages & 3) == 0 && L->max_pages <= 2048) ? 1 : 0;
-                const PipeLayout l0 = PipeLayout::make(0, NR, C, L->max_pages, kmax, chunk, two, share, pt_smem);
-                const long long budget = std::min<long long>(227 * 1024, 228 * 1024 / m - 1024) - 1024;
-                int R = (int)std::min<long long>(24, (budget - l0.total - 128) / kPipeStage);
-                if (r_env) R = std::min(R, r_env);
-                if (R < 4) continue;
-                const PipeLayout l = PipeLayout::make(R, NR, C, L->max_pages, kmax, chunk, two, share, pt_smem);
-                const size_t sm = 1024 + (size_t)l.total;
-                const double ring = (double)R * kPipeStage;
-                const double cta = NR * row_bytes / C;
-                const double lat_us = 1.5;
-                const double t_bw = total / 6.5e6;               // us at 6.5 TB/s
-                const double waves = std::ceil((double)T / ((double)m * sms));
-                const double t_cta = waves * cta / (ring / lat_us);
-                double est = std::max(t_bw, t_cta) + 2.0;         // launch ramp + tail
-                if (C > 1) est += 1.0 + (two ? 1.0 : 0.0);        // exchange + ticket merge
-                if (NR == 1) est += two ? 4.0 : 2.0;              // the exposed select(s)
-                if (est < best.est_us) {
-                    if (!ensure_func_attrs((const void *)kern, sm, true)) continue;
-                    if (max_active_clusters(kern, kPipeNT, sm, C) < std::min(ncl, (int)(m * sms / C))) continue;
-                    best.ok = true;
-                    best.NR = NR; best.C = C; best.chunk = chunk; best.R = R; best.two = two;
-                    best.share = share; best.pt_smem = pt_smem; best.sm = sm; best.est_us = est;
-                }
-                break;  // larger m only shrinks the ring
-            }
-        }
+    const int NR = nr_env ? nr_env : 2;
+    const int ncl = (rows + NR - 1) / NR;
+    int C = 1, chunk = L->max_pages;
+    for (int Cd = 1; Cd <= kMaxClusterC; ++Cd) {
+        int ch = (L->max_pages + Cd - 1) / Cd;
+        ch = (ch + kSsStagePages - 1) / kSsStagePages * kSsStagePages;
+        const int c = (L->max_pages + ch - 1) / ch;
+        if (c_env ? c != c_env : (c > 1 && (ch < 64 || (long long)ncl * c > 2 * sms))) continue;
+        C = c;
+        chunk = ch;
+        if (c_env) break;
     }
+    chunk = (chunk + kSsStagePages - 1) / kSsStagePages * kSsStagePages;
+    const int two = (C > 1 && kmax % 4 == 0 && L->max_pages > 2048 && L->max_pages >= 4 * C * kmax) ? 1 : 0;
+    const int share = ((kmax * tpp + C - 1) / C + tpp - 1) / tpp + 1;
+    const int pt_smem = ((L->max_pages & 3) == 0 && L->max_pages <= 2048) ? 1 : 0;
+    const long long T = (long long)ncl * C;
+    const int m = (int)std::min<long long>(2, std::max<long long>(1, (T + sms - 1) / sms));
+    const PipeLayout l0 = PipeLayout::make(0, NR, C, L->max_pages, kmax, chunk, two, share, pt_smem);
+    const long long budget = std::min<long long>(227 * 1024, 228 * 1024 / m - 1024) - 1024;
+    int R = (int)std::min<long long>(24, (budget - l0.total) / kPipeStage);
+    if (r_env) R = std::min(R, r_env);
+    if (R < 4) return best;
+    const PipeLayout l = PipeLayout::make(R, NR, C, L->max_pages, kmax, chunk, two, share, pt_smem);
+    const size_t sm = 1024 + (size_t)l.total;
+    if (!ensure_func_attrs((const void *)kern, sm, true)) return best;
+    if (max_active_clusters(kern, kPipeNT, sm, C) < 1) return best;
+    best.ok = true;
+    best.NR = NR; best.C = C; best.chunk = chunk; best.R = R; best.two = two;
+    best.share = share; best.pt_smem = pt_smem; best.sm = sm; best.est_us = 0;
     return best;
 }
 
@@ -644,6 +630,10 @@ ts_status launch_pipe(const ts_layout *L, PipeParams &pp, cudaStream_t st) {
     pp.pt_smem = pl.pt_smem;
     static const int trig = env_int("TS_PIPE_TRIGGER", 1);
     pp.flags = trig ? 16 : 0;
+    static const int verbose = env_int("TS_PIPE_VERBOSE", 0);
+    if (verbose)
+        fprintf(stderr, "[tinyserve] pipe plan: NR %d C %d chunk %d R %d two %d share %d pt_smem %d smem %zu est %.1f us\n",
+                pl.NR, pl.C, pl.chunk, pl.R, pl.two, pl.share, pl.pt_smem, pl.sm, pl.est_us);
     const int ncl = (pp.rows + pl.NR - 1) / pl.NR;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(ncl * pl.C);
@@ -970,6 +960,7 @@ static ts_status decode_step_impl(const ts_layout *L, const void *q, const void 
         pp.max_pages = L->max_pages;
         pp.kmax = kmax;
         pp.rows = rows;
+        pp.dbg = g_dbg_ss;
         phase_mark(0, st);
         s = k_new ? launch_pipe<true>(L, pp, st) : launch_pipe<false>(L, pp, st);
         phase_mark(3, st);

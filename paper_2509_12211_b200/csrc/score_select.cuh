@@ -67,37 +67,39 @@ struct SsSmem {
 // ---------------------------------------------------------------------------------------
 // Barrier over the NT participating threads: the whole CTA (BAR = 0) or a named barrier
 // (BAR > 0) over warps 0 .. NT/32 - 1, so that other warps (a producer) need not join.
-template <int NT, int BAR>
-TS_DEV void sel_sync() {
-    if (BAR == 0)
+// bar: runtime barrier id (0 = the whole CTA); a thread group of NT threads starting at
+// thread `tb` (a multiple of 32) may run its own select with its own named barrier.
+template <int NT>
+TS_DEV void sel_sync(int bar) {
+    if (bar == 0)
         __syncthreads();
     else
-        named_bar_sync(BAR, NT);
+        named_bar_sync(bar, NT);
 }
 
 // Block reductions (NT threads, scratch red[>= NT/32 + 2]).
 template <int NT, int BAR = 0>
-TS_DEV int block_sum(int v, int *red) {
+TS_DEV int block_sum(int v, int *red, int bar = BAR, int tb = 0) {
     v = __reduce_add_sync(0xffffffffu, v);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31, warp = (threadIdx.x - tb) >> 5;
     if (lane == 0) red[warp] = v;
-    sel_sync<NT, BAR>();
+    sel_sync<NT>(bar);
     int s = 0;
 #pragma unroll
     for (int w = 0; w < NT / 32; ++w) s += red[w];
-    sel_sync<NT, BAR>();
+    sel_sync<NT>(bar);
     return s;
 }
 template <int NT, int BAR = 0>
-TS_DEV void block_minmax(uint32_t &mn, uint32_t &mx, int *red) {
+TS_DEV void block_minmax(uint32_t &mn, uint32_t &mx, int *red, int bar = BAR, int tb = 0) {
     mn = __reduce_min_sync(0xffffffffu, mn);
     mx = __reduce_max_sync(0xffffffffu, mx);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31, warp = (threadIdx.x - tb) >> 5;
     if (lane == 0) {
         red[warp] = (int)mn;
         red[32 + warp] = (int)mx;
     }
-    sel_sync<NT, BAR>();
+    sel_sync<NT>(bar);
     uint32_t a = 0xffffffffu, b = 0u;
 #pragma unroll
     for (int w = 0; w < NT / 32; ++w) {
@@ -106,12 +108,12 @@ TS_DEV void block_minmax(uint32_t &mn, uint32_t &mx, int *red) {
     }
     mn = a;
     mx = b;
-    sel_sync<NT, BAR>();
+    sel_sync<NT>(bar);
 }
 // exclusive scan of one int per thread in thread order; *total = sum
 template <int NT, int BAR = 0>
-TS_DEV int block_scan(int v, int *red, int *total) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+TS_DEV int block_scan(int v, int *red, int *total, int bar = BAR, int tb = 0) {
+    const int lane = threadIdx.x & 31, warp = (threadIdx.x - tb) >> 5;
     int x = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -119,7 +121,7 @@ TS_DEV int block_scan(int v, int *red, int *total) {
         if (lane >= o) x += y;
     }
     if (lane == 31) red[warp] = x;
-    sel_sync<NT, BAR>();
+    sel_sync<NT>(bar);
     int before = 0, tot = 0;
 #pragma unroll
     for (int w = 0; w < NT / 32; ++w) {
@@ -127,7 +129,7 @@ TS_DEV int block_scan(int v, int *red, int *total) {
         before += w < warp ? s : 0;
         tot += s;
     }
-    sel_sync<NT, BAR>();
+    sel_sync<NT>(bar);
     *total = tot;
     return before + x - v;
 }
@@ -166,13 +168,13 @@ TS_DEV int hsw(int b) { return b ^ ((b >> 3) & 12); }
 template <int NT, int BAR, int HB = 11, typename Emit>
 TS_DEV int cta_topk(const uint32_t *keys, int n, int k, uint32_t kmin, uint32_t kmax, int *hist,
                     int *red, uint32_t *cand, Emit emit, unsigned long long *dts = nullptr,
-                    bool hist0_built = false, int nvalid = -1) {
+                    bool hist0_built = false, int nvalid = -1, int bar = BAR, int tb = 0) {
     // nvalid: number of live (non-zero) keys when keys[] holds zero padding (default n)
     // hist0_built: the first pass histogram over [kmin, kmax] (shift as below) is already
     // in hist (built in parallel by the CTAs of a cluster, score_select / step_cluster)
     // keys[] is 16-byte aligned and zero-padded to a multiple of 4 (0 < every valid key):
     // the scans below read it as uint4 for memory-level parallelism (smem latency ~30 cycles)
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tid = threadIdx.x - tb, lane = tid & 31, warp = tid >> 5;
     // HB = 0: radix width by length at run time (~1 key per bin on the first pass), one
     // instantiation instead of two (instruction-cache footprint of the fused kernel)
     const int hb = HB ? HB : (n <= 512 ? 9 : 11);
@@ -200,7 +202,7 @@ TS_DEV int cta_topk(const uint32_t *keys, int n, int k, uint32_t kmin, uint32_t 
             const int shift = bits > hb ? bits - hb : 0;
             if (pass > 0) {
                 for (int i = tid; i < (1 << hb); i += NT) hist[i] = 0;
-                sel_sync<NT, BAR>();
+                sel_sync<NT>(bar);
             }
             if (pass > 0 || !hist0_built) {
 #pragma unroll 2
@@ -214,7 +216,7 @@ TS_DEV int cta_topk(const uint32_t *keys, int n, int k, uint32_t kmin, uint32_t 
                         atomicAdd(&hist[hsw(bn)], in ? 1 : 0);
                     }
                 }
-                sel_sync<NT, BAR>();
+                sel_sync<NT>(bar);
             }
             TS_TOPK_PROF(1);
             {  // boundary bin: thread t < TT owns bins [16 t, 16 t + 16); block suffix scan
@@ -243,7 +245,7 @@ TS_DEV int cta_topk(const uint32_t *keys, int n, int k, uint32_t kmin, uint32_t 
                     if (lane == 0) red[40 + warp] = suf;  // warp total
                 }
                 TS_TOPK_PROF2(9);
-                sel_sync<NT, BAR>();
+                sel_sync<NT>(bar);
                 TS_TOPK_PROF2(10);
                 if (tid < TT) {
 #pragma unroll
@@ -271,7 +273,7 @@ TS_DEV int cta_topk(const uint32_t *keys, int n, int k, uint32_t kmin, uint32_t 
                 if (tid == 0) red[51] = 0;  // candidate counter
                 TS_TOPK_PROF2(11);
             }
-            sel_sync<NT, BAR>();
+            sel_sync<NT>(bar);
             if (dts && tid == 0 && pass == 0) dts[5] = globaltimer();
             TS_TOPK_PROF(2);
             const int bsel = red[48], above = red[49], cnt = red[50];
@@ -301,7 +303,7 @@ TS_DEV int cta_topk(const uint32_t *keys, int n, int k, uint32_t kmin, uint32_t 
                             cand[2 * at + 1] = (uint32_t)(4 * i + j);
                         }
                 }
-                sel_sync<NT, BAR>();
+                sel_sync<NT>(bar);
                 TS_TOPK_PROF(3);
                 if (warp == 0) {
                     // rank(c) = #{x : key_x > key_c or (key_x == key_c and idx_x < idx_c)}
@@ -323,7 +325,7 @@ TS_DEV int cta_topk(const uint32_t *keys, int n, int k, uint32_t kmin, uint32_t 
                         }
                     }
                 }
-                sel_sync<NT, BAR>();
+                sel_sync<NT>(bar);
                 tgt = (uint32_t)red[52];
                 teq = tgt;
                 need_eq = red[53];
@@ -342,7 +344,7 @@ TS_DEV int cta_topk(const uint32_t *keys, int n, int k, uint32_t kmin, uint32_t 
                         kmax = max(kmax, e[j]);
                     }
             }
-            block_minmax<NT, BAR>(kmin, kmax, red);
+            block_minmax<NT, BAR>(kmin, kmax, red, bar, tb);
         }
     }
     if (dts && tid == 0) dts[6] = globaltimer();
@@ -370,7 +372,7 @@ TS_DEV int cta_topk(const uint32_t *keys, int n, int k, uint32_t kmin, uint32_t 
         }
         const int n_gt = __popcll(gm), n_eq = __popcll(em);
         int tot;
-        const int before = block_scan<NT, BAR>((n_gt << 16) | n_eq, red, &tot);
+        const int before = block_scan<NT, BAR>((n_gt << 16) | n_eq, red, &tot, bar, tb);
         const int eq_before = before & 0xffff, gt_before = before >> 16;
         TS_TOPK_PROF(5);
         int pos = gt_before + min(need_eq, eq_before);
@@ -392,7 +394,7 @@ TS_DEV int cta_topk(const uint32_t *keys, int n, int k, uint32_t kmin, uint32_t 
             n_eq += (v.x == teq) + (v.y == teq) + (v.z == teq) + (v.w == teq);
         }
         int tot;
-        const int before = block_scan<NT, BAR>((n_gt << 16) | n_eq, red, &tot);
+        const int before = block_scan<NT, BAR>((n_gt << 16) | n_eq, red, &tot, bar, tb);
         const int eq_before = before & 0xffff, gt_before = before >> 16;
         TS_TOPK_PROF(5);
         int pos = gt_before + min(need_eq, eq_before);

@@ -1,27 +1,27 @@
 // step_pipe.cuh — the bf16 decode step (Alg. 1; "integrates page scoring,
 // sparse memory access, and masked attention in a single pass") as ONE kernel in
 // which a CTA (or a thread-block cluster of C CTAs) carries NR = 1 or 2 rows (b, kv head g)
-// through the four steps as a software pipeline over one shared TMA ring:
+// at once — one consumer group of 4 warps per row — fed by ONE producer warp through ONE
+// shared TMA ring, in the HBM order
 //
-//   producer warp : meta(A) meta(B) | K/V(A) once A is selected | K/V(B) once B is selected
-//   4 consumer warps: score A, select A, score B, select B, attend A (+ merge), attend B (+ merge)
+//      meta(A)  meta(B)  K/V(A)  K/V(B)
 //
-// so the exact top-K of row A (latency-bound: smem round trips and barriers, HBM idle) runs
-// while row B's metadata streams into the ring, and the top-K of row B while row A's K/V
-// streams.  With every CTA of the grid in the same phase at the same time (one wave), a
-// one-row-per-CTA kernel leaves HBM idle during the select; here the HBM stream of every CTA
-// continues through it.
+// Group A scores A, then selects A while meta(B) streams; group B scores B, then selects B
+// while K/V(A) streams; then each group attends its row.  The exact top-K (latency-bound:
+// shared-memory round trips and barriers, no HBM traffic) of one row therefore always runs
+// under the other row's stream: with every CTA of the grid in the same phase at the same time
+// (one wave), a one-row-per-CTA kernel leaves HBM idle during the select.
 //
 //  1. score (Eq. 2; Alg. 1 Step 1): the CTA's contiguous chunk of the row's
 //     metadata records (logical layout: one run per row) is bulk-copied (cp.async.bulk,
-//     L2 evict-first) in 8 KB stages of 32 pages; consumers compute [m | M] x [q^- ; q^+] on
-//     mma.m16n8k16 (exact bf16 products, fp32 sums) and the max over the GQA group (R9);
+//     L2 evict-first) in 8 KB stages of 32 pages; the group computes [m | M] x [q^- ; q^+]
+//     on mma.m16n8k16 (exact bf16 products, fp32 sums) and the max over the GQA group (R9);
 //  2. select (TopK; Alg. 1 Step 2): C > 1 — the chunk keys (one-level) or
 //     the chunk's own top-K candidates (two-level, rows >> C K) are pushed into every peer's
 //     shared memory (DSMEM stores) and announced by remote mbarrier arrives (release.cluster;
-//     no cluster-wide barrier, so the producer warp and the other row never wait for it);
-//     every CTA then runs the same exact CTA-wide radix top-K (cta_topk, lowest page id
-//     wins ties, R6) and keeps its share of the ascending selection;
+//     no cluster-wide barrier, so neither the producer nor the other group waits for it);
+//     every CTA then runs the same exact radix top-K on the group's 128 threads (cta_topk,
+//     lowest page id wins ties, R6) and keeps its share of the ascending selection;
 //  3. gather: the producer streams the share's [16 x 64] K and V tiles (2 tiles per 8 KB
 //     stage) with 2-D TMA (128-byte swizzle, L2 evict-first), 4 lanes issuing in parallel;
 //  4. attend (SparseAttn): S = Q K^T (mma.m16n8k16), fp32 online softmax
@@ -36,12 +36,11 @@
 
 namespace ts {
 
-constexpr int kPipeW = 4;                    // consumer warps
-constexpr int kPipeCT = kPipeW * 32;         // consumer threads (warps 0 .. 3)
-constexpr int kPipeNT = kPipeCT + 32;        // + the producer warp (warp 4)
-constexpr int kPipeMaxNR = 2;                // rows per CTA
+constexpr int kPipeW = 4;                    // consumer warps per group
+constexpr int kPipeCT = kPipeW * 32;         // consumer threads per group
+constexpr int kPipeMaxNR = 2;                // rows (groups) per CTA
+constexpr int kPipeNT = kPipeMaxNR * kPipeCT + 32;  // + the producer warp (warp 8)
 constexpr int kPipeStage = 8192;             // ring stage: 32 metadata records or 2 K/V tiles
-constexpr int kPipeBar = 1;                  // named barrier of the consumer warps
 
 struct PipeParams {
     const uint16_t *q;        // [B][Hq][64]
@@ -68,11 +67,14 @@ struct PipeParams {
     int share;                // sel entries per row kept by a CTA (>= its pages of the selection)
     int pt_smem;              // page-table rows prefetched into shared memory
     int flags;                // bit 4: PDL trigger after the attention loop
+    unsigned long long *dbg;  // development: per-CTA globaltimer stamps [grid][16] (nullable)
 };
 
 // Byte offsets of the shared-memory regions (from the 1024-aligned base); host and device.
+// Everything but the ring and the barriers is per group (row slot) r: base + r * gstride.
 struct PipeLayout {
-    int ring, q, hist, red, wpart, bars, kmm, sel, sc, pt, cand, total;
+    int ring, bars, grp, gstride, total;
+    int q, hist, red, wpart, kmm, sel, sc, pt, cand;  // offsets inside a group's block
     int scap, ptcap, candcap;  // per row: score entries, page-table entries, candidate words
     __host__ __device__ static int up(int x, int a) { return (x + a - 1) / a * a; }
     __host__ __device__ static PipeLayout make(int R, int NR, int C, int max_pages, int kmax, int chunk,
@@ -83,17 +85,19 @@ struct PipeLayout {
         l.ptcap = pt_smem ? mp4 : 0;
         l.candcap = two ? 2 * C * kmax : 0;
         l.ring = 0;
-        l.q = R * kPipeStage;                              // [NR][8][64] bf16
-        l.hist = l.q + NR * 8 * kRowBytes;                 // [2048] int
-        l.red = l.hist + kSsHist * 4;                      // [64] int
-        l.wpart = l.red + 64 * 4;                          // [W][8][kSaPart] fp32 (select scratch before)
-        l.bars = up(l.wpart + kPipeW * 8 * kSaPart * 4, 8);  // full[R] empty[R] q pt[NR] sel[NR] keys[NR]
-        l.kmm = l.bars + (2 * R + 1 + 3 * NR) * 8;         // [NR][2] key range
-        l.sel = up(l.kmm + NR * 8, 16);                    // [NR][share] int2 (block row, first token)
-        l.sc = up(l.sel + NR * share * 8, 16);             // [NR][scap] fp32 scores -> keys
-        l.pt = l.sc + NR * l.scap * 4;                     // [NR][ptcap] int
-        l.cand = l.pt + NR * l.ptcap * 4;                  // [NR][C][kmax] keys, then [NR][C][kmax] ids
-        l.total = l.cand + NR * l.candcap * 4;
+        l.bars = R * kPipeStage;                   // full[R] empty[R] q pt[NR] sel[NR] keys[NR]
+        l.grp = up(l.bars + (2 * R + 1 + 3 * NR) * 8, 128);
+        l.q = 0;                                   // [8][64] bf16
+        l.hist = l.q + 8 * kRowBytes;              // [2048] int
+        l.red = l.hist + kSsHist * 4;              // [64] int (+ s_last)
+        l.wpart = l.red + 64 * 4;                  // [W][8][kSaPart] fp32 (select scratch before)
+        l.kmm = l.wpart + kPipeW * 8 * kSaPart * 4;  // key range [2]
+        l.sel = up(l.kmm + 8, 16);                 // [share] int2 (block row, first token)
+        l.sc = up(l.sel + share * 8, 16);          // [scap] fp32 scores -> keys
+        l.pt = l.sc + l.scap * 4;                  // [ptcap] int
+        l.cand = up(l.pt + l.ptcap * 4, 16);       // [C][kmax] keys, then [C][kmax] ids
+        l.gstride = up(l.cand + l.candcap * 4, 128);
+        l.total = l.grp + NR * l.gstride;
         return l;
     }
 };
@@ -118,7 +122,7 @@ TS_DEV void mbar_wait_cluster(uint32_t bar, uint32_t parity) {  // acquire at cl
 }
 
 // What every thread of a CTA knows about row slot r of its cluster (from seq_lens only, so
-// every CTA of the cluster and both warp roles agree on every stage count).
+// every CTA of the cluster and every warp role agree on every stage count).
 struct PipeRow {
     int row, b, g, L, P;
     int nloc, nst;     // this CTA's valid pages of the row, metadata stages
@@ -139,7 +143,7 @@ TS_DEV PipeRow pipe_row(const PipeParams &p, int cluster, int r, int rank) {
     x.P = (x.L + p.S - 1) / p.S;
     const int j0 = rank * p.chunk;
     x.nloc = max(0, min(x.P - j0, p.chunk));
-    x.nst = (x.nloc + kSsStagePages - 1) / kSsStagePages;
+    x.nst = x.valid ? (x.nloc + kSsStagePages - 1) / kSsStagePages : 0;
     x.kk = min(p.kmax, x.P);
     const int tpp = p.S >> 4, tps = __ffs(tpp) - 1;
     const int ntile = x.kk * tpp;
@@ -148,7 +152,7 @@ TS_DEV PipeRow pipe_row(const PipeParams &p, int cluster, int r, int rank) {
     x.u0 = x.t0 >> tps;
     x.w0 = x.kk * rank / p.C;
     x.w1 = x.kk * (rank + 1) / p.C;
-    x.nkv = (x.t1 - x.t0 + 1) >> 1;
+    x.nkv = x.valid ? (x.t1 - x.t0 + 1) >> 1 : 0;
     return x;
 }
 
@@ -166,88 +170,74 @@ __global__ void __launch_bounds__(kPipeNT, 2) decode_pipe_kernel(
     const int R = p.R, NR = p.NR, C = p.C;
     const uint32_t full0 = sb + LY.bars, empty0 = full0 + 8 * R, qbar = empty0 + 8 * R;
     const uint32_t ptbar0 = qbar + 8, selbar0 = ptbar0 + 8 * NR, keybar0 = selbar0 + 8 * NR;
-    int *hist = reinterpret_cast<int *>(smem + LY.hist);
-    int *red = reinterpret_cast<int *>(smem + LY.red);
-    float *wpart = reinterpret_cast<float *>(smem + LY.wpart);
-    unsigned *kmm = reinterpret_cast<unsigned *>(smem + LY.kmm);
-    __shared__ int s_last;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int cluster = blockIdx.x / C, rank = blockIdx.x % C;
     const int j0 = rank * p.chunk;
     const int S = p.S, tpp = S >> 4, tps = __ffs(tpp) - 1;
-    cg::cluster_group cl = cg::this_cluster();
+    unsigned long long *dts = p.dbg ? p.dbg + (size_t)blockIdx.x * 16 : nullptr;
+#define PP_STAMP(e, who) \
+    if (dts && tid == (who)) dts[e] = globaltimer();
 
     if (warp == 0) {  // full[R] empty[R] q pt[NR] sel[NR]: count 1; keys[NR]: the C - 1 peers
         for (int i = lane; i < 2 * R + 1 + 2 * NR; i += 32) mbar_init(full0 + 8 * i, 1);
         if (lane < NR) mbar_init(keybar0 + 8 * lane, C > 1 ? C - 1 : 1);
-        if (lane < NR) {
-            kmm[2 * lane] = 0xffffffffu;
-            kmm[2 * lane + 1] = 0u;
-        }
         fence_mbar_init();
     } else if (warp == 1 && lane < 2) {
         prefetch_tmap(lane ? &tmV : &tmK);
+    } else if (warp >= 2 && warp < 2 + NR) {  // group block of row slot warp - 2
+        uint8_t *gb = smem + LY.grp + (warp - 2) * LY.gstride;
+        for (int i = lane; i < kSsHist / 4; i += 32) reinterpret_cast<int4 *>(gb + LY.hist)[i] = make_int4(0, 0, 0, 0);
+        if (lane == 0) {
+            reinterpret_cast<unsigned *>(gb + LY.kmm)[0] = 0xffffffffu;
+            reinterpret_cast<unsigned *>(gb + LY.kmm)[1] = 0u;
+        }
     }
-    for (int i = tid; i < kSsHist / 4; i += kPipeNT) reinterpret_cast<int4 *>(hist)[i] = make_int4(0, 0, 0, 0);
     __syncthreads();
     // "this CTA is running and initialised" (before any DSMEM access by a peer); only the
-    // consumers wait for the peers, right before their first remote store
+    // consumer groups wait for the peers, right before their first remote store
     if (C > 1) cluster_arrive_release();
     pdl_wait();  // inputs may come from the previous kernel in the stream
+    PP_STAMP(0, 0);
 
-    // stage bases: meta(row 0), meta(row 1), K/V(row 0), K/V(row 1)
-    PipeRow rw[kPipeMaxNR];
-#pragma unroll
-    for (int r = 0; r < kPipeMaxNR; ++r) rw[r] = pipe_row(p, cluster, r, rank);
-    int mbase[kPipeMaxNR], kbase[kPipeMaxNR];
-    {
-        int n = 0;
-#pragma unroll
-        for (int r = 0; r < kPipeMaxNR; ++r) {
-            mbase[r] = n;
-            n += rw[r].valid ? rw[r].nst : 0;
-        }
-#pragma unroll
-        for (int r = 0; r < kPipeMaxNR; ++r) {
-            kbase[r] = n;
-            n += rw[r].valid ? rw[r].nkv : 0;
-        }
-    }
-    auto sel_of = [&](int r) { return reinterpret_cast<int2 *>(smem + LY.sel) + r * p.share; };
-    auto sc_of = [&](int r) { return reinterpret_cast<float *>(smem + LY.sc) + r * LY.scap; };
-    auto pt_of = [&](int r) { return reinterpret_cast<int *>(smem + LY.pt) + r * LY.ptcap; };
-
-    if (warp == W) {
+    if (warp == 2 * W) {
         // ===================================== producer =====================================
+        PipeRow rw[kPipeMaxNR];
+#pragma unroll
+        for (int r = 0; r < kPipeMaxNR; ++r) rw[r] = pipe_row(p, cluster, r, rank);
+        const int nmeta0 = rw[0].nst, nmeta = rw[0].nst + rw[1].nst;
         const uint64_t pol = l2_policy_evict_first();
         if (lane == 31) {  // the rows' q groups (G x 128 B each)
             uint32_t bytes = 0;
-            for (int r = 0; r < NR; ++r) bytes += rw[r].valid ? p.G * kRowBytes : 0;
+#pragma unroll
+            for (int r = 0; r < kPipeMaxNR; ++r) bytes += rw[r].valid ? p.G * kRowBytes : 0;
             mbar_arrive_expect_tx(qbar, bytes);
-            for (int r = 0; r < NR; ++r)
+#pragma unroll
+            for (int r = 0; r < kPipeMaxNR; ++r)
                 if (rw[r].valid)
-                    bulk_load(sb + LY.q + r * 8 * kRowBytes,
+                    bulk_load(sb + LY.grp + r * LY.gstride + LY.q,
                               p.q + ((size_t)rw[r].b * p.Hq + rw[r].g * p.G) * kAttnD, p.G * kRowBytes, qbar);
         }
-        if (lane >= 28 && lane - 28 < NR) {  // page-table row -> smem (page -> block map)
-            const int r = lane - 28;
-            const PipeRow &x = rw[r];
-            if (p.pt_smem && x.valid && x.P > 0) {
-                const uint32_t ptb = min(((uint32_t)x.P * 4 + 15) & ~15u, (uint32_t)LY.ptcap * 4);
-                mbar_arrive_expect_tx(ptbar0 + 8 * r, ptb);
-                bulk_load(smem_u32(pt_of(r)), p.page_table + (size_t)x.b * p.max_pages, ptb, ptbar0 + 8 * r);
-            } else {
-                mbar_arrive(ptbar0 + 8 * r);
+#pragma unroll
+        for (int r = 0; r < kPipeMaxNR; ++r)  // page-table rows -> smem (page -> block map)
+            if (lane == 29 + r && r < NR) {
+                const PipeRow &x = rw[r];
+                if (p.pt_smem && x.valid && x.P > 0) {
+                    const uint32_t ptb = min(((uint32_t)x.P * 4 + 15) & ~15u, (uint32_t)LY.ptcap * 4);
+                    mbar_arrive_expect_tx(ptbar0 + 8 * r, ptb);
+                    bulk_load(sb + LY.grp + r * LY.gstride + LY.pt, p.page_table + (size_t)x.b * p.max_pages, ptb,
+                              ptbar0 + 8 * r);
+                } else {
+                    mbar_arrive(ptbar0 + 8 * r);
+                }
             }
-        }
-        const int nmeta = kbase[0];
         auto issue_meta = [&](int n) {
-            const int r = (NR > 1 && n >= mbase[1]) ? 1 : 0;
-            const int i = n - mbase[r], st = n % R;
-            const int np = min(kSsStagePages, rw[r].nloc - i * kSsStagePages);
+            const int r = n >= nmeta0 ? 1 : 0;
+            const int i = n - (r ? nmeta0 : 0), st = n % R;
+            const int np = min(kSsStagePages, (r ? rw[1].nloc : rw[0].nloc) - i * kSsStagePages);
             const uint32_t bytes = np * 2 * kRowBytes;
-            const uint16_t *src = p.meta + ((size_t)rw[r].row * p.max_pages + j0 + i * kSsStagePages) * 2 * kAttnD;
+            const uint16_t *src =
+                p.meta + ((size_t)(r ? rw[1].row : rw[0].row) * p.max_pages + j0 + i * kSsStagePages) * 2 * kAttnD;
             mbar_arrive_expect_tx(full0 + 8 * st, bytes);
             bulk_load_hint(sb + st * kPipeStage, src, bytes, full0 + 8 * st, pol);
         };
@@ -260,10 +250,14 @@ __global__ void __launch_bounds__(kPipeNT, 2) decode_pipe_kernel(
                 issue_meta(n);
             }
         __syncwarp();
-        for (int r = 0; r < NR; ++r) {
+        PP_STAMP(8, 2 * W * 32);
+        int kbase = nmeta;
+#pragma unroll
+        for (int r = 0; r < kPipeMaxNR; ++r) {
             const PipeRow &x = rw[r];
-            if (!x.valid || x.nkv == 0) continue;
+            if (x.nkv == 0) continue;
             mbar_wait(selbar0 + 8 * r, 0);  // the row's selection (this CTA's share) is in sel[r]
+            PP_STAMP(9 + 2 * r, 2 * W * 32);
             // the ring was last read by the generic proxy; APP: the appended K/V row (generic
             // stores of some CTA of the cluster, published through the key exchange) is read
             // by TMA below
@@ -271,9 +265,9 @@ __global__ void __launch_bounds__(kPipeNT, 2) decode_pipe_kernel(
                 fence_proxy_async_all();
             else
                 fence_proxy_async();
-            const int2 *sel = sel_of(r);
+            const int2 *sel = reinterpret_cast<const int2 *>(smem + LY.grp + r * LY.gstride + LY.sel);
             for (int i = 0; i < x.nkv; ++i) {
-                const int n = kbase[r] + i, st = n % R;
+                const int n = kbase + i, st = n % R;
                 const int nt = min(2, x.t1 - x.t0 - 2 * i);
                 if (lane == 0) {
                     if (n >= R) mbar_wait(empty0 + 8 * st, ((n / R) & 1) ^ 1);
@@ -288,45 +282,60 @@ __global__ void __launch_bounds__(kPipeNT, 2) decode_pipe_kernel(
                                 kv ? &tmV : &tmK, 0, pg.x + 16 * (tl & (tpp - 1)), full0 + 8 * st, pol);
                 }
             }
+            kbase += x.nkv;
+            PP_STAMP(10 + 2 * r, 2 * W * 32);
         }
         return;
     }
 
-    // ======================================= consumers ======================================
+    // ================================ consumer group r (row slot r) ==========================
+    const int r = warp / W, gw = warp % W, ct = tid - r * CT;
+    const int bar = 1 + r;  // the group's named barrier
+    const PipeRow x = pipe_row(p, cluster, r, rank);
+    if (!x.valid) return;  // uniform across the cluster (row index only)
+    const PipeRow xo = pipe_row(p, cluster, r ^ 1, rank);  // the other slot: stage bases only
+    const int mbase = r ? xo.nst : 0;
+    const int kbase = (r ? xo.nst + xo.nkv : 0) + x.nst + (r ? 0 : xo.nst);
+    uint8_t *gb = smem + LY.grp + r * LY.gstride;
+    const uint32_t gsb = sb + LY.grp + r * LY.gstride;
+    int *hist = reinterpret_cast<int *>(gb + LY.hist);
+    int *red = reinterpret_cast<int *>(gb + LY.red);
+    float *wpart = reinterpret_cast<float *>(gb + LY.wpart);
+    unsigned *kmm = reinterpret_cast<unsigned *>(gb + LY.kmm);
+    int2 *sel = reinterpret_cast<int2 *>(gb + LY.sel);
+    float *sc = reinterpret_cast<float *>(gb + LY.sc);
     const int gid = lane >> 2, t = lane & 3;
     mbar_wait(qbar, 0);
+
+    int ja = 0, aslot = 0, apl = -1;  // APP: the appended page (chunk-local apl when owned)
     if constexpr (APP) {
         // fused append (ts_decode_step_append; Eq. 1): the CTA whose chunk holds
-        // the newest token's page writes its K / V row (16 B per lane of warp 0); the consumer
-        // barrier + release of the key exchange publish it to every CTA's attention TMA
-        if (warp == 0 && lane < 16)
-            for (int r = 0; r < NR; ++r) {
-                const PipeRow &x = rw[r];
-                if (!x.valid || x.L == 0) continue;
-                const int ja = (x.L - 1) / S, aslot = (x.L - 1) - ja * S;
-                if (ja < j0 || ja >= j0 + x.nloc) continue;
-                const int c = lane & 7;
-                const int blk = p.page_table[(size_t)x.b * p.max_pages + ja];
-                const size_t src = ((size_t)x.b * p.Hkv + x.g) * kAttnD + c * 8;
-                const size_t dst = (((size_t)blk * p.Hkv + x.g) * S + aslot) * kAttnD + c * 8;
-                uint16_t *pool = lane < 8 ? p.k_pool : p.v_pool;
-                const uint16_t *nw = lane < 8 ? p.k_new : p.v_new;
-                *reinterpret_cast<uint4 *>(pool + dst) = *reinterpret_cast<const uint4 *>(nw + src);
-            }
-        fence_proxy_async_all();  // before any TMA read of that page
+        // the newest token's page writes its K / V row (16 B per lane of the group's warp 0);
+        // the group barrier + release of the key exchange publish it to every CTA's TMA
+        if (x.L > 0) {
+            ja = (x.L - 1) / S;
+            aslot = (x.L - 1) - ja * S;
+            if (ja >= j0 && ja < j0 + x.nloc) apl = ja - j0;
+        }
+        if (apl >= 0 && gw == 0 && lane < 16) {
+            const int c = lane & 7;
+            const int blk = p.page_table[(size_t)x.b * p.max_pages + ja];
+            const size_t src = ((size_t)x.b * p.Hkv + x.g) * kAttnD + c * 8;
+            const size_t dst = (((size_t)blk * p.Hkv + x.g) * S + aslot) * kAttnD + c * 8;
+            uint16_t *pool = lane < 8 ? p.k_pool : p.v_pool;
+            const uint16_t *nw = lane < 8 ? p.k_new : p.v_new;
+            *reinterpret_cast<uint4 *>(pool + dst) = *reinterpret_cast<const uint4 *>(nw + src);
+            fence_proxy_async_all();  // before any TMA read of that page
+        }
     }
 
-    bool cluster_ready = false;  // the start cluster barrier was waited for
-    for (int r = 0; r < NR; ++r) {
-        const PipeRow &x = rw[r];
-        if (!x.valid) continue;  // uniform across the cluster (row index only)
-        float *sc = sc_of(r);
-        const int sb0 = p.two ? 0 : j0;  // index of this CTA's first page in sc[]
-        // ------------------------------------------------------------- 1. score
+    // ------------------------------------------------------------------ 1. score
+    const int sb0 = p.two ? 0 : j0;  // index of this CTA's first page in sc[]
+    {
         uint32_t qa[8], qp[8];
         {
             const bool live = gid < p.G;
-            const uint32_t qrow = sb + LY.q + (r * 8 + gid) * kRowBytes;
+            const uint32_t qrow = gsb + LY.q + gid * kRowBytes;
             const uint4 x0 = live ? lds_v4(qrow + 16 * t) : make_uint4(0, 0, 0, 0);
             const uint4 x1 = live ? lds_v4(qrow + 16 * (t + 4)) : make_uint4(0, 0, 0, 0);
             const uint32_t u0w[4] = {x0.x, x0.y, x0.z, x0.w}, u1w[4] = {x1.x, x1.y, x1.z, x1.w};
@@ -340,19 +349,11 @@ __global__ void __launch_bounds__(kPipeNT, 2) decode_pipe_kernel(
         }
         const bool c0 = 2 * t < p.G, c1 = 2 * t + 1 < p.G;
         uint32_t kmn = 0xffffffffu, kmx = 0u;
-        int apl = -1, aslot = 0, ja = 0;  // APP: the appended page, chunk-local
         uint4 kn = make_uint4(0, 0, 0, 0);
-        if constexpr (APP) {
-            if (x.L > 0) {
-                ja = (x.L - 1) / S;
-                aslot = (x.L - 1) - ja * S;
-                if (ja >= j0 && ja < j0 + x.nloc) apl = ja - j0;
-            }
-            if (apl >= 0 && lane < 16 && (apl / kSsStagePages) % W == warp)
-                kn = *reinterpret_cast<const uint4 *>(p.k_new + ((size_t)x.b * p.Hkv + x.g) * kAttnD + (lane & 7) * 8);
-        }
-        for (int i = warp; i < x.nst; i += W) {
-            const int n = mbase[r] + i, st = n % R;
+        if (APP && apl >= 0 && lane < 16 && (apl / kSsStagePages) % W == gw)
+            kn = *reinterpret_cast<const uint4 *>(p.k_new + ((size_t)x.b * p.Hkv + x.g) * kAttnD + (lane & 7) * 8);
+        for (int i = gw; i < x.nst; i += W) {
+            const int n = mbase + i, st = n % R;
             mbar_wait(full0 + 8 * st, (n / R) & 1);
             const uint32_t kb = sb + st * kPipeStage;
             if (APP && apl >= i * kSsStagePages && apl < (i + 1) * kSsStagePages) {  // warp-uniform
@@ -415,16 +416,20 @@ __global__ void __launch_bounds__(kPipeNT, 2) decode_pipe_kernel(
         kmn = __reduce_min_sync(0xffffffffu, kmn);
         kmx = __reduce_max_sync(0xffffffffu, kmx);
         if (lane == 0 && kmn <= kmx) {
-            atomicMin(&kmm[2 * r], kmn);
-            atomicMax(&kmm[2 * r + 1], kmx);
+            atomicMin(&kmm[0], kmn);
+            atomicMax(&kmm[1], kmx);
         }
-        for (int pg = x.nst * kSsStagePages + tid; pg < p.chunk; pg += CT)  // chunk pages past P_b
-            if (j0 + pg < p.max_pages) sc[sb0 + pg] = kNegInf;
-        named_bar_sync(kPipeBar, CT);
+    }
+    for (int pg = x.nst * kSsStagePages + ct; pg < p.chunk; pg += CT)  // chunk pages past P_b
+        if (j0 + pg < p.max_pages) sc[sb0 + pg] = kNegInf;
+    named_bar_sync(bar, CT);
+    PP_STAMP(1 + 2 * r, r * CT);
 
-        // ------------------------------------------------------------- 2. select
-        const int *ptrow = p.pt_smem ? pt_of(r) : p.page_table + (size_t)x.b * p.max_pages;
-        int2 *sel = sel_of(r);
+    // ------------------------------------------------------------------ 2. select
+    {
+        cg::cluster_group cl = cg::this_cluster();
+        const int *ptrow = p.pt_smem ? reinterpret_cast<const int *>(gb + LY.pt)
+                                     : p.page_table + (size_t)x.b * p.max_pages;
         int *out_id = p.sel_ids + (size_t)x.row * p.kmax;
         uint32_t *cand = reinterpret_cast<uint32_t *>(wpart);  // select scratch (attention later)
         auto emit_pg = [&](int pos, int pg) {
@@ -432,25 +437,24 @@ __global__ void __launch_bounds__(kPipeNT, 2) decode_pipe_kernel(
             if (u >= 0 && u < p.share) sel[u] = make_int2((ptrow[pg] * p.Hkv + x.g) * S, pg * S);
             if (pos >= x.w0 && pos < x.w1) out_id[pos] = pg;
         };
-        auto exchange = [&](const uint32_t *src, uint32_t *dst_local, int n4, bool key_range) {
-            // push n4 x 16 B from src into every peer's dst_local (same offset), then announce
-            if (!cluster_ready) {
-                cluster_wait();  // every CTA of the cluster has initialised its barriers
-                cluster_ready = true;
-            }
-            for (int e = tid; e < (C - 1) * n4; e += CT) {
-                const int rr = rank + 1 + e / n4, u = e % n4;
+        // push n4 x 16 B at each of the `nsrc` local arrays into every peer's copy (same
+        // offsets), then announce it with one remote arrive per peer and wait for the peers'
+        auto exchange = [&](uint32_t *const *src, int nsrc, int n4, bool key_range) {
+            cluster_wait();  // every CTA of the cluster has initialised its barriers
+            for (int e = ct; e < nsrc * (C - 1) * n4; e += CT) {
+                const int which = e / ((C - 1) * n4), f = e % ((C - 1) * n4);
+                const int rr = rank + 1 + f / n4, u = f % n4;
                 const int peer = rr < C ? rr : rr - C;
-                reinterpret_cast<uint4 *>(cl.map_shared_rank(dst_local, peer))[u] =
-                    reinterpret_cast<const uint4 *>(src)[u];
+                reinterpret_cast<uint4 *>(cl.map_shared_rank(src[which], peer))[u] =
+                    reinterpret_cast<const uint4 *>(src[which])[u];
             }
-            if (key_range && tid >= 1 && tid < C && kmm[2 * r] <= kmm[2 * r + 1]) {
-                const int rr = rank + tid, peer = rr < C ? rr : rr - C;
-                atomicMin(cl.map_shared_rank(&kmm[2 * r], peer), kmm[2 * r]);
-                atomicMax(cl.map_shared_rank(&kmm[2 * r + 1], peer), kmm[2 * r + 1]);
+            if (key_range && ct >= 1 && ct < C && kmm[0] <= kmm[1]) {
+                const int rr = rank + ct, peer = rr < C ? rr : rr - C;
+                atomicMin(cl.map_shared_rank(&kmm[0], peer), kmm[0]);
+                atomicMax(cl.map_shared_rank(&kmm[1], peer), kmm[1]);
             }
-            named_bar_sync(kPipeBar, CT);
-            if (tid == 0) {
+            named_bar_sync(bar, CT);
+            if (ct == 0) {
                 fence_acq_rel_cluster();
                 for (int q = 1; q < C; ++q) mbar_arrive_remote(keybar0 + 8 * r, (rank + q) % C);
             }
@@ -460,89 +464,65 @@ __global__ void __launch_bounds__(kPipeNT, 2) decode_pipe_kernel(
             // two-level: this chunk's top-K (exact: a page of the row's top-K is beaten by
             // fewer than K pages of its own chunk, same order), pushed to every peer
             uint32_t *lkeys = reinterpret_cast<uint32_t *>(sc);
-            for (int i = tid; i < ((x.nloc + 3) & ~3); i += CT) lkeys[i] = i < x.nloc ? score_key(sc[i]) : 0u;
-            uint32_t *ckey = reinterpret_cast<uint32_t *>(smem + LY.cand) + r * LY.candcap;
+            for (int i = ct; i < ((x.nloc + 3) & ~3); i += CT) lkeys[i] = i < x.nloc ? score_key(sc[i]) : 0u;
+            uint32_t *ckey = reinterpret_cast<uint32_t *>(gb + LY.cand);
             int *cid = reinterpret_cast<int *>(ckey) + C * p.kmax;
             uint32_t *myk = ckey + rank * p.kmax;
             int *myi = cid + rank * p.kmax;
-            named_bar_sync(kPipeBar, CT);
-            const int kl = cta_topk<CT, kPipeBar, 0>(lkeys, x.nloc, p.kmax, kmm[2 * r], kmm[2 * r + 1], hist, red,
-                                                     cand, [&](int pos, int i) {
-                                                         myk[pos] = lkeys[i];
-                                                         myi[pos] = j0 + i;
-                                                     });
-            for (int i = kl + tid; i < p.kmax; i += CT) myk[i] = 0u;  // absent
-            for (int i = tid; i < kSsHist / 4; i += CT) reinterpret_cast<int4 *>(hist)[i] = make_int4(0, 0, 0, 0);
-            named_bar_sync(kPipeBar, CT);
-            // keys and ids of this chunk (host: kmax % 4 == 0): two pushes, one announcement
-            {
-                if (!cluster_ready) {
-                    cluster_wait();
-                    cluster_ready = true;
-                }
-                const int k4n = p.kmax >> 2;
-                for (int e = tid; e < (C - 1) * 2 * k4n; e += CT) {
-                    const int which = e / ((C - 1) * k4n), f = e % ((C - 1) * k4n);
-                    const int rr = rank + 1 + f / k4n, u = f % k4n;
-                    const int peer = rr < C ? rr : rr - C;
-                    uint32_t *base = which ? reinterpret_cast<uint32_t *>(myi) : myk;
-                    reinterpret_cast<uint4 *>(cl.map_shared_rank(base, peer))[u] = reinterpret_cast<const uint4 *>(base)[u];
-                }
-                named_bar_sync(kPipeBar, CT);
-                if (tid == 0) {
-                    fence_acq_rel_cluster();
-                    for (int q = 1; q < C; ++q) mbar_arrive_remote(keybar0 + 8 * r, (rank + q) % C);
-                }
-                mbar_wait_cluster(keybar0 + 8 * r, 0);
-            }
+            named_bar_sync(bar, CT);
+            const int kl = cta_topk<CT, 1, 0>(lkeys, x.nloc, p.kmax, kmm[0], kmm[1], hist, red, cand,
+                                              [&](int pos, int i) {
+                                                  myk[pos] = lkeys[i];
+                                                  myi[pos] = j0 + i;
+                                              }, nullptr, false, -1, bar, r * CT);
+            for (int i = kl + ct; i < p.kmax; i += CT) myk[i] = 0u;  // absent
+            for (int i = ct; i < kSsHist / 4; i += CT) reinterpret_cast<int4 *>(hist)[i] = make_int4(0, 0, 0, 0);
+            named_bar_sync(bar, CT);
+            uint32_t *const srcs[2] = {myk, reinterpret_cast<uint32_t *>(myi)};
+            exchange(srcs, 2, p.kmax >> 2, false);  // host: kmax % 4 == 0
             const int nc = C * p.kmax;
             int nlive = 0;  // live candidates: sum over chunks of min(K, chunk pages)
             for (int c = 0; c < C; ++c) nlive += min(p.kmax, max(0, min(x.P - c * p.chunk, p.chunk)));
             uint32_t mn = 0xffffffffu, mx = 0u;
-            for (int i = tid; i < nc; i += CT)
+            for (int i = ct; i < nc; i += CT)
                 if (ckey[i]) {
                     mn = min(mn, ckey[i]);
                     mx = max(mx, ckey[i]);
                 }
             mbar_wait(ptbar0 + 8 * r, 0);
-            block_minmax<CT, kPipeBar>(mn, mx, red);
+            block_minmax<CT, 1>(mn, mx, red, bar, r * CT);
             // candidates are chunk-major, ids ascending inside a chunk: entry order == id order
-            cta_topk<CT, kPipeBar, 11>(ckey, nc, p.kmax, mn, mx, hist, red, cand,
-                                       [&](int pos, int i) { emit_pg(pos, cid[i]); }, nullptr, false, nlive);
+            cta_topk<CT, 1, 11>(ckey, nc, p.kmax, mn, mx, hist, red, cand,
+                                [&](int pos, int i) { emit_pg(pos, cid[i]); }, nullptr, false, nlive, bar, r * CT);
         } else {
             uint32_t *keys = reinterpret_cast<uint32_t *>(sc);
             const int e1 = min(j0 + p.chunk, (x.P + 3) & ~3);
-            for (int i = j0 + tid; i < e1; i += CT) keys[i] = i < x.P ? score_key(sc[i]) : 0u;
+            for (int i = j0 + ct; i < e1; i += CT) keys[i] = i < x.P ? score_key(sc[i]) : 0u;
             if (C > 1) {
-                named_bar_sync(kPipeBar, CT);
-                exchange(keys + j0, keys + j0, max(0, e1 - j0) >> 2, true);
+                named_bar_sync(bar, CT);
+                uint32_t *const srcs[1] = {keys + j0};
+                exchange(srcs, 1, max(0, e1 - j0) >> 2, true);
             }
             mbar_wait(ptbar0 + 8 * r, 0);
-            named_bar_sync(kPipeBar, CT);
-            cta_topk<CT, kPipeBar, 0>(keys, x.P, p.kmax, kmm[2 * r], kmm[2 * r + 1], hist, red, cand,
-                                      [&](int pos, int i) { emit_pg(pos, i); });
+            named_bar_sync(bar, CT);
+            cta_topk<CT, 1, 0>(keys, x.P, p.kmax, kmm[0], kmm[1], hist, red, cand,
+                               [&](int pos, int i) { emit_pg(pos, i); }, nullptr, false, -1, bar, r * CT);
         }
         if (rank == 0) {
-            for (int i = x.kk + tid; i < p.kmax; i += CT) out_id[i] = -1;
-            if (tid == 0) p.sel_count[x.row] = x.kk;
+            for (int i = x.kk + ct; i < p.kmax; i += CT) out_id[i] = -1;
+            if (ct == 0) p.sel_count[x.row] = x.kk;
         }
-        for (int i = tid; i < kSsHist / 4; i += CT) reinterpret_cast<int4 *>(hist)[i] = make_int4(0, 0, 0, 0);
-        named_bar_sync(kPipeBar, CT);
-        if (tid == 0) mbar_arrive(selbar0 + 8 * r);  // release: sel[r] complete -> producer
+        named_bar_sync(bar, CT);
+        if (ct == 0) mbar_arrive(selbar0 + 8 * r);  // release: sel complete -> producer
+        PP_STAMP(2 + 2 * r, r * CT);
     }
 
-    // ------------------------------------------------------------- 3-4. attend + merge
-    const float sl2 = p.scale * kLog2e;
-    int last = -1;
-    for (int r = 0; r < NR; ++r)
-        if (rw[r].valid) last = r;
-    for (int r = 0; r < NR; ++r) {
-        const PipeRow &x = rw[r];
-        if (!x.valid) continue;
-        const int2 *sel = sel_of(r);
+    // ------------------------------------------------------------------ 3-4. attend + merge
+    {
+        const float sl2 = p.scale * kLog2e;
         uint32_t qa[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         if (gid < p.G) {
-            const uint32_t qrow = sb + LY.q + (r * 8 + gid) * kRowBytes + 32 * t;
+            const uint32_t qrow = gsb + LY.q + gid * kRowBytes + 32 * t;
             const uint4 x0 = lds_v4(qrow), x1 = lds_v4(qrow + 16);
             qa[0] = x0.x; qa[1] = x0.y; qa[2] = x0.z; qa[3] = x0.w;
             qa[4] = x1.x; qa[5] = x1.y; qa[6] = x1.z; qa[7] = x1.w;
@@ -551,8 +531,8 @@ __global__ void __launch_bounds__(kPipeNT, 2) decode_pipe_kernel(
         float oacc[8][4];
 #pragma unroll
         for (int j = 0; j < 8; ++j) oacc[j][0] = oacc[j][1] = oacc[j][2] = oacc[j][3] = 0.f;
-        for (int i = warp; i < x.nkv; i += W) {
-            const int n = kbase[r] + i, st = n % R;
+        for (int i = gw; i < x.nkv; i += W) {
+            const int n = kbase + i, st = n % R;
             const int nt = min(2, x.t1 - x.t0 - 2 * i);
             int tok0[2];
 #pragma unroll
@@ -633,7 +613,7 @@ __global__ void __launch_bounds__(kPipeNT, 2) decode_pipe_kernel(
         lp += __shfl_xor_sync(0xffffffffu, lp, 1);
         lp += __shfl_xor_sync(0xffffffffu, lp, 2);
         if (gid < p.G) {
-            float *wr = wpart + (warp * 8 + gid) * kSaPart;
+            float *wr = wpart + (gw * 8 + gid) * kSaPart;
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
                 wr[16 * t + j] = oacc[j][0];
@@ -644,94 +624,97 @@ __global__ void __launch_bounds__(kPipeNT, 2) decode_pipe_kernel(
                 wr[kAttnD + 1] = lp;
             }
         }
-        named_bar_sync(kPipeBar, CT);
-        if (r == last && (p.flags & 16)) pdl_launch_dependents();  // only the merge / tail remains
-        // ---- CTA merge of the W warp partials (C == 1: straight to o / lse)
-        for (int xi = tid; xi < p.G * 16; xi += CT) {
-            const int h = xi >> 4, d0 = (xi & 15) * 4;
-            float mw[W];
+    }
+    named_bar_sync(bar, CT);
+    PP_STAMP(5 + r, r * CT);
+    // the next kernel in the stream may launch once the last row slot's loop is done; its
+    // prologue overlaps our merge / tail
+    if ((p.flags & 16) && r == NR - 1) pdl_launch_dependents();
+    // ---- CTA merge of the W warp partials (C == 1: straight to o / lse)
+    for (int xi = ct; xi < p.G * 16; xi += CT) {
+        const int h = xi >> 4, d0 = (xi & 15) * 4;
+        float mw[W];
 #pragma unroll
-            for (int w = 0; w < W; ++w) mw[w] = wpart[(w * 8 + h) * kSaPart + kAttnD];
-            float M = kNegInf;
+        for (int w = 0; w < W; ++w) mw[w] = wpart[(w * 8 + h) * kSaPart + kAttnD];
+        float M = kNegInf;
 #pragma unroll
-            for (int w = 0; w < W; ++w) M = fmaxf(M, mw[w]);
-            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-            float l = 0.f;
-            if (M != kNegInf) {
+        for (int w = 0; w < W; ++w) M = fmaxf(M, mw[w]);
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        float l = 0.f;
+        if (M != kNegInf) {
 #pragma unroll
-                for (int w = 0; w < W; ++w) {
-                    const float *wr = wpart + (w * 8 + h) * kSaPart;
-                    const float f = mw[w] == kNegInf ? 0.f : exp2f(mw[w] - M);
-                    l += wr[kAttnD + 1] * f;
-                    const float4 v = *reinterpret_cast<const float4 *>(wr + d0);
-                    acc.x += v.x * f; acc.y += v.y * f; acc.z += v.z * f; acc.w += v.w * f;
-                }
+            for (int w = 0; w < W; ++w) {
+                const float *wr = wpart + (w * 8 + h) * kSaPart;
+                const float f = mw[w] == kNegInf ? 0.f : exp2f(mw[w] - M);
+                l += wr[kAttnD + 1] * f;
+                const float4 v = *reinterpret_cast<const float4 *>(wr + d0);
+                acc.x += v.x * f; acc.y += v.y * f; acc.z += v.z * f; acc.w += v.w * f;
             }
-            if (C == 1) {
+        }
+        if (C == 1) {
+            const size_t oh = (size_t)x.b * p.Hq + x.g * p.G + h;
+            const float inv = l > 0.f ? 1.f / l : 0.f;
+            *reinterpret_cast<float4 *>(p.o + oh * kAttnD + d0) =
+                make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+            if (p.lse && d0 == 0) p.lse[oh] = l > 0.f ? (M + log2f(l)) * kLn2 : kNegInf;
+        } else {
+            float *pr = p.part + (((size_t)x.row * C + rank) * 8 + h) * kPS;
+            *reinterpret_cast<float4 *>(pr + d0) = acc;
+            if (d0 == 0) {
+                pr[kAttnD] = M;
+                pr[kAttnD + 1] = l;
+            }
+        }
+    }
+    if (C > 1) {  // the last CTA of the row (acq_rel ticket) merges the C partials
+        int *s_last = red + 63;
+        named_bar_sync(bar, CT);
+        if (ct == 0) *s_last = atom_add_acq_rel_gpu(p.tickets + x.row, 1u) == unsigned(C - 1);
+        named_bar_sync(bar, CT);
+        if (*s_last) {
+            constexpr int kMaxC = 16;
+            const float *pb = p.part + (size_t)x.row * C * 8 * kPS;
+            for (int xi = ct; xi < p.G * 16; xi += CT) {
+                const int h = xi >> 4, d0 = (xi & 15) * 4;
+                float mr[kMaxC];
+#pragma unroll
+                for (int c = 0; c < kMaxC; ++c) mr[c] = c < C ? __ldcg(pb + (c * 8 + h) * kPS + kAttnD) : kNegInf;
+                float M = kNegInf;
+#pragma unroll
+                for (int c = 0; c < kMaxC; ++c) M = fmaxf(M, mr[c]);
+                float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+                float l = 0.f;
+                if (M != kNegInf) {
+#pragma unroll
+                    for (int c0i = 0; c0i < kMaxC; c0i += 4) {
+                        if (c0i >= C) break;
+                        float lq[4];
+                        float4 vq[4];
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const float *pr = pb + ((c0i + e) * 8 + h) * kPS;
+                            lq[e] = c0i + e < C ? __ldcg(pr + kAttnD + 1) : 0.f;
+                            vq[e] = c0i + e < C ? __ldcg(reinterpret_cast<const float4 *>(pr + d0))
+                                                : make_float4(0.f, 0.f, 0.f, 0.f);
+                        }
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const float f = mr[c0i + e] == kNegInf ? 0.f : exp2f(mr[c0i + e] - M);
+                            l += lq[e] * f;
+                            acc.x += vq[e].x * f; acc.y += vq[e].y * f; acc.z += vq[e].z * f; acc.w += vq[e].w * f;
+                        }
+                    }
+                }
                 const size_t oh = (size_t)x.b * p.Hq + x.g * p.G + h;
                 const float inv = l > 0.f ? 1.f / l : 0.f;
                 *reinterpret_cast<float4 *>(p.o + oh * kAttnD + d0) =
                     make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
                 if (p.lse && d0 == 0) p.lse[oh] = l > 0.f ? (M + log2f(l)) * kLn2 : kNegInf;
-            } else {
-                float *pr = p.part + (((size_t)x.row * C + rank) * 8 + h) * kPS;
-                *reinterpret_cast<float4 *>(pr + d0) = acc;
-                if (d0 == 0) {
-                    pr[kAttnD] = M;
-                    pr[kAttnD + 1] = l;
-                }
             }
+            if (ct == 0) p.tickets[x.row] = 0u;  // re-armed for the next launch
         }
-        if (C > 1) {  // the last CTA of the row (acq_rel ticket) merges the C partials
-            named_bar_sync(kPipeBar, CT);
-            if (tid == 0) s_last = atom_add_acq_rel_gpu(p.tickets + x.row, 1u) == unsigned(C - 1);
-            named_bar_sync(kPipeBar, CT);
-            if (s_last) {
-                constexpr int kMaxC = 16;
-                const float *pb = p.part + (size_t)x.row * C * 8 * kPS;
-                for (int xi = tid; xi < p.G * 16; xi += CT) {
-                    const int h = xi >> 4, d0 = (xi & 15) * 4;
-                    float mr[kMaxC];
-#pragma unroll
-                    for (int c = 0; c < kMaxC; ++c)
-                        mr[c] = c < C ? __ldcg(pb + (c * 8 + h) * kPS + kAttnD) : kNegInf;
-                    float M = kNegInf;
-#pragma unroll
-                    for (int c = 0; c < kMaxC; ++c) M = fmaxf(M, mr[c]);
-                    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-                    float l = 0.f;
-                    if (M != kNegInf) {
-#pragma unroll
-                        for (int c0i = 0; c0i < kMaxC; c0i += 4) {
-                            if (c0i >= C) break;
-                            float lq[4];
-                            float4 vq[4];
-#pragma unroll
-                            for (int e = 0; e < 4; ++e) {
-                                const float *pr = pb + ((c0i + e) * 8 + h) * kPS;
-                                lq[e] = c0i + e < C ? __ldcg(pr + kAttnD + 1) : 0.f;
-                                vq[e] = c0i + e < C ? __ldcg(reinterpret_cast<const float4 *>(pr + d0))
-                                                    : make_float4(0.f, 0.f, 0.f, 0.f);
-                            }
-#pragma unroll
-                            for (int e = 0; e < 4; ++e) {
-                                const float f = mr[c0i + e] == kNegInf ? 0.f : exp2f(mr[c0i + e] - M);
-                                l += lq[e] * f;
-                                acc.x += vq[e].x * f; acc.y += vq[e].y * f; acc.z += vq[e].z * f; acc.w += vq[e].w * f;
-                            }
-                        }
-                    }
-                    const size_t oh = (size_t)x.b * p.Hq + x.g * p.G + h;
-                    const float inv = l > 0.f ? 1.f / l : 0.f;
-                    *reinterpret_cast<float4 *>(p.o + oh * kAttnD + d0) =
-                        make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
-                    if (p.lse && d0 == 0) p.lse[oh] = l > 0.f ? (M + log2f(l)) * kLn2 : kNegInf;
-                }
-                if (tid == 0) p.tickets[x.row] = 0u;  // re-armed for the next launch
-            }
-        }
-        named_bar_sync(kPipeBar, CT);  // wpart / s_last reused by the next row
     }
+    PP_STAMP(13 + r, r * CT);
 }
 
 }  // namespace ts
