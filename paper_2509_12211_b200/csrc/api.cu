@@ -54,6 +54,11 @@ ts_status check_layout(const ts_layout *L) {
 
 int group_of(const ts_layout *L) { return L->num_q_heads / L->num_kv_heads; }
 
+int env_int(const char *name, int dflt) {  // development A/B knobs (read once per call site)
+    const char *v = getenv(name);
+    return v ? atoi(v) : dflt;
+}
+
 bool bf16_attn_supported(const ts_layout *L) {
     const int S = L->page_size;
     return L->kv_dtype == TS_BF16 && L->head_dim == 64 && group_of(L) <= 8 &&
@@ -562,10 +567,6 @@ struct PipePlan {
     double est_us = 1e30;
 };
 
-int env_int(const char *name, int dflt) {  // development A/B knobs (read once per call site)
-    const char *v = getenv(name);
-    return v ? atoi(v) : dflt;
-}
 
 template <bool APP>
 PipePlan plan_pipe(const ts_layout *L, int kmax) {
@@ -931,7 +932,7 @@ static ts_status decode_step_impl(const ts_layout *L, const void *q, const void 
     const cudaStream_t st = as_stream(stream);
     const int rows = L->batch * L->num_kv_heads;
     static const int two_kernels = getenv("TS_TWO_KERNELS") ? atoi(getenv("TS_TWO_KERNELS")) : 0;
-    static const int pipe = env_int("TS_PIPE", 1);
+    static const int pipe = env_int("TS_PIPE", 0);  // dev: the pipelined kernel (measured slower)
     if (L->kv_dtype == TS_BF16 && group_of(L) <= 8 && L->head_dim == 64 && !two_kernels && pipe &&
         L->page_size % 16 == 0 && rows > 0) {
         // the whole step in one pipelined kernel (step_pipe.cuh)
@@ -990,6 +991,8 @@ static ts_status decode_step_impl(const ts_layout *L, const void *q, const void 
         sp.dbg = g_dbg_ss;
         sp.k_new = static_cast<const uint16_t *>(k_new);  // fused append (nullable)
         sp.v_new = static_cast<const uint16_t *>(v_new);
+        static const int stagger_env = env_int("TS_SC_STAGGER_NS", 0);
+        sp.stagger_ns = stagger_env > 0 ? (unsigned)stagger_env : 0u;
         AttnParams ap = attn_params(L, q, k_pool, v_pool, page_table, seq_lens, ids, cnt, kmax, scale,
                                     o, lse, ws);
         phase_mark(0, st);

@@ -73,7 +73,7 @@ struct PipeParams {
 // Byte offsets of the shared-memory regions (from the 1024-aligned base); host and device.
 // Everything but the ring and the barriers is per group (row slot) r: base + r * gstride.
 struct PipeLayout {
-    int ring, bars, grp, gstride, total;
+    int ring, bars, seq, grp, gstride, total;
     int q, hist, red, wpart, kmm, sel, sc, pt, cand;  // offsets inside a group's block
     int scap, ptcap, candcap;  // per row: score entries, page-table entries, candidate words
     __host__ __device__ static int up(int x, int a) { return (x + a - 1) / a * a; }
@@ -86,7 +86,8 @@ struct PipeLayout {
         l.candcap = two ? 2 * C * kmax : 0;
         l.ring = 0;
         l.bars = R * kPipeStage;                   // full[R] empty[R] q pt[NR] sel[NR] keys[NR]
-        l.grp = up(l.bars + (2 * R + 1 + 3 * NR) * 8, 128);
+        l.seq = l.bars + (2 * R + 1 + 3 * NR) * 8;  // [R] int: the stage each slot holds
+        l.grp = up(l.seq + R * 4, 128);
         l.q = 0;                                   // [8][64] bf16
         l.hist = l.q + 8 * kRowBytes;              // [2048] int
         l.red = l.hist + kSsHist * 4;              // [64] int (+ s_last)
@@ -179,7 +180,15 @@ __global__ void __launch_bounds__(kPipeNT, 2) decode_pipe_kernel(
 #define PP_STAMP(e, who) \
     if (dts && tid == (who)) dts[e] = globaltimer();
 
+    // slot_seq[s]: the global stage number the producer last issued into slot s.  Consumers
+    // of the two groups skip each other's stages, so a warp may reach stage n of slot s while
+    // the slot's previous stage n - R has not even landed; the full barrier's parity alone
+    // would then alias (phase k - 1 in progress reads as "phase k complete").  Seeing
+    // slot_seq[s] == n first pins the barrier to stage n's phase (the slot cannot be refilled
+    // before its owner consumes stage n).
+    volatile int *slot_seq = reinterpret_cast<volatile int *>(smem + LY.seq);
     if (warp == 0) {  // full[R] empty[R] q pt[NR] sel[NR]: count 1; keys[NR]: the C - 1 peers
+        for (int i = lane; i < R; i += 32) slot_seq[i] = -1;
         for (int i = lane; i < 2 * R + 1 + 2 * NR; i += 32) mbar_init(full0 + 8 * i, 1);
         if (lane < NR) mbar_init(keybar0 + 8 * lane, C > 1 ? C - 1 : 1);
         fence_mbar_init();
@@ -238,7 +247,8 @@ __global__ void __launch_bounds__(kPipeNT, 2) decode_pipe_kernel(
             const uint32_t bytes = np * 2 * kRowBytes;
             const uint16_t *src =
                 p.meta + ((size_t)(r ? rw[1].row : rw[0].row) * p.max_pages + j0 + i * kSsStagePages) * 2 * kAttnD;
-            mbar_arrive_expect_tx(full0 + 8 * st, bytes);
+            slot_seq[st] = n;
+            mbar_arrive_expect_tx(full0 + 8 * st, bytes);  // (release: orders the slot_seq store)
             bulk_load_hint(sb + st * kPipeStage, src, bytes, full0 + 8 * st, pol);
         };
         // the ring starts empty: its first stages are issued lane-parallel (TMA issue ~100
@@ -271,6 +281,7 @@ __global__ void __launch_bounds__(kPipeNT, 2) decode_pipe_kernel(
                 const int nt = min(2, x.t1 - x.t0 - 2 * i);
                 if (lane == 0) {
                     if (n >= R) mbar_wait(empty0 + 8 * st, ((n / R) & 1) ^ 1);
+                    slot_seq[st] = n;
                     mbar_arrive_expect_tx(full0 + 8 * st, nt * 2 * 16 * kRowBytes);
                 }
                 __syncwarp();
@@ -305,6 +316,11 @@ __global__ void __launch_bounds__(kPipeNT, 2) decode_pipe_kernel(
     int2 *sel = reinterpret_cast<int2 *>(gb + LY.sel);
     float *sc = reinterpret_cast<float *>(gb + LY.sc);
     const int gid = lane >> 2, t = lane & 3;
+    auto wait_stage = [&](int n) {  // stage n is in its slot (see slot_seq above) and has landed
+        const int st = n % R;
+        while (slot_seq[st] != n) nanosleep_ns(20);
+        mbar_wait(full0 + 8 * st, (n / R) & 1);
+    };
     mbar_wait(qbar, 0);
 
     int ja = 0, aslot = 0, apl = -1;  // APP: the appended page (chunk-local apl when owned)
@@ -354,7 +370,7 @@ __global__ void __launch_bounds__(kPipeNT, 2) decode_pipe_kernel(
             kn = *reinterpret_cast<const uint4 *>(p.k_new + ((size_t)x.b * p.Hkv + x.g) * kAttnD + (lane & 7) * 8);
         for (int i = gw; i < x.nst; i += W) {
             const int n = mbase + i, st = n % R;
-            mbar_wait(full0 + 8 * st, (n / R) & 1);
+            wait_stage(n);
             const uint32_t kb = sb + st * kPipeStage;
             if (APP && apl >= i * kSsStagePages && apl < (i + 1) * kSsStagePages) {  // warp-uniform
                 if (lane < 16) {  // lanes 0-7: the m row, 8-15: the M row (16 B each)
@@ -540,7 +556,7 @@ __global__ void __launch_bounds__(kPipeNT, 2) decode_pipe_kernel(
                 const int tl = x.t0 + 2 * i + min(e, nt - 1);
                 tok0[e] = sel[(tl >> tps) - x.u0].y + 16 * (tl & (tpp - 1));
             }
-            mbar_wait(full0 + 8 * st, (n / R) & 1);
+            wait_stage(n);
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
                 if (e >= nt) break;
