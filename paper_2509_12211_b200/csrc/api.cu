@@ -12,7 +12,6 @@
 #include "attn.cuh"
 #include "common.cuh"
 #include "step_cluster.cuh"
-#include "step_pipe.cuh"
 #include "meta.cuh"
 #include "score.cuh"
 #include "score_select.cuh"
@@ -554,107 +553,6 @@ ts_status launch_step_cluster_t(const ts_layout *L, ScoreSelParams &sp, const At
 }
 
 
-// ---------------------------------------------------------------- pipelined step (step_pipe.cuh)
-// Plan: NR rows per cluster, C CTAs per cluster (chunks of each row), R ring stages.  The
-// model behind the choice: the step moves `total` bytes; a CTA moves its
-// share `cta` and, latency-bound, streams at most ring / ~1.5 us; HBM caps the whole grid at
-// ~6.5 TB/s.  Estimated time = max(total / HBM, cta / (ring / lat)) + per-row exchange and
-// merge latencies (C > 1) + the exposed select of the single-row (NR = 1) schedule.
-struct PipePlan {
-    bool ok = false;
-    int NR = 0, C = 0, chunk = 0, R = 0, two = 0, share = 0, pt_smem = 0;
-    size_t sm = 0;
-    double est_us = 1e30;
-};
-
-
-template <bool APP>
-PipePlan plan_pipe(const ts_layout *L, int kmax) {
-    // NR = 2 rows per cluster (two consumer groups per CTA); C = the widest split of a row
-    // that keeps the grid within one wave at 2 CTAs per SM (every CTA of a cluster does
-    // the same work, so the CTAs finish together) and >= 64 pages per CTA; the ring takes
-    // the shared memory left at ceil(CTAs / SMs) CTAs per SM
-    auto kern = decode_pipe_kernel<APP>;
-    PipePlan best;
-    const int rows = L->batch * L->num_kv_heads;
-    const int sms = device_sms();
-    const int tpp = L->page_size / 16;
-    static const int nr_env = env_int("TS_PIPE_NR", 0), c_env = env_int("TS_PIPE_C", 0),
-                     r_env = env_int("TS_PIPE_R", 0);
-    const int NR = nr_env ? nr_env : 2;
-    const int ncl = (rows + NR - 1) / NR;
-    int C = 1, chunk = L->max_pages;
-    for (int Cd = 1; Cd <= kMaxClusterC; ++Cd) {
-        int ch = (L->max_pages + Cd - 1) / Cd;
-        ch = (ch + kSsStagePages - 1) / kSsStagePages * kSsStagePages;
-        const int c = (L->max_pages + ch - 1) / ch;
-        if (c_env ? c != c_env : (c > 1 && (ch < 64 || (long long)ncl * c > 2 * sms))) continue;
-        C = c;
-        chunk = ch;
-        if (c_env) break;
-    }
-    chunk = (chunk + kSsStagePages - 1) / kSsStagePages * kSsStagePages;
-    const int two = (C > 1 && kmax % 4 == 0 && L->max_pages > 2048 && L->max_pages >= 4 * C * kmax) ? 1 : 0;
-    const int share = ((kmax * tpp + C - 1) / C + tpp - 1) / tpp + 1;
-    const int pt_smem = ((L->max_pages & 3) == 0 && L->max_pages <= 2048) ? 1 : 0;
-    const long long T = (long long)ncl * C;
-    const int m = (int)std::min<long long>(2, std::max<long long>(1, (T + sms - 1) / sms));
-    const PipeLayout l0 = PipeLayout::make(0, NR, C, L->max_pages, kmax, chunk, two, share, pt_smem);
-    const long long budget = std::min<long long>(227 * 1024, 228 * 1024 / m - 1024) - 1024;
-    int R = (int)std::min<long long>(24, (budget - l0.total) / kPipeStage);
-    if (r_env) R = std::min(R, r_env);
-    if (R < 4) return best;
-    const PipeLayout l = PipeLayout::make(R, NR, C, L->max_pages, kmax, chunk, two, share, pt_smem);
-    const size_t sm = 1024 + (size_t)l.total;
-    if (!ensure_func_attrs((const void *)kern, sm, true)) return best;
-    if (max_active_clusters(kern, kPipeNT, sm, C) < 1) return best;
-    best.ok = true;
-    best.NR = NR; best.C = C; best.chunk = chunk; best.R = R; best.two = two;
-    best.share = share; best.pt_smem = pt_smem; best.sm = sm; best.est_us = 0;
-    return best;
-}
-
-template <bool APP>
-ts_status launch_pipe(const ts_layout *L, PipeParams &pp, cudaStream_t st) {
-    auto kern = decode_pipe_kernel<APP>;
-    const PipePlan pl = plan_pipe<APP>(L, pp.kmax);
-    if (!pl.ok) return TS_ERR_UNSUPPORTED;
-    CUtensorMap tmK, tmV;
-    if (!make_pool_map(&tmK, pp.k_pool, L, 16) || !make_pool_map(&tmV, pp.v_pool, L, 16))
-        return TS_ERR_CUDA;
-    pp.NR = pl.NR;
-    pp.C = pl.C;
-    pp.chunk = pl.chunk;
-    pp.R = pl.R;
-    pp.two = pl.two;
-    pp.share = pl.share;
-    pp.pt_smem = pl.pt_smem;
-    static const int trig = env_int("TS_PIPE_TRIGGER", 1);
-    pp.flags = trig ? 16 : 0;
-    static const int verbose = env_int("TS_PIPE_VERBOSE", 0);
-    if (verbose)
-        fprintf(stderr, "[tinyserve] pipe plan: NR %d C %d chunk %d R %d two %d share %d pt_smem %d smem %zu est %.1f us\n",
-                pl.NR, pl.C, pl.chunk, pl.R, pl.two, pl.share, pl.pt_smem, pl.sm, pl.est_us);
-    const int ncl = (pp.rows + pl.NR - 1) / pl.NR;
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(ncl * pl.C);
-    cfg.blockDim = dim3(kPipeNT);
-    cfg.dynamicSmemBytes = pl.sm;
-    cfg.stream = st;
-    cudaLaunchAttribute at[2];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = pl.C;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[1].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 2;
-    if (cudaLaunchKernelEx(&cfg, kern, tmK, tmV, pp) != cudaSuccess) return TS_ERR_CUDA;
-    ++g_launches;
-    return launch_status();
-}
-
 ts_status launch_score_select(const ts_layout *L, const void *q, const void *meta, const int *pt,
                               const int *sl, int *ids, int *blk, int *cnt, int kmax,
                               cudaStream_t st) {
@@ -932,44 +830,6 @@ static ts_status decode_step_impl(const ts_layout *L, const void *q, const void 
     const cudaStream_t st = as_stream(stream);
     const int rows = L->batch * L->num_kv_heads;
     static const int two_kernels = getenv("TS_TWO_KERNELS") ? atoi(getenv("TS_TWO_KERNELS")) : 0;
-    static const int pipe = env_int("TS_PIPE", 0);  // dev: the pipelined kernel (measured slower)
-    if (L->kv_dtype == TS_BF16 && group_of(L) <= 8 && L->head_dim == 64 && !two_kernels && pipe &&
-        L->page_size % 16 == 0 && rows > 0) {
-        // the whole step in one pipelined kernel (step_pipe.cuh)
-        const AttnWs aw = attn_ws_layout(L, kmax, kMaxClusterC);
-        PipeParams pp{};
-        pp.q = static_cast<const uint16_t *>(q);
-        pp.meta = static_cast<const uint16_t *>(meta);
-        pp.page_table = page_table;
-        pp.seq_lens = seq_lens;
-        pp.sel_ids = ids;
-        pp.sel_count = cnt;
-        pp.k_new = static_cast<const uint16_t *>(k_new);
-        pp.v_new = static_cast<const uint16_t *>(v_new);
-        pp.k_pool = static_cast<uint16_t *>(const_cast<void *>(k_pool));
-        pp.v_pool = static_cast<uint16_t *>(const_cast<void *>(v_pool));
-        pp.o = o;
-        pp.lse = lse;
-        pp.part = reinterpret_cast<float *>(wb + aw.part);
-        pp.tickets = reinterpret_cast<unsigned *>(wb + aw.tickets);
-        pp.scale = scale;
-        pp.B = L->batch;
-        pp.Hq = L->num_q_heads;
-        pp.Hkv = L->num_kv_heads;
-        pp.G = group_of(L);
-        pp.S = L->page_size;
-        pp.max_pages = L->max_pages;
-        pp.kmax = kmax;
-        pp.rows = rows;
-        pp.dbg = g_dbg_ss;
-        phase_mark(0, st);
-        s = k_new ? launch_pipe<true>(L, pp, st) : launch_pipe<false>(L, pp, st);
-        phase_mark(3, st);
-        if (s != TS_ERR_UNSUPPORTED) {
-            g_launches = 1;
-            return s;
-        }
-    }
     if (L->kv_dtype == TS_BF16 && group_of(L) <= 8 && L->head_dim == 64 && !two_kernels &&
         L->page_size % 16 == 0 && rows > 0) {
         // the whole step in one cluster-per-row kernel (step_cluster.cuh)

@@ -169,11 +169,8 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
             *reinterpret_cast<uint4 *>(vp + dst) = *reinterpret_cast<const uint4 *>(p.v_new + src);
             fence_proxy_async_all();  // before the attention phase's TMA reads of this page
         }
-        if (lane == 0)
-            for (int i = R; i < nst; ++i) {
-                mbar_wait(mempty0 + 8 * (i % R), ((i / R) & 1) ^ 1);
-                issue(i);
-            }
+        // refills: the consumer warp that owns a slot (stage i -> warp i % W, slot i % R,
+        // R % W == 0) re-issues it right after consuming it — no producer round trip
     } else {
         mbar_wait(qbar, 0);
         uint32_t qa[8], qp[8];
@@ -256,7 +253,13 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
                 }
             }
             __syncwarp();
-            if (lane == 0) mbar_arrive(mempty0 + 8 * st);
+            if (lane == 0 && i + R < nst) {  // refill this warp's slot with stage i + R
+                fence_proxy_async();  // this warp's generic reads (and APP patch) before the async write
+                const int np = min(kSsStagePages, nloc - (i + R) * kSsStagePages);
+                mbar_arrive_expect_tx(mfull0 + 8 * st, np * 2 * kRowBytes);
+                bulk_load_hint(kb, p.meta + ((size_t)row * p.max_pages + j0 + (size_t)(i + R) * kSsStagePages) * 2 * kAttnD,
+                               np * 2 * kRowBytes, mfull0 + 8 * st, l2_policy_evict_first());
+            }
         }
         kmn = __reduce_min_sync(0xffffffffu, kmn);
         kmx = __reduce_max_sync(0xffffffffu, kmx);
@@ -384,29 +387,10 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
     // ===================================== 3-4. gather + attend ==========================
     const float sl2 = ap.scale * kLog2e;
     if (warp == W) {
-        // the ring was last accessed by the generic proxy (scoring); APP: the appended K/V
-        // row (another CTA's generic stores, published by the cluster barrier) is read by TMA
-        if constexpr (APP)
-            fence_proxy_async_all();
-        else
-            fence_proxy_async();
-        const uint64_t pol = l2_policy_evict_first();
-        auto issue = [&](int i) {
-            const int st = i % RA;
-            const int tl = t0 + i, u = tl >> tps, sub = tl & (tpp - 1);
-            const int2 pg = sel[u - u0];
-            mbar_arrive_expect_tx(afull0 + 8 * st, 2 * 16 * kRowBytes);
-            const uint32_t dst = sb + st * 2 * 16 * kRowBytes;
-            tma_load_2d(dst, &tmK, 0, pg.x + 16 * sub, afull0 + 8 * st, pol);
-            tma_load_2d(dst + 16 * kRowBytes, &tmV, 0, pg.x + 16 * sub, afull0 + 8 * st, pol);
-        };
-        const int nt = t1 - t0;
-        if (lane < RA && lane < nt) issue(lane);  // the free stages: lane-parallel issue
-        if (lane == 0)
-            for (int i = RA; i < nt; ++i) {  // refills in order, as the consumers drain
-                mbar_wait(aempty0 + 8 * (i % RA), ((i / RA) & 1) ^ 1);
-                issue(i);
-            }
+        // the producer's part ends with the metadata stream: the consumer warps gather their
+        // own K / V tiles (stage i -> warp i % W, slot i % RA, RA % W == 0), so a slot is
+        // re-issued by its owner right after it is consumed and a CTA has W issuing warps
+        // (a single issuing lane caps a CTA's 2 KB-tile gather at ~21 GB/s: scripts/gatherbench.cu)
     } else {
         uint32_t qa[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         if (gid < p.G) {
@@ -414,6 +398,29 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
             const uint4 x0 = lds_v4(qrow), x1 = lds_v4(qrow + 16);
             qa[0] = x0.x; qa[1] = x0.y; qa[2] = x0.z; qa[3] = x0.w;
             qa[4] = x1.x; qa[5] = x1.y; qa[6] = x1.z; qa[7] = x1.w;
+        }
+        // the ring was last accessed by the generic proxy (scoring); APP: the appended K/V
+        // row (another CTA's generic stores, published by the cluster barrier) is read by TMA
+        if constexpr (APP)
+            fence_proxy_async_all();
+        else
+            fence_proxy_async();
+        const uint64_t pol = l2_policy_evict_first();
+        const int ntl = t1 - t0;
+        // lane 2e + kv issues the K (kv 0) or V (kv 1) tile of this warp's e-th stage
+        auto issue_kv = [&](int i, int kv) {
+            const int st = i % RA;
+            const int tl = t0 + i, u = tl >> tps, sub = tl & (tpp - 1);
+            const int2 pg = sel[u - u0];
+            const uint32_t dst = sb + st * 2 * 16 * kRowBytes + kv * 16 * kRowBytes;
+            tma_load_2d(dst, kv ? &tmV : &tmK, 0, pg.x + 16 * sub, afull0 + 8 * st, pol);
+        };
+        {
+            const int e = lane >> 1, i = warp + W * e;
+            if (e < RA / W && i < ntl) {
+                if ((lane & 1) == 0) mbar_arrive_expect_tx(afull0 + 8 * (i % RA), 2 * 16 * kRowBytes);
+                issue_kv(i, lane & 1);
+            }
         }
         float m = kNegInf, lp = 0.f;
         float oacc[8][4];
@@ -488,7 +495,11 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
                 }
             }
             __syncwarp();
-            if (lane == 0) mbar_arrive(aempty0 + 8 * st);
+            if (lane < 2 && i + RA < ntl) {  // refill this warp's slot with stage i + RA
+                fence_proxy_async();
+                if (lane == 0) mbar_arrive_expect_tx(afull0 + 8 * st, 2 * 16 * kRowBytes);
+                issue_kv(i + RA, lane);
+            }
         }
         lp += __shfl_xor_sync(0xffffffffu, lp, 1);
         lp += __shfl_xor_sync(0xffffffffu, lp, 2);
