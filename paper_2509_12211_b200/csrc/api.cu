@@ -851,8 +851,7 @@ static ts_status decode_step_impl(const ts_layout *L, const void *q, const void 
         sp.dbg = g_dbg_ss;
         sp.k_new = static_cast<const uint16_t *>(k_new);  // fused append (nullable)
         sp.v_new = static_cast<const uint16_t *>(v_new);
-        static const int stagger_env = env_int("TS_SC_STAGGER_NS", 0);
-        sp.stagger_ns = stagger_env > 0 ? (unsigned)stagger_env : 0u;
+
         AttnParams ap = attn_params(L, q, k_pool, v_pool, page_table, seq_lens, ids, cnt, kmax, scale,
                                     o, lse, ws);
         phase_mark(0, st);

@@ -44,9 +44,6 @@ struct ScoreSelParams {
     // to append before scoring (nullable: plain decode step)
     const uint16_t *k_new;    // [B][Hkv][64]
     const uint16_t *v_new;    // [B][Hkv][64]
-    // step_cluster: rows of odd index start their metadata stream this long after the
-    // kernel starts, so that their stream runs while the even rows select (0: no stagger)
-    unsigned stagger_ns;
 };
 
 constexpr int kSsStagePages = 32;                         // pages per ring stage

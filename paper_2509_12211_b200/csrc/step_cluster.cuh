@@ -143,11 +143,6 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
             bulk_load_hint(sb + st * kSsStageBytes, mrow + (size_t)i * kSsStagePages * 2 * kAttnD, bytes,
                            mfull0 + 8 * st, pol);
         };
-        if (p.stagger_ns && (row & 1)) {  // the late half of the rows (see ScoreSelParams)
-            const uint64_t t0 = globaltimer();
-            while (globaltimer() - t0 < p.stagger_ns) nanosleep_ns(256);
-            __syncwarp();
-        }
         if (lane < R && lane < nst) issue(lane);
         if (lane == R) {
             mbar_arrive_expect_tx(qbar, p.G * kRowBytes);
