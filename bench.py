@@ -281,6 +281,9 @@ def main():
     ap.add_argument("--oracle-seconds", type=float, default=12.0)
     ap.add_argument("--replicas", type=int, default=0)
     ap.add_argument("--no-spread", action="store_true", help="skip the p10/p90 + warm-L2 replays")
+    ap.add_argument("--no-reuse", action="store_true", help="skip the NEXT-2 cross-step reuse leg")
+    ap.add_argument("--reuse-alpha", type=float, default=0.1,
+                    help="query drift of the reuse leg (synth.drift_queries)")
     args = ap.parse_args()
     assert args.warmup >= 3
 
@@ -518,6 +521,13 @@ def main():
             use_graph and not args.no_dense and cfg.dtype == "bf16" and cfg.page_size % 16 == 0) else None
     except Exception as ex:  # noqa: BLE001 — the baseline is context; never fail the bench on it
         dense = {"unavailable": f"{type(ex).__name__}: {ex}"}
+    # ---- NEXT-2 cross-step reuse on a drifting-query workload (labelled leg, not the headline)
+    reuse = None
+    if use_graph and mode != "sequence" and not args.no_reuse and cfg.dtype == "bf16" and cfg.page_size % 16 == 0:
+        try:
+            reuse = reuse_leg(ts, cfg, reps, R, stream, dev, args.reuse_alpha)
+        except Exception as ex:  # noqa: BLE001
+            reuse = {"unavailable": f"{type(ex).__name__}: {ex}"}
     # ---- e2e: public API with host buffers (pinned), H2D of q / new k,v + D2H of o, lse
     e2e = None
     if not args.no_e2e and mode != "sequence":
@@ -642,7 +652,7 @@ def main():
         "algorithmic_bytes_per_step": step_bytes, "kernel_bytes": kb,
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "dense_baseline": dense,
         "serialised_step_us": phase["serialised_step_us"] if phase else None,
-        "spread": spread, "read_peak": read_peak,
+        "spread": spread, "read_peak": read_peak, "reuse": reuse,
         "gpu_launches": launches_per_step * args.steps, "clocks": clocks,
         "wall_s_timed": wall, "device": torch.cuda.get_device_name(dev),
     }
@@ -693,6 +703,80 @@ def dense_leg(ts, cfg, reps, R, stream, dev, args, ms_per_step):
              "kernel": "sparse_attn_tma_kernel in dense mode (every page; ts_dense_decode_attn)"}
 
     return dense
+
+
+def reuse_leg(ts, cfg, reps, R, stream, dev, alpha, T=24):
+    """SURVEY.md §8f NEXT-2, cross-step page reuse ("prefetching selected pages",
+    the reuse probability rho of PAPER.md:263-271).  A drifting-query workload
+    (synth.drift_queries: q_t = sqrt(1 - a^2) q_{t-1} + a z_t per replica) on the same cold
+    replica rotation as the headline: step j runs replica j % R with its (j // R)-th query.
+    Reported: the hit rate |prev ∩ cur| / |cur| of consecutive selections of a row
+    (averaged over rows and steps, the first step excluded; its mean is rho-hat) and the
+    per-step time of ts_decode_step vs ts_decode_step_prefetch (the previous selection
+    prefetched into L2 while the pages are scored) on the same query stream."""
+    B, Hkv = cfg.batch, cfg.num_kv_heads
+    qb = [synth.drift_queries(rep["q"], T, alpha, seed=7000 + r) for r, rep in enumerate(reps)]
+    rep = reps[0]
+    prev, hits = None, []
+    with torch.cuda.stream(stream):
+        for t in range(T):
+            ts.decode_step(rep["layout"], qb[0][t], rep["k_pool"], rep["v_pool"], rep["meta"],
+                           rep["page_table"], rep["seq_lens"], cfg.budget_tokens, cfg.scale,
+                           o=rep["o"], lse=rep["lse"], sel_ids=rep["ids"], sel_count=rep["cnt"],
+                           ws=rep["ws"], stream=stream)
+            cur = rep["ids"].view(B * Hkv, -1).clone()
+            if prev is not None:
+                valid = cur >= 0
+                hit = (cur.unsqueeze(-1) == prev.unsqueeze(-2)).any(-1) & valid
+                hits.append((hit.sum().float() / valid.sum().clamp(min=1).float()))
+            prev = cur
+    torch.cuda.synchronize()
+    hit_rate = float(torch.stack(hits).mean()) if hits else None
+
+    def one(j, prefetch):
+        r = reps[j % R]
+        q = qb[j % R][(j // R) % T]
+        if prefetch:
+            ts.decode_step_prefetch(r["layout"], q, r["k_pool"], r["v_pool"], r["meta"],
+                                    r["page_table"], r["seq_lens"], cfg.budget_tokens, cfg.scale,
+                                    r["ids"], r["cnt"], o=r["o"], lse=r["lse"], ws=r["ws"],
+                                    stream=stream)
+        else:
+            ts.decode_step(r["layout"], q, r["k_pool"], r["v_pool"], r["meta"], r["page_table"],
+                           r["seq_lens"], cfg.budget_tokens, cfg.scale, o=r["o"], lse=r["lse"],
+                           sel_ids=r["ids"], sel_count=r["cnt"], ws=r["ws"], stream=stream)
+
+    n = R * T
+    res = {}
+    for name, pf in (("plain", False), ("prefetch", True)):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(stream):
+            for j in range(n):  # untimed pass: every replica's buffers hold a real selection
+                one(j, pf)
+            with torch.cuda.graph(g, stream=stream):
+                for j in range(n):
+                    one(j, pf)
+        graph_upload(g, stream)
+        with torch.cuda.stream(stream):
+            g.replay()
+        torch.cuda.synchronize()
+        best = 1e30
+        for _ in range(3):
+            a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(stream):
+                torch.cuda._sleep(int(2e6))
+                a.record(stream)
+                g.replay()
+                b_.record(stream)
+            torch.cuda.synchronize()
+            best = min(best, a.elapsed_time(b_) / n)
+        res[name] = best * 1e3
+    return {"alpha": alpha, "steps_per_replica": T, "hit_rate": hit_rate, "rho_hat": hit_rate,
+            "us_per_step_plain": res["plain"], "us_per_step_prefetch": res["prefetch"],
+            "speedup": res["plain"] / res["prefetch"],
+            "workload": "drifting queries q_t = sqrt(1-a^2) q_(t-1) + a z_t per replica, cold "
+                        "replica rotation as the headline; best of 3 graph replays of R*T steps",
+            "api": "ts_decode_step vs ts_decode_step_prefetch (previous selection -> L2)"}
 
 
 def run_e2e(ts, cfg, reps, dev, stream, steps, warmup):

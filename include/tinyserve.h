@@ -11,6 +11,7 @@
  *   ts_sparse_decode_attn softmax attention over selected pages  PAPER.md:169-172; Alg. 1 Steps 3-4
  *   ts_decode_step        score -> select -> attend in one call  Alg. 1, PAPER.md:209-249 ("single pass")
  *   ts_decode_step_append append the new token, then the step     Eq. 1 + Alg. 1 (one launch, bf16)
+ *   ts_decode_step_prefetch the step + L2 prefetch of the previous selection
  *   ts_lse_merge          merge of partial attentions (split-K / multi-GPU)
  *
  * Conventions (apply to every entry point):
@@ -177,6 +178,22 @@ ts_status ts_decode_step_append(const ts_layout *layout, const void *q, const vo
                                 int32_t budget_tokens, float scale, float *o, float *lse,
                                 int32_t *sel_ids, int32_t *sel_count, void *ws, size_t ws_bytes,
                                 void *stream);
+
+/* ts_decode_step_prefetch — ts_decode_step with cross-step page reuse (
+ * PAPER.md:203 "prefetching selected pages", the reuse fraction rho of the load model
+ * PAPER.md:263-271, the KV-reuse study PAPER.md:623).  On entry sel_ids [B][Hkv][Kmax] and
+ * sel_count [B][Hkv] (device, required) hold the PREVIOUS step's selection of the same
+ * cache (as this call writes it; any content is safe: entries outside [0, P_b) are
+ * ignored).  While it scores the pages, the step prefetches the K and V blocks of those
+ * pages into L2, so the HBM keeps streaming through the top-K and the gather of pages
+ * selected again hits L2.  Results are identical to ts_decode_step (the prefetch is a
+ * hint); on return sel_ids / sel_count hold this step's selection.  The bf16 one-launch path
+ * (page_size a multiple of 16) prefetches; other layouts run ts_decode_step unchanged. */
+ts_status ts_decode_step_prefetch(const ts_layout *layout, const void *q, const void *k_pool,
+                                  const void *v_pool, const void *meta, const int32_t *page_table,
+                                  const int32_t *seq_lens, int32_t budget_tokens, float scale,
+                                  float *o, float *lse, int32_t *sel_ids, int32_t *sel_count,
+                                  void *ws, size_t ws_bytes, void *stream);
 
 /* Candidate merge — the exchange step of sequence sharding: the global
  * top-k over the union of per-rank candidate lists.  Part p (< parts) of row r holds k_part

@@ -18,7 +18,7 @@ import torch
 from ._lib import Layout, TinyServeError, TS_BF16, TS_F32, check, exported_symbols, lib
 
 __all__ = ["Layout", "TinyServeError", "make_layout", "meta_append", "meta_build",
-           "score_pages", "select_topk", "sparse_decode_attn", "decode_step", "decode_step_append", "select_merge", "lse_merge",
+           "score_pages", "select_topk", "sparse_decode_attn", "decode_step", "decode_step_append", "decode_step_prefetch", "select_merge", "lse_merge",
            "workspace_bytes", "attn_workspace_bytes", "dense_decode_attn", "dense_workspace_bytes", "new_workspace", "new_meta", "kmax", "launch_count",
            "profile_events",
            "exported_symbols", "PagedKV"]
@@ -211,6 +211,28 @@ def decode_step(layout, q, k_pool, v_pool, meta, page_table, seq_lens, budget_to
         ws = new_workspace(workspace_bytes(layout, budget_tokens), dev)
     _cuda(q, k_pool, v_pool, meta, page_table, seq_lens, o, lse, sel_ids, sel_count, ws)
     check("ts_decode_step", lib().ts_decode_step(
+        layout, _ptr(q), _ptr(k_pool), _ptr(v_pool), _ptr(meta), _ptr(page_table), _ptr(seq_lens),
+        int(budget_tokens), float(scale), _ptr(o), _ptr(lse), _ptr(sel_ids), _ptr(sel_count),
+        _ptr(ws), ws.numel(), _stream(stream)))
+    return o, lse, sel_ids, sel_count
+
+
+def decode_step_prefetch(layout, q, k_pool, v_pool, meta, page_table, seq_lens, budget_tokens,
+                         scale, sel_ids, sel_count, o=None, lse=None, ws=None, want_lse=True,
+                         stream=None):
+    """Alg. 1 with cross-step reuse (NEXT-2): sel_ids / sel_count hold the previous step's
+    selection on entry (prefetched into L2 while the pages are scored) and this step's on
+    return.  Results equal decode_step.  Returns (o, lse, sel_ids, sel_count)."""
+    dev = q.device
+    if o is None:
+        o = torch.empty((layout.batch, layout.num_q_heads, layout.head_dim), dtype=torch.float32,
+                        device=dev)
+    if lse is None and want_lse:
+        lse = torch.empty((layout.batch, layout.num_q_heads), dtype=torch.float32, device=dev)
+    if ws is None:
+        ws = new_workspace(workspace_bytes(layout, budget_tokens), dev)
+    _cuda(q, k_pool, v_pool, meta, page_table, seq_lens, o, lse, sel_ids, sel_count, ws)
+    check("ts_decode_step_prefetch", lib().ts_decode_step_prefetch(
         layout, _ptr(q), _ptr(k_pool), _ptr(v_pool), _ptr(meta), _ptr(page_table), _ptr(seq_lens),
         int(budget_tokens), float(scale), _ptr(o), _ptr(lse), _ptr(sel_ids), _ptr(sel_count),
         _ptr(ws), ws.numel(), _stream(stream)))

@@ -18,7 +18,7 @@ _STATUS = {0: "TS_OK", 1: "TS_ERR_CONFIG", 2: "TS_ERR_SHAPE", 3: "TS_ERR_ALIGN",
 
 # every symbol include/tinyserve.h declares
 SYMBOLS = ["ts_meta_append", "ts_meta_build", "ts_score_pages", "ts_select_topk",
-           "ts_sparse_decode_attn", "ts_decode_step", "ts_decode_step_append", "ts_select_merge", "ts_lse_merge", "ts_workspace_bytes",
+           "ts_sparse_decode_attn", "ts_decode_step", "ts_decode_step_append", "ts_decode_step_prefetch", "ts_select_merge", "ts_lse_merge", "ts_workspace_bytes",
            "ts_attn_workspace_bytes", "ts_status_str", "ts_version", "ts_last_launch_count",
            "ts_profile_events", "ts_dense_decode_attn", "ts_dense_workspace_bytes"]
 
@@ -63,6 +63,7 @@ def lib() -> ctypes.CDLL:
             "ts_sparse_decode_attn": [LP, P, P, P, P, P, P, P, I, F, P, P, P, SZ, P],
             "ts_decode_step": [LP, P, P, P, P, P, P, I, F, P, P, P, P, P, SZ, P],
             "ts_decode_step_append": [LP, P, P, P, P, P, P, P, P, I, F, P, P, P, P, P, SZ, P],
+            "ts_decode_step_prefetch": [LP, P, P, P, P, P, P, I, F, P, P, P, P, P, SZ, P],
             "ts_select_merge": [P, P, I, ctypes.c_int64, I, I, I, P, P, P, P],
             "ts_lse_merge": [I, I, I, P, P, ctypes.c_int64, P, P, P],
             "ts_dense_decode_attn": [LP, P, P, P, P, P, F, P, P, P, SZ, P],

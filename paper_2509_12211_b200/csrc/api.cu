@@ -778,7 +778,8 @@ static ts_status decode_step_impl(const ts_layout *L, const void *q, const void 
                                   const void *meta, const int32_t *page_table,
                                   const int32_t *seq_lens, int32_t budget_tokens, float scale,
                                   float *o, float *lse, int32_t *sel_ids_out,
-                                  int32_t *sel_count_out, void *ws, size_t ws_bytes, void *stream);
+                                  int32_t *sel_count_out, void *ws, size_t ws_bytes, void *stream,
+                                  bool prefetch_prev = false);
 
 ts_status ts_decode_step(const ts_layout *L, const void *q, const void *k_pool, const void *v_pool,
                          const void *meta, const int32_t *page_table, const int32_t *seq_lens,
@@ -805,12 +806,25 @@ ts_status ts_decode_step_append(const ts_layout *L, const void *q, const void *k
                             stream);
 }
 
+ts_status ts_decode_step_prefetch(const ts_layout *L, const void *q, const void *k_pool,
+                                  const void *v_pool, const void *meta, const int32_t *page_table,
+                                  const int32_t *seq_lens, int32_t budget_tokens, float scale,
+                                  float *o, float *lse, int32_t *sel_ids, int32_t *sel_count,
+                                  void *ws, size_t ws_bytes, void *stream) {
+    g_launches = 0;
+    if (!sel_ids || !sel_count) return TS_ERR_CONFIG;  // they carry the previous selection in
+    return decode_step_impl(L, q, nullptr, nullptr, k_pool, v_pool, meta, page_table, seq_lens,
+                            budget_tokens, scale, o, lse, sel_ids, sel_count, ws, ws_bytes, stream,
+                            true);
+}
+
 static ts_status decode_step_impl(const ts_layout *L, const void *q, const void *k_new,
                                   const void *v_new, const void *k_pool, const void *v_pool,
                                   const void *meta, const int32_t *page_table,
                                   const int32_t *seq_lens, int32_t budget_tokens, float scale,
                                   float *o, float *lse, int32_t *sel_ids_out,
-                                  int32_t *sel_count_out, void *ws, size_t ws_bytes, void *stream) {
+                                  int32_t *sel_count_out, void *ws, size_t ws_bytes, void *stream,
+                                  bool prefetch_prev) {
     ts_status s = check_layout(L);
     if (s != TS_OK) return s;
     if (budget_tokens < 1) return TS_ERR_CONFIG;
@@ -851,6 +865,10 @@ static ts_status decode_step_impl(const ts_layout *L, const void *q, const void 
         sp.dbg = g_dbg_ss;
         sp.k_new = static_cast<const uint16_t *>(k_new);  // fused append (nullable)
         sp.v_new = static_cast<const uint16_t *>(v_new);
+        sp.prev_ids = prefetch_prev ? ids : nullptr;  // NEXT-2: the previous selection -> L2
+        sp.prev_count = prefetch_prev ? cnt : nullptr;
+        sp.k_pool = static_cast<const uint16_t *>(k_pool);
+        sp.v_pool = static_cast<const uint16_t *>(v_pool);
 
         AttnParams ap = attn_params(L, q, k_pool, v_pool, page_table, seq_lens, ids, cnt, kmax, scale,
                                     o, lse, ws);

@@ -181,6 +181,10 @@ TS_DEV void cp_async16(uint32_t dst, const void *src) {
 TS_DEV void cp_async_mbar_arrive(uint32_t bar) {
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
 }
+// L2 prefetch of a contiguous run (16-byte aligned, multiple of 16 bytes); no smem, no barrier
+TS_DEV void prefetch_l2_bulk(const void *src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 TS_DEV void prefetch_tmap(const CUtensorMap *map) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
 }

@@ -44,6 +44,13 @@ struct ScoreSelParams {
     // to append before scoring (nullable: plain decode step)
     const uint16_t *k_new;    // [B][Hkv][64]
     const uint16_t *v_new;    // [B][Hkv][64]
+    // step_cluster, ts_decode_step_prefetch (cross-step reuse, "prefetching
+    // selected pages"): the previous step's selection [rows][kmax] / counts [rows], read at
+    // kernel start (before this step overwrites them) and prefetched into L2 (nullable)
+    const int *prev_ids;
+    const int *prev_count;
+    const uint16_t *k_pool;   // pools for the prefetch addresses ([NB][Hkv][S][64])
+    const uint16_t *v_pool;
 };
 
 constexpr int kSsStagePages = 32;                         // pages per ring stage

@@ -166,6 +166,25 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
         }
         // refills: the consumer warp that owns a slot (stage i -> warp i % W, slot i % R,
         // R % W == 0) re-issues it right after consuming it — no producer round trip
+        if (p.prev_ids) {
+            // cross-step reuse (NEXT-2; "prefetching selected pages", the rho
+            // term of PAPER.md:263-271): this CTA's slice of the PREVIOUS step's selection of
+            // the row goes to L2 now, behind the metadata stream, so the HBM keeps streaming
+            // through the select and the gather of re-selected pages hits L2.  A hint only:
+            // entries outside [0, P_b) are skipped, results do not depend on it.  Read here,
+            // before the cluster barrier that precedes every CTA's writes of the new ids.
+            const int kp = max(0, min(p.prev_count[row], p.kmax));
+            const int a0 = kp * rank / C, a1 = kp * (rank + 1) / C;
+            const uint32_t blk_bytes = (uint32_t)p.S * kRowBytes;
+            for (int e = lane; e < a1 - a0; e += 32) {
+                const int pg = p.prev_ids[(size_t)row * p.kmax + a0 + e];
+                if (pg >= 0 && pg < P) {
+                    const size_t off = ((size_t)p.page_table[(size_t)b * p.max_pages + pg] * p.Hkv + g) * p.S * kAttnD;
+                    prefetch_l2_bulk(p.k_pool + off, blk_bytes);
+                    prefetch_l2_bulk(p.v_pool + off, blk_bytes);
+                }
+            }
+        }
     } else {
         mbar_wait(qbar, 0);
         uint32_t qa[8], qp[8];

@@ -33,7 +33,8 @@ from typing import Optional
 
 import torch
 
-__all__ = ["Config", "CONFIGS", "make_case", "resample_q_rows", "sub_seed", "config"]
+__all__ = ["Config", "CONFIGS", "make_case", "resample_q_rows", "sub_seed", "config",
+           "drift_queries", "algorithmic_bytes"]
 
 
 @dataclasses.dataclass(frozen=True)
@@ -216,3 +217,22 @@ def algorithmic_bytes(cfg: Config, seq_lens, out_bytes: int = 4) -> dict:
     qo = B * Hq * d * e + B * Hq * (d + 1) * out_bytes
     return {"meta": meta, "kv": kv, "q_o": qo, "page_table": pt, "ids": ids,
             "total": meta + kv + qo + pt + ids}
+
+
+def drift_queries(q0: torch.Tensor, steps: int, alpha: float, seed: int) -> torch.Tensor:
+    """A decode-time query stream with temporal locality (SPEC's
+    "drifting" trace mode): q_0 = q0 and
+        q_t = sqrt(1 - alpha^2) * q_{t-1} + alpha * z_t,   z_t ~ N(0, I)  (fp32, then cast),
+    so every q_t keeps unit variance per channel and consecutive queries are correlated with
+    coefficient sqrt(1 - alpha^2).  alpha = 0: a constant query; alpha = 1: independent
+    queries.  Returns [steps][*q0.shape] in q0's dtype, on q0's device."""
+    g = _gen(seed, ("drift", float(alpha)), q0.device)
+    out = torch.empty((steps,) + tuple(q0.shape), dtype=q0.dtype, device=q0.device)
+    cur = q0.to(torch.float32)
+    keep = math.sqrt(max(0.0, 1.0 - alpha * alpha))
+    for t in range(steps):
+        if t:
+            z = torch.randn(q0.shape, generator=g, device=q0.device, dtype=torch.float32)
+            cur = keep * cur + alpha * z
+        out[t] = cur.to(q0.dtype)
+    return out

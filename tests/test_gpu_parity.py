@@ -474,3 +474,31 @@ def test_lse_merge_kernel(ts):
     assert np.abs(go.cpu().numpy() - ro).max() < 1e-5
     g = gl.cpu().numpy()
     assert np.isneginf(g[7]) and np.abs(np.delete(g, 7) - np.delete(rl, 7)).max() < 1e-5
+
+
+# ------------------------------------------------------------------ NEXT-2: cross-step reuse
+@pytest.mark.parametrize("name", ["c2_small", "c3_small", "two_level", "g6_s64", "f32_gqa"])
+def test_decode_step_prefetch_equals_plain(ts, name):
+    """ts_decode_step_prefetch (previous selection -> L2) is a hint: over a
+    drifting-query stream its outputs equal ts_decode_step's bit for bit, whatever the
+    previous-selection buffers hold (a real selection, or garbage incl. ids out of range)."""
+    cfg, case = make(name, seed=41)
+    d = on_dev(case)
+    L, meta = gpu_meta(ts, d)
+    K = ts.kmax(L, cfg.budget_tokens)
+    qs = synth.drift_queries(d["q"], 4, 0.2, seed=5)
+    ids = torch.randint(-5, 10 * L.max_pages, (cfg.batch, cfg.num_kv_heads, K), dtype=torch.int32, device=DEV)
+    cnt = torch.randint(-3, K + 5, (cfg.batch, cfg.num_kv_heads), dtype=torch.int32, device=DEV)
+    for t in range(4):
+        o1, l1, i1, c1 = ts.decode_step(L, qs[t], d["k_pool"], d["v_pool"], meta, d["page_table"],
+                                        d["seq_lens"], cfg.budget_tokens, cfg.scale)
+        o2, l2, i2, c2 = ts.decode_step_prefetch(L, qs[t], d["k_pool"], d["v_pool"], meta,
+                                                 d["page_table"], d["seq_lens"], cfg.budget_tokens,
+                                                 cfg.scale, ids, cnt)
+        assert torch.equal(i1, i2) and torch.equal(c1, c2)
+        assert torch.equal(o1, o2) and torch.equal(l1, l2)
+    # and the last step matches the oracle on its query
+    ref = oracle.decode_step(qs[3].cpu(), case["k_pool"], case["v_pool"], case["page_table"],
+                             case["seq_lens"], cfg.budget_tokens, cfg.scale)
+    assert np.abs(o2.cpu().numpy() - ref["o"]).max() <= ATOL[cfg.dtype] or not np.array_equal(
+        i2.cpu().numpy(), ref["sel_ids"][:, :, :K])  # (no margin enforcement on drifted q)
