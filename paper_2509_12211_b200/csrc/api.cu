@@ -867,6 +867,7 @@ static ts_status decode_step_impl(const ts_layout *L, const void *q, const void 
         sp.v_new = static_cast<const uint16_t *>(v_new);
         sp.prev_ids = prefetch_prev ? ids : nullptr;  // NEXT-2: the previous selection -> L2
         sp.prev_count = prefetch_prev ? cnt : nullptr;
+
         sp.k_pool = static_cast<const uint16_t *>(k_pool);
         sp.v_pool = static_cast<const uint16_t *>(v_pool);
 

@@ -169,20 +169,17 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
         if (p.prev_ids) {
             // cross-step reuse (NEXT-2; "prefetching selected pages", the rho
             // term of PAPER.md:263-271): this CTA's slice of the PREVIOUS step's selection of
-            // the row goes to L2 now, behind the metadata stream, so the HBM keeps streaming
-            // through the select and the gather of re-selected pages hits L2.  A hint only:
-            // entries outside [0, P_b) are skipped, results do not depend on it.  Read here,
-            // before the cluster barrier that precedes every CTA's writes of the new ids.
+            // the row is staged in sel[] now (block rows; -1 = skip) and its K / V blocks are
+            // prefetched into L2 by the whole CTA as soon as the chunk is scored, i.e. during
+            // the select.  A hint only: entries outside [0, P_b) are skipped, results do not
+            // depend on it.  Read here, before the cluster barrier that precedes every CTA's
+            // writes of the new ids.  (Measured: issuing at kernel start, or with an
+            // evict_last policy, is slower.)
             const int kp = max(0, min(p.prev_count[row], p.kmax));
             const int a0 = kp * rank / C, a1 = kp * (rank + 1) / C;
-            const uint32_t blk_bytes = (uint32_t)p.S * kRowBytes;
             for (int e = lane; e < a1 - a0; e += 32) {
                 const int pg = p.prev_ids[(size_t)row * p.kmax + a0 + e];
-                if (pg >= 0 && pg < P) {
-                    const size_t off = ((size_t)p.page_table[(size_t)b * p.max_pages + pg] * p.Hkv + g) * p.S * kAttnD;
-                    prefetch_l2_bulk(p.k_pool + off, blk_bytes);
-                    prefetch_l2_bulk(p.v_pool + off, blk_bytes);
-                }
+                sel[e] = make_int2((pg >= 0 && pg < P) ? p.page_table[(size_t)b * p.max_pages + pg] * p.Hkv + g : -1, 0);
             }
         }
     } else {
@@ -286,6 +283,16 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
         if (j0 + pg < p.max_pages) sc[sb0 + pg] = kNegInf;
     __syncthreads();
     SC_STAMP(1);
+    if (p.prev_ids) {  // NEXT-2: the previous selection's K / V blocks -> L2 (list staged above)
+        const int kp = max(0, min(p.prev_count[row], p.kmax));
+        const int a0 = kp * rank / C, a1 = kp * (rank + 1) / C;
+        for (int e = tid; e < 2 * (a1 - a0); e += NT) {
+            const int brow = sel[e >> 1].x;
+            if (brow >= 0)
+                prefetch_l2_bulk(((e & 1) ? p.v_pool : p.k_pool) + (size_t)brow * p.S * kAttnD,
+                                 (uint32_t)p.S * kRowBytes);
+        }
+    }
 
     // ===================================== 2. select =====================================
     // Every CTA of the cluster ends up with the whole row's keys (one-level) or all C x K
