@@ -110,15 +110,21 @@ def graph_upload(g, stream) -> bool:
 
 
 # ------------------------------------------------------------------------------ workload
-def rank_config(name: str, world: int, rank: int):
-    """Per-rank config and sharding mode."""
+def rank_config(name: str, world: int, rank: int, batch: int = 0, slice_n: int = 1):
+    """Per-rank config and sharding mode.  world > 1: c4 splits its batch over the ranks, c5
+    shards every sequence (strong scaling); other configs run one batch per rank (weak).
+    slice_n > 1 on one GPU: time ONE rank's share of a slice_n-GPU run of c4 / c5 (the per-GPU
+    work of BASELINE.json configs 4-5), c5's two exchanges emulated by local copies."""
     cfg = synth.config(name)
-    if name == "c4" and world > 1:
-        assert cfg.batch % world == 0
-        cfg = cfg.with_(batch=cfg.batch // world)
-        return cfg, "batch", "strong"
-    if name == "c5" and world > 1:
-        return cfg, "sequence", "strong"
+    if batch:
+        cfg = cfg.with_(batch=batch)
+    shards = world if world > 1 else slice_n
+    if name == "c4" and shards > 1:
+        assert cfg.batch % shards == 0
+        cfg = cfg.with_(batch=cfg.batch // shards)
+        return cfg, ("batch" if world > 1 else "batch-slice"), "strong"
+    if name == "c5" and shards > 1:
+        return cfg, ("sequence" if world > 1 else "sequence-slice"), "strong"
     return cfg, ("batch" if world > 1 else "none"), "weak"
 
 
@@ -280,6 +286,9 @@ def main():
     ap.add_argument("--no-dense", action="store_true", help="skip the FullCache baseline leg")
     ap.add_argument("--oracle-seconds", type=float, default=12.0)
     ap.add_argument("--replicas", type=int, default=0)
+    ap.add_argument("--batch", type=int, default=0, help="override the config's batch (e.g. c5 at 1)")
+    ap.add_argument("--slice", type=int, default=1,
+                    help="on one GPU: time one rank's share of an N-GPU c4 / c5 run")
     ap.add_argument("--no-spread", action="store_true", help="skip the p10/p90 + warm-L2 replays")
     ap.add_argument("--no-reuse", action="store_true", help="skip the NEXT-2 cross-step reuse leg")
     ap.add_argument("--reuse-alpha", type=float, default=0.1,
@@ -304,7 +313,10 @@ def main():
         raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    cfg, mode, scaling = rank_config(args.config, world, rank)
+    cfg, mode, scaling = rank_config(args.config, world, rank, args.batch, args.slice)
+    # sequence sharding: shard count / this rank's index (the emulated slice is rank 0)
+    sw, sr = (world, rank) if mode == "sequence" else ((args.slice, 0) if mode == "sequence-slice" else (1, 0))
+    seq = mode in ("sequence", "sequence-slice")
 
     if args.impl == "reference":
         run_reference(args, cfg, world, rank)
@@ -328,25 +340,33 @@ def main():
     l2 = getattr(props, "L2_cache_size", 126 * 2**20) or 126 * 2**20
     L_ctx = cfg.ctx
     Kmax = min(cfg.max_pages, max(1, cfg.budget_tokens // cfg.page_size))
-    mp_local = -(-cfg.max_pages // world) if mode == "sequence" else cfg.max_pages
-    kb = kernel_bytes(cfg, L_ctx, Kmax, mp_local, world if mode == "sequence" else 1)
+    mp_local = -(-cfg.max_pages // sw) if seq else cfg.max_pages
+    kb = kernel_bytes(cfg, L_ctx, Kmax, mp_local, sw)
     alg = synth.algorithmic_bytes(cfg, [L_ctx] * cfg.batch)
-    step_bytes = alg["total"] if mode != "sequence" else kb["total"]
+    step_bytes = alg["total"] if not seq else kb["total"]
     R = args.replicas or max(2, -(-4 * l2 // max(1, step_bytes)))
+    # every replica holds a whole pool (K + V): keep them within ~60 GB of the 180 GB HBM
+    pool_bytes = cfg.batch * cfg.max_pages * cfg.num_kv_heads * cfg.page_size * cfg.head_dim * 2 * (
+        2 if cfg.dtype == "bf16" else 4)
+    R = max(2, min(R, int(60e9 // max(1, pool_bytes)))) if not args.replicas else R
     stream = torch.cuda.Stream(device=dev)
 
-    reps = [build_replica(ts, cfg, seed=1000 * rank + r, device=dev, world=world, rank=rank)
+    reps = [build_replica(ts, cfg, seed=1000 * rank + r, device=dev, world=sw, rank=sr)
             for r in range(R)]
     torch.cuda.synchronize()
 
-    if mode == "sequence":
+    if seq:
         from paper_2509_12211_b200 import sharded
         for rep in reps:
-            rep["shard"] = sharded.ShardStep(ts, rep["layout"], world, rank, cfg.budget_tokens, dev)
+            rep["shard"] = sharded.ShardStep(ts, rep["layout"], sw, sr, cfg.budget_tokens, dev)
 
         def one(rep):
-            rep["shard"].step(rep["q"], rep["k_pool"], rep["v_pool"], rep["meta"],
-                              rep["page_table"], rep["seq_lens"], cfg.scale)
+            if mode == "sequence":
+                rep["shard"].step(rep["q"], rep["k_pool"], rep["v_pool"], rep["meta"],
+                                  rep["page_table"], rep["seq_lens"], cfg.scale)
+            else:
+                rep["shard"].step_local(rep["q"], rep["k_pool"], rep["v_pool"], rep["meta"],
+                                        rep["page_table"], rep["seq_lens"], cfg.scale)
     else:
         def one(rep):
             step_fn(ts, cfg, rep, stream)
@@ -357,9 +377,9 @@ def main():
     torch.cuda.synchronize()
     # launches of our kernels per step, as reported by the C ABI for the step just run
     # (bf16: 1 = decode_cluster_kernel; sequence sharding: 5 calls + 2 collectives)
-    launches_per_step = ts.launch_count() if mode != "sequence" else 5
-    single = mode != "sequence" and launches_per_step == 1
-    fused = cfg.dtype == "bf16" and cfg.group <= 8 and mode != "sequence" and not single
+    launches_per_step = ts.launch_count() if not seq else 5
+    single = not seq and launches_per_step == 1
+    fused = cfg.dtype == "bf16" and cfg.group <= 8 and not seq and not single
 
     # ---- graphs.  The timed unit is ONE CUDA graph of exactly `steps` consecutive steps
     # (step j on replica (warmup + j) % R: cold-L2 rotation), so PDL chains every launch to
@@ -373,7 +393,7 @@ def main():
         for e in es:
             e.record(stream)
     torch.cuda.synchronize()
-    use_graph = mode != "sequence" or os.environ.get("TS_BENCH_SEQ_GRAPH", "1") == "1"
+    use_graph = not seq or os.environ.get("TS_BENCH_SEQ_GRAPH", "1") == "1"
 
     def capture(n, offset):
         g = torch.cuda.CUDAGraph()
@@ -386,7 +406,7 @@ def main():
     if use_graph:
         try:
             for r, rep in enumerate(reps):
-                if mode != "sequence":
+                if not seq:
                     pg = torch.cuda.CUDAGraph()
                     with torch.cuda.stream(stream):
                         ts.profile_events(ev[r])
@@ -466,7 +486,7 @@ def main():
         q = lambda f: us[min(len(us) - 1, int(f * len(us)))]
         spread = {"replays": len(us), "us_per_step_p10": q(0.1), "us_per_step_median": q(0.5),
                   "us_per_step_p90": q(0.9)}
-        if mode != "sequence":
+        if not seq:
             wg = torch.cuda.CUDAGraph()
             with torch.cuda.stream(stream):
                 with torch.cuda.graph(wg, stream=stream):
@@ -523,14 +543,14 @@ def main():
         dense = {"unavailable": f"{type(ex).__name__}: {ex}"}
     # ---- NEXT-2 cross-step reuse on a drifting-query workload (labelled leg, not the headline)
     reuse = None
-    if use_graph and mode != "sequence" and not args.no_reuse and cfg.dtype == "bf16" and cfg.page_size % 16 == 0:
+    if use_graph and not seq and not args.no_reuse and cfg.dtype == "bf16" and cfg.page_size % 16 == 0:
         try:
             reuse = reuse_leg(ts, cfg, reps, R, stream, dev, args.reuse_alpha)
         except Exception as ex:  # noqa: BLE001
             reuse = {"unavailable": f"{type(ex).__name__}: {ex}"}
     # ---- e2e: public API with host buffers (pinned), H2D of q / new k,v + D2H of o, lse
     e2e = None
-    if not args.no_e2e and mode != "sequence":
+    if not args.no_e2e and not seq:
         e2e = run_e2e(ts, cfg, reps, dev, stream, steps=min(args.steps, 600), warmup=5)
         if world > 1:
             tt = torch.tensor([1.0 / e2e["value"]], device=dev)
@@ -563,7 +583,7 @@ def main():
     if rank == 0 and not args.no_oracle:
         import oracle
         oracle.build()
-        if mode == "sequence":  # the ranks hold shards: time the oracle on one whole sequence
+        if seq:  # the ranks hold shards: time the oracle on one whole sequence
             c1 = cfg.with_(batch=1)
             host = synth.make_case(c1, seed=1000)
             v, cores, sample, extras = oracle_rate(c1, host, args.oracle_seconds)
@@ -575,7 +595,7 @@ def main():
             v, cores, sample, extras = oracle_rate(cfg, host, args.oracle_seconds)
         # whole job: every rank's batch (weak) or the one global batch (strong)
         v_job = v * world if scaling == "weak" else (
-            v if mode == "sequence" else v * (cfg.batch / synth.config(args.config).batch))
+            v if seq else v * (cfg.batch / (args.batch or synth.config(args.config).batch)))
         cpu = {"value": v_job, "unit": "steps/s", "cores": cores, "kind": "oracle",
                "sample": sample + (f"; x{world} ranks' batches (one host)" if world > 1 else ""),
                **extras}
@@ -586,12 +606,11 @@ def main():
         return
 
     steps_per_s = 1e3 / ms_per_step
-    if mode == "sequence" or scaling == "strong":
+    if seq or scaling == "strong":
         value = steps_per_s              # every step covers the whole (sharded) batch
     else:
         value = steps_per_s * world      # independent batches, one per rank
-    gbs = step_bytes * world / (ms_per_step * 1e-3) / 1e9 if mode != "sequence" else \
-        kb["total"] * world / (ms_per_step * 1e-3) / 1e9
+    gbs = step_bytes * world / (ms_per_step * 1e-3) / 1e9
     peak, peak_src = measured_peaks()
     roof = None
     if phase:
@@ -629,7 +648,7 @@ def main():
                 "algorithmic_bytes_per_launch": nbytes, "avg_launch_us": us, "phase_us": phase,
                 "step_achieved_gbs": step_bytes / (ms_per_step * 1e-3) / 1e9,
                 "step_frac": step_bytes / (ms_per_step * 1e-3) / 1e9 / peak}
-    if roof is None and mode == "sequence":
+    if roof is None and seq:
         # per-rank bytes (owned metadata + owned selected K/V + exchange buffers) over the
         # per-step time of the whole sharded step (5 kernels + 2 NCCL all-gathers)
         achieved = kb["total"] / (ms_per_step * 1e-3) / 1e9
@@ -645,6 +664,7 @@ def main():
         "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
         "dtype": cfg.dtype, "data": "synthetic",
         "config": config_json(cfg, world, mode, {
+            "slice_of_gpus": args.slice if mode.endswith("-slice") else None,
             "replicas": R, "l2_bytes": l2, "l2_policy": "rotate R cold replicas (R*bytes >= 4*L2)",
             "graph": "R steps per CUDA graph replay" if use_graph else False}),
         "tokens_per_s": value * cfg.batch,

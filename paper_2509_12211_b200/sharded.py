@@ -82,6 +82,16 @@ class ShardStep:
                            part_stride=self.nq + rows_q)
         return self.o, self.lse
 
+    # -- one rank's step with the exchanges emulated (bench.py --slice: per-GPU work) -------
+    def step_local(self, q, k_pool, v_pool, meta, page_table, seq_lens, scale):
+        """This rank's kernels of one step, each all-gather replaced by replicating the local
+        buffer G times (same bytes and shapes as the real exchange; no collective)."""
+        cand = self.local_candidates(q, meta, page_table, seq_lens)
+        self.cand_g.copy_(cand.unsqueeze(0).expand_as(self.cand_g))
+        part = self.partial_attention(self.cand_g, q, k_pool, v_pool, page_table, seq_lens, scale)
+        self.part_g.copy_(part.unsqueeze(0).expand_as(self.part_g))
+        return self.merge(self.part_g)
+
     # -- one step with torch.distributed (NCCL on GPUs, gloo on CPU) -----------------------
     def step(self, q, k_pool, v_pool, meta, page_table, seq_lens, scale, group=None):
         import torch.distributed as dist
