@@ -140,6 +140,25 @@ bool ensure_func_attrs(const void *kern, size_t smem, bool nonportable) {
     return true;
 }
 
+// Launch with programmatic stream serialization (PDL): the kernel's griddepcontrol.wait
+// orders it after the previous kernel in the stream, and its launch overlaps that kernel's
+// tail (every standalone kernel starts with launch_dependents + wait).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 // ---------------------------------------------------------------- TMA descriptors
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -223,10 +242,10 @@ ts_status launch_score(const ts_layout *L, const void *q, const void *meta, cons
     if (L->kv_dtype == TS_BF16 && p.G <= 8) {
         dim3 grid((L->max_pages + kScorePagesPerCta - 1) / kScorePagesPerCta, rows);
         if (L->head_dim == 64)
-            score_mma_kernel<64><<<grid, kScoreWarps * 32, 0, st>>>(
+            launch_pdl(score_mma_kernel<64>, dim3(grid), dim3(kScoreWarps * 32), 0, st, 
                 p, (const uint16_t *)q, (const uint16_t *)meta, pt, sl, scores);
         else
-            score_mma_kernel<128><<<grid, kScoreWarps * 32, 0, st>>>(
+            launch_pdl(score_mma_kernel<128>, dim3(grid), dim3(kScoreWarps * 32), 0, st, 
                 p, (const uint16_t *)q, (const uint16_t *)meta, pt, sl, scores);
     } else {
         dim3 grid((L->max_pages + kSimtPagesPerCta - 1) / kSimtPagesPerCta, rows);
@@ -235,18 +254,18 @@ ts_status launch_score(const ts_layout *L, const void *q, const void *meta, cons
         if (L->kv_dtype == TS_BF16) {
             if (L->head_dim == 64) {
                 if (!ensure_func_attrs((const void *)score_simt_kernel<uint16_t, 64>, sm, false)) return TS_ERR_CUDA;
-                score_simt_kernel<uint16_t, 64><<<grid, kSimtWarps * 32, sm, st>>>(p, (const uint16_t *)q, (const uint16_t *)meta, pt, sl, scores);
+                launch_pdl(score_simt_kernel<uint16_t, 64>, dim3(grid), dim3(kSimtWarps * 32), sm, st, p, (const uint16_t *)q, (const uint16_t *)meta, pt, sl, scores);
             } else {
                 if (!ensure_func_attrs((const void *)score_simt_kernel<uint16_t, 128>, sm, false)) return TS_ERR_CUDA;
-                score_simt_kernel<uint16_t, 128><<<grid, kSimtWarps * 32, sm, st>>>(p, (const uint16_t *)q, (const uint16_t *)meta, pt, sl, scores);
+                launch_pdl(score_simt_kernel<uint16_t, 128>, dim3(grid), dim3(kSimtWarps * 32), sm, st, p, (const uint16_t *)q, (const uint16_t *)meta, pt, sl, scores);
             }
         } else {
             if (L->head_dim == 64) {
                 if (!ensure_func_attrs((const void *)score_simt_kernel<float, 64>, sm, false)) return TS_ERR_CUDA;
-                score_simt_kernel<float, 64><<<grid, kSimtWarps * 32, sm, st>>>(p, (const float *)q, (const float *)meta, pt, sl, scores);
+                launch_pdl(score_simt_kernel<float, 64>, dim3(grid), dim3(kSimtWarps * 32), sm, st, p, (const float *)q, (const float *)meta, pt, sl, scores);
             } else {
                 if (!ensure_func_attrs((const void *)score_simt_kernel<float, 128>, sm, false)) return TS_ERR_CUDA;
-                score_simt_kernel<float, 128><<<grid, kSimtWarps * 32, sm, st>>>(p, (const float *)q, (const float *)meta, pt, sl, scores);
+                launch_pdl(score_simt_kernel<float, 128>, dim3(grid), dim3(kSimtWarps * 32), sm, st, p, (const float *)q, (const float *)meta, pt, sl, scores);
             }
         }
     }
@@ -266,7 +285,7 @@ ts_status launch_select(const float *scores, int rows, int stride, const int *ro
     if (!ensure_func_attrs((const void *)select_topk_kernel, 200 * 1024, false)) return TS_ERR_CUDA;
     SelectParams p{scores, rows, stride * parts, row_len, ids_in, id_stride, id_offset, k,
                    stride, part_stride, sel_ids, sel_scores, sel_count};
-    select_topk_kernel<<<rows, kSelThreads, sm, st>>>(p);
+    launch_pdl(select_topk_kernel, dim3(rows), dim3(kSelThreads), sm, st, p);
     ++g_launches;
     return launch_status();
 }
@@ -626,13 +645,13 @@ ts_status launch_attn(const ts_layout *L, const void *q, const void *k_pool, con
                                o, lse, ws);
     if (L->kv_dtype == TS_BF16) {
         if (!bf16_attn_supported(L) || sel_stride > kMaxSel) return TS_ERR_UNSUPPORTED;
-        return launch_sparse_attn(L, p, false, st);
+        return launch_sparse_attn(L, p, true, st);
     }
     const int threads = 32 * std::min(p.G, 8);
     if (L->head_dim == 64)
-        attn_simt_kernel<64><<<rows, threads, 0, st>>>(p, (const float *)k_pool, (const float *)v_pool);
+        launch_pdl(attn_simt_kernel<64>, dim3(rows), dim3(threads), 0, st, p, (const float *)k_pool, (const float *)v_pool);
     else
-        attn_simt_kernel<128><<<rows, threads, 0, st>>>(p, (const float *)k_pool, (const float *)v_pool);
+        launch_pdl(attn_simt_kernel<128>, dim3(rows), dim3(threads), 0, st, p, (const float *)k_pool, (const float *)v_pool);
     ++g_launches;
     return launch_status();
 }
@@ -704,11 +723,11 @@ static ts_status meta_append_impl(const ts_layout *L, const void *k_new, const v
     const int threads = L->num_kv_heads * L->head_dim / (L->kv_dtype == TS_BF16 ? 8 : 4);
     if (threads > 1024) return TS_ERR_UNSUPPORTED;
     if (L->kv_dtype == TS_BF16)
-        meta_append_kernel<uint16_t><<<L->batch, threads, 0, as_stream(stream)>>>(
+        launch_pdl(meta_append_kernel<uint16_t>, dim3(L->batch), dim3(threads), 0, as_stream(stream), 
             p, (const uint16_t *)k_new, (const uint16_t *)v_new, seq_lens, advance, page_table,
             (uint16_t *)k_pool, (uint16_t *)v_pool, (uint16_t *)meta);
     else
-        meta_append_kernel<float><<<L->batch, threads, 0, as_stream(stream)>>>(
+        launch_pdl(meta_append_kernel<float>, dim3(L->batch), dim3(threads), 0, as_stream(stream), 
             p, (const float *)k_new, (const float *)v_new, seq_lens, advance, page_table,
             (float *)k_pool, (float *)v_pool, (float *)meta);
     ++g_launches;
@@ -728,10 +747,10 @@ ts_status ts_meta_build(const ts_layout *L, const void *k_pool, const int32_t *p
                            (L->head_dim / (L->kv_dtype == TS_BF16 ? 8 : 4));
     const int grid = (int)std::min<long long>((work + 255) / 256, (long long)device_sms() * 16);
     if (L->kv_dtype == TS_BF16)
-        meta_build_kernel<uint16_t><<<grid, 256, 0, as_stream(stream)>>>(
+        launch_pdl(meta_build_kernel<uint16_t>, dim3(grid), dim3(256), 0, as_stream(stream), 
             p, (const uint16_t *)k_pool, page_table, seq_lens, (uint16_t *)meta);
     else
-        meta_build_kernel<float><<<grid, 256, 0, as_stream(stream)>>>(
+        launch_pdl(meta_build_kernel<float>, dim3(grid), dim3(256), 0, as_stream(stream), 
             p, (const float *)k_pool, page_table, seq_lens, (float *)meta);
     ++g_launches;
     return launch_status();
@@ -957,8 +976,8 @@ ts_status ts_dense_decode_attn(const ts_layout *L, const void *q, const void *k_
                                L->max_pages, scale, o, lse, ws);
     p.dense = 1;
     static const int rr = getenv("TS_SA_R") ? atoi(getenv("TS_SA_R")) : 8;
-    if (rr == 16) return launch_sat<4, 16>(L, p, false, as_stream(stream));
-    return launch_sat<4, 8>(L, p, false, as_stream(stream));
+    if (rr == 16) return launch_sat<4, 16>(L, p, true, as_stream(stream));
+    return launch_sat<4, 8>(L, p, true, as_stream(stream));
 }
 
 ts_status ts_select_merge(const float *cand_scores, const int32_t *cand_ids, int32_t parts,
@@ -980,7 +999,7 @@ ts_status ts_lse_merge(int32_t parts, int32_t rows, int32_t d, const float *o_pa
     if (rows == 0) return TS_OK;
     const long long so = part_stride ? part_stride : (long long)rows * d;
     const long long sl = part_stride ? part_stride : (long long)rows;
-    lse_merge_kernel<<<rows, 64, 0, as_stream(stream)>>>(parts, rows, d, o_parts, lse_parts, so, sl,
+    launch_pdl(lse_merge_kernel, dim3(rows), dim3(64), 0, as_stream(stream), parts, rows, d, o_parts, lse_parts, so, sl,
                                                          o, lse);
     ++g_launches;
     return launch_status();

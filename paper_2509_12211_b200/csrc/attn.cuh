@@ -47,6 +47,8 @@ constexpr int kPS = kAttnD + 4;   // floats per (split, head) partial: o[D], m, 
 template <int D>
 __global__ void __launch_bounds__(256) attn_simt_kernel(AttnParams p, const float *__restrict__ k_pool,
                                                         const float *__restrict__ v_pool) {
+    pdl_launch_dependents();
+    pdl_wait();
     constexpr int E = D / 32;  // elements per lane: d = lane + 32 e
     const int row = blockIdx.x;
     const int b = row / p.Hkv, g = row % p.Hkv;
@@ -96,6 +98,8 @@ __global__ void __launch_bounds__(256) attn_simt_kernel(AttnParams p, const floa
 __global__ void lse_merge_kernel(int parts, int rows, int d, const float *__restrict__ o_parts,
                                  const float *__restrict__ lse_parts, long long so, long long sl,
                                  float *__restrict__ o, float *__restrict__ lse) {
+    pdl_launch_dependents();
+    pdl_wait();
     const int r = blockIdx.x;
     float M = kNegInf;
     for (int q = 0; q < parts; ++q) M = fmaxf(M, lse_parts[q * sl + r]);

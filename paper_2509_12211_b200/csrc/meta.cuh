@@ -52,6 +52,8 @@ __global__ void meta_append_kernel(MetaParams p, const T *__restrict__ k_new,
                                    int advance, const int *__restrict__ page_table,
                                    T *__restrict__ k_pool, T *__restrict__ v_pool,
                                    T *__restrict__ meta) {
+    pdl_launch_dependents();
+    pdl_wait();
     using V = Vec16<T>;
     const int cpr = p.D / V::kElems;
     const int b = blockIdx.x;
@@ -98,6 +100,8 @@ template <typename T>
 __global__ void meta_build_kernel(MetaParams p, const T *__restrict__ k_pool,
                                   const int *__restrict__ page_table,
                                   const int *__restrict__ seq_lens, T *__restrict__ meta) {
+    pdl_launch_dependents();
+    pdl_wait();
     using V = Vec16<T>;
     const int cpr = p.D / V::kElems;
     const long long total = (long long)p.B * p.max_pages * p.Hkv * cpr;

@@ -131,6 +131,8 @@ __global__ void __launch_bounds__(kScoreWarps * 32)
     score_mma_kernel(ScoreParams p, const uint16_t *__restrict__ q,
                      const uint16_t *__restrict__ meta, const int *__restrict__ page_table,
                      const int *__restrict__ seq_lens, float *__restrict__ scores) {
+    pdl_launch_dependents();  // PDL: the next call's prologue may overlap this kernel
+    pdl_wait();               // inputs may come from the previous call in the stream
     score_mma_block<D>(p, q, meta, page_table, seq_lens, scores, blockIdx.y, blockIdx.x);
 }
 
@@ -151,6 +153,8 @@ __global__ void __launch_bounds__(kSimtWarps * 32)
     constexpr int CPL = CH / LPR;                     // chunks per lane
     constexpr int RPW = 32 / LPR;                     // records per warp pass
     extern __shared__ float qs[];                     // [G][D]: q^- then q^+ as one row of 2D
+    pdl_launch_dependents();
+    pdl_wait();
     const int row = blockIdx.y;
     const int b = row / p.Hkv, g = row % p.Hkv;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;

@@ -237,6 +237,8 @@ TS_DEV void select_row(const SelectParams &p, int r, uint32_t *keys, SelectSmem<
 __global__ void __launch_bounds__(kSelThreads) select_topk_kernel(SelectParams p) {
     extern __shared__ uint32_t sm[];
     __shared__ SelectSmem<kSelThreads> S;
+    pdl_launch_dependents();
+    pdl_wait();
     select_row<kSelThreads>(p, blockIdx.x, sm, S);
 }
 
