@@ -58,6 +58,14 @@ def lib():
             L.or_lse_merge.argtypes = [i32, i32, i32, P, P, P, P]
             L.or_relevance.argtypes = [P, P, P, i32]
             L.or_relevance.restype = ctypes.c_double
+            L.or_e4m3_value.argtypes = [ctypes.c_uint8]
+            L.or_e4m3_value.restype = ctypes.c_double
+            L.or_e4m3_round.argtypes = [ctypes.c_double]
+            L.or_e4m3_round.restype = ctypes.c_uint8
+            L.or_kv_exponent.argtypes = [ctypes.c_double]
+            L.or_kv_exponent.restype = ctypes.c_int
+            L.or_kv_quantize.argtypes = [ctypes.c_longlong, i32, P, P, P]
+            L.or_kv_dequantize.argtypes = [ctypes.c_longlong, i32, P, P, P]
             L.or_num_threads.restype = ctypes.c_int
             _lib = L
     return _lib
@@ -252,3 +260,56 @@ def widen(t) -> np.ndarray:
     if dc == 1:
         return (a.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
     return a.astype(np.float64)
+
+
+# ---------------------------------------------------------------- FP8 KV (reading R21)
+def e4m3_value(code: int) -> float:
+    """Value of one OCP FP8 E4M3 code (format definition)."""
+    return lib().or_e4m3_value(int(code))
+
+
+def e4m3_round(x: float) -> int:
+    """Nearest E4M3 code (ties to even, saturating at 448)."""
+    return int(lib().or_e4m3_round(float(x)))
+
+
+def kv_exponent(amax: float) -> int:
+    """Smallest e in [-64, 64] with amax <= 448 * 2^e."""
+    return int(lib().or_kv_exponent(float(amax)))
+
+
+def kv_quantize(x):
+    """Quantise bf16 rows [..., d] -> (codes uint8 [..., d], exps int8 [...]) (reading R21)."""
+    xr, dc = _raw(x)
+    assert dc == 1, "FP8 KV quantisation takes bf16 rows"
+    d = xr.shape[-1]
+    rows = int(np.prod(xr.shape[:-1]))
+    codes = np.zeros(xr.shape, np.uint8)
+    exps = np.zeros(xr.shape[:-1], np.int8)
+    lib().or_kv_quantize(rows, d, _p(np.ascontiguousarray(xr)), _p(codes), _p(exps))
+    return codes, exps
+
+
+def kv_dequantize(codes, exps) -> np.ndarray:
+    """codes [..., d] uint8, exps [...] int8 -> exact fp32 values [..., d]."""
+    codes = np.ascontiguousarray(codes, np.uint8)
+    exps = np.ascontiguousarray(exps, np.int8)
+    d = codes.shape[-1]
+    rows = int(np.prod(codes.shape[:-1]))
+    out = np.zeros(codes.shape, np.float32)
+    lib().or_kv_dequantize(rows, d, _p(codes), _p(exps), _p(out))
+    return out
+
+
+def decode_step_fp8(q, k_codes, k_exps, v_codes, v_exps, page_table, seq_lens, budget_tokens,
+                    scale, threads: int = 0, want_scores: bool = False):
+    """Alg. 1 over an FP8 cache (reading R21): the K / V pools are dequantised exactly to
+    fp32 ([NB][Hkv][S][d] codes with [NB][Hkv][S] exponents), q (bf16) is widened exactly,
+    and the float64 decode_step runs unchanged on those values — metadata over the
+    dequantised keys (Eq. 1), scores (Eq. 2), top-K, attention."""
+    import torch
+    kd = torch.from_numpy(kv_dequantize(k_codes, k_exps))
+    vd = torch.from_numpy(kv_dequantize(v_codes, v_exps))
+    qf = torch.from_numpy(widen(q).astype(np.float32))
+    return decode_step(qf, kd, vd, page_table, seq_lens, budget_tokens, scale, threads=threads,
+                       want_scores=want_scores)

@@ -375,3 +375,71 @@ int or_lse_merge(int parts, int rows, int d, const double *o_parts, const double
     }
     return 0;
 }
+
+/* ------------------------------------------------------------------------------------
+ * FP8 KV storage ("FP16/INT8 KV formats").  Reading
+ * R21: every stored K or V row (one token, one kv head, d channels) is
+ *     x_i = c_i * 2^e,   c_i an OCP FP8 E4M3 value (1 sign, 4 exponent bits with bias 7,
+ *                        3 mantissa bits; largest finite 448, no infinities),
+ *                        e an integer in [-64, 64] chosen per row:
+ *     e = the smallest integer in [-64, 64] with max_i |x_i| <= 448 * 2^e,
+ *     c_i = the E4M3 value nearest to x_i * 2^-e (ties to the even mantissa; magnitudes
+ *           beyond 448 saturate to 448).
+ * Because 2^e is a power of two, every dequantised value c_i * 2^e (4 significant bits,
+ * |e| <= 64) is exactly a bf16 / fp32 number, so the page metadata built over the
+ * dequantised keys (Eq. 1) stays exact and r (Eq. 2) stays an upper bound.
+ * ---------------------------------------------------------------------------------- */
+
+/* Value of an E4M3 code (the format definition written out). */
+double or_e4m3_value(uint8_t c) {
+    const int s = c >> 7, E = (c >> 3) & 15, m = c & 7;
+    double v;
+    if (E == 15 && m == 7) return NAN;                 /* the only NaN encodings */
+    if (E == 0) v = ldexp((double)m / 8.0, -6);        /* subnormal: m/8 * 2^(1-7) */
+    else v = ldexp(1.0 + (double)m / 8.0, E - 7);      /* normal: 1.m * 2^(E-7) */
+    return s ? -v : v;
+}
+
+/* Nearest E4M3 code to x: brute force over the 127 non-negative finite codes, ties to the
+ * even code (mantissa LSB 0), |x| > 448 saturates; the sign bit is x's. */
+uint8_t or_e4m3_round(double x) {
+    const double a = fabs(x);
+    int best = 0;
+    double bd = INFINITY;
+    for (int c = 0; c <= 126; ++c) {
+        const double dlt = fabs(or_e4m3_value((uint8_t)c) - a);
+        if (dlt < bd || (dlt == bd && (c & 1) == 0)) { bd = dlt; best = c; }
+    }
+    if (a > 448.0) best = 126;                         /* saturate (0x7e = 448) */
+    return (uint8_t)(best | (signbit(x) ? 0x80 : 0));
+}
+
+/* The row exponent: smallest e in [-64, 64] with amax <= 448 * 2^e. */
+int or_kv_exponent(double amax) {
+    int e = -64;
+    while (e < 64 && amax > ldexp(448.0, e)) ++e;
+    return e;
+}
+
+/* Quantise `rows` bf16 rows of d channels (src [rows][d] bf16 bits) into codes [rows][d]
+ * and exponents [rows]. */
+void or_kv_quantize(long long rows, int d, const uint16_t *src, uint8_t *codes, int8_t *exps) {
+    for (long long r = 0; r < rows; ++r) {
+        double amax = 0.0;
+        for (int i = 0; i < d; ++i) {
+            const double x = fabs(widen(src, 1, (size_t)r * d + i));
+            if (x > amax) amax = x;
+        }
+        const int e = or_kv_exponent(amax);
+        exps[r] = (int8_t)e;
+        for (int i = 0; i < d; ++i)
+            codes[(size_t)r * d + i] = or_e4m3_round(ldexp(widen(src, 1, (size_t)r * d + i), -e));
+    }
+}
+
+/* Dequantise to fp32 (exact): out[r][i] = value(codes[r][i]) * 2^exps[r]. */
+void or_kv_dequantize(long long rows, int d, const uint8_t *codes, const int8_t *exps, float *out) {
+    for (long long r = 0; r < rows; ++r)
+        for (int i = 0; i < d; ++i)
+            out[(size_t)r * d + i] = (float)ldexp(or_e4m3_value(codes[(size_t)r * d + i]), exps[r]);
+}
