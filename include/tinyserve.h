@@ -38,8 +38,9 @@
  *    j % shard_stride == shard_offset and stores global page j at local index
  *    j / shard_stride.  Unsharded: shard_stride = 1, shard_offset = 0.  Page ids that
  *    cross the boundary (sel_ids) are always GLOBAL.
- *  - PRECISION: q, K, V and meta share kv_dtype (bf16 or fp32); scores, o and lse are
- *    fp32 (reading R10).  K_b = min(P_b, max(1, floor(budget_tokens / page_size))).
+ *  - PRECISION: q, K, V and meta share kv_dtype (bf16 or fp32; for TS_FP8E4M3 K and V are
+ *    E4M3 codes with row exponents and q / meta are bf16); scores, o and lse are fp32
+ *    (reading R10).  K_b = min(P_b, max(1, floor(budget_tokens / page_size))).
  *  - ERRORS: host-side validation only (no device synchronisation):
  *      TS_ERR_CONFIG       non-positive size, budget < 1, unknown dtype
  *      TS_ERR_SHAPE        num_q_heads % num_kv_heads != 0, k < 1, bad shard
@@ -75,7 +76,15 @@ typedef enum {
     TS_ERR_WORKSPACE = 6
 } ts_status;
 
-typedef enum { TS_F32 = 0, TS_BF16 = 1 } ts_dtype;
+/* KV storage type.  TS_FP8E4M3 ("FP16/INT8 KV formats" PAPER.md:94,
+ * reading R21): k_pool / v_pool hold OCP FP8 E4M3 codes [num_blocks][Hkv][S][64] followed
+ * immediately by one int8 exponent per row [num_blocks][Hkv][S] (row = one token, one kv
+ * head; value = code * 2^e, e in [-64, 64] the smallest with max |x| <= 448 * 2^e), i.e.
+ * num_blocks*Hkv*S*65 bytes (ts_pool_bytes); q, meta, k_new and v_new stay bf16, and the
+ * metadata is the exact min / max of the DEQUANTISED keys.  head_dim 64 only; attention
+ * over an FP8 cache runs in ts_decode_step(_append / _prefetch) (page_size a multiple of 16,
+ * G <= 8); ts_sparse_decode_attn / ts_dense_decode_attn return TS_ERR_UNSUPPORTED for it. */
+typedef enum { TS_F32 = 0, TS_BF16 = 1, TS_FP8E4M3 = 2 } ts_dtype;
 
 typedef struct {
     int32_t batch;          /* B: sequences in the batch                                   */
@@ -227,6 +236,20 @@ ts_status ts_dense_decode_attn(const ts_layout *layout, const void *q, const voi
                                const int32_t *seq_lens, float scale, float *o, float *lse,
                                void *ws, size_t ws_bytes, void *stream);
 size_t ts_dense_workspace_bytes(const ts_layout *layout);
+
+/* FP8 KV quantisation (reading R21; ts_dtype TS_FP8E4M3): rows x 64 bf16 values at src
+ * (device, 16-byte aligned) -> codes [rows][64] uint8 (8-byte aligned) and exps [rows] int8:
+ * per row e = smallest integer in [-64, 64] with max |x| <= 448 * 2^e, code = E4M3 nearest
+ * to x * 2^-e (round to nearest even, saturating).  For a whole pool: rows =
+ * num_blocks*Hkv*S, codes = the pool, exps = pool + rows*64.  Used for prefill / cache
+ * import; decode-time appends quantise inside ts_meta_append / ts_decode_step_append.
+ * TS_ERR_UNSUPPORTED unless head_dim == 64. */
+ts_status ts_kv_quantize(int64_t rows, int32_t head_dim, const void *src, void *codes, void *exps,
+                         void *stream);
+
+/* Bytes of one K (or V) pool for the layout: num_blocks*Hkv*S*d*elem, or *65 for FP8
+ * (codes + exponents).  Host-only; 0 for an invalid layout. */
+size_t ts_pool_bytes(const ts_layout *layout);
 
 /* Workspace sizes in bytes (host-only, no CUDA call). */
 size_t ts_workspace_bytes(const ts_layout *layout, int32_t budget_tokens);

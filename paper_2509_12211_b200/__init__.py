@@ -15,12 +15,12 @@ from __future__ import annotations
 
 import torch
 
-from ._lib import Layout, TinyServeError, TS_BF16, TS_F32, check, exported_symbols, lib
+from ._lib import Layout, TinyServeError, TS_BF16, TS_F32, TS_FP8E4M3, check, exported_symbols, lib
 
 __all__ = ["Layout", "TinyServeError", "make_layout", "meta_append", "meta_build",
            "score_pages", "select_topk", "sparse_decode_attn", "decode_step", "decode_step_append", "decode_step_prefetch", "select_merge", "lse_merge",
            "workspace_bytes", "attn_workspace_bytes", "dense_decode_attn", "dense_workspace_bytes", "new_workspace", "new_meta", "kmax", "launch_count",
-           "profile_events",
+           "profile_events", "kv_quantize", "fp8_pool", "fp8_views", "pool_bytes",
            "exported_symbols", "PagedKV"]
 
 
@@ -50,8 +50,18 @@ def _stream(stream):
 
 
 def make_layout(q: torch.Tensor, k_pool: torch.Tensor, page_table: torch.Tensor,
-                shard_stride: int = 1, shard_offset: int = 0) -> Layout:
+                shard_stride: int = 1, shard_offset: int = 0, pool_shape=None) -> Layout:
+    """Layout of a cache.  An FP8 cache (reading R21) is a flat uint8 pool (codes, then row
+    exponents; see fp8_pool) and needs pool_shape = (num_blocks, Hkv, S, d); q stays bf16."""
     B, Hq, d = q.shape
+    if k_pool.dtype == torch.uint8:
+        if pool_shape is None:
+            raise ValueError("an FP8 pool needs pool_shape=(num_blocks, Hkv, S, d)")
+        nb, Hkv, S, d2 = pool_shape
+        if d2 != d or q.dtype != torch.bfloat16 or k_pool.numel() < nb * Hkv * S * (d + 1):
+            raise ValueError("FP8 cache: q must be bf16 and the pool hold num_blocks*Hkv*S*(d+1) bytes")
+        return Layout(B, Hq, Hkv, d, S, page_table.shape[1], nb, shard_stride, shard_offset,
+                      TS_FP8E4M3)
     nb, Hkv, S, d2 = k_pool.shape
     if d2 != d or q.dtype != k_pool.dtype:
         raise ValueError("q and k_pool disagree on head_dim or dtype")
@@ -106,7 +116,9 @@ def meta_append(layout, k_new, v_new, seq_lens, page_table, k_pool, v_pool, meta
 
 
 def new_meta(layout, dtype, device) -> torch.Tensor:
-    """Zeroed metadata [B][Hkv][max_pages][2][d] (logical page order)."""
+    """Zeroed metadata [B][Hkv][max_pages][2][d] (logical page order; bf16 for FP8 caches)."""
+    if layout.kv_dtype == TS_FP8E4M3:
+        dtype = torch.bfloat16
     return torch.zeros((layout.batch, layout.num_kv_heads, layout.max_pages, 2, layout.head_dim),
                        dtype=dtype, device=device)
 
@@ -118,6 +130,36 @@ def meta_build(layout, k_pool, page_table, seq_lens, meta=None, stream=None):
     check("ts_meta_build", lib().ts_meta_build(layout, _ptr(k_pool), _ptr(page_table),
                                                _ptr(seq_lens), _ptr(meta), _stream(stream)))
     return meta
+
+
+def pool_bytes(layout) -> int:
+    return lib().ts_pool_bytes(layout)
+
+
+def fp8_pool(num_blocks, num_kv_heads, page_size, head_dim, device) -> torch.Tensor:
+    """A zeroed FP8 pool (reading R21): codes [NB][Hkv][S][d] then exponents [NB][Hkv][S]."""
+    return torch.zeros(num_blocks * num_kv_heads * page_size * (head_dim + 1), dtype=torch.uint8,
+                       device=device)
+
+
+def fp8_views(pool, num_blocks, num_kv_heads, page_size, head_dim=64):
+    """(codes [NB][Hkv][S][d] uint8, exps [NB][Hkv][S] int8) views of an FP8 pool."""
+    n = num_blocks * num_kv_heads * page_size
+    codes = pool[: n * head_dim].view(num_blocks, num_kv_heads, page_size, head_dim)
+    exps = pool[n * head_dim: n * (head_dim + 1)].view(torch.int8).view(num_blocks, num_kv_heads, page_size)
+    return codes, exps
+
+
+def kv_quantize(src: torch.Tensor, out=None, stream=None) -> torch.Tensor:
+    """bf16 pool [NB][Hkv][S][d] (or any [..., d] rows) -> FP8 pool (ts_kv_quantize)."""
+    d = src.shape[-1]
+    rows = src.numel() // d
+    if out is None:
+        out = torch.empty(rows * (d + 1), dtype=torch.uint8, device=src.device)
+    _cuda(src, out)
+    check("ts_kv_quantize", lib().ts_kv_quantize(rows, d, _ptr(src), _ptr(out),
+                                                 out.data_ptr() + rows * d, _stream(stream)))
+    return out
 
 
 def score_pages(layout, q, meta, page_table, seq_lens, scores=None, stream=None):

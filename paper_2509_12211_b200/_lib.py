@@ -12,7 +12,7 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libtinyserve.so")
 
-TS_F32, TS_BF16 = 0, 1
+TS_F32, TS_BF16, TS_FP8E4M3 = 0, 1, 2
 _STATUS = {0: "TS_OK", 1: "TS_ERR_CONFIG", 2: "TS_ERR_SHAPE", 3: "TS_ERR_ALIGN",
            4: "TS_ERR_UNSUPPORTED", 5: "TS_ERR_CUDA", 6: "TS_ERR_WORKSPACE"}
 
@@ -20,7 +20,8 @@ _STATUS = {0: "TS_OK", 1: "TS_ERR_CONFIG", 2: "TS_ERR_SHAPE", 3: "TS_ERR_ALIGN",
 SYMBOLS = ["ts_meta_append", "ts_meta_build", "ts_score_pages", "ts_select_topk",
            "ts_sparse_decode_attn", "ts_decode_step", "ts_decode_step_append", "ts_decode_step_prefetch", "ts_select_merge", "ts_lse_merge", "ts_workspace_bytes",
            "ts_attn_workspace_bytes", "ts_status_str", "ts_version", "ts_last_launch_count",
-           "ts_profile_events", "ts_dense_decode_attn", "ts_dense_workspace_bytes"]
+           "ts_profile_events", "ts_dense_decode_attn", "ts_dense_workspace_bytes",
+           "ts_kv_quantize", "ts_pool_bytes"]
 
 
 class TinyServeError(RuntimeError):
@@ -67,6 +68,7 @@ def lib() -> ctypes.CDLL:
             "ts_select_merge": [P, P, I, ctypes.c_int64, I, I, I, P, P, P, P],
             "ts_lse_merge": [I, I, I, P, P, ctypes.c_int64, P, P, P],
             "ts_dense_decode_attn": [LP, P, P, P, P, P, F, P, P, P, SZ, P],
+            "ts_kv_quantize": [ctypes.c_int64, I, P, P, P, P],
         }
         for name, args in sig.items():
             fn = getattr(L, name)
@@ -78,6 +80,8 @@ def lib() -> ctypes.CDLL:
         L.ts_attn_workspace_bytes.restype = SZ
         L.ts_dense_workspace_bytes.argtypes = [LP]
         L.ts_dense_workspace_bytes.restype = SZ
+        L.ts_pool_bytes.argtypes = [LP]
+        L.ts_pool_bytes.restype = SZ
         L.ts_status_str.argtypes = [ctypes.c_int]
         L.ts_status_str.restype = ctypes.c_char_p
         L.ts_version.restype = ctypes.c_char_p

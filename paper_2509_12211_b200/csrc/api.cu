@@ -11,6 +11,7 @@
 #include "../../include/tinyserve.h"
 #include "attn.cuh"
 #include "common.cuh"
+#include "fp8.cuh"
 #include "step_cluster.cuh"
 #include "meta.cuh"
 #include "score.cuh"
@@ -43,12 +44,25 @@ ts_status check_layout(const ts_layout *L) {
     if (L->batch < 0 || L->num_q_heads < 1 || L->num_kv_heads < 1 || L->head_dim < 1 ||
         L->page_size < 1 || L->max_pages < 1 || L->num_blocks < 1)
         return TS_ERR_CONFIG;
-    if (L->kv_dtype != TS_F32 && L->kv_dtype != TS_BF16) return TS_ERR_CONFIG;
+    if (L->kv_dtype != TS_F32 && L->kv_dtype != TS_BF16 && L->kv_dtype != TS_FP8E4M3) return TS_ERR_CONFIG;
     if (L->num_q_heads % L->num_kv_heads) return TS_ERR_SHAPE;
     if (L->shard_stride < 1 || L->shard_offset < 0 || L->shard_offset >= L->shard_stride)
         return TS_ERR_SHAPE;
     if (L->head_dim != 64 && L->head_dim != 128) return TS_ERR_UNSUPPORTED;
+    if (L->kv_dtype == TS_FP8E4M3 && L->head_dim != 64) return TS_ERR_UNSUPPORTED;
     return TS_OK;
+}
+
+// FP8 pools (reading R21): codes [NB][Hkv][S][64] followed by the row exponents [NB][Hkv][S]
+size_t f8_rows(const ts_layout *L) { return (size_t)L->num_blocks * L->num_kv_heads * L->page_size; }
+const int8_t *f8_exps(const void *pool, const ts_layout *L) {
+    return static_cast<const int8_t *>(pool) + f8_rows(L) * 64;
+}
+// q and metadata of an FP8 cache are bf16: the scoring view of the layout
+ts_layout score_view(const ts_layout *L) {
+    ts_layout v = *L;
+    if (v.kv_dtype == TS_FP8E4M3) v.kv_dtype = TS_BF16;
+    return v;
 }
 
 int group_of(const ts_layout *L) { return L->num_q_heads / L->num_kv_heads; }
@@ -185,6 +199,20 @@ bool make_pool_map(CUtensorMap *map, const void *pool, const ts_layout *L, int T
     const cuuint32_t estr[2] = {1, 1};
     return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(pool), dims, strides,
               box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+              CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// FP8 code pool [NB][Hkv][S][64] bytes viewed as NB*Hkv*S rows x 64 bytes; box = TT rows,
+// 64-byte swizzle (the consumer's reads are bank-conflict free under it).
+bool make_pool_map_f8(CUtensorMap *map, const void *pool, const ts_layout *L, int TT) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    const cuuint64_t dims[2] = {64, (cuuint64_t)f8_rows(L)};
+    const cuuint64_t strides[1] = {64};
+    const cuuint32_t box[2] = {64, (cuuint32_t)TT};
+    const cuuint32_t estr[2] = {1, 1};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void *>(pool), dims, strides,
+              box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -449,9 +477,9 @@ struct StepPlan {
     size_t sm = 0;
 };
 
-template <int W, int R, bool DSM, bool APP>
+template <int W, int R, bool DSM, bool APP, bool F8>
 StepPlan plan_step(const ts_layout *L, int kmax) {
-    auto kern = decode_cluster_kernel<W, R, DSM, APP>;
+    auto kern = decode_cluster_kernel<W, R, DSM, APP, F8>;
     StepPlan pl;
     const int rows = L->batch * L->num_kv_heads;
     // flags: bit 0 page-table row prefetched to smem (rows up to 2048 pages); bit 1
@@ -508,13 +536,14 @@ StepPlan plan_step(const ts_layout *L, int kmax) {
     }
 }
 
-template <int W, int R, bool DSM, bool APP>
+template <int W, int R, bool DSM, bool APP, bool F8>
 ts_status launch_step(const ts_layout *L, ScoreSelParams &sp, const AttnParams &ap,
                       const StepPlan &pl, cudaStream_t st) {
-    auto kern = decode_cluster_kernel<W, R, DSM, APP>;
+    auto kern = decode_cluster_kernel<W, R, DSM, APP, F8>;
     const int rows = L->batch * L->num_kv_heads;
     CUtensorMap tmK, tmV;
-    if (!make_pool_map(&tmK, ap.k_pool, L, 16) || !make_pool_map(&tmV, ap.v_pool, L, 16))
+    if (F8 ? (!make_pool_map_f8(&tmK, ap.k_pool, L, 16) || !make_pool_map_f8(&tmV, ap.v_pool, L, 16))
+           : (!make_pool_map(&tmK, ap.k_pool, L, 16) || !make_pool_map(&tmV, ap.v_pool, L, 16)))
         return TS_ERR_CUDA;
     sp.C = pl.C;
     sp.chunk = pl.chunk;
@@ -546,20 +575,20 @@ ts_status launch_step(const ts_layout *L, ScoreSelParams &sp, const AttnParams &
     return launch_status();
 }
 
-template <int W, int R, bool APP>
+template <int W, int R, bool APP, bool F8>
 ts_status launch_step_cluster_app(const ts_layout *L, ScoreSelParams &sp, const AttnParams &ap,
                                  cudaStream_t st) {
     // DSMEM merge when its merge area costs no cluster width and C <= 8 (measured: faster at
     // C = 4 (C3); at C = 13 (C5) one SM receiving 13 partials loses to the L2 ticket merge)
     static const int dsm_env = getenv("TS_SC_DSM") ? atoi(getenv("TS_SC_DSM")) : -1;  // dev knob
-    const StepPlan b = plan_step<W, R, false, APP>(L, sp.kmax);
+    const StepPlan b = plan_step<W, R, false, APP, F8>(L, sp.kmax);
     if constexpr (R == 8) {
-        const StepPlan a = plan_step<W, R, true, APP>(L, sp.kmax);
+        const StepPlan a = plan_step<W, R, true, APP, F8>(L, sp.kmax);
         if (dsm_env != 0 && a.ok && a.C > 1 && (dsm_env == 1 || !b.ok || (a.C >= b.C && a.C <= 8)))
-            return launch_step<W, R, true, APP>(L, sp, ap, a, st);
+            return launch_step<W, R, true, APP, F8>(L, sp, ap, a, st);
     }
     if (!b.ok) return TS_ERR_UNSUPPORTED;
-    return launch_step<W, R, false, APP>(L, sp, ap, b, st);
+    return launch_step<W, R, false, APP, F8>(L, sp, ap, b, st);
 }
 
 // the fused-append instantiation (APP) only when the call appends: the plain step keeps the
@@ -567,8 +596,10 @@ ts_status launch_step_cluster_app(const ts_layout *L, ScoreSelParams &sp, const 
 template <int W, int R>
 ts_status launch_step_cluster_t(const ts_layout *L, ScoreSelParams &sp, const AttnParams &ap,
                                 cudaStream_t st) {
-    return sp.k_new ? launch_step_cluster_app<W, R, true>(L, sp, ap, st)
-                    : launch_step_cluster_app<W, R, false>(L, sp, ap, st);
+    if (L->kv_dtype == TS_FP8E4M3)  // the FP8 append is its own kernel (decode_step_impl)
+        return sp.k_new ? TS_ERR_UNSUPPORTED : launch_step_cluster_app<W, R, false, true>(L, sp, ap, st);
+    return sp.k_new ? launch_step_cluster_app<W, R, true, false>(L, sp, ap, st)
+                    : launch_step_cluster_app<W, R, false, false>(L, sp, ap, st);
 }
 
 
@@ -720,6 +751,15 @@ static ts_status meta_append_impl(const ts_layout *L, const void *k_new, const v
     if (L->batch == 0) return TS_OK;
     MetaParams p{L->batch, L->num_kv_heads, L->head_dim, L->page_size, L->max_pages,
                  L->shard_stride, L->shard_offset};
+    if (L->kv_dtype == TS_FP8E4M3) {  // bf16 token -> E4M3 codes + row exponent (reading R21)
+        if (L->num_kv_heads * 8 > 1024) return TS_ERR_UNSUPPORTED;
+        launch_pdl(meta_append_f8_kernel, dim3(L->batch), dim3(L->num_kv_heads * 8), 0, as_stream(stream),
+                   p, (const uint16_t *)k_new, (const uint16_t *)v_new, seq_lens, advance, page_table,
+                   (uint8_t *)k_pool, (uint8_t *)v_pool, const_cast<int8_t *>(f8_exps(k_pool, L)),
+                   const_cast<int8_t *>(f8_exps(v_pool, L)), (uint16_t *)meta);
+        ++g_launches;
+        return launch_status();
+    }
     const int threads = L->num_kv_heads * L->head_dim / (L->kv_dtype == TS_BF16 ? 8 : 4);
     if (threads > 1024) return TS_ERR_UNSUPPORTED;
     if (L->kv_dtype == TS_BF16)
@@ -744,9 +784,12 @@ ts_status ts_meta_build(const ts_layout *L, const void *k_pool, const int32_t *p
     MetaParams p{L->batch, L->num_kv_heads, L->head_dim, L->page_size, L->max_pages,
                  L->shard_stride, L->shard_offset};
     const long long work = (long long)L->batch * L->max_pages * L->num_kv_heads *
-                           (L->head_dim / (L->kv_dtype == TS_BF16 ? 8 : 4));
+                           (L->head_dim / (L->kv_dtype == TS_F32 ? 4 : 8));
     const int grid = (int)std::min<long long>((work + 255) / 256, (long long)device_sms() * 16);
-    if (L->kv_dtype == TS_BF16)
+    if (L->kv_dtype == TS_FP8E4M3)
+        launch_pdl(meta_build_f8_kernel, dim3(grid), dim3(256), 0, as_stream(stream), p,
+                   (const uint8_t *)k_pool, f8_exps(k_pool, L), page_table, seq_lens, (uint16_t *)meta);
+    else if (L->kv_dtype == TS_BF16)
         launch_pdl(meta_build_kernel<uint16_t>, dim3(grid), dim3(256), 0, as_stream(stream), 
             p, (const uint16_t *)k_pool, page_table, seq_lens, (uint16_t *)meta);
     else
@@ -763,7 +806,8 @@ ts_status ts_score_pages(const ts_layout *L, const void *q, const void *meta,
     ts_status s = check_layout(L);
     if (s != TS_OK) return s;
     if (!aligned16(q) || !aligned16(meta)) return TS_ERR_ALIGN;
-    return launch_score(L, q, meta, page_table, seq_lens, scores, as_stream(stream));
+    const ts_layout v = score_view(L);  // FP8 cache: q and metadata are bf16
+    return launch_score(&v, q, meta, page_table, seq_lens, scores, as_stream(stream));
 }
 
 ts_status ts_select_topk(const float *scores, int32_t rows, int32_t stride, const int32_t *row_len,
@@ -788,6 +832,7 @@ ts_status ts_sparse_decode_attn(const ts_layout *L, const void *q, const void *k
     if (!aligned16(q) || !aligned16(k_pool) || !aligned16(v_pool) || !aligned16(o))
         return TS_ERR_ALIGN;
     if (!ws || ws_bytes < attn_ws_layout(L, sel_stride).total) return TS_ERR_WORKSPACE;
+    if (L->kv_dtype == TS_FP8E4M3) return TS_ERR_UNSUPPORTED;  // FP8: the fused step only
     return launch_attn(L, q, k_pool, v_pool, page_table, seq_lens, sel_ids, sel_count, sel_stride,
                        scale, o, lse, ws, as_stream(stream));
 }
@@ -856,6 +901,9 @@ static ts_status decode_step_impl(const ts_layout *L, const void *q, const void 
     if (!ws || ws_bytes < w.total) return TS_ERR_WORKSPACE;
     if (L->kv_dtype == TS_BF16 && (!bf16_attn_supported(L) || kmax > kMaxSel))
         return TS_ERR_UNSUPPORTED;
+    // FP8 KV (reading R21): the one-launch cluster kernel only (d 64, S % 16 == 0, G <= 8)
+    const bool f8 = L->kv_dtype == TS_FP8E4M3;
+    if (f8 && (L->page_size % 16 != 0 || group_of(L) > 8 || kmax > kMaxSel)) return TS_ERR_UNSUPPORTED;
     char *wb = static_cast<char *>(ws);
     float *scores = reinterpret_cast<float *>(wb + w.scores);
     int *ids = sel_ids_out ? sel_ids_out : reinterpret_cast<int *>(wb + w.sel_ids);
@@ -863,7 +911,15 @@ static ts_status decode_step_impl(const ts_layout *L, const void *q, const void 
     const cudaStream_t st = as_stream(stream);
     const int rows = L->batch * L->num_kv_heads;
     static const int two_kernels = getenv("TS_TWO_KERNELS") ? atoi(getenv("TS_TWO_KERNELS")) : 0;
-    if (L->kv_dtype == TS_BF16 && group_of(L) <= 8 && L->head_dim == 64 && !two_kernels &&
+    if (f8 && k_new && rows > 0) {  // FP8 append: its own kernel, then the one-launch step
+        if ((s = meta_append_impl(L, k_new, v_new, const_cast<int32_t *>(seq_lens), -1, page_table,
+                                  const_cast<void *>(k_pool), const_cast<void *>(v_pool),
+                                  const_cast<void *>(meta), stream)) != TS_OK)
+            return s;
+        k_new = v_new = nullptr;
+    }
+    const int f8_pre = g_launches;  // the FP8 append kernel, if it ran
+    if ((f8 || (L->kv_dtype == TS_BF16 && !two_kernels)) && group_of(L) <= 8 && L->head_dim == 64 &&
         L->page_size % 16 == 0 && rows > 0) {
         // the whole step in one cluster-per-row kernel (step_cluster.cuh)
         ScoreSelParams sp{};
@@ -892,6 +948,10 @@ static ts_status decode_step_impl(const ts_layout *L, const void *q, const void 
 
         AttnParams ap = attn_params(L, q, k_pool, v_pool, page_table, seq_lens, ids, cnt, kmax, scale,
                                     o, lse, ws);
+        if (f8) {
+            ap.k_exp = f8_exps(k_pool, L);
+            ap.v_exp = f8_exps(v_pool, L);
+        }
         phase_mark(0, st);
         // ring depth: 8 stages (64 KB in flight per CTA) when the rows leave SMs for wide
         // clusters (measured: C3 / C5 faster); 4 stages when many rows need >= 3 CTAs per SM
@@ -899,8 +959,8 @@ static ts_status decode_step_impl(const ts_layout *L, const void *q, const void 
         const int ring = ring_env ? ring_env : (L->batch * L->num_kv_heads <= device_sms() ? 8 : 4);
         s = ring == 8 ? launch_step_cluster_t<4, 8>(L, sp, ap, st) : launch_step_cluster_t<4, 4>(L, sp, ap, st);
         phase_mark(3, st);
-        if (s != TS_ERR_UNSUPPORTED) {
-            g_launches = 1;
+        if (s != TS_ERR_UNSUPPORTED || f8) {
+            g_launches = f8_pre + 1;
             return s;
         }
     }
@@ -978,6 +1038,29 @@ ts_status ts_dense_decode_attn(const ts_layout *L, const void *q, const void *k_
     static const int rr = getenv("TS_SA_R") ? atoi(getenv("TS_SA_R")) : 8;
     if (rr == 16) return launch_sat<4, 16>(L, p, true, as_stream(stream));
     return launch_sat<4, 8>(L, p, true, as_stream(stream));
+}
+
+// FP8 KV storage (reading R21): quantise `rows` bf16 rows of head_dim 64.
+ts_status ts_kv_quantize(int64_t rows, int32_t head_dim, const void *src, void *codes, void *exps,
+                         void *stream) {
+    g_launches = 0;
+    if (rows < 0 || head_dim < 1) return TS_ERR_CONFIG;
+    if (head_dim != 64) return TS_ERR_UNSUPPORTED;
+    if (!aligned16(src) || (reinterpret_cast<uintptr_t>(codes) & 7u)) return TS_ERR_ALIGN;
+    if (rows == 0) return TS_OK;
+    const long long thr = rows * 8;
+    const int grid = (int)std::min<long long>((thr + 255) / 256, (long long)device_sms() * 16);
+    launch_pdl(kv_quantize_kernel, dim3(grid), dim3(256), 0, as_stream(stream), (long long)rows,
+               (const uint16_t *)src, (uint8_t *)codes, (int8_t *)exps);
+    ++g_launches;
+    return launch_status();
+}
+
+size_t ts_pool_bytes(const ts_layout *L) {
+    if (check_layout(L) != TS_OK) return 0;
+    const size_t n = (size_t)L->num_blocks * L->num_kv_heads * L->page_size;
+    if (L->kv_dtype == TS_FP8E4M3) return n * (L->head_dim + 1);
+    return n * L->head_dim * (L->kv_dtype == TS_BF16 ? 2 : 4);
 }
 
 ts_status ts_select_merge(const float *cand_scores, const int32_t *cand_ids, int32_t parts,

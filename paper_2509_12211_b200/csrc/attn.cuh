@@ -36,6 +36,8 @@ struct AttnParams {
     int splits, items;
     unsigned long long *dbg;  // development: per-CTA globaltimer stamps (nullable)
     int dense;                // 1: attend every page (FullCache baseline), sel_* unused
+    const int8_t *k_exp;      // FP8 KV (reading R21): row exponents [NB][Hkv][S] (else null)
+    const int8_t *v_exp;
 };
 
 constexpr int kAttnD = 64;        // head_dim of the tensor-core path

@@ -4,6 +4,7 @@
 #pragma once
 #include <cooperative_groups.h>
 #include <cuda.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -65,6 +66,16 @@ TS_DEV uint4 lds_v4(uint32_t saddr) {
     asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
                  : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                  : "r"(saddr));
+    return r;
+}
+TS_DEV uint2 lds_v2(uint32_t saddr) {
+    uint2 r;
+    asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "r"(saddr));
+    return r;
+}
+TS_DEV int lds_s8(uint32_t saddr) {
+    int r;
+    asm volatile("ld.shared.s8 %0, [%1];" : "=r"(r) : "r"(saddr));
     return r;
 }
 TS_DEV void sts_v4(uint32_t saddr, uint4 v) {
@@ -198,6 +209,22 @@ TS_DEV void mma_bf16_16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
         "{%8,%9}, {%0,%1,%2,%3};"
         : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
         : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+// D[16x8] += A[16x16] * B[16x8], f16 inputs, fp32 accumulate (the FP8 KV path: E4M3 codes
+// widen exactly to f16).
+TS_DEV void mma_f16_16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                          uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+        "{%8,%9}, {%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+// two fp32 -> packed f16x2 (lo = element 0), round to nearest even
+TS_DEV uint32_t f16x2_pack(float lo, float hi) {
+    uint32_t r;
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    return r;
 }
 // D[16x8] += A[16x8] * B[8x8], tf32 inputs (fp32 bit patterns), fp32 accumulate.
 TS_DEV void mma_tf32_1688(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,

@@ -20,6 +20,7 @@
 #pragma once
 #include "attn.cuh"
 #include "common.cuh"
+#include "fp8.cuh"
 #include "score_select.cuh"
 #include "sparse_attn.cuh"
 
@@ -51,13 +52,24 @@ struct ScSmem {
     }
 };
 
-template <int W, int R, bool DSM, bool APP>
+// FP8 KV (F8, reading R21): the attention stage holds the K and V code tiles (16 tokens x
+// 64 B, 64-byte swizzle) and their 16 + 16 row exponents, kF8Stage bytes (512-aligned).
+constexpr int kF8Stage = 2560;
+// token of k-slot n (0..7) of an 8-token MMA group in the FP8 consumer: chosen so that a
+// lane's 128-bit K-row reads and 64-bit V-row reads are both bank-conflict free under the
+// 64-byte swizzle (bit 0 = n0 ^ n1, bit 1 = n0, bit 2 = n2)
+TS_DEV int f8_tok(int n) { return ((n ^ (n >> 1)) & 1) | ((n & 1) << 1) | (n & 4); }
+
+template <int W, int R, bool DSM, bool APP, bool F8 = false>
 __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
     const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
     ScoreSelParams p, AttnParams ap) {
     using SM = ScSmem<W, R>;
     constexpr int NT = SM::NT;
-    constexpr int RA = 2 * R;  // attention stages (4 KB)
+    // attention stages: 4 KB (bf16) / kF8Stage (FP8) slots over the scoring ring's bytes
+    constexpr int RA = F8 ? (R * kSsStageBytes / kF8Stage) / W * W : 2 * R;
+    static_assert(!F8 || RA <= 4 * R, "FP8 stage barriers must fit the afull / aempty slots");
+    static_assert(!(F8 && APP), "the FP8 append runs as its own kernel");
     static_assert(R % W == 0 && RA % W == 0, "stage -> consumer warp must be fixed");
     extern __shared__ uint8_t sc_raw[];
     // 1024-byte aligned (TMA swizzle atoms) by pointer arithmetic on the __shared__ array
@@ -288,9 +300,14 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
         const int a0 = kp * rank / C, a1 = kp * (rank + 1) / C;
         for (int e = tid; e < 2 * (a1 - a0); e += NT) {
             const int brow = sel[e >> 1].x;
-            if (brow >= 0)
-                prefetch_l2_bulk(((e & 1) ? p.v_pool : p.k_pool) + (size_t)brow * p.S * kAttnD,
-                                 (uint32_t)p.S * kRowBytes);
+            if (brow >= 0) {
+                if constexpr (F8)  // the code rows only (the exponents are 1/64 of it)
+                    prefetch_l2_bulk(reinterpret_cast<const uint8_t *>((e & 1) ? p.v_pool : p.k_pool) +
+                                         (size_t)brow * p.S * kAttnD, (uint32_t)p.S * kAttnD);
+                else
+                    prefetch_l2_bulk(((e & 1) ? p.v_pool : p.k_pool) + (size_t)brow * p.S * kAttnD,
+                                     (uint32_t)p.S * kRowBytes);
+            }
         }
     }
 
@@ -412,6 +429,184 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
         // own K / V tiles (stage i -> warp i % W, slot i % RA, RA % W == 0), so a slot is
         // re-issued by its owner right after it is consumed and a CTA has W issuing warps
         // (a single issuing lane caps a CTA's 2 KB-tile gather at ~21 GB/s: scripts/gatherbench.cu)
+    } else if constexpr (F8) {
+        // ---- FP8 KV (reading R21): per tile, S = Q K^T over the E4M3 codes (widened exactly
+        // to f16) times 2^e_k per token; the online softmax keeps the V accumulator relative to
+        // (running max + running max V exponent E) so that P' = P * 2^(e_v - E) <= 1 enters
+        // the f16 P.V MMA as an exact-enough hi + lo pair; 2^E is applied at the end.
+        // q: per head power-of-two prescale (|q'| in [2^14, 2^15)): bf16 q is exact in f16.
+        uint32_t qh[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // f16x2 of q' channels 16t + {2i, 2i+1}
+        float qsc = 0.f;                             // scale * log2(e) * 2^sq
+        {
+            uint4 x0 = make_uint4(0, 0, 0, 0), x1 = x0;
+            if (gid < p.G) {
+                const uint32_t qrow = sb + SM::kQ + gid * kRowBytes + 32 * t;
+                x0 = lds_v4(qrow);
+                x1 = lds_v4(qrow + 16);
+            }
+            const uint32_t w[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+            float am = 0.f;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) am = fmaxf(am, fmaxf(fabsf(bf16lo_to_f32(w[i])), fabsf(bf16hi_to_f32(w[i]))));
+            am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, 1));
+            am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, 2));
+            const int ea = int(__float_as_uint(am) >> 23) - 127;  // floor(log2 am) for normal am
+            const int sq = am > 0.f ? min(max(ea - 14, -100), 100) : 0;
+            const float s = pow2i(-sq);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) qh[i] = f16x2_pack(bf16lo_to_f32(w[i]) * s, bf16hi_to_f32(w[i]) * s);
+            qsc = sl2 * pow2i(sq);
+        }
+        fence_proxy_async();  // the ring was last accessed by the generic proxy (scoring)
+        const uint64_t pol = l2_policy_evict_first();
+        const int ntl = t1 - t0;
+        const int8_t *kexp = ap.k_exp, *vexp = ap.v_exp;
+        // lane 4e + c issues part c (K codes, V codes, K exponents, V exponents) of the warp's
+        // e-th stage
+        auto issue_f8 = [&](int i, int c) {
+            const int st = i % RA;
+            const int tl = t0 + i, u = tl >> tps, sub = tl & (tpp - 1);
+            const int row0 = sel[u - u0].x + 16 * sub;  // pool row of the tile's first token
+            const uint32_t dst = sb + st * kF8Stage;
+            if (c < 2)
+                tma_load_2d(dst + c * 1024, c ? &tmV : &tmK, 0, row0, afull0 + 8 * st, pol);
+            else
+                bulk_load(dst + 2048 + (c - 2) * 16, (c == 2 ? kexp : vexp) + row0, 16, afull0 + 8 * st);
+        };
+        {
+            const int e = lane >> 2, i = warp + W * e;
+            if (e < RA / W && i < ntl) {
+                if ((lane & 3) == 0) mbar_arrive_expect_tx(afull0 + 8 * (i % RA), 2 * 1024 + 32);
+                issue_f8(i, lane & 3);
+            }
+        }
+        float m = kNegInf, lp = 0.f;
+        int E = -128;  // running max V exponent of the attended tokens (-128: none yet)
+        float oacc[8][4];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) oacc[j][0] = oacc[j][1] = oacc[j][2] = oacc[j][3] = 0.f;
+        // this lane's 4 tokens of a tile: k-slots 2t + q2 of MMA group nt
+        int trow[2][2];
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+            for (int q2 = 0; q2 < 2; ++q2) trow[nt][q2] = nt * 8 + f8_tok(2 * t + q2);
+        for (int i = warp; i < ntl; i += W) {
+            const int st = i % RA;
+            const int tl = t0 + i, tu = tl >> tps;
+            const int tok0 = sel[tu - u0].y + 16 * (tl & (tpp - 1));
+            mbar_wait(afull0 + 8 * st, (i / RA) & 1);
+            const uint32_t kb = sb + st * kF8Stage, vb = kb + 1024, eb = kb + 2048;
+            float sacc[2][4];
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) {
+                sacc[nt][0] = sacc[nt][1] = sacc[nt][2] = sacc[nt][3] = 0.f;
+                const int r = nt * 8 + f8_tok(gid);  // B column gid = this K row
+                const uint4 k = lds_v4(kb + r * 64 + ((t ^ ((r >> 1) & 3)) << 4));
+                const uint32_t kw[4] = {k.x, k.y, k.z, k.w};
+#pragma unroll
+                for (int kc = 0; kc < 4; ++kc)
+                    mma_f16_16816(sacc[nt], qh[2 * kc], 0u, qh[2 * kc + 1], 0u, f8x2_to_f16x2(kw[kc] & 0xffffu),
+                                  f8x2_to_f16x2(kw[kc] >> 16));
+            }
+            float x[2][2];
+            bool ok[2][2];
+            int ev[2][2];
+            float tmax = kNegInf;
+            int evmax = -128;
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                for (int q2 = 0; q2 < 2; ++q2) {
+                    const int r = trow[nt][q2];
+                    ok[nt][q2] = tok0 + r < L;
+                    const int ek = lds_s8(eb + r);
+                    ev[nt][q2] = lds_s8(eb + 16 + r);
+                    x[nt][q2] = ok[nt][q2] ? sacc[nt][q2] * qsc * pow2i(ek) : kNegInf;
+                    tmax = fmaxf(tmax, x[nt][q2]);
+                    if (ok[nt][q2]) evmax = max(evmax, ev[nt][q2]);
+                }
+            tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 1));
+            tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 2));
+            evmax = max(evmax, __shfl_xor_sync(0xffffffffu, evmax, 1));
+            evmax = max(evmax, __shfl_xor_sync(0xffffffffu, evmax, 2));
+            const int En = max(E, evmax);
+            const float mnew = fmaxf(m, tmax);
+            const float mref = mnew == kNegInf ? 0.f : mnew;
+            const float corr = exp2f(m - mref);
+            const float corr_o = corr * exp2f((float)(E - En));
+            m = mnew;
+            E = En;
+            float pr[2][2];
+            float psum = 0.f;
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                for (int q2 = 0; q2 < 2; ++q2) {
+                    const float pw = exp2f(x[nt][q2] - mref);
+                    psum += pw;
+                    const int de = ev[nt][q2] - E;  // <= 0 for attended tokens
+                    pr[nt][q2] = ok[nt][q2] && de >= -126 ? pw * pow2i(de) : 0.f;
+                }
+            lp = lp * corr + psum;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                oacc[j][0] *= corr_o;
+                oacc[j][1] *= corr_o;
+            }
+            // A = P' (rows = heads, k-slots = this lane's tokens), hi + lo f16 parts
+            const uint32_t ah0 = f16x2_pack(pr[0][0], pr[0][1]), ah2 = f16x2_pack(pr[1][0], pr[1][1]);
+            const float2 h0 = __half22float2(*reinterpret_cast<const __half2 *>(&ah0));
+            const float2 h2 = __half22float2(*reinterpret_cast<const __half2 *>(&ah2));
+            const uint32_t al0 = f16x2_pack(pr[0][0] - h0.x, pr[0][1] - h0.y);
+            const uint32_t al2 = f16x2_pack(pr[1][0] - h2.x, pr[1][1] - h2.y);
+            // B = V codes: 8 channels (8 gid .. 8 gid + 7) of this lane's 4 token rows
+            uint2 vr[2][2];
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                for (int q2 = 0; q2 < 2; ++q2) {
+                    const int r = trow[nt][q2];
+                    const uint2 v = lds_v2(vb + r * 64 + ((((gid >> 1) ^ ((r >> 1) & 3))) << 4) + (gid & 1) * 8);
+                    vr[nt][q2] = ok[nt][q2] ? v : make_uint2(0, 0);  // past seq_len: may be anything
+                }
+#pragma unroll
+            for (int jp = 0; jp < 4; ++jp) {  // channel pairs (2 jp, 2 jp + 1)
+                const uint32_t sel_ = (jp & 1) ? 0x7362u : 0x5140u;
+                const uint32_t a0 = jp < 2 ? vr[0][0].x : vr[0][0].y, a1 = jp < 2 ? vr[0][1].x : vr[0][1].y;
+                const uint32_t c0 = jp < 2 ? vr[1][0].x : vr[1][0].y, c1 = jp < 2 ? vr[1][1].x : vr[1][1].y;
+                const uint32_t pb0 = __byte_perm(a0, a1, sel_), pb1 = __byte_perm(c0, c1, sel_);
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int j = 2 * jp + h;
+                    const uint32_t b0 = f8x2_to_f16x2(h ? pb0 >> 16 : pb0 & 0xffffu);
+                    const uint32_t b1 = f8x2_to_f16x2(h ? pb1 >> 16 : pb1 & 0xffffu);
+                    mma_f16_16816(oacc[j], ah0, 0u, ah2, 0u, b0, b1);
+                    mma_f16_16816(oacc[j], al0, 0u, al2, 0u, b0, b1);
+                }
+            }
+            __syncwarp();
+            if (lane < 4 && i + RA < ntl) {  // refill this warp's slot with stage i + RA
+                fence_proxy_async();
+                if (lane == 0) mbar_arrive_expect_tx(afull0 + 8 * st, 2 * 1024 + 32);
+                issue_f8(i + RA, lane);
+            }
+        }
+        lp += __shfl_xor_sync(0xffffffffu, lp, 1);
+        lp += __shfl_xor_sync(0xffffffffu, lp, 2);
+        if (gid < p.G) {
+            const float s2e = E > -128 ? pow2i(E) : 1.f;  // back from the V-exponent reference
+            float *wr = wpart + (warp * 8 + gid) * kSaPart;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                wr[16 * t + j] = oacc[j][0] * s2e;
+                wr[16 * t + 8 + j] = oacc[j][1] * s2e;
+            }
+            if (t == 0) {
+                wr[kAttnD] = m;
+                wr[kAttnD + 1] = lp;
+            }
+        }
     } else {
         uint32_t qa[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         if (gid < p.G) {
