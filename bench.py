@@ -151,14 +151,18 @@ def kernel_bytes(cfg, L: int, Kmax: int, mp_local: int, world: int = 1):
     return {"score": score, "select": select, "attn": attn, "total": score + select + attn}
 
 
-def build_replica(ts, cfg, seed, device, world=1, rank=0):
+def build_replica(ts, cfg, seed, device, world=1, rank=0, kv=""):
     case = synth.make_case(cfg, seed=seed, device=device)
     pt = case["page_table"]
     if world > 1 and cfg.name == "c5":
         from paper_2509_12211_b200 import sharded
         pt = sharded.shard_page_table(pt, world, rank)
+    shape = tuple(case["k_pool"].shape)
+    if kv == "fp8":  # FP8 cache (reading R21): quantised once on the GPU (ts_kv_quantize)
+        case["k_pool"] = ts.kv_quantize(case["k_pool"])
+        case["v_pool"] = ts.kv_quantize(case["v_pool"])
     L = ts.make_layout(case["q"], case["k_pool"], pt, world if cfg.name == "c5" else 1,
-                       rank if cfg.name == "c5" else 0)
+                       rank if cfg.name == "c5" else 0, pool_shape=shape if kv == "fp8" else None)
     meta = ts.meta_build(L, case["k_pool"], pt, case["seq_lens"])
     rep = dict(case, page_table=pt, layout=L, meta=meta)
     B, Hq, Hkv, d = cfg.batch, cfg.num_q_heads, cfg.num_kv_heads, cfg.head_dim
@@ -291,6 +295,8 @@ def main():
                     help="on one GPU: time one rank's share of an N-GPU c4 / c5 run")
     ap.add_argument("--no-spread", action="store_true", help="skip the p10/p90 + warm-L2 replays")
     ap.add_argument("--no-reuse", action="store_true", help="skip the NEXT-2 cross-step reuse leg")
+    ap.add_argument("--kv", default="bf16", choices=["bf16", "fp8"],
+                    help="KV storage: bf16, or FP8 E4M3 with per-row power-of-two scales (NEXT-3)")
     ap.add_argument("--reuse-alpha", type=float, default=0.1,
                     help="query drift of the reuse leg (synth.drift_queries)")
     args = ap.parse_args()
@@ -342,16 +348,19 @@ def main():
     Kmax = min(cfg.max_pages, max(1, cfg.budget_tokens // cfg.page_size))
     mp_local = -(-cfg.max_pages // sw) if seq else cfg.max_pages
     kb = kernel_bytes(cfg, L_ctx, Kmax, mp_local, sw)
-    alg = synth.algorithmic_bytes(cfg, [L_ctx] * cfg.batch)
+    kvq = "fp8" if args.kv == "fp8" else ""
+    if kvq and (seq or cfg.dtype != "bf16"):
+        raise SystemExit("bench.py: --kv fp8 runs the unsharded bf16-config step only")
+    alg = synth.algorithmic_bytes(cfg, [L_ctx] * cfg.batch, kv=kvq)
     step_bytes = alg["total"] if not seq else kb["total"]
     R = args.replicas or max(2, -(-4 * l2 // max(1, step_bytes)))
     # every replica holds a whole pool (K + V): keep them within ~60 GB of the 180 GB HBM
     pool_bytes = cfg.batch * cfg.max_pages * cfg.num_kv_heads * cfg.page_size * cfg.head_dim * 2 * (
-        2 if cfg.dtype == "bf16" else 4)
+        2 if cfg.dtype == "bf16" else 4)  # (bf16 staging of an FP8 cache: the same bound)
     R = max(2, min(R, int(60e9 // max(1, pool_bytes)))) if not args.replicas else R
     stream = torch.cuda.Stream(device=dev)
 
-    reps = [build_replica(ts, cfg, seed=1000 * rank + r, device=dev, world=sw, rank=sr)
+    reps = [build_replica(ts, cfg, seed=1000 * rank + r, device=dev, world=sw, rank=sr, kv=kvq)
             for r in range(R)]
     torch.cuda.synchronize()
 
@@ -538,7 +547,8 @@ def main():
     dense = None
     try:
         dense = dense_leg(ts, cfg, reps, R, stream, dev, args, ms_per_step) if (
-            use_graph and not args.no_dense and cfg.dtype == "bf16" and cfg.page_size % 16 == 0) else None
+            use_graph and not args.no_dense and cfg.dtype == "bf16" and cfg.page_size % 16 == 0
+            and not kvq) else None
     except Exception as ex:  # noqa: BLE001 — the baseline is context; never fail the bench on it
         dense = {"unavailable": f"{type(ex).__name__}: {ex}"}
     # ---- NEXT-2 cross-step reuse on a drifting-query workload (labelled leg, not the headline)
@@ -592,7 +602,15 @@ def main():
             sample += f"; 1 of the {cfg.batch} sequences, steps/s scaled to the batch"
         else:
             host = {k: reps[0][k].cpu() for k in ("q", "k_pool", "v_pool", "page_table", "seq_lens")}
+            if kvq:  # the oracle's FP8 step: exact dequantisation, then the float64 step
+                nbk = reps[0]["layout"].num_blocks
+                for kk in ("k_pool", "v_pool"):
+                    c_, e_ = ts.fp8_views(host[kk], nbk, cfg.num_kv_heads, cfg.page_size, cfg.head_dim)
+                    host[kk] = torch.from_numpy(oracle.kv_dequantize(c_.numpy(), e_.numpy()))
+                host["q"] = host["q"].float()
             v, cores, sample, extras = oracle_rate(cfg, host, args.oracle_seconds)
+            if kvq:
+                sample += "; FP8 cache: codes dequantised exactly to fp32 first (untimed)"
         # whole job: every rank's batch (weak) or the one global batch (strong)
         v_job = v * world if scaling == "weak" else (
             v if seq else v * (cfg.batch / (args.batch or synth.config(args.config).batch)))
@@ -662,11 +680,13 @@ def main():
         "metric": "decode steps/s", "value": value, "unit": "steps/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
         "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
-        "dtype": cfg.dtype, "data": "synthetic",
+        "dtype": "fp8e4m3-kv" if kvq else cfg.dtype, "data": "synthetic",
         "config": config_json(cfg, world, mode, {
             "slice_of_gpus": args.slice if mode.endswith("-slice") else None,
             "replicas": R, "l2_bytes": l2, "l2_policy": "rotate R cold replicas (R*bytes >= 4*L2)",
-            "graph": "R steps per CUDA graph replay" if use_graph else False}),
+            "graph": "R steps per CUDA graph replay" if use_graph else False,
+            "kv_storage": ("fp8 e4m3 codes + one power-of-two exponent byte per row (reading R21); "
+                           "q / metadata bf16, fp32 compute") if kvq else cfg.dtype}),
         "tokens_per_s": value * cfg.batch,
         "hbm_gbs": gbs, "frac_of_8tbs": gbs / PEAK_SPEC_GBS, "frac_of_measured": gbs / peak,
         "algorithmic_bytes_per_step": step_bytes, "kernel_bytes": kb,

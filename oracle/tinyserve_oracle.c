@@ -400,17 +400,23 @@ double or_e4m3_value(uint8_t c) {
     return s ? -v : v;
 }
 
-/* Nearest E4M3 code to x: brute force over the 127 non-negative finite codes, ties to the
- * even code (mantissa LSB 0), |x| > 448 saturates; the sign bit is x's. */
+/* Nearest E4M3 code to x, ties to the even code (mantissa LSB 0), |x| > 448 saturates; the
+ * sign bit is x's.  The non-negative finite codes 0..126 have increasing values, so the
+ * answer is the lower or the upper neighbour of |x| among them (found by bisection). */
 uint8_t or_e4m3_round(double x) {
     const double a = fabs(x);
-    int best = 0;
-    double bd = INFINITY;
-    for (int c = 0; c <= 126; ++c) {
-        const double dlt = fabs(or_e4m3_value((uint8_t)c) - a);
-        if (dlt < bd || (dlt == bd && (c & 1) == 0)) { bd = dlt; best = c; }
+    int best;
+    if (a >= 448.0) {
+        best = 126;                                    /* saturate (0x7e = 448) */
+    } else {
+        int lo = 0, hi = 126;                          /* value(lo) <= a < value(hi) */
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) / 2;
+            if (or_e4m3_value((uint8_t)mid) <= a) lo = mid; else hi = mid;
+        }
+        const double dl = a - or_e4m3_value((uint8_t)lo), dh = or_e4m3_value((uint8_t)hi) - a;
+        best = (dl < dh || (dl == dh && (lo & 1) == 0)) ? lo : hi;
     }
-    if (a > 448.0) best = 126;                         /* saturate (0x7e = 448) */
     return (uint8_t)(best | (signbit(x) ? 0x80 : 0));
 }
 

@@ -77,8 +77,10 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
     uint8_t *smem = sc_raw + ((1024u - (smem_u32(sc_raw) & 1023u)) & 1023u);
     const uint32_t sb = smem_u32(smem);
     const uint32_t mfull0 = sb + SM::kBars, mempty0 = mfull0 + 8 * R;
-    const uint32_t afull0 = mempty0 + 8 * R, aempty0 = afull0 + 8 * RA;
-    const uint32_t qbar = aempty0 + 8 * RA, ptbar = qbar + 8;
+    // barrier slots (6R + 2): mfull[R], mempty[R], afull[2R], aempty[2R], q, pt; the FP8
+    // attention stages (RA <= 4R) use the afull and (otherwise unused) aempty slots
+    const uint32_t afull0 = mempty0 + 8 * R, aempty0 = afull0 + 8 * 2 * R;
+    const uint32_t qbar = aempty0 + 8 * 2 * R, ptbar = qbar + 8;
     const int mp4 = (p.max_pages + 3) & ~3;
     float *sc = reinterpret_cast<float *>(smem + SM::scores_off(p.kmax));
     const bool pt_bulk = p.flags & 1, two = (p.flags & 2) && p.C > 1;

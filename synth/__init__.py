@@ -192,7 +192,7 @@ def resample_q_rows(case: dict, rows, attempt: int) -> None:
         q[b, g * G:(g + 1) * G, :] = new.to(q.dtype).to(q.device)
 
 
-def algorithmic_bytes(cfg: Config, seq_lens, out_bytes: int = 4) -> dict:
+def algorithmic_bytes(cfg: Config, seq_lens, out_bytes: int = 4, kv: str = "") -> dict:
     """Bytes the method must move per decode step, by term.
 
     Counts: metadata of every page (2*d*e per (page, kv-head)), the K and V rows of the
@@ -203,6 +203,9 @@ def algorithmic_bytes(cfg: Config, seq_lens, out_bytes: int = 4) -> dict:
     """
     e = 2 if cfg.dtype == "bf16" else 4
     S, d, Hkv, Hq = cfg.page_size, cfg.head_dim, cfg.num_kv_heads, cfg.num_q_heads
+    # bytes of one stored K (or V) row: d elements, or d E4M3 codes + 1 exponent byte for
+    # an FP8 cache (reading R21; q and metadata stay bf16)
+    row = d + 1 if kv == "fp8" else d * e
     meta = kv = pt = ids = 0
     for L in seq_lens:
         L = int(L)
@@ -210,7 +213,7 @@ def algorithmic_bytes(cfg: Config, seq_lens, out_bytes: int = 4) -> dict:
         K = min(P, max(1, cfg.budget_tokens // S))
         meta += Hkv * P * 2 * d * e
         toks = min(K * S, L)
-        kv += Hkv * toks * 2 * d * e
+        kv += Hkv * toks * 2 * row
         pt += P * 4
         ids += Hkv * K * 4
     B = len(seq_lens)

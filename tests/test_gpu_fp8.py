@@ -80,11 +80,11 @@ def deq_case(case, orc_q):
 
 def enforce_fp8(case, orc_q, budget, rel=1e-4):
     """oracle.margin's rule on the dequantised cache (redraws q rows only)."""
-    cv = deq_case(case, orc_q)
-    kc, ke, vc, ve = orc_q
+    cv = deq_case(case, orc_q)  # dequantised once (= oracle.decode_step_fp8's first step)
     for attempt in range(64):
-        ref = oracle.decode_step_fp8(case["q"], kc, ke, vc, ve, case["page_table"], case["seq_lens"],
-                                     budget, case["cfg"].scale, want_scores=True)
+        qf = torch.from_numpy(oracle.widen(case["q"]).astype(np.float32))
+        ref = oracle.decode_step(qf, cv["k_pool"], cv["v_pool"], case["page_table"], case["seq_lens"],
+                                 budget, case["cfg"].scale, want_scores=True)
         bad, _ = oracle.margin.violations(cv, budget, rel, ref=ref)
         if not bad:
             return ref
@@ -164,9 +164,11 @@ def test_meta_append_fp8_incremental(ts):
     vc, ve = oracle.kv_quantize(case["v_pool"])
     gkc, gke = ts.fp8_views(kq, nb, Hkv, S, d)
     gvc, gve = ts.fp8_views(vq, nb, Hkv, S, d)
-    used = np.unique(ptn[:, : -(-cfg.ctx // S)])
-    assert np.array_equal(gkc.cpu().numpy()[used], kc[used]) and np.array_equal(gke.cpu().numpy()[used], ke[used])
-    assert np.array_equal(gvc.cpu().numpy()[used], vc[used]) and np.array_equal(gve.cpu().numpy()[used], ve[used])
+    written = [(ptn[b, t // S], t % S) for b in range(cfg.batch) for t in range(cfg.ctx)]
+    blk = np.array([w[0] for w in written])
+    slot = np.array([w[1] for w in written])
+    for g_, o_ in ((gkc, kc), (gke, ke), (gvc, vc), (gve, ve)):
+        assert np.array_equal(g_.cpu().numpy()[blk, :, slot], o_[blk, :, slot])
     omin, omax = oracle.meta_build(torch.from_numpy(oracle.kv_dequantize(kc, ke)), pt, case["seq_lens"])
     m = oracle.widen(meta.cpu())
     assert np.array_equal(m[:, :, :, 0], omin) and np.array_equal(m[:, :, :, 1], omax)

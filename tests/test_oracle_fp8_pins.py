@@ -52,6 +52,22 @@ def test_e4m3_round_matches_torch_on_every_bf16(orc):
     assert np.array_equal(mine, ref)
 
 
+def test_e4m3_round_equals_brute_force_nearest(orc):
+    """The bisection equals the plain definition: the nearest of all 127 finite magnitudes,
+    ties to the even code."""
+    vals = [orc.e4m3_value(c) for c in range(127)]
+    rng = np.random.default_rng(3)
+    xs = np.concatenate([rng.uniform(0, 470, 3000), rng.uniform(0, 2.0 ** -5, 2000),
+                         np.array(vals), (np.array(vals[:-1]) + np.array(vals[1:])) / 2])
+    for x in xs:
+        d = [abs(v - x) for v in vals]
+        m = min(d)
+        best = min(c for c in range(127) if d[c] == m and (c % 2 == 0 or d.count(m) == 1)) \
+            if x < 448 else 126
+        assert orc.e4m3_round(float(x)) == best, x
+        assert orc.e4m3_round(float(-x)) == best | 0x80, x
+
+
 def test_e4m3_round_matches_torch_on_random_doubles(orc):
     rng = np.random.default_rng(7)
     x = np.concatenate([rng.normal(0, 30, 4000), rng.uniform(-448, 448, 4000),
