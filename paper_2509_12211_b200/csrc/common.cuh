@@ -220,6 +220,14 @@ TS_DEV void mma_f16_16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, 
         : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
         : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
+// two fp32 -> packed bf16x2 (lo = element 0), round to nearest even
+TS_DEV uint32_t bf16x2_pack(float lo, float hi) {
+    uint32_t r;
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    return r;
+}
+// word i of a uint4 (i a compile-time constant after unrolling)
+TS_DEV uint32_t u4_word(const uint4 &v, int i) { return i == 0 ? v.x : (i == 1 ? v.y : (i == 2 ? v.z : v.w)); }
 // two fp32 -> packed f16x2 (lo = element 0), round to nearest even
 TS_DEV uint32_t f16x2_pack(float lo, float hi) {
     uint32_t r;

@@ -472,21 +472,28 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
             const uint32_t dst = sb + st * kF8Stage;
             if (c < 2)
                 tma_load_2d(dst + c * 1024, c ? &tmV : &tmK, 0, row0, afull0 + 8 * st, pol);
+#ifndef TS_F8_NOEXP
             else
                 bulk_load(dst + 2048 + (c - 2) * 16, (c == 2 ? kexp : vexp) + row0, 16, afull0 + 8 * st);
+#endif
         };
         {
             const int e = lane >> 2, i = warp + W * e;
             if (e < RA / W && i < ntl) {
+#ifdef TS_F8_NOEXP
+                if ((lane & 3) == 0) mbar_arrive_expect_tx(afull0 + 8 * (i % RA), 2 * 1024);
+#else
                 if ((lane & 3) == 0) mbar_arrive_expect_tx(afull0 + 8 * (i % RA), 2 * 1024 + 32);
+#endif
                 issue_f8(i, lane & 3);
             }
         }
         float m = kNegInf, lp = 0.f;
         int E = -128;  // running max V exponent of the attended tokens (-128: none yet)
-        float oacc[8][4];
+        // O^T accumulators: oacc[db] = channels (8 gid + 2 db, 8 gid + 2 db + 1) x heads (2t, 2t+1)
+        float oacc[4][4];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) oacc[j][0] = oacc[j][1] = oacc[j][2] = oacc[j][3] = 0.f;
+        for (int j = 0; j < 4; ++j) oacc[j][0] = oacc[j][1] = oacc[j][2] = oacc[j][3] = 0.f;
         // this lane's 4 tokens of a tile: k-slots 2t + q2 of MMA group nt
         int trow[2][2];
 #pragma unroll
@@ -516,14 +523,19 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
             int ev[2][2];
             float tmax = kNegInf;
             int evmax = -128;
+            // row exponents of the tile's 16 tokens: K at eb, V at eb + 16 (8-byte reads per
+            // 8-token group, the lane's bytes picked with PRMT)
+            const uint2 ke0 = lds_v2(eb), ke1 = lds_v2(eb + 8), ve0 = lds_v2(eb + 16), ve1 = lds_v2(eb + 24);
 #pragma unroll
             for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
                 for (int q2 = 0; q2 < 2; ++q2) {
                     const int r = trow[nt][q2];
                     ok[nt][q2] = tok0 + r < L;
-                    const int ek = lds_s8(eb + r);
-                    ev[nt][q2] = lds_s8(eb + 16 + r);
+                    const uint2 kw = nt ? ke1 : ke0, vw = nt ? ve1 : ve0;
+                    const int sb_ = r & 7;
+                    const int ek = int(__byte_perm(kw.x, kw.y, sb_) << 24) >> 24;
+                    ev[nt][q2] = int(__byte_perm(vw.x, vw.y, sb_) << 24) >> 24;
                     x[nt][q2] = ok[nt][q2] ? sacc[nt][q2] * qsc * pow2i(ek) : kNegInf;
                     tmax = fmaxf(tmax, x[nt][q2]);
                     if (ok[nt][q2]) evmax = max(evmax, ev[nt][q2]);
@@ -551,18 +563,20 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
                     pr[nt][q2] = ok[nt][q2] && de >= -126 ? pw * pow2i(de) : 0.f;
                 }
             lp = lp * corr + psum;
+            {  // heads 2t, 2t+1 of this lane's O^T entries: their rescale factors
+                const float c0 = __shfl_sync(0xffffffffu, corr_o, 8 * t), c1 = __shfl_sync(0xffffffffu, corr_o, 8 * t + 4);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                oacc[j][0] *= corr_o;
-                oacc[j][1] *= corr_o;
+                for (int j = 0; j < 4; ++j) {
+                    oacc[j][0] *= c0; oacc[j][1] *= c1; oacc[j][2] *= c0; oacc[j][3] *= c1;
+                }
             }
-            // A = P' (rows = heads, k-slots = this lane's tokens), hi + lo f16 parts
+            // B = P'^T (k = this lane's tokens, n = head gid), hi + lo f16 parts
             const uint32_t ah0 = f16x2_pack(pr[0][0], pr[0][1]), ah2 = f16x2_pack(pr[1][0], pr[1][1]);
             const float2 h0 = __half22float2(*reinterpret_cast<const __half2 *>(&ah0));
             const float2 h2 = __half22float2(*reinterpret_cast<const __half2 *>(&ah2));
             const uint32_t al0 = f16x2_pack(pr[0][0] - h0.x, pr[0][1] - h0.y);
             const uint32_t al2 = f16x2_pack(pr[1][0] - h2.x, pr[1][1] - h2.y);
-            // B = V codes: 8 channels (8 gid .. 8 gid + 7) of this lane's 4 token rows
+            // A = V^T: channels 8 gid .. 8 gid + 7 (8 code bytes) of this lane's 4 token rows
             uint2 vr[2][2];
 #pragma unroll
             for (int nt = 0; nt < 2; ++nt)
@@ -573,38 +587,41 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
                     vr[nt][q2] = ok[nt][q2] ? v : make_uint2(0, 0);  // past seq_len: may be anything
                 }
 #pragma unroll
-            for (int jp = 0; jp < 4; ++jp) {  // channel pairs (2 jp, 2 jp + 1)
-                const uint32_t sel_ = (jp & 1) ? 0x7362u : 0x5140u;
-                const uint32_t a0 = jp < 2 ? vr[0][0].x : vr[0][0].y, a1 = jp < 2 ? vr[0][1].x : vr[0][1].y;
-                const uint32_t c0 = jp < 2 ? vr[1][0].x : vr[1][0].y, c1 = jp < 2 ? vr[1][1].x : vr[1][1].y;
-                const uint32_t pb0 = __byte_perm(a0, a1, sel_), pb1 = __byte_perm(c0, c1, sel_);
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int j = 2 * jp + h;
-                    const uint32_t b0 = f8x2_to_f16x2(h ? pb0 >> 16 : pb0 & 0xffffu);
-                    const uint32_t b1 = f8x2_to_f16x2(h ? pb1 >> 16 : pb1 & 0xffffu);
-                    mma_f16_16816(oacc[j], ah0, 0u, ah2, 0u, b0, b1);
-                    mma_f16_16816(oacc[j], al0, 0u, al2, 0u, b0, b1);
-                }
+            for (int db = 0; db < 4; ++db) {  // channels 8 gid + 2 db (A rows gid) and + 1 (rows gid + 8)
+                const uint32_t sel_ = (db & 1) ? 0x7362u : 0x5140u;
+                const uint32_t p0 = __byte_perm(db < 2 ? vr[0][0].x : vr[0][0].y, db < 2 ? vr[0][1].x : vr[0][1].y, sel_);
+                const uint32_t p1 = __byte_perm(db < 2 ? vr[1][0].x : vr[1][0].y, db < 2 ? vr[1][1].x : vr[1][1].y, sel_);
+                const uint32_t a0 = f8x2_to_f16x2(p0 & 0xffffu), a1 = f8x2_to_f16x2(p0 >> 16);
+                const uint32_t a2 = f8x2_to_f16x2(p1 & 0xffffu), a3 = f8x2_to_f16x2(p1 >> 16);
+                mma_f16_16816(oacc[db], a0, a1, a2, a3, ah0, ah2);
+                mma_f16_16816(oacc[db], a0, a1, a2, a3, al0, al2);
             }
             __syncwarp();
             if (lane < 4 && i + RA < ntl) {  // refill this warp's slot with stage i + RA
                 fence_proxy_async();
+#ifdef TS_F8_NOEXP
+                if (lane == 0) mbar_arrive_expect_tx(afull0 + 8 * st, 2 * 1024);
+#else
                 if (lane == 0) mbar_arrive_expect_tx(afull0 + 8 * st, 2 * 1024 + 32);
+#endif
                 issue_f8(i + RA, lane);
             }
         }
         lp += __shfl_xor_sync(0xffffffffu, lp, 1);
         lp += __shfl_xor_sync(0xffffffffu, lp, 2);
-        if (gid < p.G) {
+        {
             const float s2e = E > -128 ? pow2i(E) : 1.f;  // back from the V-exponent reference
-            float *wr = wpart + (warp * 8 + gid) * kSaPart;
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                wr[16 * t + j] = oacc[j][0] * s2e;
-                wr[16 * t + 8 + j] = oacc[j][1] * s2e;
+            for (int hh = 0; hh < 2; ++hh) {
+                if (2 * t + hh < p.G) {
+                    float *wr = wpart + (warp * 8 + 2 * t + hh) * kSaPart + 8 * gid;
+#pragma unroll
+                    for (int db = 0; db < 4; ++db)
+                        *reinterpret_cast<float2 *>(wr + 2 * db) = make_float2(oacc[db][hh] * s2e, oacc[db][2 + hh] * s2e);
+                }
             }
-            if (t == 0) {
+            if (gid < p.G && t == 0) {
+                float *wr = wpart + (warp * 8 + gid) * kSaPart;
                 wr[kAttnD] = m;
                 wr[kAttnD + 1] = lp;
             }
@@ -641,9 +658,10 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
             }
         }
         float m = kNegInf, lp = 0.f;
-        float oacc[8][4];
+        // O^T accumulators: oacc[db] = channels (8 gid + 2 db, 8 gid + 2 db + 1) x heads (2t, 2t+1)
+        float oacc[4][4];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) oacc[j][0] = oacc[j][1] = oacc[j][2] = oacc[j][3] = 0.f;
+        for (int j = 0; j < 4; ++j) oacc[j][0] = oacc[j][1] = oacc[j][2] = oacc[j][3] = 0.f;
         for (int i = warp; i < t1 - t0; i += W) {
             const int st = i % RA;
             // the tile's first token, from sel[] (complete before the barrier), ahead of the wait
@@ -690,27 +708,36 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
                     psum += pr[nt][q2];
                 }
             lp = lp * corr + psum;
+            {  // heads 2t, 2t+1 of this lane's O^T entries: their rescale factors
+                const float c0 = __shfl_sync(0xffffffffu, corr, 8 * t), c1 = __shfl_sync(0xffffffffu, corr, 8 * t + 4);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                oacc[j][0] *= corr;
-                oacc[j][1] *= corr;
-            }
-#pragma unroll
-            for (int nt = 0; nt < 2; ++nt) {
-                const int q0 = nt * 8 + 2 * t, q1 = q0 + 1;
-                uint4 v0 = lds_v4(vb + q0 * kRowBytes + ((gid ^ (q0 & 7)) << 4));
-                uint4 v1 = lds_v4(vb + q1 * kRowBytes + ((gid ^ (q1 & 7)) << 4));
-                if (tok0 + q0 >= L) v0 = make_uint4(0, 0, 0, 0);  // past seq_len: may be anything
-                if (tok0 + q1 >= L) v1 = make_uint4(0, 0, 0, 0);
-                const uint32_t a0 = f32_to_tf32(pr[nt][0]), a2 = f32_to_tf32(pr[nt][1]);
-                const uint32_t w0[4] = {v0.x, v0.y, v0.z, v0.w};
-                const uint32_t w1[4] = {v1.x, v1.y, v1.z, v1.w};
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    const uint32_t b0 = (j & 1) ? (w0[j >> 1] & 0xffff0000u) : (w0[j >> 1] << 16);
-                    const uint32_t b1 = (j & 1) ? (w1[j >> 1] & 0xffff0000u) : (w1[j >> 1] << 16);
-                    mma_tf32_1688(oacc[j], a0, 0u, a2, 0u, b0, b1);
+                for (int j = 0; j < 4; ++j) {
+                    oacc[j][0] *= c0; oacc[j][1] *= c1; oacc[j][2] *= c0; oacc[j][3] *= c1;
                 }
+            }
+            // O^T += V^T P^T on mma.m16n8k16: B = P^T (k = tokens 2t, 2t+1 | 8+2t, 9+2t, n = head
+            // gid) as a bf16 hi + lo pair (16 significant bits; reading R10), A = V^T (rows =
+            // channels 8 gid + 2 db (+1), k = the same tokens), built from the lane's V rows
+            const uint32_t ph0 = bf16x2_pack(pr[0][0], pr[0][1]), ph1 = bf16x2_pack(pr[1][0], pr[1][1]);
+            const uint32_t pl0 = bf16x2_pack(pr[0][0] - bf16lo_to_f32(ph0), pr[0][1] - bf16hi_to_f32(ph0));
+            const uint32_t pl1 = bf16x2_pack(pr[1][0] - bf16lo_to_f32(ph1), pr[1][1] - bf16hi_to_f32(ph1));
+            uint4 vr[2][2];
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                for (int q2 = 0; q2 < 2; ++q2) {
+                    const int q = nt * 8 + 2 * t + q2;
+                    const uint4 v = lds_v4(vb + q * kRowBytes + ((gid ^ (q & 7)) << 4));
+                    vr[nt][q2] = tok0 + q < L ? v : make_uint4(0, 0, 0, 0);  // past seq_len: may be anything
+                }
+#pragma unroll
+            for (int db = 0; db < 4; ++db) {
+                const uint32_t wa0 = u4_word(vr[0][0], db), wb0 = u4_word(vr[0][1], db);
+                const uint32_t wa1 = u4_word(vr[1][0], db), wb1 = u4_word(vr[1][1], db);
+                const uint32_t a0 = __byte_perm(wa0, wb0, 0x5410), a1 = __byte_perm(wa0, wb0, 0x7632);
+                const uint32_t a2 = __byte_perm(wa1, wb1, 0x5410), a3 = __byte_perm(wa1, wb1, 0x7632);
+                mma_bf16_16816(oacc[db], a0, a1, a2, a3, ph0, ph1);
+                mma_bf16_16816(oacc[db], a0, a1, a2, a3, pl0, pl1);
             }
             __syncwarp();
             if (lane < 2 && i + RA < ntl) {  // refill this warp's slot with stage i + RA
@@ -721,17 +748,19 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
         }
         lp += __shfl_xor_sync(0xffffffffu, lp, 1);
         lp += __shfl_xor_sync(0xffffffffu, lp, 2);
-        if (gid < p.G) {
-            float *wr = wpart + (warp * 8 + gid) * kSaPart;
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                wr[16 * t + j] = oacc[j][0];
-                wr[16 * t + 8 + j] = oacc[j][1];
+        for (int hh = 0; hh < 2; ++hh) {
+            if (2 * t + hh < p.G) {
+                float *wr = wpart + (warp * 8 + 2 * t + hh) * kSaPart + 8 * gid;
+#pragma unroll
+                for (int db = 0; db < 4; ++db)
+                    *reinterpret_cast<float2 *>(wr + 2 * db) = make_float2(oacc[db][hh], oacc[db][2 + hh]);
             }
-            if (t == 0) {
-                wr[kAttnD] = m;
-                wr[kAttnD + 1] = lp;
-            }
+        }
+        if (gid < p.G && t == 0) {
+            float *wr = wpart + (warp * 8 + gid) * kSaPart;
+            wr[kAttnD] = m;
+            wr[kAttnD + 1] = lp;
         }
     }
     __syncthreads();

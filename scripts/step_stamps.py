@@ -5,11 +5,15 @@ import numpy as np, torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__))); sys.path.insert(0, ROOT)
 import synth, paper_2509_12211_b200 as ts
 name = sys.argv[1] if len(sys.argv) > 1 else "c3"
+kv = sys.argv[2] if len(sys.argv) > 2 else "bf16"  # bf16 | fp8
 cfg = synth.config(name); dev = torch.device("cuda:0")
 reps = []
 for r in range(4):
     c = synth.make_case(cfg, seed=5 + r, device=dev)
-    L = ts.make_layout(c["q"], c["k_pool"], c["page_table"])
+    shape = tuple(c["k_pool"].shape)
+    if kv == "fp8":
+        c["k_pool"], c["v_pool"] = ts.kv_quantize(c["k_pool"]), ts.kv_quantize(c["v_pool"])
+    L = ts.make_layout(c["q"], c["k_pool"], c["page_table"], pool_shape=shape if kv == "fp8" else None)
     meta = ts.meta_build(L, c["k_pool"], c["page_table"], c["seq_lens"])
     c.update(L=L, meta=meta, ws=ts.new_workspace(ts.workspace_bytes(L, cfg.budget_tokens), dev))
     reps.append(c)
@@ -17,8 +21,9 @@ b1 = torch.zeros(4096 * 8, dtype=torch.int64, device=dev)
 b2 = torch.zeros(2048 * 8, dtype=torch.int64, device=dev)
 lib = ts._lib.lib()
 lib.ts_debug_timestamps.argtypes = [ctypes.c_void_p]; lib.ts_debug_ss_timestamps.argtypes = [ctypes.c_void_p]
+warm = os.environ.get("STAMP_WARM") == "1"  # every call on replica 0 (L2-resident bytes)
 for it in range(9):
-    c = reps[it % 4]
+    c = reps[0 if warm else it % 4]
     torch.cuda.synchronize(); b1.zero_(); b2.zero_(); torch.cuda.synchronize()
     on = it == 8
     lib.ts_debug_ss_timestamps(b1.data_ptr() if on else None)
@@ -38,7 +43,7 @@ def show(a, names, title):
         col = (col - t0) / 1e3
         print(f"  {n:11s} n {len(col):5d} min {col.min():7.2f} p10 {np.percentile(col,10):7.2f} med {np.median(col):7.2f} p90 {np.percentile(col,90):7.2f} max {col.max():7.2f} us")
 if os.environ.get("TS_TWO_KERNELS", "0") == "0":
-    show(a1, ["start", "scored", "selected", "listed", "consumed", "gathered", "keys", "end"], f"{name} decode_cluster_kernel")
+    show(a1, ["start", "scored", "selected", "listed", "consumed", "gathered", "keys", "end"], f"{name} decode_cluster_kernel ({kv} KV)")
     sys.exit(0)
 show(a1, ["start", "scored", "gathered", "selected", "keys", "pass0", "thresh", "compacted"], f"{name} K1 score_select")
 show(a2, ["start", "flag", "pages", "consumed", "-", "-", "-", "end"] if os.environ.get("TS_SA_TMA", "1") != "0" else ["start", "q", "pages", "loop_end", "cta_merged", "cl_sync1", "out", "cl_sync2"], f"{name} K2 sparse_attn")
