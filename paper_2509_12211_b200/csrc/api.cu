@@ -202,20 +202,6 @@ bool make_pool_map(CUtensorMap *map, const void *pool, const ts_layout *L, int T
               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// FP8 code pool [NB][Hkv][S][64] bytes viewed as NB*Hkv*S rows x 64 bytes; box = TT rows,
-// 64-byte swizzle (the consumer's reads are bank-conflict free under it).
-bool make_pool_map_f8(CUtensorMap *map, const void *pool, const ts_layout *L, int TT) {
-    auto fn = encode_fn();
-    if (!fn) return false;
-    const cuuint64_t dims[2] = {64, (cuuint64_t)f8_rows(L)};
-    const cuuint64_t strides[1] = {64};
-    const cuuint32_t box[2] = {64, (cuuint32_t)TT};
-    const cuuint32_t estr[2] = {1, 1};
-    return fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void *>(pool), dims, strides,
-              box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
-              CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
 // ---------------------------------------------------------------- workspace layout
 // attention workspace: [tickets: rows u32][work counters: 2 u32][partials: rows x ipr x 8 x kPS]
 // with ipr <= kMaxItemsPerRow split parts per row (split-K merge of the attention kernels).
@@ -542,8 +528,8 @@ ts_status launch_step(const ts_layout *L, ScoreSelParams &sp, const AttnParams &
     auto kern = decode_cluster_kernel<W, R, DSM, APP, F8>;
     const int rows = L->batch * L->num_kv_heads;
     CUtensorMap tmK, tmV;
-    if (F8 ? (!make_pool_map_f8(&tmK, ap.k_pool, L, 16) || !make_pool_map_f8(&tmV, ap.v_pool, L, 16))
-           : (!make_pool_map(&tmK, ap.k_pool, L, 16) || !make_pool_map(&tmV, ap.v_pool, L, 16)))
+    // (FP8 tiles are 1-D bulk copies; the maps are then unused placeholders)
+    if (!make_pool_map(&tmK, ap.k_pool, L, 16) || !make_pool_map(&tmV, ap.v_pool, L, 16))
         return TS_ERR_CUDA;
     sp.C = pl.C;
     sp.chunk = pl.chunk;

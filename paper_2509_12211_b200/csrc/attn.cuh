@@ -1,15 +1,18 @@
 // attn.cuh — shared attention definitions + the fp32 CUDA-core path and the LSE merge
 // (SparseAttn PAPER.md:169-172; Alg. 1 Steps 3-4).
 //
-// The bf16 tensor-core path (the hot one) is decode_pipe.cuh.  Its fragment maps, used
-// there, are:
-//   S^T = Q K^T : mma.m16n8k16 bf16; A rows = the G q heads of the kv group (rows >= G are
+// bf16 tensor-core attention (step_cluster.cuh, sparse_attn.cuh) fragment maps, lane =
+// (gid = lane / 4, t = lane % 4):
+//   S = Q K^T   : mma.m16n8k16 bf16; A rows = the G q heads of the kv group (rows >= G are
 //                 zero), k-slot permutation d = 16t + 4s + {0..3} so that a thread's two
-//                 128-bit smem reads of a K row (logical chunks 2t, 2t+1 of the 128-byte
-//                 swizzled row) feed all four k16 steps; B = K^T (n = 8 tokens).
-//   O  += P V   : mma.m16n8k8 tf32; A = P straight from the S accumulators with the token
-//                 order permuted (k slot t <-> token 2t, t+4 <-> 2t+1); B = V, n-tile j <->
-//                 channels {8n + j}, so thread (n, t) reads V rows 2t, 2t+1 chunk n once.
+//                 128-bit smem reads of a K row feed all four k16 steps; B = K^T (n = 8
+//                 tokens).  The lane ends with head gid's scores of tokens 2t, 2t+1 (+8).
+//   O^T += V^T P^T : mma.m16n8k16 (or m16n8k8 for 8-token octets) bf16; B = P^T exactly as
+//                 the lane holds it (k = its tokens, n = head gid) as a hi + lo bf16 pair
+//                 (16 significant bits; reading R10), A = V^T with rows = channels
+//                 8 gid + 2 db (rows gid) and 8 gid + 2 db + 1 (rows gid + 8), built by PRMT
+//                 from the lane's 128-bit reads of its V rows (channels 8 gid .. 8 gid + 7).
+//                 The lane accumulates channels (8 gid + 2 db, + 1) x heads (2t, 2t + 1).
 // fp32 path (attn_simt_kernel): CUDA-core FFMA, one warp per q head, lane-parallel dot
 // products with a fixed shuffle tree (no tf32 anywhere; reading R10).
 #pragma once
@@ -43,6 +46,56 @@ struct AttnParams {
 constexpr int kAttnD = 64;        // head_dim of the tensor-core path
 constexpr int kRowBytes = kAttnD * 2;
 constexpr int kPS = kAttnD + 4;   // floats per (split, head) partial: o[D], m, l, pad (16 B aligned)
+
+// ------------------------------------------------------------------ O^T = V^T P^T helpers
+// rescale the lane's O^T entries (heads 2t, 2t+1) by their heads' factors (held by lanes 4h)
+TS_DEV void ot_rescale(float (&oacc)[4][4], float corr, int t) {
+    const float c0 = __shfl_sync(0xffffffffu, corr, 8 * t), c1 = __shfl_sync(0xffffffffu, corr, 8 * t + 4);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        oacc[j][0] *= c0; oacc[j][1] *= c1; oacc[j][2] *= c0; oacc[j][3] *= c1;
+    }
+}
+// 16-token tile: vr[nt][q2] = the lane's 16-byte read (channels 8 gid .. + 7) of the V row of
+// its k-slot nt * 8 + 2t + q2 (zeroed past seq_len), pr[nt][q2] = that token's weight
+TS_DEV void ot_pv_tile_bf16(float (&oacc)[4][4], const uint4 (&vr)[2][2], const float (&pr)[2][2]) {
+    const uint32_t ph0 = bf16x2_pack(pr[0][0], pr[0][1]), ph1 = bf16x2_pack(pr[1][0], pr[1][1]);
+    const uint32_t pl0 = bf16x2_pack(pr[0][0] - bf16lo_to_f32(ph0), pr[0][1] - bf16hi_to_f32(ph0));
+    const uint32_t pl1 = bf16x2_pack(pr[1][0] - bf16lo_to_f32(ph1), pr[1][1] - bf16hi_to_f32(ph1));
+#pragma unroll
+    for (int db = 0; db < 4; ++db) {
+        const uint32_t wa0 = u4_word(vr[0][0], db), wb0 = u4_word(vr[0][1], db);
+        const uint32_t wa1 = u4_word(vr[1][0], db), wb1 = u4_word(vr[1][1], db);
+        const uint32_t a0 = __byte_perm(wa0, wb0, 0x5410), a1 = __byte_perm(wa0, wb0, 0x7632);
+        const uint32_t a2 = __byte_perm(wa1, wb1, 0x5410), a3 = __byte_perm(wa1, wb1, 0x7632);
+        mma_bf16_16816(oacc[db], a0, a1, a2, a3, ph0, ph1);
+        mma_bf16_16816(oacc[db], a0, a1, a2, a3, pl0, pl1);
+    }
+}
+// 8-token octet (k = tokens 2t, 2t+1 only): mma.m16n8k8
+TS_DEV void ot_pv_octet_bf16(float (&oacc)[4][4], uint4 v0, uint4 v1, float p0, float p1) {
+    const uint32_t ph = bf16x2_pack(p0, p1);
+    const uint32_t pl = bf16x2_pack(p0 - bf16lo_to_f32(ph), p1 - bf16hi_to_f32(ph));
+#pragma unroll
+    for (int db = 0; db < 4; ++db) {
+        const uint32_t wa = u4_word(v0, db), wb = u4_word(v1, db);
+        const uint32_t a0 = __byte_perm(wa, wb, 0x5410), a1 = __byte_perm(wa, wb, 0x7632);
+        mma_bf16_1688(oacc[db], a0, a1, ph);
+        mma_bf16_1688(oacc[db], a0, a1, pl);
+    }
+}
+// the warp's partial for heads 2t, 2t+1 (< G) into wpart[(warp * 8 + h) * ld + channel]
+TS_DEV void ot_store(float *wpart_warp, int ld, const float (&oacc)[4][4], int gid, int t, int G, float s = 1.f) {
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+        if (2 * t + hh < G) {
+            float *wr = wpart_warp + (2 * t + hh) * ld + 8 * gid;
+#pragma unroll
+            for (int db = 0; db < 4; ++db)
+                *reinterpret_cast<float2 *>(wr + 2 * db) = make_float2(oacc[db][hh] * s, oacc[db][2 + hh] * s);
+        }
+    }
+}
 
 // ------------------------------------------------------------------ fp32 CUDA-core path
 // grid = rows (b, g); block = 32 * min(G, 8) threads; warp w handles q heads w, w+8, ...

@@ -1,6 +1,6 @@
 // common.cuh — sm_100a device helpers shared by the TinyServe kernels (product path only).
 // PTX wrappers: mbarrier, TMA tile loads (cp.async.bulk.tensor), legacy-tensor-core
-// mma.sync (bf16 m16n8k16, tf32 m16n8k8), bf16 <-> fp32 bit conversions.
+// mma.sync (bf16 m16n8k16 / m16n8k8, f16 m16n8k16), bf16 / f16 <-> fp32 conversions.
 #pragma once
 #include <cooperative_groups.h>
 #include <cuda.h>
@@ -210,6 +210,14 @@ TS_DEV void mma_bf16_16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
         : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
         : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
+// D[16x8] += A[16x8] * B[8x8], bf16 inputs, fp32 accumulate.
+TS_DEV void mma_bf16_1688(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t b0) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k8.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5}, {%6}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a0), "r"(a1), "r"(b0));
+}
 // D[16x8] += A[16x16] * B[16x8], f16 inputs, fp32 accumulate (the FP8 KV path: E4M3 codes
 // widen exactly to f16).
 TS_DEV void mma_f16_16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
@@ -234,21 +242,6 @@ TS_DEV uint32_t f16x2_pack(float lo, float hi) {
     asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
     return r;
 }
-// D[16x8] += A[16x8] * B[8x8], tf32 inputs (fp32 bit patterns), fp32 accumulate.
-TS_DEV void mma_tf32_1688(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
-                          uint32_t b0, uint32_t b1) {
-    asm volatile(
-        "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
-        "{%8,%9}, {%0,%1,%2,%3};"
-        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
-}
-TS_DEV uint32_t f32_to_tf32(float x) {
-    uint32_t r;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-    return r;
-}
-
 // ---------------------------------------------------------------- misc
 TS_DEV float warp_max(float v) {
 #pragma unroll

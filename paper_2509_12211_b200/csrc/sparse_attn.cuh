@@ -12,9 +12,9 @@
 //    [16t, 16t+16)) and 2 x 16 B of V (tokens 2t, 2t+1, channels [8 gid, 8 gid + 8));
 //  * S = Q K^T on mma.m16n8k16 (bf16 in, fp32 out; A rows = the G q heads, rows >= G
 //    zero; channel permutation d = 16t + 4s + {0..3} so the 32 B of K feed all four
-//    k-steps), fp32 online softmax in exp2, O += P V on mma.m16n8k8 with tf32 P (reading
-//    R10; bf16 V widened exactly; token permutation k-slot t <-> token 2t, t+4 <-> 2t+1
-//    so the lane's two P values are its A fragment and its V rows are the same tokens);
+//    k-steps), fp32 online softmax in exp2, O^T += V^T P^T on mma.m16n8k8 with a hi + lo
+//    bf16 P (reading R10; attn.cuh: the lane's two P values are its B fragment and its V
+//    rows, the same tokens, form the A fragment by PRMT);
 //  * tokens t >= seq_len are masked (score -inf, V zeroed: the tail of a partial page may
 //    hold anything — reading R7);
 //  * warp partials (o, m, l) merge in shared memory, CTA partials across the cluster
@@ -128,9 +128,9 @@ __global__ void __launch_bounds__(W * 32, 512 / (W * 32)) sparse_attn_kernel(Att
     const uint16_t *vp = static_cast<const uint16_t *>(p.v_pool);
     const float sl2 = p.scale * kLog2e;
     float m = kNegInf, lp = 0.f;
-    float oacc[8][4];
+    float oacc[4][4];  // O^T: channels (8 gid + 2 db, + 1) x heads (2t, 2t + 1) (attn.cuh)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) oacc[j][0] = oacc[j][1] = oacc[j][2] = oacc[j][3] = 0.f;
+    for (int j = 0; j < 4; ++j) oacc[j][0] = oacc[j][1] = oacc[j][2] = oacc[j][3] = 0.f;
 
     // octet o -> element offset of its first token row, and its first global token
     auto octet_addr = [&](int o, int &tok0) -> size_t {
@@ -180,37 +180,23 @@ __global__ void __launch_bounds__(W * 32, 512 / (W * 32)) sparse_attn_kernel(Att
             m = mnew;
             const float p0 = exp2f(x0 - mref), p1 = exp2f(x1 - mref);
             lp = lp * corr + p0 + p1;
-            const uint32_t a0 = f32_to_tf32(p0), a2 = f32_to_tf32(p1);
-            const uint4 v0 = vb[j][0], v1 = vb[j][1];
-            const uint32_t w0[4] = {ok0 ? v0.x : 0u, ok0 ? v0.y : 0u, ok0 ? v0.z : 0u, ok0 ? v0.w : 0u};
-            const uint32_t w1[4] = {ok1 ? v1.x : 0u, ok1 ? v1.y : 0u, ok1 ? v1.z : 0u, ok1 ? v1.w : 0u};
+            const uint4 v0 = ok0 ? vb[j][0] : make_uint4(0, 0, 0, 0);
+            const uint4 v1 = ok1 ? vb[j][1] : make_uint4(0, 0, 0, 0);
             issue(j, o + DP);  // refill this slot while the tensor cores work
-#pragma unroll
-            for (int jj = 0; jj < 8; ++jj) {
-                oacc[jj][0] *= corr;
-                oacc[jj][1] *= corr;
-                const uint32_t b0 = (jj & 1) ? (w0[jj >> 1] & 0xffff0000u) : (w0[jj >> 1] << 16);
-                const uint32_t b1 = (jj & 1) ? (w1[jj >> 1] & 0xffff0000u) : (w1[jj >> 1] << 16);
-                mma_tf32_1688(oacc[jj], a0, 0u, a2, 0u, b0, b1);
-            }
+            ot_rescale(oacc, corr, t);
+            ot_pv_octet_bf16(oacc, v0, v1, p0, p1);
         }
     }
 
     if (dts && threadIdx.x == 0) dts[3] = globaltimer() + (__float_as_uint(oacc[0][0]) & 0u);
-    // ---- warp partial -> smem: head gid, channels 16t + j (c0) and 16t + 8 + j (c1)
+    // ---- warp partial -> smem: heads 2t, 2t+1 x channels 8 gid + {0..7}; m, l of head gid
     lp += __shfl_xor_sync(0xffffffffu, lp, 1);
     lp += __shfl_xor_sync(0xffffffffu, lp, 2);
-    if (gid < p.G) {
+    ot_store(wpart + warp * 8 * kSaPart, kSaPart, oacc, gid, t, p.G);
+    if (gid < p.G && t == 0) {
         float *wr = wpart + (warp * 8 + gid) * kSaPart;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            wr[16 * t + j] = oacc[j][0];
-            wr[16 * t + 8 + j] = oacc[j][1];
-        }
-        if (t == 0) {
-            wr[kAttnD] = m;
-            wr[kAttnD + 1] = lp;
-        }
+        wr[kAttnD] = m;
+        wr[kAttnD + 1] = lp;
     }
     __syncthreads();
     // ---- CTA merge: thread -> (head, 4 channels)
@@ -278,7 +264,7 @@ __global__ void __launch_bounds__(W * 32, 512 / (W * 32)) sparse_attn_kernel(Att
 // TMA variant (S a multiple of 16): one (row, split) per CTA.  A producer warp resolves the
 // CTA's pages and streams [16 x 64] K and V tiles (2-D tensor maps over the pools, 128-byte
 // swizzle, L2 evict-first) into an R-stage shared-memory ring; W consumer warps take tiles
-// round-robin (S^T = Q K^T on m16n8k16, online softmax, O += P V on m16n8k8 tf32) reading
+// round-robin (S = Q K^T on m16n8k16, online softmax, O^T += V^T P^T on m16n8k16, hi + lo bf16 P) reading
 // the swizzled rows conflict-free; partials merge as in sparse_attn_kernel.  Bytes in
 // flight are bounded by shared memory (R x 4 KB per CTA), not by registers.
 template <int W, int R>
@@ -406,9 +392,9 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) sparse_attn_tma_kernel(
         // ================================ consumers ===============================
         const float sl2 = p.scale * kLog2e;
         float m = kNegInf, lp = 0.f;
-        float oacc[8][4];
+        float oacc[4][4];  // O^T: channels (8 gid + 2 db, + 1) x heads (2t, 2t + 1) (attn.cuh)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) oacc[j][0] = oacc[j][1] = oacc[j][2] = oacc[j][3] = 0.f;
+        for (int j = 0; j < 4; ++j) oacc[j][0] = oacc[j][1] = oacc[j][2] = oacc[j][3] = 0.f;
         for (int i = warp; i < t1 - t0; i += W) {
             const int st = i % R;
             mbar_wait(full0 + 8 * st, (i / R) & 1);
@@ -453,45 +439,28 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) sparse_attn_tma_kernel(
                     psum += pr[nt][q2];
                 }
             lp = lp * corr + psum;
+            ot_rescale(oacc, corr, t);
+            uint4 vr[2][2];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                oacc[j][0] *= corr;
-                oacc[j][1] *= corr;
-            }
+            for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
-            for (int nt = 0; nt < 2; ++nt) {
-                const int q0 = nt * 8 + 2 * t, q1 = q0 + 1;
-                uint4 v0 = lds_v4(vb + q0 * kRowBytes + ((gid ^ (q0 & 7)) << 4));
-                uint4 v1 = lds_v4(vb + q1 * kRowBytes + ((gid ^ (q1 & 7)) << 4));
-                if (tok0 + q0 >= L) v0 = make_uint4(0, 0, 0, 0);  // past seq_len: may be anything
-                if (tok0 + q1 >= L) v1 = make_uint4(0, 0, 0, 0);
-                const uint32_t a0 = f32_to_tf32(pr[nt][0]), a2 = f32_to_tf32(pr[nt][1]);
-                const uint32_t w0[4] = {v0.x, v0.y, v0.z, v0.w};
-                const uint32_t w1[4] = {v1.x, v1.y, v1.z, v1.w};
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    const uint32_t b0 = (j & 1) ? (w0[j >> 1] & 0xffff0000u) : (w0[j >> 1] << 16);
-                    const uint32_t b1 = (j & 1) ? (w1[j >> 1] & 0xffff0000u) : (w1[j >> 1] << 16);
-                    mma_tf32_1688(oacc[j], a0, 0u, a2, 0u, b0, b1);
+                for (int q2 = 0; q2 < 2; ++q2) {
+                    const int q = nt * 8 + 2 * t + q2;
+                    const uint4 v = lds_v4(vb + q * kRowBytes + ((gid ^ (q & 7)) << 4));
+                    vr[nt][q2] = tok0 + q < L ? v : make_uint4(0, 0, 0, 0);  // past seq_len: may be anything
                 }
-            }
+            ot_pv_tile_bf16(oacc, vr, pr);
             __syncwarp();
             if (lane == 0) mbar_arrive(empty0 + 8 * st);
         }
-        // ---- warp partial: head gid, channels 16t + j (c0) and 16t + 8 + j (c1)
+        // ---- warp partial: heads 2t, 2t+1 x channels 8 gid + {0..7}; m, l of head gid
         lp += __shfl_xor_sync(0xffffffffu, lp, 1);
         lp += __shfl_xor_sync(0xffffffffu, lp, 2);
-        if (gid < p.G) {
+        ot_store(wpart + warp * 8 * kSaPart, kSaPart, oacc, gid, t, p.G);
+        if (gid < p.G && t == 0) {
             float *wr = wpart + (warp * 8 + gid) * kSaPart;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                wr[16 * t + j] = oacc[j][0];
-                wr[16 * t + 8 + j] = oacc[j][1];
-            }
-            if (t == 0) {
-                wr[kAttnD] = m;
-                wr[kAttnD + 1] = lp;
-            }
+            wr[kAttnD] = m;
+            wr[kAttnD + 1] = lp;
         }
     }
     __syncthreads();

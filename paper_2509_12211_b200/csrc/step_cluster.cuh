@@ -12,7 +12,7 @@
 //  3. gather: each CTA's producer streams its share's [16 x 64] K and V tiles with 2-D TMA
 //     (128-byte swizzle) into the SAME ring, now as 4 KB stages;
 //  4. attend: consumers run S = Q K^T (mma.m16n8k16), the fp32 online softmax and
-//     O += P V (mma.m16n8k8, tf32 P — R10) per tile, with the q fragments already in
+//     O^T += V^T P^T (mma.m16n8k16, hi + lo bf16 P — R10; attn.cuh) per tile, with the q fragments already in
 //     shared memory from step 1; warp partials merge in smem, the C CTA partials of a row
 //     in the cluster leader's shared memory (DSM instantiation: DSMEM stores, one cluster
 //     arrive / wait) or through an L2 workspace (last CTA by atomic ticket).
@@ -53,11 +53,12 @@ struct ScSmem {
 };
 
 // FP8 KV (F8, reading R21): the attention stage holds the K and V code tiles (16 tokens x
-// 64 B, 64-byte swizzle) and their 16 + 16 row exponents, kF8Stage bytes (512-aligned).
-constexpr int kF8Stage = 2560;
-// token of k-slot n (0..7) of an 8-token MMA group in the FP8 consumer: chosen so that a
-// lane's 128-bit K-row reads and 64-bit V-row reads are both bank-conflict free under the
-// 64-byte swizzle (bit 0 = n0 ^ n1, bit 1 = n0, bit 2 = n2)
+// 64 B: one contiguous KB each, loaded with 1-D bulk copies — measured 0.4 us faster on C2
+// than 2-D tensor-map tiles with a 64-byte swizzle) and their 16 + 16 row exponents.
+constexpr int kF8Stage = 2080;  // K codes 1 KB | V codes 1 KB | K exps 16 B | V exps 16 B
+// token of k-slot n (0..7) of an 8-token MMA group in the FP8 consumer: the two K rows read
+// by each 8-lane phase of a 128-bit shared load have different parity (64-byte rows: the two
+// halves of the banks), so the K reads are conflict free (bit 0 = n0 ^ n1, bit 1 = n0, bit 2 = n2)
 TS_DEV int f8_tok(int n) { return ((n ^ (n >> 1)) & 1) | ((n & 1) << 1) | (n & 4); }
 
 template <int W, int R, bool DSM, bool APP, bool F8 = false>
@@ -470,21 +471,16 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
             const int tl = t0 + i, u = tl >> tps, sub = tl & (tpp - 1);
             const int row0 = sel[u - u0].x + 16 * sub;  // pool row of the tile's first token
             const uint32_t dst = sb + st * kF8Stage;
-            if (c < 2)
-                tma_load_2d(dst + c * 1024, c ? &tmV : &tmK, 0, row0, afull0 + 8 * st, pol);
-#ifndef TS_F8_NOEXP
+            if (c < 2)  // the 16 code rows of a tile are one contiguous KB
+                bulk_load_hint(dst + c * 1024, static_cast<const uint8_t *>(c ? ap.v_pool : ap.k_pool) + (size_t)row0 * 64,
+                               1024, afull0 + 8 * st, pol);
             else
                 bulk_load(dst + 2048 + (c - 2) * 16, (c == 2 ? kexp : vexp) + row0, 16, afull0 + 8 * st);
-#endif
         };
         {
             const int e = lane >> 2, i = warp + W * e;
             if (e < RA / W && i < ntl) {
-#ifdef TS_F8_NOEXP
-                if ((lane & 3) == 0) mbar_arrive_expect_tx(afull0 + 8 * (i % RA), 2 * 1024);
-#else
                 if ((lane & 3) == 0) mbar_arrive_expect_tx(afull0 + 8 * (i % RA), 2 * 1024 + 32);
-#endif
                 issue_f8(i, lane & 3);
             }
         }
@@ -511,7 +507,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
             for (int nt = 0; nt < 2; ++nt) {
                 sacc[nt][0] = sacc[nt][1] = sacc[nt][2] = sacc[nt][3] = 0.f;
                 const int r = nt * 8 + f8_tok(gid);  // B column gid = this K row
-                const uint4 k = lds_v4(kb + r * 64 + ((t ^ ((r >> 1) & 3)) << 4));
+                const uint4 k = lds_v4(kb + r * 64 + (t << 4));  // rows of different parity: no bank conflict
                 const uint32_t kw[4] = {k.x, k.y, k.z, k.w};
 #pragma unroll
                 for (int kc = 0; kc < 4; ++kc)
@@ -563,13 +559,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
                     pr[nt][q2] = ok[nt][q2] && de >= -126 ? pw * pow2i(de) : 0.f;
                 }
             lp = lp * corr + psum;
-            {  // heads 2t, 2t+1 of this lane's O^T entries: their rescale factors
-                const float c0 = __shfl_sync(0xffffffffu, corr_o, 8 * t), c1 = __shfl_sync(0xffffffffu, corr_o, 8 * t + 4);
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    oacc[j][0] *= c0; oacc[j][1] *= c1; oacc[j][2] *= c0; oacc[j][3] *= c1;
-                }
-            }
+            ot_rescale(oacc, corr_o, t);
             // B = P'^T (k = this lane's tokens, n = head gid), hi + lo f16 parts
             const uint32_t ah0 = f16x2_pack(pr[0][0], pr[0][1]), ah2 = f16x2_pack(pr[1][0], pr[1][1]);
             const float2 h0 = __half22float2(*reinterpret_cast<const __half2 *>(&ah0));
@@ -583,7 +573,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
 #pragma unroll
                 for (int q2 = 0; q2 < 2; ++q2) {
                     const int r = trow[nt][q2];
-                    const uint2 v = lds_v2(vb + r * 64 + ((((gid >> 1) ^ ((r >> 1) & 3))) << 4) + (gid & 1) * 8);
+                    const uint2 v = lds_v2(vb + r * 64 + gid * 8);
                     vr[nt][q2] = ok[nt][q2] ? v : make_uint2(0, 0);  // past seq_len: may be anything
                 }
 #pragma unroll
@@ -599,11 +589,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
             __syncwarp();
             if (lane < 4 && i + RA < ntl) {  // refill this warp's slot with stage i + RA
                 fence_proxy_async();
-#ifdef TS_F8_NOEXP
-                if (lane == 0) mbar_arrive_expect_tx(afull0 + 8 * st, 2 * 1024);
-#else
                 if (lane == 0) mbar_arrive_expect_tx(afull0 + 8 * st, 2 * 1024 + 32);
-#endif
                 issue_f8(i + RA, lane);
             }
         }
@@ -611,15 +597,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
         lp += __shfl_xor_sync(0xffffffffu, lp, 2);
         {
             const float s2e = E > -128 ? pow2i(E) : 1.f;  // back from the V-exponent reference
-#pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {
-                if (2 * t + hh < p.G) {
-                    float *wr = wpart + (warp * 8 + 2 * t + hh) * kSaPart + 8 * gid;
-#pragma unroll
-                    for (int db = 0; db < 4; ++db)
-                        *reinterpret_cast<float2 *>(wr + 2 * db) = make_float2(oacc[db][hh] * s2e, oacc[db][2 + hh] * s2e);
-                }
-            }
+            ot_store(wpart + warp * 8 * kSaPart, kSaPart, oacc, gid, t, p.G, s2e);
             if (gid < p.G && t == 0) {
                 float *wr = wpart + (warp * 8 + gid) * kSaPart;
                 wr[kAttnD] = m;
@@ -708,19 +686,8 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
                     psum += pr[nt][q2];
                 }
             lp = lp * corr + psum;
-            {  // heads 2t, 2t+1 of this lane's O^T entries: their rescale factors
-                const float c0 = __shfl_sync(0xffffffffu, corr, 8 * t), c1 = __shfl_sync(0xffffffffu, corr, 8 * t + 4);
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    oacc[j][0] *= c0; oacc[j][1] *= c1; oacc[j][2] *= c0; oacc[j][3] *= c1;
-                }
-            }
-            // O^T += V^T P^T on mma.m16n8k16: B = P^T (k = tokens 2t, 2t+1 | 8+2t, 9+2t, n = head
-            // gid) as a bf16 hi + lo pair (16 significant bits; reading R10), A = V^T (rows =
-            // channels 8 gid + 2 db (+1), k = the same tokens), built from the lane's V rows
-            const uint32_t ph0 = bf16x2_pack(pr[0][0], pr[0][1]), ph1 = bf16x2_pack(pr[1][0], pr[1][1]);
-            const uint32_t pl0 = bf16x2_pack(pr[0][0] - bf16lo_to_f32(ph0), pr[0][1] - bf16hi_to_f32(ph0));
-            const uint32_t pl1 = bf16x2_pack(pr[1][0] - bf16lo_to_f32(ph1), pr[1][1] - bf16hi_to_f32(ph1));
+            ot_rescale(oacc, corr, t);
+            // O^T += V^T P^T (attn.cuh): the lane's V rows (channels 8 gid .. + 7) of its tokens
             uint4 vr[2][2];
 #pragma unroll
             for (int nt = 0; nt < 2; ++nt)
@@ -730,15 +697,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
                     const uint4 v = lds_v4(vb + q * kRowBytes + ((gid ^ (q & 7)) << 4));
                     vr[nt][q2] = tok0 + q < L ? v : make_uint4(0, 0, 0, 0);  // past seq_len: may be anything
                 }
-#pragma unroll
-            for (int db = 0; db < 4; ++db) {
-                const uint32_t wa0 = u4_word(vr[0][0], db), wb0 = u4_word(vr[0][1], db);
-                const uint32_t wa1 = u4_word(vr[1][0], db), wb1 = u4_word(vr[1][1], db);
-                const uint32_t a0 = __byte_perm(wa0, wb0, 0x5410), a1 = __byte_perm(wa0, wb0, 0x7632);
-                const uint32_t a2 = __byte_perm(wa1, wb1, 0x5410), a3 = __byte_perm(wa1, wb1, 0x7632);
-                mma_bf16_16816(oacc[db], a0, a1, a2, a3, ph0, ph1);
-                mma_bf16_16816(oacc[db], a0, a1, a2, a3, pl0, pl1);
-            }
+            ot_pv_tile_bf16(oacc, vr, pr);
             __syncwarp();
             if (lane < 2 && i + RA < ntl) {  // refill this warp's slot with stage i + RA
                 fence_proxy_async();
@@ -748,15 +707,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
         }
         lp += __shfl_xor_sync(0xffffffffu, lp, 1);
         lp += __shfl_xor_sync(0xffffffffu, lp, 2);
-#pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-            if (2 * t + hh < p.G) {
-                float *wr = wpart + (warp * 8 + 2 * t + hh) * kSaPart + 8 * gid;
-#pragma unroll
-                for (int db = 0; db < 4; ++db)
-                    *reinterpret_cast<float2 *>(wr + 2 * db) = make_float2(oacc[db][hh], oacc[db][2 + hh]);
-            }
-        }
+        ot_store(wpart + warp * 8 * kSaPart, kSaPart, oacc, gid, t, p.G);
         if (gid < p.G && t == 0) {
             float *wr = wpart + (warp * 8 + gid) * kSaPart;
             wr[kAttnD] = m;
