@@ -297,6 +297,11 @@ def main():
     ap.add_argument("--no-reuse", action="store_true", help="skip the NEXT-2 cross-step reuse leg")
     ap.add_argument("--kv", default="bf16", choices=["bf16", "fp8"],
                     help="KV storage: bf16, or FP8 E4M3 with per-row power-of-two scales (NEXT-3)")
+    ap.add_argument("--sweep", action="store_true",
+                    help="NEXT-4: S x K/P sweep (steps/s, FullCache speedup, error vs the float64 dense oracle)")
+    ap.add_argument("--sweep-S", default="4,8,16,32,64")
+    ap.add_argument("--sweep-ratios", default="0.1,0.2,0.3,0.5")
+    ap.add_argument("--sweep-hot", default="4,2.0", help="query-local workload: n_hot pages, beta")
     ap.add_argument("--reuse-alpha", type=float, default=0.1,
                     help="query drift of the reuse leg (synth.drift_queries)")
     args = ap.parse_args()
@@ -326,6 +331,10 @@ def main():
 
     if args.impl == "reference":
         run_reference(args, cfg, world, rank)
+        return
+    if args.sweep:
+        if rank == 0:
+            sweep_main(args)
         return
 
     import paper_2509_12211_b200 as ts
@@ -699,6 +708,142 @@ def main():
     print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
+
+
+def time_graph(fn, n_inner, stream, reps=5):
+    """Per-call time of fn() (enqueues one call) captured n_inner times in a CUDA graph: best of
+    `reps` replays behind a head-start spin, CUDA events on the launching stream."""
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(stream):
+        for _ in range(2):
+            fn()
+        with torch.cuda.graph(g, stream=stream):
+            for _ in range(n_inner):
+                fn()
+        g.replay()
+    torch.cuda.synchronize()
+    best = 1e30
+    for _ in range(reps):
+        a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            torch.cuda._sleep(int(2e6))
+            a.record(stream)
+            g.replay()
+            b_.record(stream)
+        torch.cuda.synchronize()
+        best = min(best, a.elapsed_time(b_) / n_inner)
+    return best * 1e3  # us
+
+
+def sweep_main(args):
+    """the synthetic analogue of the paper's page-size and budget-ratio
+    ablations (§4.3, 688-707 §4.11).  For S in --sweep-S and K/P in
+    --sweep-ratios on the config's shape (ctx fixed, P = ctx / S, K = round(ratio * P)):
+      * us/step of ts_decode_step (cold replica rotation, CUDA graphs) and of the FullCache
+        baseline over the same pools (ts_dense_decode_attn; S < 16: ts_sparse_decode_attn
+        with every page selected, the same computation), and their ratio;
+      * accuracy on a query-local workload (synth q_local: queries aimed at a few hot pages,
+        as real decode queries are) and on random queries, for a sample of sequences:
+        relative L2 error of the GPU sparse output against the FLOAT64 DENSE ORACLE
+        (oracle.sparse_attn over every page) and the attention recall exp(lse_sel - lse_dense)
+        = the dense softmax mass on the selected pages.
+    Prints one JSON line with the table."""
+    import numpy as np
+    import oracle
+    import paper_2509_12211_b200 as ts
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.Stream(device=dev)
+    base = synth.config(args.config)
+    Ss = [int(x) for x in args.sweep_S.split(",")]
+    ratios = [float(x) for x in args.sweep_ratios.split(",")]
+    props = torch.cuda.get_device_properties(dev)
+    l2 = getattr(props, "L2_cache_size", 126 * 2**20) or 126 * 2**20
+    rows_out = []
+    for S in Ss:
+        cfg = base.with_(page_size=S, budget_tokens=S)
+        P = cfg.max_pages
+        per_rep = synth.algorithmic_bytes(cfg.with_(budget_tokens=int(0.3 * P) * S), [cfg.ctx] * cfg.batch)["total"]
+        R = max(2, min(8, -(-4 * l2 // per_rep)))
+        reps = [build_replica(ts, cfg, seed=500 + r, device=dev) for r in range(R)]
+        acc_cases = {}
+        n_hot, beta = args.sweep_hot.split(",")
+        for kind, ql in (("local", (int(n_hot), float(beta))), ("random", None)):
+            ca = synth.make_case(cfg.with_(batch=2), seed=77, q_local=ql)
+            dd = {k: (v.to(dev) if isinstance(v, torch.Tensor) else v) for k, v in ca.items()}
+            La = ts.make_layout(dd["q"], dd["k_pool"], dd["page_table"])
+            ma = ts.meta_build(La, dd["k_pool"], dd["page_table"], dd["seq_lens"])
+            allp = np.tile(np.arange(P, dtype=np.int32), (2, cfg.num_kv_heads, 1))
+            cnt = np.full((2, cfg.num_kv_heads), P, np.int32)
+            od, ld = oracle.sparse_attn(ca["q"], ca["k_pool"], ca["v_pool"], ca["page_table"],
+                                        ca["seq_lens"], allp, cnt, cfg.scale)
+            acc_cases[kind] = (dd, La, ma, od, ld)
+        dense_us = None
+        for ratio in ratios:
+            K = max(1, int(round(ratio * P)))
+            budget = K * S
+            for rep in reps:
+                rep["ws_s"] = ts.new_workspace(ts.workspace_bytes(rep["layout"], budget), dev)
+                rep["ids_s"] = torch.empty((cfg.batch, cfg.num_kv_heads, K), dtype=torch.int32, device=dev)
+            state = {"i": 0}
+
+            def step():
+                rep = reps[state["i"] % R]
+                state["i"] += 1
+                ts.decode_step(rep["layout"], rep["q"], rep["k_pool"], rep["v_pool"], rep["meta"],
+                               rep["page_table"], rep["seq_lens"], budget, cfg.scale, o=rep["o"],
+                               lse=rep["lse"], sel_ids=rep["ids_s"], sel_count=rep["cnt"],
+                               ws=rep["ws_s"], stream=stream)
+            us = time_graph(step, 8 * R, stream)
+            launches = ts.launch_count()
+            if dense_us is None:
+                dstate = {"i": 0}
+                if S % 16 == 0:
+                    dws = [ts.new_workspace(ts.dense_workspace_bytes(r_["layout"]), dev) for r_ in reps]
+
+                    def dstep():
+                        r_ = reps[dstate["i"] % R]
+                        ts.dense_decode_attn(r_["layout"], r_["q"], r_["k_pool"], r_["v_pool"], r_["page_table"],
+                                             r_["seq_lens"], cfg.scale, o=r_["o"], lse=r_["lse"],
+                                             ws=dws[dstate["i"] % R], stream=stream)
+                        dstate["i"] += 1
+                else:  # every page selected through the sparse attention kernel
+                    allg = torch.arange(P, dtype=torch.int32, device=dev).repeat(cfg.batch, cfg.num_kv_heads, 1).contiguous()
+                    cntg = torch.full((cfg.batch, cfg.num_kv_heads), P, dtype=torch.int32, device=dev)
+                    dws = [ts.new_workspace(ts.attn_workspace_bytes(r_["layout"], P), dev) for r_ in reps]
+
+                    def dstep():
+                        r_ = reps[dstate["i"] % R]
+                        ts.sparse_decode_attn(r_["layout"], r_["q"], r_["k_pool"], r_["v_pool"], r_["page_table"],
+                                              r_["seq_lens"], allg, cntg, cfg.scale, o=r_["o"], lse=r_["lse"],
+                                              ws=dws[dstate["i"] % R], stream=stream)
+                        dstate["i"] += 1
+                dense_us = time_graph(dstep, 2 * R, stream)
+                del dws
+            alg = synth.algorithmic_bytes(cfg.with_(budget_tokens=budget), [cfg.ctx] * cfg.batch)["total"]
+            row = {"S": S, "ratio": ratio, "K": K, "P": P, "budget_tokens": budget,
+                   "us_per_step": us, "steps_per_s": 1e6 / us, "launches_per_step": launches,
+                   "alg_bytes": alg, "gbs": alg / (us * 1e-6) / 1e9, "dense_us": dense_us,
+                   "speedup_vs_dense": dense_us / us}
+            for kind, (dd, La, ma, od, ld) in acc_cases.items():
+                o, lse, _, _ = ts.decode_step(La, dd["q"], dd["k_pool"], dd["v_pool"], ma, dd["page_table"],
+                                              dd["seq_lens"], budget, cfg.scale)
+                o = o.cpu().numpy().astype(np.float64)
+                lse = lse.cpu().numpy().astype(np.float64)
+                row[f"rel_l2_err_{kind}"] = float(np.linalg.norm(o - od) / np.linalg.norm(od))
+                row[f"recall_{kind}"] = float(np.mean(np.exp(lse - ld)))
+            rows_out.append(row)
+            print(f"sweep S={S} K/P={ratio}: {us:.2f} us ({row['speedup_vs_dense']:.2f}x dense), "
+                  f"err local {row['rel_l2_err_local']:.3g} random {row['rel_l2_err_random']:.3g}, "
+                  f"recall local {row['recall_local']:.3f}", file=sys.stderr, flush=True)
+        del reps
+        torch.cuda.empty_cache()
+    line = {"metric": "NEXT-4 sweep: decode steps/s and output error vs the float64 dense oracle",
+            "config": {"workload": f"{base.name}: {base.note}", "ctx": base.ctx, "batch": base.batch,
+                       "accuracy_sample": f"2 sequences; q_local = ({args.sweep_hot}: hot pages, beta) and random q",
+                       "timing": "cold replica rotation, CUDA graphs, best of 5 replays"},
+            "rows": rows_out, "device": torch.cuda.get_device_name(dev)}
+    print(json.dumps(line), flush=True)
 
 
 def dense_leg(ts, cfg, reps, R, stream, dev, args, ms_per_step):

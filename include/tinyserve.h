@@ -53,7 +53,7 @@
  *    seq_len == 0 is valid: the sequence selects nothing, o = 0, lse = -inf (reading R8).
  *  - Compiled set: head_dim 64 or 128 for metadata, scoring and fp32 attention; the bf16
  *    attention (ts_sparse_decode_attn, ts_decode_step) needs head_dim 64, page_size in
- *    {8, 16, 32, 64} and group size 1..8 (tensor-core tiles); fp32 takes any page_size
+ *    {4, 8, 16, 32, 64} and group size 1..8 (tensor-core tiles); fp32 takes any page_size
  *    and group size.  At most 4096 selected pages per row.
  */
 #ifndef TINYSERVE_H

@@ -33,7 +33,8 @@ inline void phase_mark(int i, cudaStream_t st) {
     if (g_phase_ev[i]) cudaEventRecordWithFlags(g_phase_ev[i], st, cudaEventRecordExternal);
 }
 
-constexpr int kMaxSel = 4096;      // max selected pages per row
+constexpr int kMaxSel = 4096;      // max selected pages per row (decode step)
+constexpr int kMaxSelAttn = 8192;  // max pages per row handed to the attention kernels (8 B of smem each)
 
 inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
@@ -75,7 +76,7 @@ int env_int(const char *name, int dflt) {  // development A/B knobs (read once p
 bool bf16_attn_supported(const ts_layout *L) {
     const int S = L->page_size;
     return L->kv_dtype == TS_BF16 && L->head_dim == 64 && group_of(L) <= 8 &&
-           (S == 8 || S == 16 || S == 32 || S == 64);
+           (S == 4 || S == 8 || S == 16 || S == 32 || S == 64);
 }
 
 ts_status launch_status() {
@@ -396,7 +397,7 @@ ts_status launch_sparse_attn(const ts_layout *L, const AttnParams &p, bool pdl, 
         if (rr == 16) return launch_sat<4, 16>(L, p, pdl, st);
         return launch_sat<4, 8>(L, p, pdl, st);
     }
-    const int n_oct = p.sel_stride * (L->page_size / 8);  // upper bound per row
+    const int n_oct = p.sel_stride * std::max(1, L->page_size / 8);  // upper bound per row
     static const int cmax_env = std::min(kMaxClusterC, getenv("TS_SA_CMAX") ? std::max(1, atoi(getenv("TS_SA_CMAX"))) : 16);
     int W = rows >= 2 * sms ? 4 : (rows * 16 < sms ? 16 : 8);
     static const int w_env = getenv("TS_SA_W") ? atoi(getenv("TS_SA_W")) : 0;
@@ -661,7 +662,7 @@ ts_status launch_attn(const ts_layout *L, const void *q, const void *k_pool, con
     AttnParams p = attn_params(L, q, k_pool, v_pool, pt, sl, sel_ids, sel_count, sel_stride, scale,
                                o, lse, ws);
     if (L->kv_dtype == TS_BF16) {
-        if (!bf16_attn_supported(L) || sel_stride > kMaxSel) return TS_ERR_UNSUPPORTED;
+        if (!bf16_attn_supported(L) || sel_stride > kMaxSelAttn) return TS_ERR_UNSUPPORTED;
         return launch_sparse_attn(L, p, true, st);
     }
     const int threads = 32 * std::min(p.G, 8);

@@ -119,7 +119,10 @@ __global__ void __launch_bounds__(W * 32, 512 / (W * 32)) sparse_attn_kernel(Att
     __syncthreads();
     SA_STAMP(2);
     const int n_own = s_nown;
-    const int ops = p.S >> 3;  // octets per page
+    // octets per page; a page of S = 4 tokens is one half-filled octet (rows >= 4 of it
+    // belong to other (block, head) runs: never loaded, masked like tokens past seq_len)
+    const int ops = p.S >= 8 ? p.S >> 3 : 1;
+    const int orows = p.S >= 8 ? 8 : p.S;  // token rows per octet
     const int n_oct = n_own * ops;
     const int nw = C * W, wg = rank * W + warp;
     const int o0 = (int)((long long)n_oct * wg / nw), o1 = (int)((long long)n_oct * (wg + 1) / nw);
@@ -144,11 +147,11 @@ __global__ void __launch_bounds__(W * 32, 512 / (W * 32)) sparse_attn_kernel(Att
         if (o < o1) {
             const size_t e = octet_addr(o, tk[j]);
             const uint16_t *kr = kp + e + gid * kAttnD + 16 * t;
-            kb[j][0] = ldg_nc_v4(kr);
-            kb[j][1] = ldg_nc_v4(kr + 8);
+            kb[j][0] = gid < orows ? ldg_nc_v4(kr) : make_uint4(0, 0, 0, 0);
+            kb[j][1] = gid < orows ? ldg_nc_v4(kr + 8) : make_uint4(0, 0, 0, 0);
             const uint16_t *vr = vp + e + (2 * t) * kAttnD + 8 * gid;
-            vb[j][0] = ldg_nc_v4(vr);
-            vb[j][1] = ldg_nc_v4(vr + kAttnD);
+            vb[j][0] = 2 * t < orows ? ldg_nc_v4(vr) : make_uint4(0, 0, 0, 0);
+            vb[j][1] = 2 * t + 1 < orows ? ldg_nc_v4(vr + kAttnD) : make_uint4(0, 0, 0, 0);
         }
     };
 #pragma unroll
@@ -166,7 +169,7 @@ __global__ void __launch_bounds__(W * 32, 512 / (W * 32)) sparse_attn_kernel(Att
             mma_bf16_16816(s, qa[4], 0u, qa[5], 0u, kb[j][1].x, kb[j][1].y);
             mma_bf16_16816(s, qa[6], 0u, qa[7], 0u, kb[j][1].z, kb[j][1].w);
             const int tok = tk[j] + 2 * t;
-            const bool ok0 = tok < L, ok1 = tok + 1 < L;
+            const bool ok0 = tok < L && 2 * t < orows, ok1 = tok + 1 < L && 2 * t + 1 < orows;
             const float x0 = ok0 ? s[0] * sl2 : kNegInf;
             const float x1 = ok1 ? s[1] * sl2 : kNegInf;
             float tmax = fmaxf(x0, x1);

@@ -110,12 +110,21 @@ def _randint(lo, hi, shape, seed, tag, device):
 def make_case(cfg: Config, seed: int = 42, *, device="cpu", mode: str = "clustered",
               ragged: bool = False, seq_lens: Optional[list] = None,
               identity_table: bool = False, sigma_c: float = 1.0, sigma_n: float = 1.0,
-              poison_tail: bool = False, spare_blocks: int = 0) -> dict:
+              poison_tail: bool = False, spare_blocks: int = 0,
+              q_local: Optional[tuple] = None) -> dict:
     """Draw one synthetic paged-KV decode case.
 
     seed 42 is the paper's seed.  `poison_tail` writes NaN into the
     unused slots past seq_len of every partial last page, so that a kernel that reads
     them (instead of masking) fails the parity tests loudly.
+
+    `q_local = (n_hot, beta)` (clustered mode; SURVEY.md §8d "query locality toward n_hot
+    pages", the NEXT-4 accuracy workload): per (sequence, kv head) n_hot logical pages are
+    drawn among the valid ones and q head h of the group becomes
+        q = beta * c_hot(h) + z,   z ~ N(0, I),
+    c_hot(h) the key centre of hot page h mod n_hot, so decode attention concentrates on a
+    few pages as it does for a real model's queries (random queries see near-flat
+    attention over the whole context).
     """
     B, Hq, Hkv, d, S = cfg.batch, cfg.num_q_heads, cfg.num_kv_heads, cfg.head_dim, cfg.page_size
     mp = cfg.max_pages
@@ -149,6 +158,22 @@ def make_case(cfg: Config, seed: int = 42, *, device="cpu", mode: str = "cluster
     else:
         perm = torch.randperm(nb, generator=_gen(seed, "perm", "cpu"))
     page_table = perm[: B * mp].reshape(B, mp).to(torch.int32)
+
+    if q_local is not None:
+        assert mode == "clustered"
+        n_hot, beta = int(q_local[0]), float(q_local[1])
+        G = Hq // Hkv
+        gh = _gen(seed, "hot", "cpu")
+        cen = centre.to("cpu")
+        qc = q.to("cpu").clone()
+        for b, L in enumerate(lens):
+            P = max(1, -(-L // S))
+            for g in range(Hkv):
+                hot = torch.randint(0, P, (n_hot,), generator=gh)
+                for h in range(G):
+                    blk = int(page_table[b, int(hot[h % n_hot])])
+                    qc[b, g * G + h] += beta * cen[blk, g, 0]
+        q = qc.to(dev)
 
     k_pool = k.to(dt)
     v_pool = v.to(dt)

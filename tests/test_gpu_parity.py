@@ -60,6 +60,11 @@ CASES = {
     "c3_small": ("c3", dict(batch=2, ctx=3000, budget_tokens=512), True),
     "g4_s32": ("c3", dict(batch=2, num_q_heads=16, ctx=2500, page_size=32, budget_tokens=512), True),
     "g2_s8": ("c3", dict(batch=3, num_q_heads=8, ctx=900, page_size=8, budget_tokens=128), True),
+    # S = 4 (the smallest page of the paper's page-size table): half-filled octets
+    "g8_s4": ("c3", dict(batch=2, ctx=700, page_size=4, budget_tokens=96), True),
+    # NEXT-4 sweep shape at S = 4: P 2048 pages, K = P / 2 (the margin rule cannot be met at
+    # the sweep's P = 8192: boundary gaps below 1e-4 L1 are the norm there)
+    "s4_long": ("c3", dict(batch=1, ctx=8192, page_size=4, budget_tokens=4096), True),
     "c5_like": ("c5", dict(batch=1, ctx=40000, budget_tokens=1024), True),
     "f32_gqa": ("c1", dict(batch=2, num_q_heads=8, num_kv_heads=2, ctx=700, page_size=16,
                            budget_tokens=160), True),
@@ -85,7 +90,7 @@ def make(name, seed=7, **kw):
 
 
 # ------------------------------------------------------------------ a1: metadata
-@pytest.mark.parametrize("name", ["c1_ragged", "c2_small", "g4_s32", "g2_s8", "bf16_d128_score"])
+@pytest.mark.parametrize("name", ["c1_ragged", "c2_small", "g4_s32", "g2_s8", "g8_s4", "bf16_d128_score"])
 def test_meta_build_bit_exact(ts, name):
     cfg, case = make(name)
     d = on_dev(case)
