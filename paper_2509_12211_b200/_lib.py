@@ -10,7 +10,10 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtinyserve.so")
+# the release library; TS_DEV_LIB=1 (development / test child processes only) loads the dev
+# build of the same source instead (A/B knobs, timestamp hooks, TS_DEBUG error word)
+LIB_PATH = os.path.join(HERE, "libtinyserve_dev.so" if os.environ.get("TS_DEV_LIB") == "1"
+                        else "libtinyserve.so")
 
 TS_F32, TS_BF16, TS_FP8E4M3 = 0, 1, 2
 _STATUS = {0: "TS_OK", 1: "TS_ERR_CONFIG", 2: "TS_ERR_SHAPE", 3: "TS_ERR_ALIGN",

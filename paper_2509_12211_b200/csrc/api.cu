@@ -68,9 +68,17 @@ ts_layout score_view(const ts_layout *L) {
 
 int group_of(const ts_layout *L) { return L->num_q_heads / L->num_kv_heads; }
 
-int env_int(const char *name, int dflt) {  // development A/B knobs (read once per call site)
+// Development A/B knobs: read from the environment (once per call site) only in the dev
+// build (libtinyserve_dev.so, -DTS_DEV_KNOBS); the release library always takes the
+// measured defaults (DESIGN.md §5 "Development knobs").
+int env_int(const char *name, int dflt) {
+#ifdef TS_DEV_KNOBS
     const char *v = getenv(name);
     return v ? atoi(v) : dflt;
+#else
+    (void)name;
+    return dflt;
+#endif
 }
 
 bool bf16_attn_supported(const ts_layout *L) {
@@ -363,7 +371,7 @@ ts_status launch_sat(const ts_layout *L, const AttnParams &p, bool pdl, cudaStre
         return TS_ERR_CUDA;
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (W + 1) * 32, sm);
-    static const int cmax_env = std::min(kMaxClusterC, getenv("TS_SA_CMAX") ? std::max(1, atoi(getenv("TS_SA_CMAX"))) : 16);
+    static const int cmax_env = std::min(kMaxClusterC, std::max(1, env_int("TS_SA_CMAX", 16)));
     const int ntile = p.sel_stride * (L->page_size / 16);  // upper bound per row
     // splits per row: fill one wave (rows x C <= CTAs resident), each warp >= 2 tiles
     int C = std::max(1, std::min(cmax_env, device_sms() * std::max(1, per_sm) / std::max(1, rows)));
@@ -390,17 +398,17 @@ ts_status launch_sat(const ts_layout *L, const AttnParams &p, bool pdl, cudaStre
 ts_status launch_sparse_attn(const ts_layout *L, const AttnParams &p, bool pdl, cudaStream_t st) {
     const int rows = L->batch * L->num_kv_heads;
     const int sms = device_sms();
-    static const int tma = getenv("TS_SA_TMA") ? atoi(getenv("TS_SA_TMA")) : 1;
+    static const int tma = env_int("TS_SA_TMA", 1);
     if (tma && L->page_size % 16 == 0) {
-        static const int rr = getenv("TS_SA_R") ? atoi(getenv("TS_SA_R")) : 8;
+        static const int rr = env_int("TS_SA_R", 8);
         if (rr == 12) return launch_sat<4, 12>(L, p, pdl, st);
         if (rr == 16) return launch_sat<4, 16>(L, p, pdl, st);
         return launch_sat<4, 8>(L, p, pdl, st);
     }
     const int n_oct = p.sel_stride * std::max(1, L->page_size / 8);  // upper bound per row
-    static const int cmax_env = std::min(kMaxClusterC, getenv("TS_SA_CMAX") ? std::max(1, atoi(getenv("TS_SA_CMAX"))) : 16);
+    static const int cmax_env = std::min(kMaxClusterC, std::max(1, env_int("TS_SA_CMAX", 16)));
     int W = rows >= 2 * sms ? 4 : (rows * 16 < sms ? 16 : 8);
-    static const int w_env = getenv("TS_SA_W") ? atoi(getenv("TS_SA_W")) : 0;
+    static const int w_env = env_int("TS_SA_W", 0);
     if (w_env == 4 || w_env == 8 || w_env == 16) W = w_env;
     const int per_sm = W == 4 ? 4 : (W == 8 ? 2 : 1);
     int C = std::max(1, std::min(cmax_env, sms * per_sm / std::max(1, rows)));
@@ -444,7 +452,7 @@ ts_status launch_ss_t(ScoreSelParams &p, int rows, int cdesired, cudaStream_t st
     at[0].val.clusterDim.z = 1;
     // PDL: the prologue (barriers, histogram, cluster arrival) overlaps the previous kernel's
     // tail; griddepcontrol.wait precedes every read of q / metadata / page table
-    static const bool pdl = !getenv("TS_NO_PDL");
+    static const bool pdl = env_int("TS_NO_PDL", 0) == 0;
     at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[1].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
     cfg.attrs = at;
@@ -473,12 +481,12 @@ StepPlan plan_step(const ts_layout *L, int kmax) {
     // two-level select when rows are much longer than the candidates; bit 2 DSMEM merge
     // area (DSM); bits 3 / 4 early / late PDL trigger (set at launch)
     int fl = (((L->max_pages & 3) == 0 && L->max_pages <= 2048) ? 1 : 0) | (DSM ? 4 : 0);
-    static const int two_env = getenv("TS_SC_TWO") ? atoi(getenv("TS_SC_TWO")) : -1;
+    static const int two_env = env_int("TS_SC_TWO", -1);
     const bool two_ok = two_env == 1 || (two_env != 0 && L->max_pages > 2048);  // long rows only
     auto allow = [&](size_t smb) -> bool {  // grow the opt-in shared memory on demand
         return ensure_func_attrs((const void *)kern, smb, true);
     };
-    static const int cmax = std::min(kMaxClusterC, getenv("TS_SC_CMAX") ? std::max(1, atoi(getenv("TS_SC_CMAX"))) : 16);
+    static const int cmax = std::min(kMaxClusterC, std::max(1, env_int("TS_SC_CMAX", 16)));
     const int max_c = std::max(1, std::min(cmax, (L->max_pages + 63) / 64));  // >= 64 pages per CTA
     auto chunk_of = [&](int c) {
         int ch = (L->max_pages + c - 1) / c;
@@ -539,7 +547,7 @@ ts_status launch_step(const ts_layout *L, ScoreSelParams &sp, const AttnParams &
     // the attention loop (bit 4) with clusters of <= 8 CTAs — measured 0.9 % faster than at
     // kernel start (bit 3, TS_SC_TRIGGER=1) on C2 / C4, equal on C3; none with C5's 13-CTA
     // clusters (either trigger: 23 -> 28-32 us)
-    static const int trig_env = getenv("TS_SC_TRIGGER") ? atoi(getenv("TS_SC_TRIGGER")) : -1;
+    static const int trig_env = env_int("TS_SC_TRIGGER", -1);
     if (trig_env == 1) sp.flags |= 8;
     if (trig_env == 2 || (trig_env < 0 && pl.C <= 8)) sp.flags |= 16;
     cudaLaunchConfig_t cfg{};
@@ -552,7 +560,7 @@ ts_status launch_step(const ts_layout *L, ScoreSelParams &sp, const AttnParams &
     at[0].val.clusterDim.x = pl.C;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
-    static const bool pdl = !getenv("TS_NO_PDL");
+    static const bool pdl = env_int("TS_NO_PDL", 0) == 0;
     at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[1].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
     cfg.attrs = at;
@@ -567,7 +575,7 @@ ts_status launch_step_cluster_app(const ts_layout *L, ScoreSelParams &sp, const 
                                  cudaStream_t st) {
     // DSMEM merge when its merge area costs no cluster width and C <= 8 (measured: faster at
     // C = 4 (C3); at C = 13 (C5) one SM receiving 13 partials loses to the L2 ticket merge)
-    static const int dsm_env = getenv("TS_SC_DSM") ? atoi(getenv("TS_SC_DSM")) : -1;  // dev knob
+    static const int dsm_env = env_int("TS_SC_DSM", -1);  // dev knob
     const StepPlan b = plan_step<W, R, false, APP, F8>(L, sp.kmax);
     if constexpr (R == 8) {
         const StepPlan a = plan_step<W, R, true, APP, F8>(L, sp.kmax);
@@ -611,8 +619,8 @@ ts_status launch_score_select(const ts_layout *L, const void *q, const void *met
     p.max_pages = L->max_pages;
     p.kmax = kmax;
     p.dbg = g_dbg_ss;
-    static const int per_sm = getenv("TS_SS_PER_SM") ? atoi(getenv("TS_SS_PER_SM")) : 3;
-    static const int cmax = std::min(kMaxClusterC, getenv("TS_SS_CMAX") ? std::max(1, atoi(getenv("TS_SS_CMAX"))) : 16);
+    static const int per_sm = env_int("TS_SS_PER_SM", 3);
+    static const int cmax = std::min(kMaxClusterC, std::max(1, env_int("TS_SS_CMAX", 16)));
     const int target = device_sms() * per_sm;
     const int max_c = std::max(1, std::min(cmax, (L->max_pages + 63) / 64));  // >= 64 pages per CTA
     const int C = std::max(1, std::min(max_c, (target + rows - 1) / rows));
@@ -696,9 +704,25 @@ const char *ts_version(void) { return "tinyserve-b200 0.1 (sm_100a)"; }
 
 int32_t ts_last_launch_count(void) { return g_launches; }
 
-// development hook (not in the public header): device buffer for attention CTA timestamps
+#ifdef TS_DEV_KNOBS
+// TS_DEBUG error word (common.cuh, dev build only): synchronises the device, returns the
+// OR of the fault bits raised since the last reset (bit 0 seq_len out of range, bit 1
+// page-table entry out of range), and clears it if `reset` != 0.
+int32_t ts_debug_error_word(int32_t reset) {
+    cudaDeviceSynchronize();
+    unsigned v = 0;
+    if (cudaMemcpyFromSymbol(&v, g_ts_debug_err, sizeof(v)) != cudaSuccess) return -1;
+    if (reset) {
+        const unsigned z = 0;
+        cudaMemcpyToSymbol(g_ts_debug_err, &z, sizeof(z));
+    }
+    return (int32_t)v;
+}
+// development hooks of the dev build only (not in the public header): device buffers for
+// per-CTA globaltimer phase stamps (scripts/step_stamps.py)
 void ts_debug_timestamps(void *buf) { g_dbg_ts = static_cast<unsigned long long *>(buf); }
 void ts_debug_ss_timestamps(void *buf) { g_dbg_ss = static_cast<unsigned long long *>(buf); }
+#endif
 
 void ts_profile_events(void *const *events, int32_t n) {
     for (int i = 0; i < 4; ++i)
@@ -737,7 +761,7 @@ static ts_status meta_append_impl(const ts_layout *L, const void *k_new, const v
         return TS_ERR_ALIGN;
     if (L->batch == 0) return TS_OK;
     MetaParams p{L->batch, L->num_kv_heads, L->head_dim, L->page_size, L->max_pages,
-                 L->shard_stride, L->shard_offset};
+                 L->shard_stride, L->shard_offset, L->num_blocks};
     if (L->kv_dtype == TS_FP8E4M3) {  // bf16 token -> E4M3 codes + row exponent (reading R21)
         if (L->num_kv_heads * 8 > 1024) return TS_ERR_UNSUPPORTED;
         launch_pdl(meta_append_f8_kernel, dim3(L->batch), dim3(L->num_kv_heads * 8), 0, as_stream(stream),
@@ -769,7 +793,7 @@ ts_status ts_meta_build(const ts_layout *L, const void *k_pool, const int32_t *p
     if (!aligned16(k_pool) || !aligned16(meta)) return TS_ERR_ALIGN;
     if (L->batch == 0) return TS_OK;
     MetaParams p{L->batch, L->num_kv_heads, L->head_dim, L->page_size, L->max_pages,
-                 L->shard_stride, L->shard_offset};
+                 L->shard_stride, L->shard_offset, L->num_blocks};
     const long long work = (long long)L->batch * L->max_pages * L->num_kv_heads *
                            (L->head_dim / (L->kv_dtype == TS_F32 ? 4 : 8));
     const int grid = (int)std::min<long long>((work + 255) / 256, (long long)device_sms() * 16);
@@ -897,7 +921,7 @@ static ts_status decode_step_impl(const ts_layout *L, const void *q, const void 
     int *cnt = sel_count_out ? sel_count_out : reinterpret_cast<int *>(wb + w.sel_count);
     const cudaStream_t st = as_stream(stream);
     const int rows = L->batch * L->num_kv_heads;
-    static const int two_kernels = getenv("TS_TWO_KERNELS") ? atoi(getenv("TS_TWO_KERNELS")) : 0;
+    static const int two_kernels = env_int("TS_TWO_KERNELS", 0);
     if (f8 && k_new && rows > 0) {  // FP8 append: its own kernel, then the one-launch step
         if ((s = meta_append_impl(L, k_new, v_new, const_cast<int32_t *>(seq_lens), -1, page_table,
                                   const_cast<void *>(k_pool), const_cast<void *>(v_pool),
@@ -942,7 +966,7 @@ static ts_status decode_step_impl(const ts_layout *L, const void *q, const void 
         phase_mark(0, st);
         // ring depth: 8 stages (64 KB in flight per CTA) when the rows leave SMs for wide
         // clusters (measured: C3 / C5 faster); 4 stages when many rows need >= 3 CTAs per SM
-        static const int ring_env = getenv("TS_SC_R") ? atoi(getenv("TS_SC_R")) : 0;  // dev knob
+        static const int ring_env = env_int("TS_SC_R", 0);  // dev knob
         const int ring = ring_env ? ring_env : (L->batch * L->num_kv_heads <= device_sms() ? 8 : 4);
         s = ring == 8 ? launch_step_cluster_t<4, 8>(L, sp, ap, st) : launch_step_cluster_t<4, 4>(L, sp, ap, st);
         phase_mark(3, st);
@@ -971,7 +995,7 @@ static ts_status decode_step_impl(const ts_layout *L, const void *q, const void 
             AttnParams p = attn_params(L, q, k_pool, v_pool, page_table, seq_lens, ids, cnt, kmax,
                                        scale, o, lse, ws);
             p.sel_blk = blk;
-            static const bool pdl = !getenv("TS_NO_PDL");
+            static const bool pdl = env_int("TS_NO_PDL", 0) == 0;
             if ((s = launch_sparse_attn(L, p, pdl, st)) != TS_OK) return s;
         }
         phase_mark(3, st);
@@ -1022,7 +1046,7 @@ ts_status ts_dense_decode_attn(const ts_layout *L, const void *q, const void *k_
     AttnParams p = attn_params(L, q, k_pool, v_pool, page_table, seq_lens, nullptr, nullptr,
                                L->max_pages, scale, o, lse, ws);
     p.dense = 1;
-    static const int rr = getenv("TS_SA_R") ? atoi(getenv("TS_SA_R")) : 8;
+    static const int rr = env_int("TS_SA_R", 8);
     if (rr == 16) return launch_sat<4, 16>(L, p, true, as_stream(stream));
     return launch_sat<4, 8>(L, p, true, as_stream(stream));
 }

@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(256) attn_simt_kernel(AttnParams p, const floa
         for (int u = 0; u < cnt; ++u) {
             const int j = ids[u];
             if (j < 0 || j % p.stride != p.offset) continue;
-            const int blk = p.page_table[(size_t)b * p.max_pages + j / p.stride];
+            const int blk = checked_block(p.page_table[(size_t)b * p.max_pages + j / p.stride], p.num_blocks);
             const int nv = min(p.S, L - j * p.S);
             for (int s = 0; s < nv; ++s) {
                 const size_t base = (((size_t)blk * p.Hkv + g) * p.S + s) * D;

@@ -254,11 +254,33 @@ TS_DEV float warp_sum(float v) {
     return v;
 }
 
+// ---------------------------------------------------------------- TS_DEBUG error word
+// Data-dependent faults the host cannot see without a sync (include/tinyserve.h "ERRORS"):
+// in the dev build (-DTS_DEV_KNOBS, libtinyserve_dev.so) the kernels OR a bit into a device
+// word, read back by ts_debug_error_word(); the release build compiles the checks away.
+//   bit 0: seq_len < 0 or beyond the page-table row's capacity (max_pages * stride * S)
+//   bit 1: a page-table entry the kernel dereferences is outside [0, num_blocks)
+constexpr unsigned kDbgSeqLen = 1u, kDbgBlock = 2u;
+#ifdef TS_DEV_KNOBS
+__device__ unsigned g_ts_debug_err = 0u;
+TS_DEV void debug_flag(bool bad, unsigned bit) {
+    if (bad) atomicOr(&g_ts_debug_err, bit);
+}
+#else
+TS_DEV void debug_flag(bool, unsigned) {}
+#endif
+// a physical block read from the page table (checked in the dev build)
+TS_DEV int checked_block(int blk, int num_blocks) {
+    debug_flag(blk < 0 || blk >= num_blocks, kDbgBlock);
+    return blk;
+}
+
 // Sequence length as the kernels see it: at most the capacity of the page-table row
 // (global pages < max_pages * stride).  seq_len beyond it is a caller error (undefined per
 // include/tinyserve.h); clamping keeps every read inside the row and the pools' pages.
 TS_DEV int clamp_len(int L, int max_pages, int stride, int S) {
     const long long cap = (long long)max_pages * stride * S;
+    debug_flag(L < 0 || L > cap, kDbgSeqLen);
     return L < cap ? L : (int)cap;
 }
 

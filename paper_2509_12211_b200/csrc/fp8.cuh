@@ -128,7 +128,7 @@ __global__ void meta_append_f8_kernel(MetaParams p, const uint16_t *__restrict__
     if (jl >= p.max_pages) return;
     const bool live = h < p.Hkv;
     const int hh = live ? h : 0;
-    const int blk = page_table[(size_t)b * p.max_pages + jl];
+    const int blk = checked_block(page_table[(size_t)b * p.max_pages + jl], p.num_blocks);
     const size_t src = ((size_t)b * p.Hkv + hh) * 64 + c * 8;
     const uint4 k = *reinterpret_cast<const uint4 *>(k_new + src);
     const uint4 v = *reinterpret_cast<const uint4 *>(v_new + src);
@@ -179,7 +179,7 @@ __global__ void meta_build_f8_kernel(MetaParams p, const uint8_t *__restrict__ k
         const long long nvalid = (long long)seq_lens[b] - j * p.S;
         if (nvalid <= 0) continue;
         const int n = nvalid < p.S ? int(nvalid) : p.S;
-        const int blk = page_table[(size_t)b * p.max_pages + jl];
+        const int blk = checked_block(page_table[(size_t)b * p.max_pages + jl], p.num_blocks);
         const size_t row0 = ((size_t)blk * p.Hkv + h) * p.S;
         uint4 lo = make_uint4(0, 0, 0, 0), hi = lo;
         for (int s = 0; s < n; ++s) {

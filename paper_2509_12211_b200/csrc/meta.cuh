@@ -11,7 +11,7 @@
 namespace ts {
 
 struct MetaParams {
-    int B, Hkv, D, S, max_pages, stride, offset;
+    int B, Hkv, D, S, max_pages, stride, offset, num_blocks;
 };
 
 template <typename T>
@@ -75,7 +75,7 @@ __global__ void meta_append_kernel(MetaParams p, const T *__restrict__ k_new,
     if (j % p.stride != p.offset) return;  // page owned by another rank
     const int jl = j / p.stride;
     if (jl >= p.max_pages) return;
-    const int blk = page_table[(size_t)b * p.max_pages + jl];
+    const int blk = checked_block(page_table[(size_t)b * p.max_pages + jl], p.num_blocks);
     const size_t src = ((size_t)b * p.Hkv + h) * p.D + c * V::kElems;
     const uint4 k = *reinterpret_cast<const uint4 *>(k_new + src);
     const uint4 v = *reinterpret_cast<const uint4 *>(v_new + src);
@@ -114,11 +114,12 @@ __global__ void meta_build_kernel(MetaParams p, const T *__restrict__ k_pool,
         const int jl = int(r % p.max_pages);
         const int b = int(r / p.max_pages);
         const int L = seq_lens[b];
+        debug_flag(L < 0 || L > (long long)p.max_pages * p.stride * p.S, kDbgSeqLen);
         const long long j = (long long)jl * p.stride + p.offset;  // global page id
         const long long nvalid = (long long)L - j * p.S;
         if (nvalid <= 0) continue;
         const int n = nvalid < p.S ? int(nvalid) : p.S;
-        const int blk = page_table[(size_t)b * p.max_pages + jl];
+        const int blk = checked_block(page_table[(size_t)b * p.max_pages + jl], p.num_blocks);
         const T *src = k_pool + ((size_t)blk * p.Hkv + h) * p.S * p.D + c * V::kElems;
         uint4 lo = *reinterpret_cast<const uint4 *>(src);
         uint4 hi = lo;

@@ -85,14 +85,14 @@ __global__ void __launch_bounds__(W * 32, 512 / (W * 32)) sparse_attn_kernel(Att
     if (p.sel_blk) {  // fused step: the selector already resolved the blocks
         const int *blks = p.sel_blk + (size_t)row * p.sel_stride;
         for (int u = threadIdx.x; u < cnt; u += blockDim.x) {
-            s_base[u] = (__ldcg(blks + u) * p.Hkv + g) * p.S;
+            s_base[u] = (checked_block(__ldcg(blks + u), p.num_blocks) * p.Hkv + g) * p.S;
             s_tok[u] = __ldcg(ids + u) * p.S;
         }
         if (threadIdx.x == 0) s_nown = cnt;
     } else if (p.stride == 1) {
         for (int u = threadIdx.x; u < cnt; u += blockDim.x) {
             const int j = __ldg(ids + u);
-            const int blk = __ldg(p.page_table + (size_t)b * p.max_pages + j);
+            const int blk = checked_block(__ldg(p.page_table + (size_t)b * p.max_pages + j), p.num_blocks);
             s_base[u] = (blk * p.Hkv + g) * p.S;  // in 64-channel rows
             s_tok[u] = j * p.S;
         }
@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(W * 32, 512 / (W * 32)) sparse_attn_kernel(Att
                 const unsigned m = __ballot_sync(0xffffffffu, own);
                 if (own) {
                     const int pos = n + __popc(m & ((1u << lane) - 1u));
-                    const int blk = __ldg(p.page_table + (size_t)b * p.max_pages + j / p.stride);
+                    const int blk = checked_block(__ldg(p.page_table + (size_t)b * p.max_pages + j / p.stride), p.num_blocks);
                     s_base[pos] = (blk * p.Hkv + g) * p.S;
                     s_tok[pos] = j * p.S;
                 }
@@ -336,7 +336,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) sparse_attn_tma_kernel(
         // j < P_b of the row, in order, through the same gather + attention machinery
         const int P = (L + p.S - 1) / p.S;
         for (int u = threadIdx.x; u < P; u += blockDim.x) {
-            const int blk = __ldg(p.page_table + (size_t)b * p.max_pages + u);
+            const int blk = checked_block(__ldg(p.page_table + (size_t)b * p.max_pages + u), p.num_blocks);
             pages[u] = make_int2((blk * p.Hkv + g) * p.S, u * p.S);
         }
         if (threadIdx.x == 0) s_nown = P;
@@ -348,7 +348,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) sparse_attn_tma_kernel(
         const int *blks = p.sel_blk ? p.sel_blk + (size_t)row * p.sel_stride : nullptr;
         for (int u = threadIdx.x; u < cnt; u += blockDim.x) {
             const int j = __ldcg(ids + u);
-            const int blk = blks ? __ldcg(blks + u) : __ldg(p.page_table + (size_t)b * p.max_pages + j);
+            const int blk = checked_block(blks ? __ldcg(blks + u) : __ldg(p.page_table + (size_t)b * p.max_pages + j), p.num_blocks);
             pages[u] = make_int2((blk * p.Hkv + g) * p.S, j * p.S);
         }
         if (threadIdx.x == 0) s_nown = cnt;
@@ -362,7 +362,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) sparse_attn_tma_kernel(
             const bool own = j >= 0 && j % p.stride == p.offset;
             const unsigned m = __ballot_sync(0xffffffffu, own);
             if (own) {
-                const int blk = __ldg(p.page_table + (size_t)b * p.max_pages + j / p.stride);
+                const int blk = checked_block(__ldg(p.page_table + (size_t)b * p.max_pages + j / p.stride), p.num_blocks);
                 pages[n + __popc(m & ((1u << lane) - 1u))] = make_int2((blk * p.Hkv + g) * p.S, j * p.S);
             }
             n += __popc(m);

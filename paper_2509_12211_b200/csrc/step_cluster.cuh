@@ -170,7 +170,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
         }
         if (own && lane >= 16 && lane < 24) {  // the new token's K and V rows (16 B per lane)
             const int c = lane - 16;
-            const int blk = p.page_table[(size_t)b * p.max_pages + max(ja, 0)];  // (ja >= 0 when own)
+            const int blk = checked_block(p.page_table[(size_t)b * p.max_pages + max(ja, 0)], ap.num_blocks);  // (ja >= 0 when own)
             const size_t src = ((size_t)b * p.Hkv + g) * kAttnD + c * 8;
             const size_t dst = (((size_t)blk * p.Hkv + g) * p.S + aslot) * kAttnD + c * 8;
             uint16_t *kp = const_cast<uint16_t *>(static_cast<const uint16_t *>(ap.k_pool));
@@ -334,7 +334,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
     int *out_id = p.sel_ids + (size_t)row * p.kmax;
     uint32_t *cand = reinterpret_cast<uint32_t *>(wpart);  // free until the attention ends
     auto emit_pg = [&](int pos, int pg) {
-        if (pos >= u0 && pos < u1) sel[pos - u0] = make_int2((ptrow[pg] * p.Hkv + g) * S, pg * S);
+        if (pos >= u0 && pos < u1) sel[pos - u0] = make_int2((checked_block(ptrow[pg], ap.num_blocks) * p.Hkv + g) * S, pg * S);
         if (pos >= w0 && pos < w1) out_id[pos] = pg;
     };
     if (two) {

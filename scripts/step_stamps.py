@@ -3,6 +3,8 @@ score_select_kernel (K1) and sparse_attn_kernel (K2) in one ts_decode_step."""
 import ctypes, os, sys
 import numpy as np, torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__))); sys.path.insert(0, ROOT)
+os.environ["TS_DEV_LIB"] = "1"  # the timestamp hooks exist in the dev build only
+from paper_2509_12211_b200 import _build; _build.build(dev=True)
 import synth, paper_2509_12211_b200 as ts
 name = sys.argv[1] if len(sys.argv) > 1 else "c3"
 kv = sys.argv[2] if len(sys.argv) > 2 else "bf16"  # bf16 | fp8
