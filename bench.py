@@ -266,6 +266,19 @@ def run_reference(args, cfg, world, rank):
     print(json.dumps(line), flush=True)
 
 
+def traffic_key(args, cfg):
+    """profiles/traffic.json key of a bench workload: config, then -b<batch> / -slice<N> /
+    -fp8 when they apply (scripts/r2_evidence.sh writes the same keys)."""
+    k = cfg.name
+    if args.batch:
+        k += f"-b{args.batch}"
+    if args.slice > 1:
+        k += f"-slice{args.slice}"
+    if args.kv == "fp8":
+        k += "-fp8"
+    return k
+
+
 def config_json(cfg, world, mode, extra=None):
     c = {"workload": f"{cfg.name}: {cfg.note}", "batch_per_rank": cfg.batch,
          "num_q_heads": cfg.num_q_heads, "num_kv_heads": cfg.num_kv_heads,
@@ -663,7 +676,7 @@ def main():
         traffic, tsrc = None, None
         try:  # DRAM bytes per launch of this kernel from the committed ncu capture
             with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-                tj = json.load(f).get(cfg.name)
+                tj = json.load(f).get(traffic_key(args, cfg))
             if tj and dom in tj["per_launch_bytes"]:
                 traffic = tj["per_launch_bytes"][dom]
                 tsrc = "ncu --set full: dram__bytes_read.sum + dram__bytes_write.sum, profiles/" + tj["report"]
