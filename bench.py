@@ -211,6 +211,7 @@ def oracle_rate(cfg, rep_cpu, budget_s: float, max_rows=None):
                            threads=threads)
         return time.perf_counter() - t0
 
+    cores = oracle.num_threads()  # before the 1-thread variant sets the OpenMP team to 1
     t1 = run(1)
     nseq = max(1, min(nb, int(budget_s / 4 / max(t1, 1e-6))))
     calls = [run(nseq) for _ in range(3)]
@@ -219,7 +220,8 @@ def oracle_rate(cfg, rep_cpu, budget_s: float, max_rows=None):
     extras = {"best_of": 3, "cpu_model": cpu_model(),
               "threads1_steps_per_s": 1.0 / (one * B),
               "affinity_cores": len(os.sched_getaffinity(0))}
-    return 1.0 / (best / nseq * B), oracle.num_threads(), (
+    run(1, threads=cores)  # restore the OpenMP team size for later oracle calls
+    return 1.0 / (best / nseq * B), cores, (
         f"best of 3 oracle decode_step calls on {nseq}/{B} sequences (all {cfg.num_q_heads} q "
         f"heads, metadata recomputed from K, OpenMP over rows), {sum(calls):.1f} s; 1-thread "
         f"figure: best of 3 calls on 1 sequence; steps/s scaled to the full batch"), extras
