@@ -52,12 +52,12 @@ DEV void umma_f16(uint32_t tmem, uint64_t ad, uint64_t bd, uint32_t idesc, uint3
                  ::"r"(tmem), "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
 }
 
-template <int MODE>  // 0 = mma.sync, 1 = tcgen05
+template <int MODE>  // 0 = mma.sync, 1 = tcgen05 (serial), 2 = tcgen05 double-buffered (issue block i+1 before reading i)
 __global__ void __launch_bounds__(128) bench(const uint16_t *kg, const uint16_t *qg, int iters,
                                              float *out, unsigned long long *cyc) {
     extern __shared__ __align__(1024) uint8_t sm[];
     uint8_t *base = sm + ((1024u - (smem_u32(sm) & 1023u)) & 1023u);
-    const uint32_t kb = smem_u32(base), qb = kb + 128 * 128, bar = qb + 1024;
+    const uint32_t kb = smem_u32(base), qb = kb + 128 * 128, bar = qb + 1024, bar2 = bar + 8;
     __shared__ uint32_t tmem_base;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     // stage K [128][64] and q [8][64] with the 128-byte swizzle (16 B chunk c of row r at c ^ (r & 7))
@@ -69,8 +69,8 @@ __global__ void __launch_bounds__(128) bench(const uint16_t *kg, const uint16_t 
         const int r = i >> 3, c = i & 7;
         *reinterpret_cast<uint4 *>(base + 128 * 128 + r * 128 + ((c ^ (r & 7)) << 4)) = reinterpret_cast<const uint4 *>(qg)[i];
     }
-    if (tid == 0) mbar_init(bar, 1);
-    if (MODE == 1 && warp == 0) {
+    if (tid == 0) { mbar_init(bar, 1); mbar_init(bar2, 1); }
+    if (MODE >= 1 && warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;" ::"r"(smem_u32(&tmem_base)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
@@ -78,7 +78,12 @@ __global__ void __launch_bounds__(128) bench(const uint16_t *kg, const uint16_t 
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint32_t tm = MODE == 1 ? tmem_base : 0u;
+    const uint32_t tm = MODE >= 1 ? tmem_base : 0u;
+    if (MODE == 2 && tid == 0) {  // prologue: block 0 into columns [0, 8)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) umma_f16(tm, sw128_desc(kb + 32 * k), sw128_desc(qb + 32 * k), kIdesc, k > 0);
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+    }
     const int gid = lane >> 2, t = lane & 3;
     float acc = 0.f;
     float s[8];
@@ -113,6 +118,29 @@ __global__ void __launch_bounds__(128) bench(const uint16_t *kg, const uint16_t 
                 }
                 acc += sacc[0][0] + sacc[1][1];
             }
+        } else if (MODE == 2) {
+            const uint32_t cur = (it & 1) * 8, nxt = ((it + 1) & 1) * 8;
+            if (tid == 0 && it + 1 < iters) {  // block it+1 into the other column set
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+                for (int k = 0; k < 4; ++k) umma_f16(tm + nxt, sw128_desc(kb + 32 * k), sw128_desc(qb + 32 * k), kIdesc, k > 0);
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"((it + 1) & 1 ? bar2 : bar) : "memory");
+            }
+            mbar_wait((it & 1) ? bar2 : bar, (it >> 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            uint32_t r[8];
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                         : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                         : "r"(tm + cur + ((uint32_t)(warp * 32) << 16)));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+            for (int j = 0; j < 8; ++j) s[j] = __uint_as_float(r[j]);
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            if (it == iters - 1)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) out[((size_t)blockIdx.x * 128 + warp * 32 + lane) * 8 + j] = s[j];
+            acc += s[0] + s[7];
+            __syncthreads();  // columns `cur` are free for block it+2
         } else {
             if (warp == 0 && lane == 0) {
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -142,7 +170,7 @@ __global__ void __launch_bounds__(128) bench(const uint16_t *kg, const uint16_t 
     unsigned long long t1 = clock64();
     if (tid == 0) cyc[blockIdx.x] = t1 - t0;
     if (acc == 1.2345f) out[0] = acc;
-    if (MODE == 1) {
+    if (MODE >= 1) {
         __syncthreads();
         if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;" ::"r"(tm));
     }
@@ -168,22 +196,30 @@ int main() {
     const size_t smb = 1024 + 128 * 128 + 1024 + 64;
     cudaFuncSetAttribute(bench<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb);
     cudaFuncSetAttribute(bench<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb);
+    cudaFuncSetAttribute(bench<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb);
     const int iters = 2000;
-    std::vector<unsigned long long> c(sms);
-    for (int mode = 0; mode < 2; ++mode) {
-        for (int rep = 0; rep < 2; ++rep) {
-            if (mode == 0) bench<0><<<sms, 128, smb>>>(dk, dq, iters, o0, cyc);
-            else bench<1><<<sms, 128, smb>>>(dk, dq, iters, o1, cyc);
+    const char *names[3] = {"mma.sync m16n8k16 (64 HMMA, 4 warps)", "tcgen05.mma M128 N8 x4, serial issue->commit->wait->ld",
+                            "tcgen05.mma M128 N8 x4, double-buffered TMEM (issue i+1 before ld of i)"};
+    for (int bps : {1, 4}) {
+        const int grid = sms * bps;
+        std::vector<unsigned long long> c(grid);
+        cudaFree(cyc); cudaMalloc(&cyc, grid * 8);
+        cudaFree(o0); cudaFree(o1); cudaMalloc(&o0, grid * 128 * 8 * 4); cudaMalloc(&o1, grid * 128 * 8 * 4);
+        for (int mode = 0; mode < 3; ++mode) {
+            for (int rep = 0; rep < 2; ++rep) {
+                if (mode == 0) bench<0><<<grid, 128, smb>>>(dk, dq, iters, o0, cyc);
+                else if (mode == 1) bench<1><<<grid, 128, smb>>>(dk, dq, iters, o1, cyc);
+                else bench<2><<<grid, 128, smb>>>(dk, dq, iters, o1, cyc);
+            }
+            cudaError_t e = cudaDeviceSynchronize();
+            if (e != cudaSuccess) { printf("mode %d: %s\n", mode, cudaGetErrorString(e)); return 1; }
+            cudaMemcpy(c.data(), cyc, grid * 8, cudaMemcpyDeviceToHost);
+            double mean = 0;
+            for (auto x : c) mean += x;
+            mean /= grid;
+            printf("%d CTA/SM  %-75s %7.1f cycles per block per CTA, %6.1f per block per SM\n", bps, names[mode],
+                   mean / iters, mean / iters / bps);
         }
-        cudaError_t e = cudaDeviceSynchronize();
-        if (e != cudaSuccess) { printf("mode %d: %s\n", mode, cudaGetErrorString(e)); return 1; }
-        cudaMemcpy(c.data(), cyc, sms * 8, cudaMemcpyDeviceToHost);
-        double mean = 0;
-        for (auto x : c) mean += x;
-        mean /= sms;
-        printf("%s: %.1f cycles per 128-token x 8-head score block (QK^T), one CTA / SM\n",
-               mode == 0 ? "mma.sync m16n8k16 (4 warps, 64 HMMA)" : "tcgen05.mma M128 N8 K16 x4 + commit + mbarrier + tcgen05.ld",
-               mean / iters);
     }
     std::vector<float> a(sms * 128 * 8), b(sms * 128 * 8);
     cudaMemcpy(a.data(), o0, a.size() * 4, cudaMemcpyDeviceToHost);
