@@ -410,7 +410,7 @@ def main():
     torch.cuda.synchronize()
     # launches of our kernels per step, as reported by the C ABI for the step just run
     # (bf16: 1 = decode_cluster_kernel; sequence sharding: 5 calls + 2 collectives)
-    launches_per_step = ts.launch_count() if not seq else 5
+    launches_per_step = ts.launch_count() if not seq else (3 if reps[0]["shard"].fused else 5)
     single = not seq and launches_per_step == 1
     fused = cfg.dtype == "bf16" and cfg.group <= 8 and not seq and not single
 
@@ -694,8 +694,10 @@ def main():
         # per-rank bytes (owned metadata + owned selected K/V + exchange buffers) over the
         # per-step time of the whole sharded step (5 kernels + 2 NCCL all-gathers)
         achieved = kb["total"] / (ms_per_step * 1e-3) / 1e9
-        roof = {"bound": "hbm", "kernel": "sequence-sharded step per rank (score, select, "
-                "select_merge, sparse_attn, lse_merge + 2 NCCL all-gathers)",
+        roof = {"bound": "hbm", "kernel": ("sequence-sharded step per rank (select_candidates, "
+                "shard_attend, lse_merge + 2 all-gathers)" if reps[0]["shard"].fused else
+                "sequence-sharded step per rank (score, select, select_merge, sparse_attn, "
+                "lse_merge + 2 all-gathers)"),
                 "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": None, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": kb["total"], "avg_launch_us": ms_per_step * 1e3}

@@ -12,7 +12,10 @@
  *   ts_decode_step        score -> select -> attend in one call  Alg. 1, PAPER.md:209-249 ("single pass")
  *   ts_decode_step_append append the new token, then the step     Eq. 1 + Alg. 1 (one launch, bf16)
  *   ts_decode_step_prefetch the step + L2 prefetch of the previous selection
+ *   ts_select_candidates  score + local top-k of a sequence shard (one launch)
+ *   ts_shard_attend       candidate merge + partial attention of a shard (one launch)
  *   ts_lse_merge          merge of partial attentions (split-K / multi-GPU)
+ *   ts_kv_quantize        bf16 rows -> FP8 E4M3 codes + row exponents (NEXT-3, reading R21)
  *
  * Conventions (apply to every entry point):
  *  - POINTERS: every tensor argument is a DEVICE pointer (cudaMalloc'd or torch CUDA
@@ -215,6 +218,38 @@ ts_status ts_decode_step_prefetch(const ts_layout *layout, const void *q, const 
 ts_status ts_select_merge(const float *cand_scores, const int32_t *cand_ids, int32_t parts,
                           int64_t part_stride, int32_t rows, int32_t k_part, int32_t k,
                           int32_t *sel_ids, float *sel_scores, int32_t *sel_count, void *stream);
+
+/* Sequence sharding, fused (the north star's "each GPU scores its pages and
+ * keeps a local top-k of candidates ... computes partial (o, m, l) on its own selected
+ * pages"): the two halves of one rank's step, one launch each, around the two exchanges.
+ *
+ * ts_select_candidates — ts_score_pages + ts_select_topk in one launch: for every row
+ * (b, g), the k owned pages with the largest scores (Eq. 2, reading R9), ties to the lower
+ * id, as GLOBAL ids ascending in cand_ids [rows][k] (-1 padding) with their fp32 scores in
+ * cand_scores [rows][k] (-inf padding) and the count in cand_count [rows].  Equals
+ * ts_score_pages followed by ts_select_topk(id_stride = shard_stride, id_offset =
+ * shard_offset).  bf16 q / metadata (bf16 or FP8 caches), head_dim 64, G <= 8, k <= 4096;
+ * TS_ERR_UNSUPPORTED otherwise (compose the two calls instead). */
+ts_status ts_select_candidates(const ts_layout *layout, const void *q, const void *meta,
+                               const int32_t *page_table, const int32_t *seq_lens, int32_t k,
+                               float *cand_scores, int32_t *cand_ids, int32_t *cand_count,
+                               void *stream);
+
+/* ts_shard_attend — ts_select_merge + ts_sparse_decode_attn in one launch: the global top-k
+ * over `parts` candidate lists (part p of row r: k entries at p*part_stride + r*k of
+ * cand_scores / cand_ids, e.g. the all-gathered ts_select_candidates outputs; part_stride 0
+ * = rows*k; -inf entries ignored; ties to the lower global id), then the partial attention
+ * over the OWNED selected pages exactly as ts_sparse_decode_attn: o [B][Hq][d], lse [B][Hq]
+ * (o = 0, lse = -inf for a row with no owned selected page).  The selection itself is
+ * written to sel_ids_out [rows][k] / sel_count_out [rows] when non-NULL (identical on every
+ * rank).  bf16 K/V, head_dim 64, page_size a multiple of 16, G <= 8, parts*k <= 4096;
+ * ws >= ts_attn_workspace_bytes(layout, k), zero-filled once; TS_ERR_UNSUPPORTED otherwise. */
+ts_status ts_shard_attend(const ts_layout *layout, const void *q, const void *k_pool,
+                          const void *v_pool, const int32_t *page_table, const int32_t *seq_lens,
+                          const float *cand_scores, const int32_t *cand_ids, int32_t parts,
+                          int64_t part_stride, int32_t k, float scale, float *o, float *lse,
+                          int32_t *sel_ids_out, int32_t *sel_count_out, void *ws, size_t ws_bytes,
+                          void *stream);
 
 /* Log-sum-exp merge of `parts` partial attentions over disjoint token sets.  Part p of
  * o_parts starts at p*part_stride and holds [rows][d]; part p of lse_parts starts at

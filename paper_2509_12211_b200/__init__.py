@@ -21,6 +21,7 @@ __all__ = ["Layout", "TinyServeError", "make_layout", "meta_append", "meta_build
            "score_pages", "select_topk", "sparse_decode_attn", "decode_step", "decode_step_append", "decode_step_prefetch", "select_merge", "lse_merge",
            "workspace_bytes", "attn_workspace_bytes", "dense_decode_attn", "dense_workspace_bytes", "new_workspace", "new_meta", "kmax", "launch_count",
            "profile_events", "kv_quantize", "fp8_pool", "fp8_views", "pool_bytes",
+           "select_candidates", "shard_attend",
            "exported_symbols", "PagedKV"]
 
 
@@ -327,6 +328,46 @@ def select_merge(cand_scores, cand_ids, k, parts=None, rows=None, k_part=None, p
         cand_scores.data_ptr(), cand_ids.data_ptr(), parts, part_stride, rows, k_part, k,
         _ptr(sel_ids), _ptr(sel_scores), _ptr(sel_count), _stream(stream)))
     return sel_ids, sel_scores, sel_count
+
+
+def select_candidates(layout, q, meta, page_table, seq_lens, k, cand_scores=None, cand_ids=None,
+                      cand_count=None, stream=None):
+    """One rank's local half of the sequence-sharded step (ts_select_candidates): the k owned
+    pages with the largest scores per row, GLOBAL ids ascending.  Returns (scores, ids, count)."""
+    rows, dev = layout.batch * layout.num_kv_heads, q.device
+    if cand_scores is None:
+        cand_scores = torch.empty((rows, k), dtype=torch.float32, device=dev)
+    if cand_ids is None:
+        cand_ids = torch.empty((rows, k), dtype=torch.int32, device=dev)
+    if cand_count is None:
+        cand_count = torch.empty((rows,), dtype=torch.int32, device=dev)
+    _cuda(q, meta, page_table, seq_lens, cand_scores, cand_ids, cand_count)
+    check("ts_select_candidates", lib().ts_select_candidates(
+        layout, _ptr(q), _ptr(meta), _ptr(page_table), _ptr(seq_lens), int(k), _ptr(cand_scores),
+        _ptr(cand_ids), _ptr(cand_count), _stream(stream)))
+    return cand_scores, cand_ids, cand_count
+
+
+def shard_attend(layout, q, k_pool, v_pool, page_table, seq_lens, cand_scores, cand_ids, parts, k,
+                 scale, part_stride=0, o=None, lse=None, sel_ids=None, sel_count=None, ws=None,
+                 stream=None):
+    """Candidate merge + partial attention over the owned selected pages (ts_shard_attend).
+    cand_scores / cand_ids: `parts` lists of [rows][k] (part_stride elements apart; 0 =
+    contiguous).  Returns (o, lse, sel_ids, sel_count)."""
+    dev = q.device
+    if o is None:
+        o = torch.empty((layout.batch, layout.num_q_heads, layout.head_dim), dtype=torch.float32, device=dev)
+    if lse is None:
+        lse = torch.empty((layout.batch, layout.num_q_heads), dtype=torch.float32, device=dev)
+    if ws is None:
+        ws = new_workspace(attn_workspace_bytes(layout, k), dev)
+    _cuda(q, k_pool, v_pool, page_table, seq_lens, o, lse, sel_ids, sel_count, ws)
+    check("ts_shard_attend", lib().ts_shard_attend(
+        layout, _ptr(q), _ptr(k_pool), _ptr(v_pool), _ptr(page_table), _ptr(seq_lens),
+        cand_scores.data_ptr(), cand_ids.data_ptr(), int(parts), int(part_stride), int(k),
+        float(scale), _ptr(o), _ptr(lse), _ptr(sel_ids), _ptr(sel_count), _ptr(ws), ws.numel(),
+        _stream(stream)))
+    return o, lse, sel_ids, sel_count
 
 
 def lse_merge(o_parts, lse_parts, o=None, lse=None, parts=None, rows=None, d=None,

@@ -24,7 +24,7 @@ SYMBOLS = ["ts_meta_append", "ts_meta_build", "ts_score_pages", "ts_select_topk"
            "ts_sparse_decode_attn", "ts_decode_step", "ts_decode_step_append", "ts_decode_step_prefetch", "ts_select_merge", "ts_lse_merge", "ts_workspace_bytes",
            "ts_attn_workspace_bytes", "ts_status_str", "ts_version", "ts_last_launch_count",
            "ts_profile_events", "ts_dense_decode_attn", "ts_dense_workspace_bytes",
-           "ts_kv_quantize", "ts_pool_bytes"]
+           "ts_kv_quantize", "ts_pool_bytes", "ts_select_candidates", "ts_shard_attend"]
 
 
 class TinyServeError(RuntimeError):
@@ -72,6 +72,8 @@ def lib() -> ctypes.CDLL:
             "ts_lse_merge": [I, I, I, P, P, ctypes.c_int64, P, P, P],
             "ts_dense_decode_attn": [LP, P, P, P, P, P, F, P, P, P, SZ, P],
             "ts_kv_quantize": [ctypes.c_int64, I, P, P, P, P],
+            "ts_select_candidates": [LP, P, P, P, P, I, P, P, P, P],
+            "ts_shard_attend": [LP, P, P, P, P, P, P, P, I, ctypes.c_int64, I, F, P, P, P, P, P, SZ, P],
         }
         for name, args in sig.items():
             fn = getattr(L, name)

@@ -600,7 +600,7 @@ ts_status launch_step_cluster_t(const ts_layout *L, ScoreSelParams &sp, const At
 
 ts_status launch_score_select(const ts_layout *L, const void *q, const void *meta, const int *pt,
                               const int *sl, int *ids, int *blk, int *cnt, int kmax,
-                              cudaStream_t st) {
+                              cudaStream_t st, float *sel_scores = nullptr) {
     const int rows = L->batch * L->num_kv_heads;
     if (rows == 0) return TS_OK;
     ScoreSelParams p{};
@@ -619,6 +619,9 @@ ts_status launch_score_select(const ts_layout *L, const void *q, const void *met
     p.max_pages = L->max_pages;
     p.kmax = kmax;
     p.dbg = g_dbg_ss;
+    p.stride = L->shard_stride;
+    p.offset = L->shard_offset;
+    p.sel_scores = sel_scores;
     static const int per_sm = env_int("TS_SS_PER_SM", 3);
     static const int cmax = std::min(kMaxClusterC, std::max(1, env_int("TS_SS_CMAX", 16)));
     const int target = device_sms() * per_sm;
@@ -1072,6 +1075,53 @@ size_t ts_pool_bytes(const ts_layout *L) {
     const size_t n = (size_t)L->num_blocks * L->num_kv_heads * L->page_size;
     if (L->kv_dtype == TS_FP8E4M3) return n * (L->head_dim + 1);
     return n * L->head_dim * (L->kv_dtype == TS_BF16 ? 2 : 4);
+}
+
+// The two halves of one rank's sequence-sharded step, one launch each.
+ts_status ts_select_candidates(const ts_layout *L, const void *q, const void *meta,
+                               const int32_t *page_table, const int32_t *seq_lens, int32_t k,
+                               float *cand_scores, int32_t *cand_ids, int32_t *cand_count,
+                               void *stream) {
+    g_launches = 0;
+    ts_status s = check_layout(L);
+    if (s != TS_OK) return s;
+    if (k < 1) return TS_ERR_SHAPE;
+    if (!aligned16(q) || !aligned16(meta)) return TS_ERR_ALIGN;
+    if (L->kv_dtype == TS_F32 || group_of(L) > 8 || L->head_dim != 64 || k > kMaxSel)
+        return TS_ERR_UNSUPPORTED;  // (the composed ts_score_pages + ts_select_topk cover these)
+    const ts_layout v = score_view(L);
+    return launch_score_select(&v, q, meta, page_table, seq_lens, cand_ids, nullptr, cand_count, k,
+                               as_stream(stream), cand_scores);
+}
+
+ts_status ts_shard_attend(const ts_layout *L, const void *q, const void *k_pool, const void *v_pool,
+                          const int32_t *page_table, const int32_t *seq_lens,
+                          const float *cand_scores, const int32_t *cand_ids, int32_t parts,
+                          int64_t part_stride, int32_t k, float scale, float *o, float *lse,
+                          int32_t *sel_ids_out, int32_t *sel_count_out, void *ws, size_t ws_bytes,
+                          void *stream) {
+    g_launches = 0;
+    ts_status s = check_layout(L);
+    if (s != TS_OK) return s;
+    if (parts < 1 || k < 1 || part_stride < 0) return TS_ERR_SHAPE;
+    if (!aligned16(q) || !aligned16(k_pool) || !aligned16(v_pool) || !aligned16(o)) return TS_ERR_ALIGN;
+    if (!bf16_attn_supported(L) || L->page_size % 16 != 0 || k > kMaxSel) return TS_ERR_UNSUPPORTED;
+    const long long pg = (long long)L->max_pages * L->shard_stride;  // global pages of a row
+    const size_t scratch = (size_t)((parts * k + 3) & ~3) * 8 + (size_t)((pg + 31) / 32 + 4) * 8 +
+                           (kSsHistM + 64 + 128 + (size_t)k) * 4;
+    if (scratch > (size_t)8 * SatSmem<4, 8>::kStage || (long long)parts * k > 4096) return TS_ERR_UNSUPPORTED;
+    if (!ws || ws_bytes < attn_ws_layout(L, k).total) return TS_ERR_WORKSPACE;
+    if (L->batch == 0) return TS_OK;
+    AttnParams p = attn_params(L, q, k_pool, v_pool, page_table, seq_lens, nullptr, nullptr, k, scale,
+                               o, lse, ws);
+    p.cand_scores = cand_scores;
+    p.cand_ids = cand_ids;
+    p.cand_parts = parts;
+    p.cand_k = k;
+    p.cand_part_stride = part_stride ? part_stride : (long long)L->batch * L->num_kv_heads * k;
+    p.sel_out = sel_ids_out;
+    p.sel_cnt_out = sel_count_out;
+    return launch_sat<4, 8>(L, p, true, as_stream(stream));
 }
 
 ts_status ts_select_merge(const float *cand_scores, const int32_t *cand_ids, int32_t parts,

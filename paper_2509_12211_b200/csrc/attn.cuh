@@ -41,6 +41,15 @@ struct AttnParams {
     int dense;                // 1: attend every page (FullCache baseline), sel_* unused
     const int8_t *k_exp;      // FP8 KV (reading R21): row exponents [NB][Hkv][S] (else null)
     const int8_t *v_exp;
+    // ts_shard_attend (sequence sharding): the selection is the global top-k
+    // over `cand_parts` candidate lists (part q of row r: cand_k entries at
+    // q * cand_part_stride + r * cand_k; -inf = none), merged in the kernel's prologue;
+    // rank-0 CTAs write it to sel_out / sel_cnt_out (nullable)
+    const float *cand_scores;
+    const int *cand_ids;
+    int cand_parts, cand_k;
+    long long cand_part_stride;
+    int *sel_out, *sel_cnt_out;
 };
 
 constexpr int kAttnD = 64;        // head_dim of the tensor-core path

@@ -284,6 +284,13 @@ TS_DEV int clamp_len(int L, int max_pages, int stride, int S) {
     return L < cap ? L : (int)cap;
 }
 
+// local page count of a sequence of L tokens under block-cyclic ownership:
+// global pages j < ceil(L / S) with j % stride == offset
+TS_DEV int local_pages(int L, int S, int stride, int offset) {
+    const int P = (L + S - 1) / S;
+    return P > offset ? (P - offset + stride - 1) / stride : 0;
+}
+
 // Orderable key of an fp32 score: larger score <-> larger unsigned key; -0.0 == +0.0.
 TS_DEV uint32_t score_key(float s) {
     uint32_t u = __float_as_uint(s + 0.0f);  // -0.0 + 0.0 = +0.0 (round-to-nearest)

@@ -26,11 +26,6 @@ struct ScoreParams {
     int B, Hq, Hkv, G, D, S, max_pages, stride, offset;
 };
 
-// local page count of row b under block-cyclic ownership
-TS_DEV int local_pages(int L, int S, int stride, int offset) {
-    const int P = (L + S - 1) / S;
-    return P > offset ? (P - offset + stride - 1) / stride : 0;
-}
 
 // ------------------------------------------------------------------ tensor-core path
 // D = 64 or 128 (bf16).  CTA = 4 warps, each warp 2 tiles of 16 pages -> 128 pages/CTA.

@@ -51,6 +51,11 @@ struct ScoreSelParams {
     const int *prev_count;
     const uint16_t *k_pool;   // pools for the prefetch addresses ([NB][Hkv][S][64])
     const uint16_t *v_pool;
+    // score_select_kernel, ts_select_candidates (the local half of the sequence-sharded step,
+    // DESIGN.md §6): block-cyclic ownership (stride > 1: local page jl = global jl * stride +
+    // offset); the selection is emitted with GLOBAL ids and, if sel_scores is set, its scores
+    int stride, offset;
+    float *sel_scores;        // [rows][kmax] (nullable), -inf padding
 };
 
 constexpr int kSsStagePages = 32;                         // pages per ring stage
@@ -470,10 +475,12 @@ __global__ void __launch_bounds__((W + 1) * 32) score_select_kernel(ScoreSelPara
     if (p.C > 1) cluster_arrive_relaxed();  // "this CTA is running" (before any DSMEM access)
     pdl_wait();  // inputs may come from the previous kernel in the stream (PDL launch)
 
-    const int L = clamp_len(p.seq_lens[b], p.max_pages, 1, p.S);
-    const int P = (L + p.S - 1) / p.S;
+    const int sst = p.stride > 1 ? p.stride : 1;  // block-cyclic sharding (ts_select_candidates)
+    const int L = clamp_len(p.seq_lens[b], p.max_pages, sst, p.S);
+    const int P = sst > 1 ? local_pages(L, p.S, sst, p.offset) : (L + p.S - 1) / p.S;  // local pages
     const int j0 = rank * p.chunk;
-    const bool pt_bulk = (p.max_pages & 3) == 0;  // row start 16-byte aligned
+    // page-table row -> smem only when the blocks of the selection are wanted (sel_blk)
+    const bool pt_bulk = (p.max_pages & 3) == 0 && p.sel_blk != nullptr;  // row start 16-byte aligned
     const int nloc = max(0, min(P - j0, p.chunk));  // valid pages of this CTA
     const int nst = (nloc + kSsStagePages - 1) / kSsStagePages;
 
@@ -599,17 +606,20 @@ __global__ void __launch_bounds__((W + 1) * 32) score_select_kernel(ScoreSelPara
     __syncthreads();
     SS_STAMP(4);
     int *out_id = p.sel_ids + (size_t)row * p.kmax;
-    int *out_blk = p.sel_blk + (size_t)row * p.kmax;
+    int *out_blk = p.sel_blk ? p.sel_blk + (size_t)row * p.kmax : nullptr;
+    float *out_sc = p.sel_scores ? p.sel_scores + (size_t)row * p.kmax : nullptr;
     uint32_t *cand = reinterpret_cast<uint32_t *>(smem + SM::kQ);  // q is in registers by now
     const int kk = cta_topk<NT, 0>(keys, P, p.kmax, *s_kmin, *s_kmax, hist, red, cand,
                                 [&](int pos, int i) {
-                                    out_id[pos] = i;
-                                    out_blk[pos] = ptrow[i];
+                                    out_id[pos] = i * sst + (sst > 1 ? p.offset : 0);  // global id
+                                    if (out_blk) out_blk[pos] = ptrow[i];
+                                    if (out_sc) out_sc[pos] = key_score(keys[i]);
                                 }, dts);
     SS_STAMP(7);
     for (int i = kk + tid; i < p.kmax; i += NT) {
         out_id[i] = -1;
-        out_blk[i] = 0;
+        if (out_blk) out_blk[i] = 0;
+        if (out_sc) out_sc[i] = kNegInf;
     }
     if (tid == 0) p.sel_count[row] = kk;
     SS_STAMP(3);

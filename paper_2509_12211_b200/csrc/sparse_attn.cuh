@@ -26,8 +26,11 @@
 
 #include "attn.cuh"
 #include "common.cuh"
+#include "score_select.cuh"  // cta_topk, block_scan (the candidate merge of ts_shard_attend)
 
 namespace ts {
+
+constexpr int kSsHistM = 2048;  // radix bins of the candidate merge
 
 
 
@@ -340,6 +343,90 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) sparse_attn_tma_kernel(
             pages[u] = make_int2((blk * p.Hkv + g) * p.S, u * p.S);
         }
         if (threadIdx.x == 0) s_nown = P;
+    } else if (p.cand_scores) {
+        // ts_shard_attend: the global top-k over the ranks' candidates (the exchange step of
+        // sequence sharding), merged here instead of by a separate kernel.
+        // The candidates are placed in ascending GLOBAL page id order (a bitmap over the
+        // row's pages + a prefix count: ids are unique), so cta_topk's lower-index tie-break
+        // is the lower-global-id rule (reading R6) and the output comes out ascending.
+        // Scratch lives in the TMA ring, which is idle until the producer starts.
+        const int Pg = (L + p.S - 1) / p.S;  // global pages of the row
+        const int nw = (Pg + 31) >> 5;
+        const int ncand = p.cand_parts * p.cand_k;
+        const int n4 = (ncand + 3) & ~3;
+        uint32_t *mkeys = reinterpret_cast<uint32_t *>(smem + SM::kRing);
+        int *mids = reinterpret_cast<int *>(mkeys + n4);
+        const int nw4 = (nw + 3) & ~3;  // 16-byte aligned sub-arrays (cta_topk reads int4 / uint4)
+        uint32_t *bits = reinterpret_cast<uint32_t *>(mids + n4);
+        int *wpre = reinterpret_cast<int *>(bits + nw4);
+        int *mhist = wpre + nw4;
+        int *mred = mhist + kSsHistM;
+        uint32_t *mcand = reinterpret_cast<uint32_t *>(mred + 64);
+        int *msel = reinterpret_cast<int *>(mcand + 2 * 64);
+        constexpr int NT = (W + 1) * 32;
+        for (int i = threadIdx.x; i < nw; i += NT) bits[i] = 0u;
+        for (int i = threadIdx.x; i < kSsHistM; i += NT) mhist[i] = 0;
+        __syncthreads();
+        for (int e = threadIdx.x; e < ncand; e += NT) {
+            const size_t at = (size_t)(e / p.cand_k) * p.cand_part_stride + (size_t)row * p.cand_k + e % p.cand_k;
+            const int id = __ldcg(p.cand_ids + at);
+            if (__ldcg(p.cand_scores + at) != kNegInf && id >= 0 && id < Pg) atomicOr(&bits[id >> 5], 1u << (id & 31));
+        }
+        __syncthreads();
+        {  // exclusive prefix of the word popcounts (contiguous runs of words per thread)
+            const int per = (nw + NT - 1) / NT, w0 = threadIdx.x * per, w1 = min(nw, w0 + per);
+            int c = 0;
+            for (int w = w0; w < w1; ++w) c += __popc(bits[w]);
+            int tot;
+            int before = block_scan<NT>(c, mred, &tot);
+            for (int w = w0; w < w1; ++w) {
+                wpre[w] = before;
+                before += __popc(bits[w]);
+            }
+            if (threadIdx.x == 0) mred[63] = tot;
+        }
+        __syncthreads();
+        const int nlive = mred[63];
+        uint32_t kmn = 0xffffffffu, kmx = 0u;
+        for (int e = threadIdx.x; e < ncand; e += NT) {
+            const size_t at = (size_t)(e / p.cand_k) * p.cand_part_stride + (size_t)row * p.cand_k + e % p.cand_k;
+            const int id = __ldcg(p.cand_ids + at);
+            const float sv = __ldcg(p.cand_scores + at);
+            if (sv != kNegInf && id >= 0 && id < Pg) {
+                const int pos = wpre[id >> 5] + __popc(bits[id >> 5] & ((1u << (id & 31)) - 1u));
+                const uint32_t key = score_key(sv);
+                mkeys[pos] = key;
+                mids[pos] = id;
+                kmn = min(kmn, key);
+                kmx = max(kmx, key);
+            }
+        }
+        for (int i = nlive + threadIdx.x; i < n4; i += NT) mkeys[i] = 0u;
+        block_minmax<NT>(kmn, kmx, mred);  // (barriers inside)
+        const int kk = cta_topk<NT, 0, 11>(mkeys, nlive, p.cand_k, kmn, kmx, mhist, mred, mcand,
+                                           [&](int pos, int i) { msel[pos] = mids[i]; });
+        __syncthreads();
+        if (rank == 0) {  // the global selection (identical on every rank)
+            int *out = p.sel_out ? p.sel_out + (size_t)row * p.cand_k : nullptr;
+            for (int i = threadIdx.x; out && i < p.cand_k; i += NT) out[i] = i < kk ? msel[i] : -1;
+            if (p.sel_cnt_out && threadIdx.x == 0) p.sel_cnt_out[row] = kk;
+        }
+        if (warp == W) {  // owned pages, compacted in id order
+            int n = 0;
+            for (int u0 = 0; u0 < kk; u0 += 32) {
+                const int u = u0 + lane;
+                const int j = u < kk ? msel[u] : -1;
+                const bool own = j >= 0 && j % p.stride == p.offset;
+                const unsigned m = __ballot_sync(0xffffffffu, own);
+                if (own) {
+                    const int blk = checked_block(__ldg(p.page_table + (size_t)b * p.max_pages + j / p.stride), p.num_blocks);
+                    pages[n + __popc(m & ((1u << lane) - 1u))] = make_int2((blk * p.Hkv + g) * p.S, j * p.S);
+                }
+                n += __popc(m);
+            }
+            if (lane == 0) s_nown = n;
+        }
+        fence_proxy_async();  // every thread: its generic writes to the ring scratch precede the TMA fills
     } else if (p.stride == 1) {
         // every selected page is owned: all threads resolve entries in parallel (one load
         // round for the ids / blocks, one more for the page table when not pre-resolved)

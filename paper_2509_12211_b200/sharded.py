@@ -12,6 +12,11 @@ Block-cyclic ownership: global page j lives on rank j % G at local index j // G
   6. all-gather #2        partials [B*Hq*d | B*Hq] fp32
   7. ts_lse_merge         o = sum_r exp(lse_r - lse) o_r
 
+With the bf16 tensor-core layouts the rank's kernels are fused to two launches: steps 1-2 are
+ts_select_candidates and steps 4-5 are ts_shard_attend (candidate merge in the attention
+kernel's prologue), so one step is 3 launches + 2 all-gathers; other layouts (or an `ops`
+object without the fused calls, e.g. the CPU tests') run the composed sequence above.
+
 Every arithmetic step runs in libtinyserve.so; this module only sequences the calls and
 moves bytes (torch.distributed all_gather_into_tensor over NCCL on GPUs).  The protocol is
 written against an `ops` object with the binding's signatures so the same sequencing is
@@ -43,10 +48,26 @@ class ShardStep:
         self.o = torch.empty((B, Hq, d), dtype=torch.float32, device=device)
         self.lse = torch.empty((B, Hq), dtype=torch.float32, device=device)
         self.ws = None
+        # fused two-launch form when the ops provide it (decided on first use: a layout the
+        # fused kernels do not cover raises TS_ERR_UNSUPPORTED and falls back)
+        self.fused = hasattr(ops, "select_candidates") and hasattr(ops, "shard_attend")
+
+    def _unsupported(self, ex) -> bool:
+        return getattr(ex, "name", "") == "TS_ERR_UNSUPPORTED"
 
     # -- phase 1: local scores + local candidates ------------------------------------------
     def local_candidates(self, q, meta, page_table, seq_lens):
         ops, L = self.ops, self.L
+        if self.fused:
+            try:
+                ops.select_candidates(L, q, meta, page_table, seq_lens, self.K,
+                                      cand_scores=self.cand[0].view(torch.float32),
+                                      cand_ids=self.cand[1], cand_count=self.sel_count.view(-1))
+                return self.cand
+            except Exception as ex:  # noqa: BLE001
+                if not self._unsupported(ex):
+                    raise
+                self.fused = False
         ops.score_pages(L, q, meta, page_table, seq_lens, scores=self.scores)
         cs = self.cand[0].view(torch.float32)
         ci = self.cand[1]
@@ -59,15 +80,26 @@ class ShardStep:
     def partial_attention(self, cand_g, q, k_pool, v_pool, page_table, seq_lens, scale):
         ops, L = self.ops, self.L
         flat = cand_g.view(-1)
+        o_r = self.part[: self.nq].view(L.batch, L.num_q_heads, L.head_dim)
+        lse_r = self.part[self.nq:].view(L.batch, L.num_q_heads)
+        if self.ws is None:
+            self.ws = ops.new_workspace(ops.attn_workspace_bytes(L, self.K), q.device)
+        if self.fused:
+            try:
+                ops.shard_attend(L, q, k_pool, v_pool, page_table, seq_lens, flat.view(torch.float32),
+                                 flat[self.rows * self.K:], self.G, self.K, scale,
+                                 part_stride=2 * self.rows * self.K, o=o_r, lse=lse_r,
+                                 sel_ids=self.sel_ids, sel_count=self.sel_count, ws=self.ws)
+                return self.part
+            except Exception as ex:  # noqa: BLE001
+                if not self._unsupported(ex):
+                    raise
+                self.fused = False
         ops.select_merge(flat.view(torch.float32), flat[self.rows * self.K:], self.K,
                          parts=self.G, rows=self.rows, k_part=self.K,
                          part_stride=2 * self.rows * self.K,
                          sel_ids=self.sel_ids.view(self.rows, self.K), want_scores=False,
                          sel_count=self.sel_count.view(-1))
-        o_r = self.part[: self.nq].view(L.batch, L.num_q_heads, L.head_dim)
-        lse_r = self.part[self.nq:].view(L.batch, L.num_q_heads)
-        if self.ws is None:
-            self.ws = ops.new_workspace(ops.attn_workspace_bytes(L, self.K), q.device)
         ops.sparse_decode_attn(L, q, k_pool, v_pool, page_table, seq_lens, self.sel_ids,
                                self.sel_count, scale, o=o_r, lse=lse_r, ws=self.ws)
         return self.part
@@ -113,7 +145,7 @@ def shard_page_table(page_table: torch.Tensor, world: int, rank: int) -> torch.T
 
 
 def emulate(ops, layout_global, world, q, k_pool, v_pool, page_table, seq_lens, budget_tokens,
-            scale, metas=None):
+            scale, metas=None, fused=True):
     """Run the G-rank protocol in one process on one device (shard emulation):
     the exchanges are concatenations.  Every rank reads the same global pool through its
     local page table.  Returns (o, lse, sel_ids, sel_count) of rank 0 plus every rank's
@@ -126,6 +158,7 @@ def emulate(ops, layout_global, world, q, k_pool, v_pool, page_table, seq_lens, 
                    layout_global.head_dim, layout_global.page_size, pt.shape[1],
                    layout_global.num_blocks, world, r, layout_global.kv_dtype)
         steps.append(ShardStep(ops, L, world, r, budget_tokens, q.device))
+        steps[-1].fused = steps[-1].fused and fused
         pts.append(pt)
     if metas is None:
         metas = [meta_build(s.L, k_pool, pts[r], seq_lens) for r, s in enumerate(steps)]

@@ -46,6 +46,12 @@ def show(a, names, title):
         print(f"  {n:11s} n {len(col):5d} min {col.min():7.2f} p10 {np.percentile(col,10):7.2f} med {np.median(col):7.2f} p90 {np.percentile(col,90):7.2f} max {col.max():7.2f} us")
 if os.environ.get("TS_TWO_KERNELS", "0") == "0":
     show(a1, ["start", "scored", "selected", "listed", "consumed", "gathered", "keys", "end"], f"{name} decode_cluster_kernel ({kv} KV)")
+    # per-CTA phase durations (us): score = 0->1, exchange = 1->5, select = 6->2, attend = 3->4, merge = 4->7
+    for nm, (i, j) in (("score", (0, 1)), ("exchange", (1, 5)), ("ptwait", (5, 6)), ("select", (6, 2)), ("attend", (3, 4)), ("merge", (4, 7))):
+        d = (a1[:, j] - a1[:, i]) / 1e3
+        d = d[(a1[:, i] > 0) & (a1[:, j] > 0)]
+        if len(d):
+            print(f"  per-CTA {nm:9s} p10 {np.percentile(d,10):6.2f} med {np.median(d):6.2f} p90 {np.percentile(d,90):6.2f} us")
     sys.exit(0)
 show(a1, ["start", "scored", "gathered", "selected", "keys", "pass0", "thresh", "compacted"], f"{name} K1 score_select")
 show(a2, ["start", "flag", "pages", "consumed", "-", "-", "-", "end"] if os.environ.get("TS_SA_TMA", "1") != "0" else ["start", "q", "pages", "loop_end", "cta_merged", "cl_sync1", "out", "cl_sync2"], f"{name} K2 sparse_attn")

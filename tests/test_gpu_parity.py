@@ -396,7 +396,8 @@ def test_cuda_graph_and_determinism(ts):
 
 # ------------------------------------------------------------------ e: shard emulation
 @pytest.mark.parametrize("world", [2, 3, 4, 8])
-def test_shard_emulation_matches_unsharded(ts, world):
+@pytest.mark.parametrize("fused", [True, False])
+def test_shard_emulation_matches_unsharded(ts, world, fused):
     """Block-cyclic G-way sequence sharding on one GPU (exchanges = concatenation): the
     selection is bit-identical to the unsharded kernel's (any input, ties included) and o
     matches the oracle."""
@@ -409,7 +410,8 @@ def test_shard_emulation_matches_unsharded(ts, world):
     o1, l1, i1, c1 = ts.decode_step(L, d["q"], d["k_pool"], d["v_pool"], meta, d["page_table"],
                                     d["seq_lens"], cfg.budget_tokens, cfg.scale)
     o, lse, ids, cnts = sharded.emulate(ts, L, world, d["q"], d["k_pool"], d["v_pool"],
-                                        d["page_table"], d["seq_lens"], cfg.budget_tokens, cfg.scale)
+                                        d["page_table"], d["seq_lens"], cfg.budget_tokens, cfg.scale,
+                                        fused=fused)
     for r in range(world):
         assert torch.equal(ids[r], i1) and torch.equal(cnts[r], c1)
     assert np.array_equal(i1.cpu().numpy(), ref["sel_ids"])
@@ -421,7 +423,8 @@ def test_shard_emulation_matches_unsharded(ts, world):
 
 
 @pytest.mark.parametrize("world", [2, 3, 8])
-def test_shard_emulation_integer_ties(ts, world):
+@pytest.mark.parametrize("fused", [True, False])
+def test_shard_emulation_integer_ties(ts, world, fused):
     """Real score ties (integer q, k; no margin enforcement): the G-shard selection is
     bit-identical to the unsharded one and to the oracle's lower-global-id rule (a page's
     score bits do not depend on the sharding; the candidate merge breaks ties by global id)."""
@@ -439,7 +442,8 @@ def test_shard_emulation_integer_ties(ts, world):
                                     d["seq_lens"], cfg.budget_tokens, cfg.scale)
     assert np.array_equal(i1.cpu().numpy(), ref["sel_ids"])
     o, lse, ids, cnts = sharded.emulate(ts, L, world, d["q"], d["k_pool"], d["v_pool"],
-                                        d["page_table"], d["seq_lens"], cfg.budget_tokens, cfg.scale)
+                                        d["page_table"], d["seq_lens"], cfg.budget_tokens, cfg.scale,
+                                        fused=fused)
     for r in range(world):
         assert torch.equal(ids[r], i1) and torch.equal(cnts[r], c1)
     assert np.abs(o.cpu().numpy() - ref["o"]).max() <= 2e-3
