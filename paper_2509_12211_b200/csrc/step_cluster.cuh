@@ -55,7 +55,10 @@ struct ScSmem {
 // FP8 KV (F8, reading R21): the attention stage holds the K and V code tiles (16 tokens x
 // 64 B: one contiguous KB each, loaded with 1-D bulk copies — measured 0.4 us faster on C2
 // than 2-D tensor-map tiles with a 64-byte swizzle) and their 16 + 16 row exponents.
-constexpr int kF8Stage = 2080;  // K codes 1 KB | V codes 1 KB | K exps 16 B | V exps 16 B
+// The stage's 32 exponent bytes live outside the ring, in the radix-histogram area (idle
+// during the attention phase), so the ring holds 2 KB stages: 16 (R = 4) / 32 (R = 8) of
+// them, 4 / 8 per consumer warp in flight.
+constexpr int kF8Stage = 2048;  // K codes 1 KB | V codes 1 KB
 // token of k-slot n (0..7) of an 8-token MMA group in the FP8 consumer: the two K rows read
 // by each 8-lane phase of a 128-bit shared load have different parity (64-byte rows: the two
 // halves of the banks), so the K reads are conflict free (bit 0 = n0 ^ n1, bit 1 = n0, bit 2 = n2)
@@ -68,8 +71,10 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
     using SM = ScSmem<W, R>;
     constexpr int NT = SM::NT;
     // attention stages: 4 KB (bf16) / kF8Stage (FP8) slots over the scoring ring's bytes
-    constexpr int RA = F8 ? (R * kSsStageBytes / kF8Stage) / W * W : 2 * R;
+    // (FP8: at most 6 stages per consumer warp — 8 measured slower on C3)
+    constexpr int RA = F8 ? ((R * kSsStageBytes / kF8Stage) / W * W < 6 * W ? (R * kSsStageBytes / kF8Stage) / W * W : 6 * W) : 2 * R;
     static_assert(!F8 || RA <= 4 * R, "FP8 stage barriers must fit the afull / aempty slots");
+    static_assert(!F8 || RA * 32 <= kSsHist * 4, "FP8 exponent slots must fit the histogram area");
     static_assert(!(F8 && APP), "the FP8 append runs as its own kernel");
     static_assert(R % W == 0 && RA % W == 0, "stage -> consumer warp must be fixed");
     extern __shared__ uint8_t sc_raw[];
@@ -475,7 +480,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
                 bulk_load_hint(dst + c * 1024, static_cast<const uint8_t *>(c ? ap.v_pool : ap.k_pool) + (size_t)row0 * 64,
                                1024, afull0 + 8 * st, pol);
             else
-                bulk_load(dst + 2048 + (c - 2) * 16, (c == 2 ? kexp : vexp) + row0, 16, afull0 + 8 * st);
+                bulk_load(sb + SM::kHist + st * 32 + (c - 2) * 16, (c == 2 ? kexp : vexp) + row0, 16, afull0 + 8 * st);
         };
         {
             const int e = lane >> 2, i = warp + W * e;
@@ -501,7 +506,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
             const int tl = t0 + i, tu = tl >> tps;
             const int tok0 = sel[tu - u0].y + 16 * (tl & (tpp - 1));
             mbar_wait(afull0 + 8 * st, (i / RA) & 1);
-            const uint32_t kb = sb + st * kF8Stage, vb = kb + 1024, eb = kb + 2048;
+            const uint32_t kb = sb + st * kF8Stage, vb = kb + 1024, eb = sb + SM::kHist + st * 32;
             float sacc[2][4];
 #pragma unroll
             for (int nt = 0; nt < 2; ++nt) {
