@@ -511,3 +511,24 @@ def test_decode_step_prefetch_equals_plain(ts, name):
                              case["seq_lens"], cfg.budget_tokens, cfg.scale)
     assert np.abs(o2.cpu().numpy() - ref["o"]).max() <= ATOL[cfg.dtype] or not np.array_equal(
         i2.cpu().numpy(), ref["sel_ids"][:, :, :K])  # (no margin enforcement on drifted q)
+
+
+@pytest.mark.parametrize("world", [2, 8])
+def test_select_candidates_equals_composed(ts, world):
+    """ts_select_candidates (one launch) == ts_score_pages + ts_select_topk(id_stride = G,
+    id_offset = r) on every rank's shard: the same global ids, count and score bits."""
+    from paper_2509_12211_b200 import sharded
+    cfg = synth.config("c5", batch=2, ctx=30000, budget_tokens=2048)
+    case = synth.make_case(cfg, seed=37, ragged=True)
+    d = on_dev(case)
+    K = cfg.budget_tokens // cfg.page_size
+    for r in range(world):
+        pt = sharded.shard_page_table(d["page_table"], world, r)
+        L = ts.make_layout(d["q"], d["k_pool"], pt, world, r)
+        meta = ts.meta_build(L, d["k_pool"], pt, d["seq_lens"])
+        cs, ci, cc = ts.select_candidates(L, d["q"], meta, pt, d["seq_lens"], K)
+        sc = ts.score_pages(L, d["q"], meta, pt, d["seq_lens"])
+        rows = L.batch * L.num_kv_heads
+        ri, rs, rc = ts.select_topk(sc.view(rows, L.max_pages), K, id_stride=world, id_offset=r)
+        assert torch.equal(ci, ri) and torch.equal(cc, rc)
+        assert torch.equal(cs.view(torch.int32), rs.view(torch.int32))
