@@ -619,7 +619,12 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
         }
         // the ring was last accessed by the generic proxy (scoring); APP: the appended K/V
         // row (another CTA's generic stores, published by the cluster barrier) is read by TMA
-        if constexpr (APP)
+        bool reads_app = false;  // does this CTA gather the appended page? (then a global proxy fence)
+        if constexpr (APP) {
+            for (int u = lane; app && u < u1 - u0; u += 32) reads_app |= sel[u].y == ja * p.S;
+            reads_app = __any_sync(0xffffffffu, reads_app);
+        }
+        if (reads_app)
             fence_proxy_async_all();
         else
             fence_proxy_async();
