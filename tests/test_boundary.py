@@ -109,3 +109,35 @@ def test_no_cpu_fallback(ts):
     q = torch.zeros(1, 1, 64, dtype=torch.bfloat16)
     with pytest.raises(TypeError, match="CUDA"):
         ts.score_pages(ts.Layout(1, 1, 1, 64, 16, 4, 4, 1, 0, ts.TS_BF16), q, q, q, q)
+
+
+def test_round2_entry_points_validate_before_launch(ts):
+    """FP8 KV (R21), the fused sequence-sharding halves and the release / dev split."""
+    L = ts._lib.lib()
+    good = 0x2000
+    f8 = ts.Layout(2, 16, 4, 64, 16, 8, 16, 1, 0, ts.TS_FP8E4M3)
+    assert L.ts_pool_bytes(f8) == 16 * 4 * 16 * 65                 # codes + one exponent byte per row
+    bf = ts.Layout(2, 16, 4, 64, 16, 8, 16, 1, 0, ts.TS_BF16)
+    assert L.ts_pool_bytes(bf) == 16 * 4 * 16 * 64 * 2
+    f8.head_dim = 128
+    assert L.ts_pool_bytes(f8) == 0                               # FP8: head_dim 64 only
+    assert L.ts_kv_quantize(-1, 64, good, good, good, None) == 1  # rows < 0
+    assert L.ts_kv_quantize(4, 128, good, good, good, None) == 4  # head_dim 128 unsupported
+    assert L.ts_kv_quantize(4, 64, 0x1008, good, good, None) == 3  # src not 16-byte aligned
+    sh = ts.Layout(2, 16, 4, 64, 16, 8, 16, 2, 1, ts.TS_BF16)
+    assert L.ts_select_candidates(sh, good, good, good, good, 0, good, good, good, None) == 2  # k < 1
+    assert L.ts_shard_attend(sh, good, good, good, good, good, good, good, 0, 0, 64, 1.0, good, good,
+                             None, None, good, 1 << 30, None) == 2                            # parts < 1
+    assert L.ts_shard_attend(sh, good, good, good, good, good, good, good, 2, 0, 64, 1.0, good, good,
+                             None, None, None, 0, None) == 6                                  # no workspace
+    f32 = ts.Layout(2, 16, 4, 64, 16, 8, 16, 2, 1, ts.TS_F32)
+    assert L.ts_select_candidates(f32, good, good, good, good, 8, good, good, good, None) == 4
+
+
+def test_release_library_has_no_dev_hooks(ts):
+    """The A/B knobs and timestamp / debug hooks exist only in libtinyserve_dev.so."""
+    lib = ctypes.CDLL(ts._lib.LIB_PATH)
+    for sym in ("ts_debug_timestamps", "ts_debug_ss_timestamps", "ts_debug_error_word"):
+        assert not hasattr(lib, sym), sym
+    raw = open(ts._lib.LIB_PATH, "rb").read()
+    assert b"TS_SC_R" not in raw and b"TS_TWO_KERNELS" not in raw  # no getenv of a knob
