@@ -571,8 +571,7 @@ def main():
     dense = None
     try:
         dense = dense_leg(ts, cfg, reps, R, stream, dev, args, ms_per_step) if (
-            use_graph and not args.no_dense and cfg.dtype == "bf16" and cfg.page_size % 16 == 0
-            and not kvq) else None
+            use_graph and not args.no_dense and cfg.dtype == "bf16" and cfg.page_size % 16 == 0) else None
     except Exception as ex:  # noqa: BLE001 — the baseline is context; never fail the bench on it
         dense = {"unavailable": f"{type(ex).__name__}: {ex}"}
     # ---- NEXT-2 cross-step reuse on a drifting-query workload (labelled leg, not the headline)
@@ -897,12 +896,14 @@ def dense_leg(ts, cfg, reps, R, stream, dev, args, ms_per_step):
     torch.cuda.synchronize()
     dms = e0.elapsed_time(e1) / (nd * R)
     e = 2
-    dbytes = (cfg.batch * cfg.num_kv_heads * cfg.ctx * 2 * cfg.head_dim * e
+    row = cfg.head_dim + 1 if args.kv == "fp8" else cfg.head_dim * e  # bytes per stored K (or V) row
+    dbytes = (cfg.batch * cfg.num_kv_heads * cfg.ctx * 2 * row
               + cfg.batch * cfg.num_q_heads * cfg.head_dim * (e + 4) + cfg.batch * cfg.num_q_heads * 4)
     dense = {"ms_per_step": dms, "steps_per_s": 1e3 / dms, "bytes_per_step": dbytes,
              "hbm_gbs": dbytes / (dms * 1e-3) / 1e9,
              "speedup_sparse_vs_dense": dms / ms_per_step,
-             "kernel": "sparse_attn_tma_kernel in dense mode (every page; ts_dense_decode_attn)"}
+             "kernel": "sparse_attn_tma_kernel in dense mode (every page; ts_dense_decode_attn)"
+                       + (", FP8 KV" if args.kv == "fp8" else "")}
 
     return dense
 

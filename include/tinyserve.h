@@ -85,8 +85,8 @@ typedef enum {
  * head; value = code * 2^e, e in [-64, 64] the smallest with max |x| <= 448 * 2^e), i.e.
  * num_blocks*Hkv*S*65 bytes (ts_pool_bytes); q, meta, k_new and v_new stay bf16, and the
  * metadata is the exact min / max of the DEQUANTISED keys.  head_dim 64 only; attention
- * over an FP8 cache runs in ts_decode_step(_append / _prefetch) (page_size a multiple of 16,
- * G <= 8); ts_sparse_decode_attn / ts_dense_decode_attn return TS_ERR_UNSUPPORTED for it. */
+ * over an FP8 cache (ts_decode_step(_append / _prefetch), ts_sparse_decode_attn,
+ * ts_dense_decode_attn, ts_shard_attend) needs page_size a multiple of 16 and G <= 8. */
 typedef enum { TS_F32 = 0, TS_BF16 = 1, TS_FP8E4M3 = 2 } ts_dtype;
 
 typedef struct {
@@ -242,7 +242,7 @@ ts_status ts_select_candidates(const ts_layout *layout, const void *q, const voi
  * over the OWNED selected pages exactly as ts_sparse_decode_attn: o [B][Hq][d], lse [B][Hq]
  * (o = 0, lse = -inf for a row with no owned selected page).  The selection itself is
  * written to sel_ids_out [rows][k] / sel_count_out [rows] when non-NULL (identical on every
- * rank).  bf16 K/V, head_dim 64, page_size a multiple of 16, G <= 8, parts*k <= 4096;
+ * rank).  bf16 or FP8 K/V, head_dim 64, page_size a multiple of 16, G <= 8, parts*k <= 4096;
  * ws >= ts_attn_workspace_bytes(layout, k), zero-filled once; TS_ERR_UNSUPPORTED otherwise. */
 ts_status ts_shard_attend(const ts_layout *layout, const void *q, const void *k_pool,
                           const void *v_pool, const int32_t *page_table, const int32_t *seq_lens,

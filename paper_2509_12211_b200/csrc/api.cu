@@ -359,9 +359,9 @@ ts_status launch_sa(const AttnParams &p, int rows, int cdesired, bool pdl, cudaS
 }
 
 // TMA-ring attention (sparse_attn_tma_kernel), S % 16 == 0: one (row, split) per CTA.
-template <int W, int R>
+template <int W, int R, bool F8 = false>
 ts_status launch_sat(const ts_layout *L, const AttnParams &p, bool pdl, cudaStream_t st) {
-    auto kern = sparse_attn_tma_kernel<W, R>;
+    auto kern = sparse_attn_tma_kernel<W, R, F8>;
     const int rows = L->batch * L->num_kv_heads;
     const size_t sm = SatSmem<W, R>::bytes(p.sel_stride);
     if (sm > 227 * 1024) return TS_ERR_UNSUPPORTED;
@@ -662,6 +662,10 @@ AttnParams attn_params(const ts_layout *L, const void *q, const void *k_pool, co
     p.splits = 1;
     p.items = L->batch * L->num_kv_heads;
     p.dbg = g_dbg_ts;
+    if (L->kv_dtype == TS_FP8E4M3) {  // FP8 pools: codes, then the row exponents (R21)
+        p.k_exp = f8_exps(k_pool, L);
+        p.v_exp = f8_exps(v_pool, L);
+    }
     return p;
 }
 
@@ -675,6 +679,10 @@ ts_status launch_attn(const ts_layout *L, const void *q, const void *k_pool, con
     if (L->kv_dtype == TS_BF16) {
         if (!bf16_attn_supported(L) || sel_stride > kMaxSelAttn) return TS_ERR_UNSUPPORTED;
         return launch_sparse_attn(L, p, true, st);
+    }
+    if (L->kv_dtype == TS_FP8E4M3) {  // the TMA-ring kernel's F8 instantiation
+        if (L->page_size % 16 != 0 || group_of(L) > 8 || sel_stride > kMaxSelAttn) return TS_ERR_UNSUPPORTED;
+        return launch_sat<4, 8, true>(L, p, true, st);
     }
     const int threads = 32 * std::min(p.G, 8);
     if (L->head_dim == 64)
@@ -846,7 +854,6 @@ ts_status ts_sparse_decode_attn(const ts_layout *L, const void *q, const void *k
     if (!aligned16(q) || !aligned16(k_pool) || !aligned16(v_pool) || !aligned16(o))
         return TS_ERR_ALIGN;
     if (!ws || ws_bytes < attn_ws_layout(L, sel_stride).total) return TS_ERR_WORKSPACE;
-    if (L->kv_dtype == TS_FP8E4M3) return TS_ERR_UNSUPPORTED;  // FP8: the fused step only
     return launch_attn(L, q, k_pool, v_pool, page_table, seq_lens, sel_ids, sel_count, sel_stride,
                        scale, o, lse, ws, as_stream(stream));
 }
@@ -1043,12 +1050,15 @@ ts_status ts_dense_decode_attn(const ts_layout *L, const void *q, const void *k_
     if (L->shard_stride != 1) return TS_ERR_UNSUPPORTED;
     if (!aligned16(q) || !aligned16(k_pool) || !aligned16(v_pool) || !aligned16(o))
         return TS_ERR_ALIGN;
-    if (!bf16_attn_supported(L) || L->page_size % 16 != 0) return TS_ERR_UNSUPPORTED;
+    const bool f8 = L->kv_dtype == TS_FP8E4M3;
+    if ((!f8 && !bf16_attn_supported(L)) || L->page_size % 16 != 0 || group_of(L) > 8)
+        return TS_ERR_UNSUPPORTED;
     if (!ws || ws_bytes < attn_ws_layout(L, L->max_pages).total) return TS_ERR_WORKSPACE;
     if (L->batch == 0) return TS_OK;
     AttnParams p = attn_params(L, q, k_pool, v_pool, page_table, seq_lens, nullptr, nullptr,
                                L->max_pages, scale, o, lse, ws);
     p.dense = 1;
+    if (f8) return launch_sat<4, 8, true>(L, p, true, as_stream(stream));
     static const int rr = env_int("TS_SA_R", 8);
     if (rr == 16) return launch_sat<4, 16>(L, p, true, as_stream(stream));
     return launch_sat<4, 8>(L, p, true, as_stream(stream));
@@ -1105,7 +1115,9 @@ ts_status ts_shard_attend(const ts_layout *L, const void *q, const void *k_pool,
     if (s != TS_OK) return s;
     if (parts < 1 || k < 1 || part_stride < 0) return TS_ERR_SHAPE;
     if (!aligned16(q) || !aligned16(k_pool) || !aligned16(v_pool) || !aligned16(o)) return TS_ERR_ALIGN;
-    if (!bf16_attn_supported(L) || L->page_size % 16 != 0 || k > kMaxSel) return TS_ERR_UNSUPPORTED;
+    const bool f8 = L->kv_dtype == TS_FP8E4M3;
+    if ((!f8 && !bf16_attn_supported(L)) || L->page_size % 16 != 0 || group_of(L) > 8 || k > kMaxSel)
+        return TS_ERR_UNSUPPORTED;
     const long long pg = (long long)L->max_pages * L->shard_stride;  // global pages of a row
     const size_t scratch = (size_t)((parts * k + 3) & ~3) * 8 + (size_t)((pg + 31) / 32 + 4) * 8 +
                            (kSsHistM + 64 + 128 + (size_t)k) * 4;
@@ -1121,7 +1133,7 @@ ts_status ts_shard_attend(const ts_layout *L, const void *q, const void *k_pool,
     p.cand_part_stride = part_stride ? part_stride : (long long)L->batch * L->num_kv_heads * k;
     p.sel_out = sel_ids_out;
     p.sel_cnt_out = sel_count_out;
-    return launch_sat<4, 8>(L, p, true, as_stream(stream));
+    return f8 ? launch_sat<4, 8, true>(L, p, true, as_stream(stream)) : launch_sat<4, 8>(L, p, true, as_stream(stream));
 }
 
 ts_status ts_select_merge(const float *cand_scores, const int32_t *cand_ids, int32_t parts,

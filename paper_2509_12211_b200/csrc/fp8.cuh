@@ -14,6 +14,7 @@
 //   meta_append_f8_kernel  the append (Eq. 1 maintenance) of a bf16 token into an FP8 cache
 //   meta_build_f8_kernel   metadata over the dequantised keys of every page
 #pragma once
+#include "attn.cuh"
 #include "common.cuh"
 #include "meta.cuh"
 
@@ -193,6 +194,155 @@ __global__ void meta_build_f8_kernel(MetaParams p, const uint8_t *__restrict__ k
         uint16_t *mrec = meta + (((size_t)b * p.Hkv + h) * p.max_pages + jl) * 2 * 64 + c * 8;
         *reinterpret_cast<uint4 *>(mrec) = lo;
         *reinterpret_cast<uint4 *>(mrec + 64) = hi;
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// The FP8 attention consumer (reading R21), shared by decode_cluster_kernel (F8) and
+// sparse_attn_tma_kernel (F8).  Per 16-token tile, lane (gid, t):
+//  S = Q'·K_code^T on mma.m16n8k16 f16 (E4M3 widens exactly to f16; q' = q * 2^-sq per head,
+//  |q'| in [2^14, 2^15), so bf16 q is exact in f16), times 2^(e_k + sq) per token; the online
+//  softmax keeps the V accumulator relative to (running max, running max V exponent E), so
+//  P' = P * 2^(e_v - E) <= 1 enters O^T += V_code^T P'^T as a hi + lo f16 pair; 2^E is applied
+//  when the partial is stored.  Token order in each 8-token MMA group: f8_tok (the two 64-byte
+//  K rows read by each 8-lane phase of a 128-bit shared load have different parity: no bank
+//  conflicts without a swizzle).
+TS_DEV int f8_tok(int n) { return ((n ^ (n >> 1)) & 1) | ((n & 1) << 1) | (n & 4); }
+
+struct F8Q {
+    uint32_t qh[8];  // f16x2 of q' channels 16t + {2i, 2i+1} (head gid)
+    float qsc;       // softmax scale * log2(e) * 2^sq
+};
+// x0, x1: the lane's 32 bytes of q (bf16 channels 16t .. 16t + 15 of head gid; zero if gid >= G)
+TS_DEV F8Q f8_q_prep(uint4 x0, uint4 x1, float sl2) {
+    F8Q f;
+    const uint32_t w[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+    float am = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) am = fmaxf(am, fmaxf(fabsf(bf16lo_to_f32(w[i])), fabsf(bf16hi_to_f32(w[i]))));
+    am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, 1));
+    am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, 2));
+    const int ea = int(__float_as_uint(am) >> 23) - 127;  // floor(log2 am) for normal am
+    const int sq = am > 0.f ? min(max(ea - 14, -100), 100) : 0;
+    const float s = pow2i(-sq);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) f.qh[i] = f16x2_pack(bf16lo_to_f32(w[i]) * s, bf16hi_to_f32(w[i]) * s);
+    f.qsc = sl2 * pow2i(sq);
+    return f;
+}
+
+struct F8Acc {
+    float m = kNegInf, lp = 0.f;
+    int E = -128;  // running max V exponent of the attended tokens (-128: none yet)
+    float oacc[4][4];  // O^T: channels (8 gid + 2 db, + 1) x heads (2t, 2t+1)
+    TS_DEV F8Acc() {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) oacc[j][0] = oacc[j][1] = oacc[j][2] = oacc[j][3] = 0.f;
+    }
+};
+
+// One 16-token tile: K codes at kb ([16][64] bytes), V codes at vb, the tile's 16 K then 16 V
+// exponent bytes at eb; tokens tok0 + r, valid while < L.
+TS_DEV void f8_attend_tile(F8Acc &a, const F8Q &q, uint32_t kb, uint32_t vb, uint32_t eb, int tok0, int L,
+                           int gid, int t) {
+    int trow[2][2];
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int q2 = 0; q2 < 2; ++q2) trow[nt][q2] = nt * 8 + f8_tok(2 * t + q2);
+    float sacc[2][4];
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+        sacc[nt][0] = sacc[nt][1] = sacc[nt][2] = sacc[nt][3] = 0.f;
+        const int r = nt * 8 + f8_tok(gid);  // B column gid = this K row
+        const uint4 k = lds_v4(kb + r * 64 + (t << 4));
+        const uint32_t kw[4] = {k.x, k.y, k.z, k.w};
+#pragma unroll
+        for (int kc = 0; kc < 4; ++kc)
+            mma_f16_16816(sacc[nt], q.qh[2 * kc], 0u, q.qh[2 * kc + 1], 0u, f8x2_to_f16x2(kw[kc] & 0xffffu),
+                          f8x2_to_f16x2(kw[kc] >> 16));
+    }
+    float x[2][2];
+    bool ok[2][2];
+    int ev[2][2];
+    float tmax = kNegInf;
+    int evmax = -128;
+    // row exponents: 8-byte reads per 8-token group, the lane's bytes picked with PRMT
+    const uint2 ke0 = lds_v2(eb), ke1 = lds_v2(eb + 8), ve0 = lds_v2(eb + 16), ve1 = lds_v2(eb + 24);
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int q2 = 0; q2 < 2; ++q2) {
+            const int r = trow[nt][q2];
+            ok[nt][q2] = tok0 + r < L;
+            const uint2 kw = nt ? ke1 : ke0, vw = nt ? ve1 : ve0;
+            const int sb_ = r & 7;
+            const int ek = int(__byte_perm(kw.x, kw.y, sb_) << 24) >> 24;
+            ev[nt][q2] = int(__byte_perm(vw.x, vw.y, sb_) << 24) >> 24;
+            x[nt][q2] = ok[nt][q2] ? sacc[nt][q2] * q.qsc * pow2i(ek) : kNegInf;
+            tmax = fmaxf(tmax, x[nt][q2]);
+            if (ok[nt][q2]) evmax = max(evmax, ev[nt][q2]);
+        }
+    tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 1));
+    tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 2));
+    evmax = max(evmax, __shfl_xor_sync(0xffffffffu, evmax, 1));
+    evmax = max(evmax, __shfl_xor_sync(0xffffffffu, evmax, 2));
+    const int En = max(a.E, evmax);
+    const float mnew = fmaxf(a.m, tmax);
+    const float mref = mnew == kNegInf ? 0.f : mnew;
+    const float corr = exp2f(a.m - mref);
+    const float corr_o = corr * exp2f((float)(a.E - En));
+    a.m = mnew;
+    a.E = En;
+    float pr[2][2];
+    float psum = 0.f;
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int q2 = 0; q2 < 2; ++q2) {
+            const float pw = exp2f(x[nt][q2] - mref);
+            psum += pw;
+            const int de = ev[nt][q2] - a.E;  // <= 0 for attended tokens
+            pr[nt][q2] = ok[nt][q2] && de >= -126 ? pw * pow2i(de) : 0.f;
+        }
+    a.lp = a.lp * corr + psum;
+    ot_rescale(a.oacc, corr_o, t);
+    // B = P'^T (k = this lane's tokens, n = head gid), hi + lo f16 parts
+    const uint32_t ah0 = f16x2_pack(pr[0][0], pr[0][1]), ah2 = f16x2_pack(pr[1][0], pr[1][1]);
+    const float2 h0 = __half22float2(*reinterpret_cast<const __half2 *>(&ah0));
+    const float2 h2 = __half22float2(*reinterpret_cast<const __half2 *>(&ah2));
+    const uint32_t al0 = f16x2_pack(pr[0][0] - h0.x, pr[0][1] - h0.y);
+    const uint32_t al2 = f16x2_pack(pr[1][0] - h2.x, pr[1][1] - h2.y);
+    // A = V^T: channels 8 gid .. 8 gid + 7 (8 code bytes) of this lane's 4 token rows
+    uint2 vr[2][2];
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int q2 = 0; q2 < 2; ++q2) {
+            const uint2 v = lds_v2(vb + trow[nt][q2] * 64 + gid * 8);
+            vr[nt][q2] = ok[nt][q2] ? v : make_uint2(0, 0);  // past seq_len: may be anything
+        }
+#pragma unroll
+    for (int db = 0; db < 4; ++db) {  // channels 8 gid + 2 db (A rows gid) and + 1 (rows gid + 8)
+        const uint32_t sel_ = (db & 1) ? 0x7362u : 0x5140u;
+        const uint32_t p0 = __byte_perm(db < 2 ? vr[0][0].x : vr[0][0].y, db < 2 ? vr[0][1].x : vr[0][1].y, sel_);
+        const uint32_t p1 = __byte_perm(db < 2 ? vr[1][0].x : vr[1][0].y, db < 2 ? vr[1][1].x : vr[1][1].y, sel_);
+        const uint32_t a0 = f8x2_to_f16x2(p0 & 0xffffu), a1 = f8x2_to_f16x2(p0 >> 16);
+        const uint32_t a2 = f8x2_to_f16x2(p1 & 0xffffu), a3 = f8x2_to_f16x2(p1 >> 16);
+        mma_f16_16816(a.oacc[db], a0, a1, a2, a3, ah0, ah2);
+        mma_f16_16816(a.oacc[db], a0, a1, a2, a3, al0, al2);
+    }
+}
+
+// the warp's partial: O^T rows of heads 2t, 2t+1 (x 2^E) and (m, l) of head gid
+TS_DEV void f8_store_partial(float *wpart_warp, int ld, F8Acc &a, int gid, int t, int G) {
+    a.lp += __shfl_xor_sync(0xffffffffu, a.lp, 1);
+    a.lp += __shfl_xor_sync(0xffffffffu, a.lp, 2);
+    const float s2e = a.E > -128 ? pow2i(a.E) : 1.f;  // back from the V-exponent reference
+    ot_store(wpart_warp, ld, a.oacc, gid, t, G, s2e);
+    if (gid < G && t == 0) {
+        wpart_warp[gid * ld + kAttnD] = a.m;
+        wpart_warp[gid * ld + kAttnD + 1] = a.lp;
     }
 }
 

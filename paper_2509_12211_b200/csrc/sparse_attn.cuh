@@ -26,6 +26,7 @@
 
 #include "attn.cuh"
 #include "common.cuh"
+#include "fp8.cuh"           // the FP8 tile consumer (F8 instantiation)
 #include "score_select.cuh"  // cta_topk, block_scan (the candidate merge of ts_shard_attend)
 
 namespace ts {
@@ -286,7 +287,9 @@ struct SatSmem {
     static size_t bytes(int sel_stride) { return 1024 + kPages + (size_t)sel_stride * 8; }
 };
 
-template <int W, int R>
+// F8: FP8 KV (reading R21) — a stage holds the tile's K codes (1 KB), V codes (1 KB) and its
+// 16 + 16 exponent bytes (1-D bulk copies), consumed by f8_attend_tile (fp8.cuh).
+template <int W, int R, bool F8 = false>
 __global__ void __launch_bounds__((W + 1) * 32, 4) sparse_attn_tma_kernel(
     const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, AttnParams p,
     int C) {
@@ -472,12 +475,41 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) sparse_attn_tma_kernel(
                 const int tl = t0 + i, u = tl / tpp, sub = tl - u * tpp;
                 const int2 pg = pages[u];
                 info[st] = make_int2(pg.y + 16 * sub, 0);
-                mbar_arrive_expect_tx(full0 + 8 * st, SM::kStage);
                 const uint32_t dst = sb + SM::kRing + st * SM::kStage;
-                tma_load_2d(dst, &tmK, 0, pg.x + 16 * sub, full0 + 8 * st, pol);
-                tma_load_2d(dst + SM::kTile, &tmV, 0, pg.x + 16 * sub, full0 + 8 * st, pol);
+                if constexpr (F8) {
+                    const int row0 = pg.x + 16 * sub;  // pool row of the tile's first token
+                    mbar_arrive_expect_tx(full0 + 8 * st, 2 * 1024 + 32);
+                    bulk_load_hint(dst, static_cast<const uint8_t *>(p.k_pool) + (size_t)row0 * 64, 1024, full0 + 8 * st, pol);
+                    bulk_load_hint(dst + 1024, static_cast<const uint8_t *>(p.v_pool) + (size_t)row0 * 64, 1024, full0 + 8 * st, pol);
+                    bulk_load(dst + 2048, p.k_exp + row0, 16, full0 + 8 * st);
+                    bulk_load(dst + 2064, p.v_exp + row0, 16, full0 + 8 * st);
+                } else {
+                    mbar_arrive_expect_tx(full0 + 8 * st, SM::kStage);
+                    tma_load_2d(dst, &tmK, 0, pg.x + 16 * sub, full0 + 8 * st, pol);
+                    tma_load_2d(dst + SM::kTile, &tmV, 0, pg.x + 16 * sub, full0 + 8 * st, pol);
+                }
             }
         }
+    } else if constexpr (F8) {
+        // ================================ consumers (FP8) ==========================
+        uint4 x0 = make_uint4(0, 0, 0, 0), x1 = x0;
+        if (gid < p.G) {
+            const uint16_t *qr =
+                static_cast<const uint16_t *>(p.q) + ((size_t)b * p.Hq + g * p.G + gid) * kAttnD + 16 * t;
+            x0 = ldg_nc_v4(qr);
+            x1 = ldg_nc_v4(qr + 8);
+        }
+        const F8Q fq = f8_q_prep(x0, x1, p.scale * kLog2e);
+        F8Acc acc;
+        for (int i = warp; i < t1 - t0; i += W) {
+            const int st = i % R;
+            mbar_wait(full0 + 8 * st, (i / R) & 1);
+            const uint32_t kb = sb + SM::kRing + st * SM::kStage;
+            f8_attend_tile(acc, fq, kb, kb + 1024, kb + 2048, info[st].x, L, gid, t);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty0 + 8 * st);
+        }
+        f8_store_partial(wpart + warp * 8 * kSaPart, kSaPart, acc, gid, t, p.G);
     } else {
         // ================================ consumers ===============================
         const float sl2 = p.scale * kLog2e;

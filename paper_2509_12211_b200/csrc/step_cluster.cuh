@@ -59,10 +59,6 @@ struct ScSmem {
 // during the attention phase), so the ring holds 2 KB stages: 16 (R = 4) / 32 (R = 8) of
 // them, 4 / 8 per consumer warp in flight.
 constexpr int kF8Stage = 2048;  // K codes 1 KB | V codes 1 KB
-// token of k-slot n (0..7) of an 8-token MMA group in the FP8 consumer: the two K rows read
-// by each 8-lane phase of a 128-bit shared load have different parity (64-byte rows: the two
-// halves of the banks), so the K reads are conflict free (bit 0 = n0 ^ n1, bit 1 = n0, bit 2 = n2)
-TS_DEV int f8_tok(int n) { return ((n ^ (n >> 1)) & 1) | ((n & 1) << 1) | (n & 4); }
 
 template <int W, int R, bool DSM, bool APP, bool F8 = false>
 __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
@@ -438,33 +434,15 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
         // re-issued by its owner right after it is consumed and a CTA has W issuing warps
         // (a single issuing lane caps a CTA's 2 KB-tile gather at ~21 GB/s: scripts/gatherbench.cu)
     } else if constexpr (F8) {
-        // ---- FP8 KV (reading R21): per tile, S = Q K^T over the E4M3 codes (widened exactly
-        // to f16) times 2^e_k per token; the online softmax keeps the V accumulator relative to
-        // (running max + running max V exponent E) so that P' = P * 2^(e_v - E) <= 1 enters
-        // the f16 P.V MMA as an exact-enough hi + lo pair; 2^E is applied at the end.
-        // q: per head power-of-two prescale (|q'| in [2^14, 2^15)): bf16 q is exact in f16.
-        uint32_t qh[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // f16x2 of q' channels 16t + {2i, 2i+1}
-        float qsc = 0.f;                             // scale * log2(e) * 2^sq
-        {
-            uint4 x0 = make_uint4(0, 0, 0, 0), x1 = x0;
-            if (gid < p.G) {
-                const uint32_t qrow = sb + SM::kQ + gid * kRowBytes + 32 * t;
-                x0 = lds_v4(qrow);
-                x1 = lds_v4(qrow + 16);
-            }
-            const uint32_t w[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
-            float am = 0.f;
-#pragma unroll
-            for (int i = 0; i < 8; ++i) am = fmaxf(am, fmaxf(fabsf(bf16lo_to_f32(w[i])), fabsf(bf16hi_to_f32(w[i]))));
-            am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, 1));
-            am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, 2));
-            const int ea = int(__float_as_uint(am) >> 23) - 127;  // floor(log2 am) for normal am
-            const int sq = am > 0.f ? min(max(ea - 14, -100), 100) : 0;
-            const float s = pow2i(-sq);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) qh[i] = f16x2_pack(bf16lo_to_f32(w[i]) * s, bf16hi_to_f32(w[i]) * s);
-            qsc = sl2 * pow2i(sq);
+        // ---- FP8 KV (reading R21; fp8.cuh f8_attend_tile): per-head f16 q' fragments, the
+        // tiles' E4M3 codes by 1-D bulk copies, exponent bytes in the idle histogram area
+        uint4 x0 = make_uint4(0, 0, 0, 0), x1 = x0;
+        if (gid < p.G) {
+            const uint32_t qrow = sb + SM::kQ + gid * kRowBytes + 32 * t;
+            x0 = lds_v4(qrow);
+            x1 = lds_v4(qrow + 16);
         }
+        const F8Q fq = f8_q_prep(x0, x1, sl2);
         fence_proxy_async();  // the ring was last accessed by the generic proxy (scoring)
         const uint64_t pol = l2_policy_evict_first();
         const int ntl = t1 - t0;
@@ -489,108 +467,14 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
                 issue_f8(i, lane & 3);
             }
         }
-        float m = kNegInf, lp = 0.f;
-        int E = -128;  // running max V exponent of the attended tokens (-128: none yet)
-        // O^T accumulators: oacc[db] = channels (8 gid + 2 db, 8 gid + 2 db + 1) x heads (2t, 2t+1)
-        float oacc[4][4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) oacc[j][0] = oacc[j][1] = oacc[j][2] = oacc[j][3] = 0.f;
-        // this lane's 4 tokens of a tile: k-slots 2t + q2 of MMA group nt
-        int trow[2][2];
-#pragma unroll
-        for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-            for (int q2 = 0; q2 < 2; ++q2) trow[nt][q2] = nt * 8 + f8_tok(2 * t + q2);
+        F8Acc acc;
         for (int i = warp; i < ntl; i += W) {
             const int st = i % RA;
             const int tl = t0 + i, tu = tl >> tps;
             const int tok0 = sel[tu - u0].y + 16 * (tl & (tpp - 1));
             mbar_wait(afull0 + 8 * st, (i / RA) & 1);
-            const uint32_t kb = sb + st * kF8Stage, vb = kb + 1024, eb = sb + SM::kHist + st * 32;
-            float sacc[2][4];
-#pragma unroll
-            for (int nt = 0; nt < 2; ++nt) {
-                sacc[nt][0] = sacc[nt][1] = sacc[nt][2] = sacc[nt][3] = 0.f;
-                const int r = nt * 8 + f8_tok(gid);  // B column gid = this K row
-                const uint4 k = lds_v4(kb + r * 64 + (t << 4));  // rows of different parity: no bank conflict
-                const uint32_t kw[4] = {k.x, k.y, k.z, k.w};
-#pragma unroll
-                for (int kc = 0; kc < 4; ++kc)
-                    mma_f16_16816(sacc[nt], qh[2 * kc], 0u, qh[2 * kc + 1], 0u, f8x2_to_f16x2(kw[kc] & 0xffffu),
-                                  f8x2_to_f16x2(kw[kc] >> 16));
-            }
-            float x[2][2];
-            bool ok[2][2];
-            int ev[2][2];
-            float tmax = kNegInf;
-            int evmax = -128;
-            // row exponents of the tile's 16 tokens: K at eb, V at eb + 16 (8-byte reads per
-            // 8-token group, the lane's bytes picked with PRMT)
-            const uint2 ke0 = lds_v2(eb), ke1 = lds_v2(eb + 8), ve0 = lds_v2(eb + 16), ve1 = lds_v2(eb + 24);
-#pragma unroll
-            for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-                for (int q2 = 0; q2 < 2; ++q2) {
-                    const int r = trow[nt][q2];
-                    ok[nt][q2] = tok0 + r < L;
-                    const uint2 kw = nt ? ke1 : ke0, vw = nt ? ve1 : ve0;
-                    const int sb_ = r & 7;
-                    const int ek = int(__byte_perm(kw.x, kw.y, sb_) << 24) >> 24;
-                    ev[nt][q2] = int(__byte_perm(vw.x, vw.y, sb_) << 24) >> 24;
-                    x[nt][q2] = ok[nt][q2] ? sacc[nt][q2] * qsc * pow2i(ek) : kNegInf;
-                    tmax = fmaxf(tmax, x[nt][q2]);
-                    if (ok[nt][q2]) evmax = max(evmax, ev[nt][q2]);
-                }
-            tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 1));
-            tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 2));
-            evmax = max(evmax, __shfl_xor_sync(0xffffffffu, evmax, 1));
-            evmax = max(evmax, __shfl_xor_sync(0xffffffffu, evmax, 2));
-            const int En = max(E, evmax);
-            const float mnew = fmaxf(m, tmax);
-            const float mref = mnew == kNegInf ? 0.f : mnew;
-            const float corr = exp2f(m - mref);
-            const float corr_o = corr * exp2f((float)(E - En));
-            m = mnew;
-            E = En;
-            float pr[2][2];
-            float psum = 0.f;
-#pragma unroll
-            for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-                for (int q2 = 0; q2 < 2; ++q2) {
-                    const float pw = exp2f(x[nt][q2] - mref);
-                    psum += pw;
-                    const int de = ev[nt][q2] - E;  // <= 0 for attended tokens
-                    pr[nt][q2] = ok[nt][q2] && de >= -126 ? pw * pow2i(de) : 0.f;
-                }
-            lp = lp * corr + psum;
-            ot_rescale(oacc, corr_o, t);
-            // B = P'^T (k = this lane's tokens, n = head gid), hi + lo f16 parts
-            const uint32_t ah0 = f16x2_pack(pr[0][0], pr[0][1]), ah2 = f16x2_pack(pr[1][0], pr[1][1]);
-            const float2 h0 = __half22float2(*reinterpret_cast<const __half2 *>(&ah0));
-            const float2 h2 = __half22float2(*reinterpret_cast<const __half2 *>(&ah2));
-            const uint32_t al0 = f16x2_pack(pr[0][0] - h0.x, pr[0][1] - h0.y);
-            const uint32_t al2 = f16x2_pack(pr[1][0] - h2.x, pr[1][1] - h2.y);
-            // A = V^T: channels 8 gid .. 8 gid + 7 (8 code bytes) of this lane's 4 token rows
-            uint2 vr[2][2];
-#pragma unroll
-            for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-                for (int q2 = 0; q2 < 2; ++q2) {
-                    const int r = trow[nt][q2];
-                    const uint2 v = lds_v2(vb + r * 64 + gid * 8);
-                    vr[nt][q2] = ok[nt][q2] ? v : make_uint2(0, 0);  // past seq_len: may be anything
-                }
-#pragma unroll
-            for (int db = 0; db < 4; ++db) {  // channels 8 gid + 2 db (A rows gid) and + 1 (rows gid + 8)
-                const uint32_t sel_ = (db & 1) ? 0x7362u : 0x5140u;
-                const uint32_t p0 = __byte_perm(db < 2 ? vr[0][0].x : vr[0][0].y, db < 2 ? vr[0][1].x : vr[0][1].y, sel_);
-                const uint32_t p1 = __byte_perm(db < 2 ? vr[1][0].x : vr[1][0].y, db < 2 ? vr[1][1].x : vr[1][1].y, sel_);
-                const uint32_t a0 = f8x2_to_f16x2(p0 & 0xffffu), a1 = f8x2_to_f16x2(p0 >> 16);
-                const uint32_t a2 = f8x2_to_f16x2(p1 & 0xffffu), a3 = f8x2_to_f16x2(p1 >> 16);
-                mma_f16_16816(oacc[db], a0, a1, a2, a3, ah0, ah2);
-                mma_f16_16816(oacc[db], a0, a1, a2, a3, al0, al2);
-            }
+            const uint32_t kb = sb + st * kF8Stage;
+            f8_attend_tile(acc, fq, kb, kb + 1024, sb + SM::kHist + st * 32, tok0, L, gid, t);
             __syncwarp();
             if (lane < 4 && i + RA < ntl) {  // refill this warp's slot with stage i + RA
                 fence_proxy_async();
@@ -598,17 +482,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
                 issue_f8(i + RA, lane);
             }
         }
-        lp += __shfl_xor_sync(0xffffffffu, lp, 1);
-        lp += __shfl_xor_sync(0xffffffffu, lp, 2);
-        {
-            const float s2e = E > -128 ? pow2i(E) : 1.f;  // back from the V-exponent reference
-            ot_store(wpart + warp * 8 * kSaPart, kSaPart, oacc, gid, t, p.G, s2e);
-            if (gid < p.G && t == 0) {
-                float *wr = wpart + (warp * 8 + gid) * kSaPart;
-                wr[kAttnD] = m;
-                wr[kAttnD + 1] = lp;
-            }
-        }
+        f8_store_partial(wpart + warp * 8 * kSaPart, kSaPart, acc, gid, t, p.G);
     } else {
         uint32_t qa[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         if (gid < p.G) {

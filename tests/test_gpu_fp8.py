@@ -278,3 +278,52 @@ def test_fp8_full_size_c3(ts):
     kq, vq, oq = quantize_both(ts, case)
     ref = enforce_fp8(case, oq, cfg.budget_tokens)
     _fp8_step(ts, cfg, case, kq, vq, ref)
+
+
+# ------------------------------------------------------------------ standalone entry points
+def test_sparse_and_dense_attention_fp8(ts):
+    """ts_sparse_decode_attn / ts_dense_decode_attn over an FP8 cache (the TMA attention
+    kernel's F8 instantiation) vs the oracle's attention over the dequantised values."""
+    cfg, case = make("c3_small", seed=51)
+    kq, vq, oq = quantize_both(ts, case)
+    cv = deq_case(case, oq)
+    qf = torch.from_numpy(oracle.widen(case["q"]).astype(np.float32))
+    d = {k: (v.to(DEV) if isinstance(v, torch.Tensor) else v) for k, v in case.items()}
+    L = ts.make_layout(d["q"], kq, d["page_table"], pool_shape=tuple(case["k_pool"].shape))
+    P = cfg.max_pages
+    g = torch.Generator().manual_seed(2)
+    K = 40
+    ids = np.stack([np.stack([np.sort(torch.randperm(-(-int(l) // cfg.page_size), generator=g)[:K].numpy())
+                              for _ in range(cfg.num_kv_heads)]) for l in case["seq_lens"].tolist()]).astype(np.int32)
+    cnt = np.full((cfg.batch, cfg.num_kv_heads), K, np.int32)
+    ro, rl = oracle.sparse_attn(qf, cv["k_pool"], cv["v_pool"], case["page_table"], case["seq_lens"], ids, cnt, cfg.scale)
+    o, lse = ts.sparse_decode_attn(L, d["q"], kq, vq, d["page_table"], d["seq_lens"],
+                                   torch.from_numpy(ids).to(DEV), torch.from_numpy(cnt).to(DEV), cfg.scale)
+    assert np.abs(o.cpu().numpy() - ro).max() <= 2e-3
+    assert np.abs(lse.cpu().numpy() - rl).max() <= 1e-3
+    allp = np.tile(np.arange(P, dtype=np.int32), (cfg.batch, cfg.num_kv_heads, 1))
+    allc = np.array([[-(-int(l) // cfg.page_size)] * cfg.num_kv_heads for l in case["seq_lens"].tolist()], np.int32)
+    do, dl = oracle.sparse_attn(qf, cv["k_pool"], cv["v_pool"], case["page_table"], case["seq_lens"], allp, allc, cfg.scale)
+    o2, l2 = ts.dense_decode_attn(L, d["q"], kq, vq, d["page_table"], d["seq_lens"], cfg.scale)
+    assert np.abs(o2.cpu().numpy() - do).max() <= 2e-3
+    assert np.abs(l2.cpu().numpy() - dl).max() <= 1e-3
+
+
+@pytest.mark.parametrize("fused", [True, False])
+def test_sharded_fp8_matches_oracle(ts, fused):
+    """Sequence sharding over an FP8 cache (shard emulation, 4 ranks): the selection equals
+    the unsharded FP8 step's and the oracle's; o within 2e-3 of the oracle."""
+    from paper_2509_12211_b200 import sharded
+    cfg = synth.config("c5", batch=2, ctx=20000, budget_tokens=1024)
+    case = synth.make_case(cfg, seed=53, ragged=True)
+    kq, vq, oq = quantize_both(ts, case)
+    ref = enforce_fp8(case, oq, cfg.budget_tokens)
+    d = {k: (v.to(DEV) if isinstance(v, torch.Tensor) else v) for k, v in case.items()}
+    shape = tuple(case["k_pool"].shape)
+    L = ts.make_layout(d["q"], kq, d["page_table"], pool_shape=shape)
+    o, lse, ids, cnts = sharded.emulate(ts, L, 4, d["q"], kq, vq, d["page_table"], d["seq_lens"],
+                                        cfg.budget_tokens, cfg.scale, fused=fused)
+    K = ids[0].shape[-1]
+    for r in range(4):
+        assert np.array_equal(ids[r].cpu().numpy(), ref["sel_ids"][:, :, :K])
+    assert np.abs(o.cpu().numpy().reshape(ref["o"].shape) - ref["o"]).max() <= 2e-3
