@@ -591,8 +591,9 @@ ts_status launch_step_cluster_app(const ts_layout *L, ScoreSelParams &sp, const 
 template <int W, int R>
 ts_status launch_step_cluster_t(const ts_layout *L, ScoreSelParams &sp, const AttnParams &ap,
                                 cudaStream_t st) {
-    if (L->kv_dtype == TS_FP8E4M3)  // the FP8 append is its own kernel (decode_step_impl)
-        return sp.k_new ? TS_ERR_UNSUPPORTED : launch_step_cluster_app<W, R, false, true>(L, sp, ap, st);
+    if (L->kv_dtype == TS_FP8E4M3)
+        return sp.k_new ? launch_step_cluster_app<W, R, true, true>(L, sp, ap, st)
+                        : launch_step_cluster_app<W, R, false, true>(L, sp, ap, st);
     return sp.k_new ? launch_step_cluster_app<W, R, true, false>(L, sp, ap, st)
                     : launch_step_cluster_app<W, R, false, false>(L, sp, ap, st);
 }
@@ -932,14 +933,6 @@ static ts_status decode_step_impl(const ts_layout *L, const void *q, const void 
     const cudaStream_t st = as_stream(stream);
     const int rows = L->batch * L->num_kv_heads;
     static const int two_kernels = env_int("TS_TWO_KERNELS", 0);
-    if (f8 && k_new && rows > 0) {  // FP8 append: its own kernel, then the one-launch step
-        if ((s = meta_append_impl(L, k_new, v_new, const_cast<int32_t *>(seq_lens), -1, page_table,
-                                  const_cast<void *>(k_pool), const_cast<void *>(v_pool),
-                                  const_cast<void *>(meta), stream)) != TS_OK)
-            return s;
-        k_new = v_new = nullptr;
-    }
-    const int f8_pre = g_launches;  // the FP8 append kernel, if it ran
     if ((f8 || (L->kv_dtype == TS_BF16 && !two_kernels)) && group_of(L) <= 8 && L->head_dim == 64 &&
         L->page_size % 16 == 0 && rows > 0) {
         // the whole step in one cluster-per-row kernel (step_cluster.cuh)
@@ -981,7 +974,7 @@ static ts_status decode_step_impl(const ts_layout *L, const void *q, const void 
         s = ring == 8 ? launch_step_cluster_t<4, 8>(L, sp, ap, st) : launch_step_cluster_t<4, 4>(L, sp, ap, st);
         phase_mark(3, st);
         if (s != TS_ERR_UNSUPPORTED || f8) {
-            g_launches = f8_pre + 1;
+            g_launches = 1;
             return s;
         }
     }

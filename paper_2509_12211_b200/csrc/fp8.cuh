@@ -61,8 +61,9 @@ TS_DEV uint2 f8x4_dequant_bf16(uint32_t w, float sc) {
 }
 
 // Quantise 8 bf16 channels (one lane of an aligned group of 8 lanes holding a 64-channel
-// row): returns the 8 codes and the row exponent (same in all 8 lanes).
-TS_DEV uint2 f8_quantize8(uint4 x, int &e_out) {
+// row): returns the 8 codes and the row exponent (same in all 8 lanes).  `mask`: the lanes
+// executing the call (each aligned group of 8 complete).
+TS_DEV uint2 f8_quantize8(uint4 x, int &e_out, unsigned mask = 0xffffffffu) {
     const uint32_t w[4] = {x.x, x.y, x.z, x.w};
     float f[8];
     float amax = 0.f;
@@ -72,9 +73,9 @@ TS_DEV uint2 f8_quantize8(uint4 x, int &e_out) {
         f[2 * i + 1] = bf16hi_to_f32(w[i]);
         amax = fmaxf(amax, fmaxf(fabsf(f[2 * i]), fabsf(f[2 * i + 1])));
     }
-    amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 1));
-    amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 2));
-    amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 4));
+    amax = fmaxf(amax, __shfl_xor_sync(mask, amax, 1));
+    amax = fmaxf(amax, __shfl_xor_sync(mask, amax, 2));
+    amax = fmaxf(amax, __shfl_xor_sync(mask, amax, 4));
     const int e = f8_row_exp(amax);
     const float s = pow2i(-e);  // exact scaling
     e_out = e;

@@ -71,7 +71,6 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
     constexpr int RA = F8 ? ((R * kSsStageBytes / kF8Stage) / W * W < 6 * W ? (R * kSsStageBytes / kF8Stage) / W * W : 6 * W) : 2 * R;
     static_assert(!F8 || RA <= 4 * R, "FP8 stage barriers must fit the afull / aempty slots");
     static_assert(!F8 || RA * 32 <= kSsHist * 4, "FP8 exponent slots must fit the histogram area");
-    static_assert(!(F8 && APP), "the FP8 append runs as its own kernel");
     static_assert(R % W == 0 && RA % W == 0, "stage -> consumer warp must be fixed");
     extern __shared__ uint8_t sc_raw[];
     // 1024-byte aligned (TMA swizzle atoms) by pointer arithmetic on the __shared__ array
@@ -173,11 +172,26 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
             const int c = lane - 16;
             const int blk = checked_block(p.page_table[(size_t)b * p.max_pages + max(ja, 0)], ap.num_blocks);  // (ja >= 0 when own)
             const size_t src = ((size_t)b * p.Hkv + g) * kAttnD + c * 8;
-            const size_t dst = (((size_t)blk * p.Hkv + g) * p.S + aslot) * kAttnD + c * 8;
-            uint16_t *kp = const_cast<uint16_t *>(static_cast<const uint16_t *>(ap.k_pool));
-            uint16_t *vp = const_cast<uint16_t *>(static_cast<const uint16_t *>(ap.v_pool));
-            *reinterpret_cast<uint4 *>(kp + dst) = *reinterpret_cast<const uint4 *>(p.k_new + src);
-            *reinterpret_cast<uint4 *>(vp + dst) = *reinterpret_cast<const uint4 *>(p.v_new + src);
+            const size_t prow = ((size_t)blk * p.Hkv + g) * p.S + aslot;  // pool row of the token
+            const uint4 kx = *reinterpret_cast<const uint4 *>(p.k_new + src);
+            const uint4 vx = *reinterpret_cast<const uint4 *>(p.v_new + src);
+            if constexpr (F8) {  // quantise (reading R21): codes + one exponent byte per row
+                int ek, ev;
+                const uint2 kq = f8_quantize8(kx, ek, 0x00ff0000u), vq = f8_quantize8(vx, ev, 0x00ff0000u);
+                uint8_t *kp = const_cast<uint8_t *>(static_cast<const uint8_t *>(ap.k_pool));
+                uint8_t *vp = const_cast<uint8_t *>(static_cast<const uint8_t *>(ap.v_pool));
+                *reinterpret_cast<uint2 *>(kp + prow * kAttnD + c * 8) = kq;
+                *reinterpret_cast<uint2 *>(vp + prow * kAttnD + c * 8) = vq;
+                if (c == 0) {
+                    const_cast<int8_t *>(ap.k_exp)[prow] = (int8_t)ek;
+                    const_cast<int8_t *>(ap.v_exp)[prow] = (int8_t)ev;
+                }
+            } else {
+                uint16_t *kp = const_cast<uint16_t *>(static_cast<const uint16_t *>(ap.k_pool));
+                uint16_t *vp = const_cast<uint16_t *>(static_cast<const uint16_t *>(ap.v_pool));
+                *reinterpret_cast<uint4 *>(kp + prow * kAttnD + c * 8) = kx;
+                *reinterpret_cast<uint4 *>(vp + prow * kAttnD + c * 8) = vx;
+            }
             fence_proxy_async_all();  // before the attention phase's TMA reads of this page
         }
         // refills: the consumer warp that owns a slot (stage i -> warp i % W, slot i % R,
@@ -219,8 +233,16 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
         uint32_t kmn = 0xffffffffu, kmx = 0u;
         const int apl = own ? ja - j0 : -1;  // the appended page, chunk-local
         uint4 kn = make_uint4(0, 0, 0, 0);
-        if (own && lane < 16 && (apl / kSsStagePages) % W == warp)
+        if (own && lane < 16 && (apl / kSsStagePages) % W == warp) {
             kn = *reinterpret_cast<const uint4 *>(p.k_new + ((size_t)b * p.Hkv + g) * kAttnD + (lane & 7) * 8);
+            if constexpr (F8) {  // Eq. 1 over the DEQUANTISED key (exact bf16; reading R21)
+                int ek;
+                const uint2 kq = f8_quantize8(kn, ek, 0x0000ffffu);
+                const float sc = pow2i(ek);
+                const uint2 d0 = f8x4_dequant_bf16(kq.x, sc), d1 = f8x4_dequant_bf16(kq.y, sc);
+                kn = make_uint4(d0.x, d0.y, d1.x, d1.y);
+            }
+        }
         for (int i = warp; i < nst; i += W) {
             const int st = i % R;
             mbar_wait(mfull0 + 8 * st, (i / R) & 1);

@@ -264,7 +264,14 @@ def test_decode_step_append_fp8(ts, name):
     meta = ts.meta_build(L, kq, dpt, torch.clamp(dl - 1, min=0).to(torch.int32))
     o, lse, ids, cnt = ts.decode_step_append(L, dq, k_new.to(DEV), v_new.to(DEV), kq, vq, meta, dpt, dl,
                                              cfg.budget_tokens, cfg.scale)
+    assert ts.launch_count() == 1  # the quantising append rides in the step's launch
     kc, ke, vc, ve = oq
+    # metadata == the oracle's over the dequantised keys of the full cache (Eq. 1)
+    omin, omax = oracle.meta_build(deq_case(case, oq)["k_pool"], case["page_table"], lens)
+    m = oracle.widen(meta.cpu())
+    for b, Lb in enumerate(lens.tolist()):
+        P = -(-Lb // S)
+        assert np.array_equal(m[b, :, :P, 0], omin[b, :, :P]) and np.array_equal(m[b, :, :P, 1], omax[b, :, :P])
     assert np.array_equal(gkc.cpu().numpy(), kc) and np.array_equal(gke.cpu().numpy(), ke)
     assert np.array_equal(gvc.cpu().numpy(), vc) and np.array_equal(gve.cpu().numpy(), ve)
     assert np.array_equal(ids.cpu().numpy(), ref["sel_ids"][:, :, :ids.shape[2]])
