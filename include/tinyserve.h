@@ -178,9 +178,10 @@ ts_status ts_decode_step(const ts_layout *layout, const void *q, const void *k_p
  * kv_dtype, device) are written to slot t % page_size of the block holding logical page
  * t / page_size, the (m, M) record of that page is updated as ts_meta_append does (Eq. 1,
  * PAPER.md:177-178; m = M = k for the first key of a page), and then the step runs exactly
- * as ts_decode_step with the same arguments — in ONE launch for the bf16 cluster path (the
+ * as ts_decode_step with the same arguments — in ONE launch for the bf16 and FP8 cluster path (the
  * page's scorer patches its staged record and persists it; the K/V row is published to the
- * attention phase by the cluster barrier).  Other layouts fall back to ts_meta_append's
+ * attention phase by the cluster barrier; FP8: the row is quantised as ts_kv_quantize and the
+ * record updated with the dequantised key).  Other layouts fall back to ts_meta_append's
  * kernel followed by ts_decode_step.  k_pool, v_pool and meta are modified in place; the
  * results equal ts_meta_append(seq_lens - 1) followed by ts_decode_step bit for bit in the
  * metadata and the page sets.  Unsharded layouts only (TS_ERR_UNSUPPORTED otherwise). */
