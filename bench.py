@@ -628,7 +628,7 @@ def main():
             if kvq:  # the oracle's FP8 step: exact dequantisation, then the float64 step
                 nbk = reps[0]["layout"].num_blocks
                 for kk in ("k_pool", "v_pool"):
-                    c_, e_ = ts.fp8_views(host[kk], nbk, cfg.num_kv_heads, cfg.page_size, cfg.head_dim)
+                    c_, e_ = ts.fp8_split(host[kk], nbk, cfg.num_kv_heads, cfg.page_size, cfg.head_dim)
                     host[kk] = torch.from_numpy(oracle.kv_dequantize(c_.numpy(), e_.numpy()))
                 host["q"] = host["q"].float()
             v, cores, sample, extras = oracle_rate(cfg, host, args.oracle_seconds)

@@ -80,10 +80,13 @@ typedef enum {
 } ts_status;
 
 /* KV storage type.  TS_FP8E4M3 ("FP16/INT8 KV formats" PAPER.md:94,
- * reading R21): k_pool / v_pool hold OCP FP8 E4M3 codes [num_blocks][Hkv][S][64] followed
- * immediately by one int8 exponent per row [num_blocks][Hkv][S] (row = one token, one kv
- * head; value = code * 2^e, e in [-64, 64] the smallest with max |x| <= 448 * 2^e), i.e.
- * num_blocks*Hkv*S*65 bytes (ts_pool_bytes); q, meta, k_new and v_new stay bf16, and the
+ * reading R21): each stored row (one token, one kv head) is 64 OCP FP8 E4M3 codes plus one
+ * int8 exponent e (value = code * 2^e, e in [-64, 64] the smallest with max |x| <= 448 * 2^e).
+ * k_pool / v_pool are sequences of 1040-byte SUB-PAGE RECORDS, one per 16 consecutive rows of
+ * [num_blocks][Hkv][S] (S a multiple of 16): the 16 rows' codes [16][64], then their 16
+ * exponent bytes — so row r's codes are at (r/16)*1040 + (r%16)*64 and its exponent at
+ * (r/16)*1040 + 1024 + r%16; num_blocks*Hkv*S*65 bytes (ts_pool_bytes).  q, meta, k_new and
+ * v_new stay bf16, and the
  * metadata is the exact min / max of the DEQUANTISED keys.  head_dim 64 only; attention
  * over an FP8 cache (ts_decode_step(_append / _prefetch), ts_sparse_decode_attn,
  * ts_dense_decode_attn, ts_shard_attend) needs page_size a multiple of 16 and G <= 8. */
@@ -274,14 +277,13 @@ ts_status ts_dense_decode_attn(const ts_layout *layout, const void *q, const voi
 size_t ts_dense_workspace_bytes(const ts_layout *layout);
 
 /* FP8 KV quantisation (reading R21; ts_dtype TS_FP8E4M3): rows x 64 bf16 values at src
- * (device, 16-byte aligned) -> codes [rows][64] uint8 (8-byte aligned) and exps [rows] int8:
- * per row e = smallest integer in [-64, 64] with max |x| <= 448 * 2^e, code = E4M3 nearest
- * to x * 2^-e (round to nearest even, saturating).  For a whole pool: rows =
- * num_blocks*Hkv*S, codes = the pool, exps = pool + rows*64.  Used for prefill / cache
- * import; decode-time appends quantise inside ts_meta_append / ts_decode_step_append.
+ * (device, 16-byte aligned; e.g. a bf16 pool [num_blocks][Hkv][S][64]) -> the FP8 pool format
+ * above at pool (device, 16-byte aligned, rows*65 bytes): per row e = smallest integer in
+ * [-64, 64] with max |x| <= 448 * 2^e, code = E4M3 nearest to x * 2^-e (round to nearest
+ * even, saturating).  Used for prefill / cache import; decode-time appends quantise inside
+ * ts_meta_append / ts_decode_step_append.  TS_ERR_SHAPE unless rows % 16 == 0;
  * TS_ERR_UNSUPPORTED unless head_dim == 64. */
-ts_status ts_kv_quantize(int64_t rows, int32_t head_dim, const void *src, void *codes, void *exps,
-                         void *stream);
+ts_status ts_kv_quantize(int64_t rows, int32_t head_dim, const void *src, void *pool, void *stream);
 
 /* Bytes of one K (or V) pool for the layout: num_blocks*Hkv*S*d*elem, or *65 for FP8
  * (codes + exponents).  Host-only; 0 for an invalid layout. */

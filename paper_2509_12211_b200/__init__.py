@@ -20,7 +20,7 @@ from ._lib import Layout, TinyServeError, TS_BF16, TS_F32, TS_FP8E4M3, check, ex
 __all__ = ["Layout", "TinyServeError", "make_layout", "meta_append", "meta_build",
            "score_pages", "select_topk", "sparse_decode_attn", "decode_step", "decode_step_append", "decode_step_prefetch", "select_merge", "lse_merge",
            "workspace_bytes", "attn_workspace_bytes", "dense_decode_attn", "dense_workspace_bytes", "new_workspace", "new_meta", "kmax", "launch_count",
-           "profile_events", "kv_quantize", "fp8_pool", "fp8_views", "pool_bytes",
+           "profile_events", "kv_quantize", "fp8_pool", "fp8_views", "fp8_split", "pool_bytes",
            "select_candidates", "shard_attend",
            "exported_symbols", "PagedKV"]
 
@@ -138,28 +138,37 @@ def pool_bytes(layout) -> int:
 
 
 def fp8_pool(num_blocks, num_kv_heads, page_size, head_dim, device) -> torch.Tensor:
-    """A zeroed FP8 pool (reading R21): codes [NB][Hkv][S][d] then exponents [NB][Hkv][S]."""
+    """A zeroed FP8 pool (reading R21): 1040-byte sub-page records of 16 rows (codes [16][64]
+    then the 16 row exponents), NB*Hkv*S*65 bytes."""
     return torch.zeros(num_blocks * num_kv_heads * page_size * (head_dim + 1), dtype=torch.uint8,
                        device=device)
 
 
 def fp8_views(pool, num_blocks, num_kv_heads, page_size, head_dim=64):
-    """(codes [NB][Hkv][S][d] uint8, exps [NB][Hkv][S] int8) views of an FP8 pool."""
-    n = num_blocks * num_kv_heads * page_size
-    codes = pool[: n * head_dim].view(num_blocks, num_kv_heads, page_size, head_dim)
-    exps = pool[n * head_dim: n * (head_dim + 1)].view(torch.int8).view(num_blocks, num_kv_heads, page_size)
+    """(codes [NB][Hkv][S/16][16][64] uint8, exps [NB][Hkv][S/16][16] int8): writable views of
+    an FP8 pool's sub-page records (token slot s of a block is [s // 16][s % 16])."""
+    rec = pool.view(num_blocks, num_kv_heads, page_size // 16, 16 * head_dim + 16)
+    codes = rec[..., : 16 * head_dim].unflatten(-1, (16, head_dim))
+    exps = rec[..., 16 * head_dim:].view(torch.int8)
     return codes, exps
 
 
+def fp8_split(pool, num_blocks, num_kv_heads, page_size, head_dim=64):
+    """Contiguous copies (codes [NB][Hkv][S][64] uint8, exps [NB][Hkv][S] int8) of an FP8 pool."""
+    c, e = fp8_views(pool, num_blocks, num_kv_heads, page_size, head_dim)
+    return (c.reshape(num_blocks, num_kv_heads, page_size, head_dim).contiguous(),
+            e.reshape(num_blocks, num_kv_heads, page_size).contiguous())
+
+
 def kv_quantize(src: torch.Tensor, out=None, stream=None) -> torch.Tensor:
-    """bf16 pool [NB][Hkv][S][d] (or any [..., d] rows) -> FP8 pool (ts_kv_quantize)."""
+    """bf16 rows [..., d] (a pool [NB][Hkv][S][d]; rows a multiple of 16) -> FP8 pool
+    (ts_kv_quantize)."""
     d = src.shape[-1]
     rows = src.numel() // d
     if out is None:
         out = torch.empty(rows * (d + 1), dtype=torch.uint8, device=src.device)
     _cuda(src, out)
-    check("ts_kv_quantize", lib().ts_kv_quantize(rows, d, _ptr(src), _ptr(out),
-                                                 out.data_ptr() + rows * d, _stream(stream)))
+    check("ts_kv_quantize", lib().ts_kv_quantize(rows, d, _ptr(src), _ptr(out), _stream(stream)))
     return out
 
 

@@ -71,7 +71,7 @@ def lib() -> ctypes.CDLL:
             "ts_select_merge": [P, P, I, ctypes.c_int64, I, I, I, P, P, P, P],
             "ts_lse_merge": [I, I, I, P, P, ctypes.c_int64, P, P, P],
             "ts_dense_decode_attn": [LP, P, P, P, P, P, F, P, P, P, SZ, P],
-            "ts_kv_quantize": [ctypes.c_int64, I, P, P, P, P],
+            "ts_kv_quantize": [ctypes.c_int64, I, P, P, P],
             "ts_select_candidates": [LP, P, P, P, P, I, P, P, P, P],
             "ts_shard_attend": [LP, P, P, P, P, P, P, P, I, ctypes.c_int64, I, F, P, P, P, P, P, SZ, P],
         }

@@ -50,15 +50,12 @@ ts_status check_layout(const ts_layout *L) {
     if (L->shard_stride < 1 || L->shard_offset < 0 || L->shard_offset >= L->shard_stride)
         return TS_ERR_SHAPE;
     if (L->head_dim != 64 && L->head_dim != 128) return TS_ERR_UNSUPPORTED;
-    if (L->kv_dtype == TS_FP8E4M3 && L->head_dim != 64) return TS_ERR_UNSUPPORTED;
+    if (L->kv_dtype == TS_FP8E4M3 && (L->head_dim != 64 || L->page_size % 16 != 0)) return TS_ERR_UNSUPPORTED;
     return TS_OK;
 }
 
-// FP8 pools (reading R21): codes [NB][Hkv][S][64] followed by the row exponents [NB][Hkv][S]
+// FP8 pools (reading R21): 1040-byte sub-page records of 16 rows (fp8.cuh)
 size_t f8_rows(const ts_layout *L) { return (size_t)L->num_blocks * L->num_kv_heads * L->page_size; }
-const int8_t *f8_exps(const void *pool, const ts_layout *L) {
-    return static_cast<const int8_t *>(pool) + f8_rows(L) * 64;
-}
 // q and metadata of an FP8 cache are bf16: the scoring view of the layout
 ts_layout score_view(const ts_layout *L) {
     ts_layout v = *L;
@@ -663,10 +660,6 @@ AttnParams attn_params(const ts_layout *L, const void *q, const void *k_pool, co
     p.splits = 1;
     p.items = L->batch * L->num_kv_heads;
     p.dbg = g_dbg_ts;
-    if (L->kv_dtype == TS_FP8E4M3) {  // FP8 pools: codes, then the row exponents (R21)
-        p.k_exp = f8_exps(k_pool, L);
-        p.v_exp = f8_exps(v_pool, L);
-    }
     return p;
 }
 
@@ -778,8 +771,7 @@ static ts_status meta_append_impl(const ts_layout *L, const void *k_new, const v
         if (L->num_kv_heads * 8 > 1024) return TS_ERR_UNSUPPORTED;
         launch_pdl(meta_append_f8_kernel, dim3(L->batch), dim3(L->num_kv_heads * 8), 0, as_stream(stream),
                    p, (const uint16_t *)k_new, (const uint16_t *)v_new, seq_lens, advance, page_table,
-                   (uint8_t *)k_pool, (uint8_t *)v_pool, const_cast<int8_t *>(f8_exps(k_pool, L)),
-                   const_cast<int8_t *>(f8_exps(v_pool, L)), (uint16_t *)meta);
+                   (uint8_t *)k_pool, (uint8_t *)v_pool, (uint16_t *)meta);
         ++g_launches;
         return launch_status();
     }
@@ -811,7 +803,7 @@ ts_status ts_meta_build(const ts_layout *L, const void *k_pool, const int32_t *p
     const int grid = (int)std::min<long long>((work + 255) / 256, (long long)device_sms() * 16);
     if (L->kv_dtype == TS_FP8E4M3)
         launch_pdl(meta_build_f8_kernel, dim3(grid), dim3(256), 0, as_stream(stream), p,
-                   (const uint8_t *)k_pool, f8_exps(k_pool, L), page_table, seq_lens, (uint16_t *)meta);
+                   (const uint8_t *)k_pool, page_table, seq_lens, (uint16_t *)meta);
     else if (L->kv_dtype == TS_BF16)
         launch_pdl(meta_build_kernel<uint16_t>, dim3(grid), dim3(256), 0, as_stream(stream), 
             p, (const uint16_t *)k_pool, page_table, seq_lens, (uint16_t *)meta);
@@ -962,10 +954,6 @@ static ts_status decode_step_impl(const ts_layout *L, const void *q, const void 
 
         AttnParams ap = attn_params(L, q, k_pool, v_pool, page_table, seq_lens, ids, cnt, kmax, scale,
                                     o, lse, ws);
-        if (f8) {
-            ap.k_exp = f8_exps(k_pool, L);
-            ap.v_exp = f8_exps(v_pool, L);
-        }
         phase_mark(0, st);
         // ring depth: 8 stages (64 KB in flight per CTA) when the rows leave SMs for wide
         // clusters (measured: C3 / C5 faster); 4 stages when many rows need >= 3 CTAs per SM
@@ -1058,17 +1046,17 @@ ts_status ts_dense_decode_attn(const ts_layout *L, const void *q, const void *k_
 }
 
 // FP8 KV storage (reading R21): quantise `rows` bf16 rows of head_dim 64.
-ts_status ts_kv_quantize(int64_t rows, int32_t head_dim, const void *src, void *codes, void *exps,
-                         void *stream) {
+ts_status ts_kv_quantize(int64_t rows, int32_t head_dim, const void *src, void *pool, void *stream) {
     g_launches = 0;
     if (rows < 0 || head_dim < 1) return TS_ERR_CONFIG;
     if (head_dim != 64) return TS_ERR_UNSUPPORTED;
-    if (!aligned16(src) || (reinterpret_cast<uintptr_t>(codes) & 7u)) return TS_ERR_ALIGN;
+    if (rows % 16) return TS_ERR_SHAPE;  // whole sub-page records
+    if (!aligned16(src) || !aligned16(pool)) return TS_ERR_ALIGN;
     if (rows == 0) return TS_OK;
     const long long thr = rows * 8;
     const int grid = (int)std::min<long long>((thr + 255) / 256, (long long)device_sms() * 16);
     launch_pdl(kv_quantize_kernel, dim3(grid), dim3(256), 0, as_stream(stream), (long long)rows,
-               (const uint16_t *)src, (uint8_t *)codes, (int8_t *)exps);
+               (const uint16_t *)src, (uint8_t *)pool);
     ++g_launches;
     return launch_status();
 }

@@ -39,8 +39,6 @@ struct AttnParams {
     int splits, items;
     unsigned long long *dbg;  // development: per-CTA globaltimer stamps (nullable)
     int dense;                // 1: attend every page (FullCache baseline), sel_* unused
-    const int8_t *k_exp;      // FP8 KV (reading R21): row exponents [NB][Hkv][S] (else null)
-    const int8_t *v_exp;
     // ts_shard_attend (sequence sharding): the selection is the global top-k
     // over `cand_parts` candidate lists (part q of row r: cand_k entries at
     // q * cand_part_stride + r * cand_k; -inf = none), merged in the kernel's prologue;

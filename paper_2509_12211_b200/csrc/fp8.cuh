@@ -7,8 +7,10 @@
 // Dequantised values c_i * 2^e are exact bf16 numbers, so the metadata (bf16, Eq. 1) over
 // the dequantised keys is exact and r (Eq. 2) remains an upper bound of q.k.
 //
-// Pool layout (include/tinyserve.h): an FP8 pool is [NB][Hkv][S][64] codes followed by
-// [NB][Hkv][S] int8 exponents (one byte per row), i.e. NB*Hkv*S*65 bytes.
+// Pool layout (include/tinyserve.h): an FP8 pool is a sequence of 1040-byte SUB-PAGE RECORDS,
+// one per 16 consecutive rows (token, kv head) of [NB][Hkv][S] (S a multiple of 16): the 16
+// rows' codes [16][64] then their 16 exponent bytes.  A 16-token attention tile and its scales
+// are one contiguous 1040-byte bulk copy; NB*Hkv*S*65 bytes in total.
 //
 //   kv_quantize_kernel     bf16 rows -> codes + exponents (prefill / cache import)
 //   meta_append_f8_kernel  the append (Eq. 1 maintenance) of a bf16 token into an FP8 cache
@@ -21,6 +23,10 @@
 namespace ts {
 
 constexpr int kF8MinExp = -64, kF8MaxExp = 64;
+constexpr int kF8Rec = 16 * 64 + 16;  // one sub-page record: 16 rows of codes + 16 exponents
+// byte offsets of row r's codes / exponent in an FP8 pool
+TS_DEV size_t f8_code_off(size_t r) { return (r >> 4) * kF8Rec + (r & 15) * 64; }
+TS_DEV size_t f8_exp_off(size_t r) { return (r >> 4) * kF8Rec + 16 * 64 + (r & 15); }
 
 // 2^e as an fp32 (|e| <= 126)
 TS_DEV float pow2i(int e) { return __uint_as_float(uint32_t(127 + e) << 23); }
@@ -83,9 +89,9 @@ TS_DEV uint2 f8_quantize8(uint4 x, int &e_out, unsigned mask = 0xffffffffu) {
                       f8x4_pack(f[4] * s, f[5] * s, f[6] * s, f[7] * s));
 }
 
-// ts_kv_quantize: rows of 64 bf16 -> codes [rows][64] + exps [rows]; 8 lanes per row.
+// ts_kv_quantize: rows of 64 bf16 -> an FP8 pool (sub-page records); 8 lanes per row.
 __global__ void kv_quantize_kernel(long long rows, const uint16_t *__restrict__ src,
-                                   uint8_t *__restrict__ codes, int8_t *__restrict__ exps) {
+                                   uint8_t *__restrict__ pool) {
     pdl_launch_dependents();
     pdl_wait();
     const long long nthr = rows * 8;
@@ -98,8 +104,8 @@ __global__ void kv_quantize_kernel(long long rows, const uint16_t *__restrict__ 
         int e;
         const uint2 q = f8_quantize8(x, e);
         if (live) {
-            *reinterpret_cast<uint2 *>(codes + r * 64 + c * 8) = q;
-            if (c == 0) exps[r] = (int8_t)e;
+            *reinterpret_cast<uint2 *>(pool + f8_code_off(r) + c * 8) = q;
+            if (c == 0) pool[f8_exp_off(r)] = (uint8_t)(int8_t)e;
         }
     }
 }
@@ -110,7 +116,6 @@ __global__ void meta_append_f8_kernel(MetaParams p, const uint16_t *__restrict__
                                       const uint16_t *__restrict__ v_new, int *__restrict__ seq_lens,
                                       int advance, const int *__restrict__ page_table,
                                       uint8_t *__restrict__ k_pool, uint8_t *__restrict__ v_pool,
-                                      int8_t *__restrict__ k_exp, int8_t *__restrict__ v_exp,
                                       uint16_t *__restrict__ meta) {
     pdl_launch_dependents();
     pdl_wait();
@@ -139,11 +144,11 @@ __global__ void meta_append_f8_kernel(MetaParams p, const uint16_t *__restrict__
     const uint2 vq = f8_quantize8(v, ev);
     if (!live) return;
     const size_t row = ((size_t)blk * p.Hkv + h) * p.S + slot;
-    *reinterpret_cast<uint2 *>(k_pool + row * 64 + c * 8) = kq;
-    *reinterpret_cast<uint2 *>(v_pool + row * 64 + c * 8) = vq;
+    *reinterpret_cast<uint2 *>(k_pool + f8_code_off(row) + c * 8) = kq;
+    *reinterpret_cast<uint2 *>(v_pool + f8_code_off(row) + c * 8) = vq;
     if (c == 0) {
-        k_exp[row] = (int8_t)ek;
-        v_exp[row] = (int8_t)ev;
+        k_pool[f8_exp_off(row)] = (uint8_t)(int8_t)ek;
+        v_pool[f8_exp_off(row)] = (uint8_t)(int8_t)ev;
     }
     // metadata over the dequantised key (exact bf16)
     const float sc = pow2i(ek);
@@ -163,7 +168,6 @@ __global__ void meta_append_f8_kernel(MetaParams p, const uint16_t *__restrict__
 
 // Metadata over the dequantised keys: one thread per (b, local page, kv head, 8 channels).
 __global__ void meta_build_f8_kernel(MetaParams p, const uint8_t *__restrict__ k_pool,
-                                     const int8_t *__restrict__ k_exp,
                                      const int *__restrict__ page_table,
                                      const int *__restrict__ seq_lens, uint16_t *__restrict__ meta) {
     pdl_launch_dependents();
@@ -185,8 +189,8 @@ __global__ void meta_build_f8_kernel(MetaParams p, const uint8_t *__restrict__ k
         const size_t row0 = ((size_t)blk * p.Hkv + h) * p.S;
         uint4 lo = make_uint4(0, 0, 0, 0), hi = lo;
         for (int s = 0; s < n; ++s) {
-            const uint2 q = *reinterpret_cast<const uint2 *>(k_pool + (row0 + s) * 64 + c * 8);
-            const float sc = pow2i(k_exp[row0 + s]);
+            const uint2 q = *reinterpret_cast<const uint2 *>(k_pool + f8_code_off(row0 + s) + c * 8);
+            const float sc = pow2i((int8_t)k_pool[f8_exp_off(row0 + s)]);
             const uint2 d0 = f8x4_dequant_bf16(q.x, sc), d1 = f8x4_dequant_bf16(q.y, sc);
             const uint4 x = make_uint4(d0.x, d0.y, d1.x, d1.y);
             lo = s ? Vec16<uint16_t>::vmin(lo, x) : x;
@@ -242,10 +246,9 @@ struct F8Acc {
     }
 };
 
-// One 16-token tile: K codes at kb ([16][64] bytes), V codes at vb, the tile's 16 K then 16 V
-// exponent bytes at eb; tokens tok0 + r, valid while < L.
-TS_DEV void f8_attend_tile(F8Acc &a, const F8Q &q, uint32_t kb, uint32_t vb, uint32_t eb, int tok0, int L,
-                           int gid, int t) {
+// One 16-token tile: the K and V sub-page records at kb / vb (codes [16][64] bytes, then the 16
+// exponent bytes at +1024); tokens tok0 + r, valid while < L.
+TS_DEV void f8_attend_tile(F8Acc &a, const F8Q &q, uint32_t kb, uint32_t vb, int tok0, int L, int gid, int t) {
     int trow[2][2];
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt)
@@ -269,7 +272,7 @@ TS_DEV void f8_attend_tile(F8Acc &a, const F8Q &q, uint32_t kb, uint32_t vb, uin
     float tmax = kNegInf;
     int evmax = -128;
     // row exponents: 8-byte reads per 8-token group, the lane's bytes picked with PRMT
-    const uint2 ke0 = lds_v2(eb), ke1 = lds_v2(eb + 8), ve0 = lds_v2(eb + 16), ve1 = lds_v2(eb + 24);
+    const uint2 ke0 = lds_v2(kb + 1024), ke1 = lds_v2(kb + 1032), ve0 = lds_v2(vb + 1024), ve1 = lds_v2(vb + 1032);
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt)
 #pragma unroll

@@ -287,8 +287,8 @@ struct SatSmem {
     static size_t bytes(int sel_stride) { return 1024 + kPages + (size_t)sel_stride * 8; }
 };
 
-// F8: FP8 KV (reading R21) — a stage holds the tile's K codes (1 KB), V codes (1 KB) and its
-// 16 + 16 exponent bytes (1-D bulk copies), consumed by f8_attend_tile (fp8.cuh).
+// F8: FP8 KV (reading R21) — a stage holds the tile's K and V sub-page records (codes +
+// exponents, 1040 B each, 1-D bulk copies), consumed by f8_attend_tile (fp8.cuh).
 template <int W, int R, bool F8 = false>
 __global__ void __launch_bounds__((W + 1) * 32, 4) sparse_attn_tma_kernel(
     const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, AttnParams p,
@@ -476,13 +476,11 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) sparse_attn_tma_kernel(
                 const int2 pg = pages[u];
                 info[st] = make_int2(pg.y + 16 * sub, 0);
                 const uint32_t dst = sb + SM::kRing + st * SM::kStage;
-                if constexpr (F8) {
-                    const int row0 = pg.x + 16 * sub;  // pool row of the tile's first token
-                    mbar_arrive_expect_tx(full0 + 8 * st, 2 * 1024 + 32);
-                    bulk_load_hint(dst, static_cast<const uint8_t *>(p.k_pool) + (size_t)row0 * 64, 1024, full0 + 8 * st, pol);
-                    bulk_load_hint(dst + 1024, static_cast<const uint8_t *>(p.v_pool) + (size_t)row0 * 64, 1024, full0 + 8 * st, pol);
-                    bulk_load(dst + 2048, p.k_exp + row0, 16, full0 + 8 * st);
-                    bulk_load(dst + 2064, p.v_exp + row0, 16, full0 + 8 * st);
+                if constexpr (F8) {  // the tile's K and V sub-page records (codes + exponents)
+                    const size_t rec = (size_t)(pg.x >> 4) + sub;
+                    mbar_arrive_expect_tx(full0 + 8 * st, 2 * kF8Rec);
+                    bulk_load_hint(dst, static_cast<const uint8_t *>(p.k_pool) + rec * kF8Rec, kF8Rec, full0 + 8 * st, pol);
+                    bulk_load_hint(dst + kF8Rec, static_cast<const uint8_t *>(p.v_pool) + rec * kF8Rec, kF8Rec, full0 + 8 * st, pol);
                 } else {
                     mbar_arrive_expect_tx(full0 + 8 * st, SM::kStage);
                     tma_load_2d(dst, &tmK, 0, pg.x + 16 * sub, full0 + 8 * st, pol);
@@ -505,7 +503,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) sparse_attn_tma_kernel(
             const int st = i % R;
             mbar_wait(full0 + 8 * st, (i / R) & 1);
             const uint32_t kb = sb + SM::kRing + st * SM::kStage;
-            f8_attend_tile(acc, fq, kb, kb + 1024, kb + 2048, info[st].x, L, gid, t);
+            f8_attend_tile(acc, fq, kb, kb + kF8Rec, info[st].x, L, gid, t);
             __syncwarp();
             if (lane == 0) mbar_arrive(empty0 + 8 * st);
         }

@@ -52,13 +52,9 @@ struct ScSmem {
     }
 };
 
-// FP8 KV (F8, reading R21): the attention stage holds the K and V code tiles (16 tokens x
-// 64 B: one contiguous KB each, loaded with 1-D bulk copies — measured 0.4 us faster on C2
-// than 2-D tensor-map tiles with a 64-byte swizzle) and their 16 + 16 row exponents.
-// The stage's 32 exponent bytes live outside the ring, in the radix-histogram area (idle
-// during the attention phase), so the ring holds 2 KB stages: 16 (R = 4) / 32 (R = 8) of
-// them, 4 / 8 per consumer warp in flight.
-constexpr int kF8Stage = 2048;  // K codes 1 KB | V codes 1 KB
+// FP8 KV (F8, reading R21): an attention stage holds the tile's K and V sub-page records
+// (16 code rows + 16 exponent bytes each, 1040 B, one 1-D bulk copy apiece).
+constexpr int kF8Stage = 2 * kF8Rec;
 
 template <int W, int R, bool DSM, bool APP, bool F8 = false>
 __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
@@ -70,7 +66,6 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
     // (FP8: at most 6 stages per consumer warp — 8 measured slower on C3)
     constexpr int RA = F8 ? ((R * kSsStageBytes / kF8Stage) / W * W < 6 * W ? (R * kSsStageBytes / kF8Stage) / W * W : 6 * W) : 2 * R;
     static_assert(!F8 || RA <= 4 * R, "FP8 stage barriers must fit the afull / aempty slots");
-    static_assert(!F8 || RA * 32 <= kSsHist * 4, "FP8 exponent slots must fit the histogram area");
     static_assert(R % W == 0 && RA % W == 0, "stage -> consumer warp must be fixed");
     extern __shared__ uint8_t sc_raw[];
     // 1024-byte aligned (TMA swizzle atoms) by pointer arithmetic on the __shared__ array
@@ -180,11 +175,11 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
                 const uint2 kq = f8_quantize8(kx, ek, 0x00ff0000u), vq = f8_quantize8(vx, ev, 0x00ff0000u);
                 uint8_t *kp = const_cast<uint8_t *>(static_cast<const uint8_t *>(ap.k_pool));
                 uint8_t *vp = const_cast<uint8_t *>(static_cast<const uint8_t *>(ap.v_pool));
-                *reinterpret_cast<uint2 *>(kp + prow * kAttnD + c * 8) = kq;
-                *reinterpret_cast<uint2 *>(vp + prow * kAttnD + c * 8) = vq;
+                *reinterpret_cast<uint2 *>(kp + f8_code_off(prow) + c * 8) = kq;
+                *reinterpret_cast<uint2 *>(vp + f8_code_off(prow) + c * 8) = vq;
                 if (c == 0) {
-                    const_cast<int8_t *>(ap.k_exp)[prow] = (int8_t)ek;
-                    const_cast<int8_t *>(ap.v_exp)[prow] = (int8_t)ev;
+                    kp[f8_exp_off(prow)] = (uint8_t)(int8_t)ek;
+                    vp[f8_exp_off(prow)] = (uint8_t)(int8_t)ev;
                 }
             } else {
                 uint16_t *kp = const_cast<uint16_t *>(static_cast<const uint16_t *>(ap.k_pool));
@@ -327,9 +322,9 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
         for (int e = tid; e < 2 * (a1 - a0); e += NT) {
             const int brow = sel[e >> 1].x;
             if (brow >= 0) {
-                if constexpr (F8)  // the code rows only (the exponents are 1/64 of it)
+                if constexpr (F8)  // the block's S / 16 sub-page records are contiguous
                     prefetch_l2_bulk(reinterpret_cast<const uint8_t *>((e & 1) ? p.v_pool : p.k_pool) +
-                                         (size_t)brow * p.S * kAttnD, (uint32_t)p.S * kAttnD);
+                                         (size_t)brow * (p.S >> 4) * kF8Rec, (uint32_t)(p.S >> 4) * kF8Rec);
                 else
                     prefetch_l2_bulk(((e & 1) ? p.v_pool : p.k_pool) + (size_t)brow * p.S * kAttnD,
                                      (uint32_t)p.S * kRowBytes);
@@ -456,8 +451,8 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
         // re-issued by its owner right after it is consumed and a CTA has W issuing warps
         // (a single issuing lane caps a CTA's 2 KB-tile gather at ~21 GB/s: scripts/gatherbench.cu)
     } else if constexpr (F8) {
-        // ---- FP8 KV (reading R21; fp8.cuh f8_attend_tile): per-head f16 q' fragments, the
-        // tiles' E4M3 codes by 1-D bulk copies, exponent bytes in the idle histogram area
+        // ---- FP8 KV (reading R21; fp8.cuh f8_attend_tile): per-head f16 q' fragments, each
+        // tile's K and V sub-page records (codes + exponents) by one 1-D bulk copy apiece
         uint4 x0 = make_uint4(0, 0, 0, 0), x1 = x0;
         if (gid < p.G) {
             const uint32_t qrow = sb + SM::kQ + gid * kRowBytes + 32 * t;
@@ -468,25 +463,20 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
         fence_proxy_async();  // the ring was last accessed by the generic proxy (scoring)
         const uint64_t pol = l2_policy_evict_first();
         const int ntl = t1 - t0;
-        const int8_t *kexp = ap.k_exp, *vexp = ap.v_exp;
-        // lane 4e + c issues part c (K codes, V codes, K exponents, V exponents) of the warp's
-        // e-th stage
-        auto issue_f8 = [&](int i, int c) {
+        // lane 2e + kv issues the K (kv 0) or V (kv 1) sub-page record of the warp's e-th stage
+        auto issue_f8 = [&](int i, int kv) {
             const int st = i % RA;
             const int tl = t0 + i, u = tl >> tps, sub = tl & (tpp - 1);
-            const int row0 = sel[u - u0].x + 16 * sub;  // pool row of the tile's first token
-            const uint32_t dst = sb + st * kF8Stage;
-            if (c < 2)  // the 16 code rows of a tile are one contiguous KB
-                bulk_load_hint(dst + c * 1024, static_cast<const uint8_t *>(c ? ap.v_pool : ap.k_pool) + (size_t)row0 * 64,
-                               1024, afull0 + 8 * st, pol);
-            else
-                bulk_load(sb + SM::kHist + st * 32 + (c - 2) * 16, (c == 2 ? kexp : vexp) + row0, 16, afull0 + 8 * st);
+            const int rec = (sel[u - u0].x >> 4) + sub;  // the tile's sub-page record
+            bulk_load_hint(sb + st * kF8Stage + kv * kF8Rec,
+                           static_cast<const uint8_t *>(kv ? ap.v_pool : ap.k_pool) + (size_t)rec * kF8Rec,
+                           kF8Rec, afull0 + 8 * st, pol);
         };
         {
-            const int e = lane >> 2, i = warp + W * e;
+            const int e = lane >> 1, i = warp + W * e;
             if (e < RA / W && i < ntl) {
-                if ((lane & 3) == 0) mbar_arrive_expect_tx(afull0 + 8 * (i % RA), 2 * 1024 + 32);
-                issue_f8(i, lane & 3);
+                if ((lane & 1) == 0) mbar_arrive_expect_tx(afull0 + 8 * (i % RA), kF8Stage);
+                issue_f8(i, lane & 1);
             }
         }
         F8Acc acc;
@@ -496,11 +486,11 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
             const int tok0 = sel[tu - u0].y + 16 * (tl & (tpp - 1));
             mbar_wait(afull0 + 8 * st, (i / RA) & 1);
             const uint32_t kb = sb + st * kF8Stage;
-            f8_attend_tile(acc, fq, kb, kb + 1024, sb + SM::kHist + st * 32, tok0, L, gid, t);
+            f8_attend_tile(acc, fq, kb, kb + kF8Rec, tok0, L, gid, t);
             __syncwarp();
-            if (lane < 4 && i + RA < ntl) {  // refill this warp's slot with stage i + RA
+            if (lane < 2 && i + RA < ntl) {  // refill this warp's slot with stage i + RA
                 fence_proxy_async();
-                if (lane == 0) mbar_arrive_expect_tx(afull0 + 8 * st, 2 * 1024 + 32);
+                if (lane == 0) mbar_arrive_expect_tx(afull0 + 8 * st, kF8Stage);
                 issue_f8(i + RA, lane);
             }
         }

@@ -1,4 +1,5 @@
 set -u
-python -m paper_2509_12211_b200._build > /dev/null 2>&1 || exit 1
-timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "append" 2>&1 | tail -1
-for c in c2 c3 c5; do timeout 300 python scripts/app_vs_plain.py $c; done
+for v in "" "-DTS_EXP_F8_NOKCVT" "-DTS_EXP_F8_NOLO"; do
+  TS_NVCC_EXTRA="$v" python -m paper_2509_12211_b200._build --force > /dev/null 2>&1 || exit 1
+  echo "== $v"; timeout 300 python scripts/dense_fp8_time.py c3 2>&1 | grep dense
+done

@@ -121,9 +121,12 @@ def test_round2_entry_points_validate_before_launch(ts):
     assert L.ts_pool_bytes(bf) == 16 * 4 * 16 * 64 * 2
     f8.head_dim = 128
     assert L.ts_pool_bytes(f8) == 0                               # FP8: head_dim 64 only
-    assert L.ts_kv_quantize(-1, 64, good, good, good, None) == 1  # rows < 0
-    assert L.ts_kv_quantize(4, 128, good, good, good, None) == 4  # head_dim 128 unsupported
-    assert L.ts_kv_quantize(4, 64, 0x1008, good, good, None) == 3  # src not 16-byte aligned
+    assert L.ts_kv_quantize(-1, 64, good, good, None) == 1    # rows < 0
+    assert L.ts_kv_quantize(16, 128, good, good, None) == 4   # head_dim 128 unsupported
+    assert L.ts_kv_quantize(8, 64, good, good, None) == 2     # not whole 16-row sub-page records
+    assert L.ts_kv_quantize(16, 64, 0x1008, good, None) == 3  # src not 16-byte aligned
+    f8s = ts.Layout(2, 16, 4, 64, 8, 8, 16, 1, 0, ts.TS_FP8E4M3)
+    assert L.ts_pool_bytes(f8s) == 0                          # FP8 needs page_size % 16 == 0
     sh = ts.Layout(2, 16, 4, 64, 16, 8, 16, 2, 1, ts.TS_BF16)
     assert L.ts_select_candidates(sh, good, good, good, good, 0, good, good, good, None) == 2  # k < 1
     assert L.ts_shard_attend(sh, good, good, good, good, good, good, good, 0, 0, 64, 1.0, good, good,

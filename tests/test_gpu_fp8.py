@@ -67,8 +67,9 @@ def quantize_both(ts, case, poison=True):
             for b, L in enumerate(case["seq_lens"].tolist()):
                 if L % S:
                     blk = int(pt[b, L // S])
-                    codes[blk, :, L % S:, :] = 0x7F  # E4M3 NaN
-                    exps[blk, :, L % S:] = 127
+                    for sl in range(L % S, S):
+                        codes[blk, :, sl // 16, sl % 16, :] = 0x7F  # E4M3 NaN
+                        exps[blk, :, sl // 16, sl % 16] = 127
     return kq, vq, (kc, ke, vc, ve)
 
 
@@ -98,14 +99,14 @@ def test_kv_quantize_bit_exact(ts, scale_kv):
     cfg, case = make("c3_small", scale_kv=scale_kv)
     kq, _, (kc, ke, _, _) = quantize_both(ts, case, poison=False)
     nb, Hkv, S, d = case["k_pool"].shape
-    codes, exps = ts.fp8_views(kq, nb, Hkv, S, d)
+    codes, exps = ts.fp8_split(kq, nb, Hkv, S, d)
     assert np.array_equal(exps.cpu().numpy(), ke)
     assert np.array_equal(codes.cpu().numpy(), kc)
 
 
 def test_kv_quantize_edge_rows(ts):
     """all-zero rows (e = -64), a row at the exponent clamps, ties, subnormal codes."""
-    rows = torch.zeros(8, 64)
+    rows = torch.zeros(16, 64)  # one sub-page record (rows 8..15 stay zero)
     rows[1, 0] = 448.0                       # e = 0 exactly
     rows[2, :] = torch.linspace(-1, 1, 64)   # mixed
     rows[3, 0] = 3e30                        # e clamped at 64, saturating codes
@@ -117,8 +118,8 @@ def test_kv_quantize_edge_rows(ts):
     x = rows.to(torch.bfloat16)
     q = ts.kv_quantize(x.to(DEV))
     kc, ke = oracle.kv_quantize(x)
-    assert np.array_equal(q[512:].view(torch.int8).cpu().numpy(), ke)
-    g = q[:512].view(8, 64).cpu().numpy()
+    assert np.array_equal(q[1024:].view(torch.int8).cpu().numpy(), ke)
+    g = q[:1024].view(16, 64).cpu().numpy()
     # -0.0 rounds to the sign-bearing zero on both sides; compare values where both are zero
     zero = (kc & 0x7F) == 0
     assert np.array_equal(g[~zero], kc[~zero]) and np.all((g[zero] & 0x7F) == 0)
@@ -162,8 +163,8 @@ def test_meta_append_fp8_incremental(ts):
     assert lens.cpu().tolist() == [cfg.ctx] * cfg.batch
     kc, ke = oracle.kv_quantize(case["k_pool"])
     vc, ve = oracle.kv_quantize(case["v_pool"])
-    gkc, gke = ts.fp8_views(kq, nb, Hkv, S, d)
-    gvc, gve = ts.fp8_views(vq, nb, Hkv, S, d)
+    gkc, gke = ts.fp8_split(kq, nb, Hkv, S, d)
+    gvc, gve = ts.fp8_split(vq, nb, Hkv, S, d)
     written = [(ptn[b, t // S], t % S) for b in range(cfg.batch) for t in range(cfg.ctx)]
     blk = np.array([w[0] for w in written])
     slot = np.array([w[1] for w in written])
@@ -258,7 +259,8 @@ def test_decode_step_append_fp8(ts, name):
     gvc, gve = ts.fp8_views(vq, nb, Hkv, S, d)
     for b, Lb in enumerate(lens.tolist()):  # stale content in the newest slot
         blk, sl = pt[b, (Lb - 1) // S], (Lb - 1) % S
-        gkc[blk, :, sl], gke[blk, :, sl], gvc[blk, :, sl], gve[blk, :, sl] = 0x55, 9, 0x33, -9
+        a_, r_ = sl // 16, sl % 16
+        gkc[blk, :, a_, r_], gke[blk, :, a_, r_], gvc[blk, :, a_, r_], gve[blk, :, a_, r_] = 0x55, 9, 0x33, -9
     dq, dpt, dl = case["q"].to(DEV), case["page_table"].to(DEV), lens.to(DEV)
     L = ts.make_layout(dq, kq, dpt, pool_shape=(nb, Hkv, S, d))
     meta = ts.meta_build(L, kq, dpt, torch.clamp(dl - 1, min=0).to(torch.int32))
@@ -266,6 +268,8 @@ def test_decode_step_append_fp8(ts, name):
                                              cfg.budget_tokens, cfg.scale)
     assert ts.launch_count() == 1  # the quantising append rides in the step's launch
     kc, ke, vc, ve = oq
+    gkc, gke = ts.fp8_split(kq, nb, Hkv, S, d)
+    gvc, gve = ts.fp8_split(vq, nb, Hkv, S, d)
     # metadata == the oracle's over the dequantised keys of the full cache (Eq. 1)
     omin, omax = oracle.meta_build(deq_case(case, oq)["k_pool"], case["page_table"], lens)
     m = oracle.widen(meta.cpu())
