@@ -54,8 +54,6 @@ ts_status check_layout(const ts_layout *L) {
     return TS_OK;
 }
 
-// FP8 pools (reading R21): 1040-byte sub-page records of 16 rows (fp8.cuh)
-size_t f8_rows(const ts_layout *L) { return (size_t)L->num_blocks * L->num_kv_heads * L->page_size; }
 // q and metadata of an FP8 cache are bf16: the scoring view of the layout
 ts_layout score_view(const ts_layout *L) {
     ts_layout v = *L;
@@ -360,7 +358,7 @@ template <int W, int R, bool F8 = false>
 ts_status launch_sat(const ts_layout *L, const AttnParams &p, bool pdl, cudaStream_t st) {
     auto kern = sparse_attn_tma_kernel<W, R, F8>;
     const int rows = L->batch * L->num_kv_heads;
-    const size_t sm = SatSmem<W, R>::bytes(p.sel_stride);
+    const size_t sm = SatSmemT<W, R, F8>::bytes(p.sel_stride);
     if (sm > 227 * 1024) return TS_ERR_UNSUPPORTED;
     if (!ensure_func_attrs((const void *)kern, sm, true)) return TS_ERR_CUDA;
     CUtensorMap tmK, tmV;
@@ -676,7 +674,7 @@ ts_status launch_attn(const ts_layout *L, const void *q, const void *k_pool, con
     }
     if (L->kv_dtype == TS_FP8E4M3) {  // the TMA-ring kernel's F8 instantiation
         if (L->page_size % 16 != 0 || group_of(L) > 8 || sel_stride > kMaxSelAttn) return TS_ERR_UNSUPPORTED;
-        return launch_sat<4, 8, true>(L, p, true, st);
+        return launch_sat<4, 16, true>(L, p, true, st);  // 2 KB stages: 16 in the bf16 ring's bytes
     }
     const int threads = 32 * std::min(p.G, 8);
     if (L->head_dim == 64)
@@ -1039,7 +1037,7 @@ ts_status ts_dense_decode_attn(const ts_layout *L, const void *q, const void *k_
     AttnParams p = attn_params(L, q, k_pool, v_pool, page_table, seq_lens, nullptr, nullptr,
                                L->max_pages, scale, o, lse, ws);
     p.dense = 1;
-    if (f8) return launch_sat<4, 8, true>(L, p, true, as_stream(stream));
+    if (f8) return launch_sat<4, 16, true>(L, p, true, as_stream(stream));
     static const int rr = env_int("TS_SA_R", 8);
     if (rr == 16) return launch_sat<4, 16>(L, p, true, as_stream(stream));
     return launch_sat<4, 8>(L, p, true, as_stream(stream));
@@ -1114,7 +1112,7 @@ ts_status ts_shard_attend(const ts_layout *L, const void *q, const void *k_pool,
     p.cand_part_stride = part_stride ? part_stride : (long long)L->batch * L->num_kv_heads * k;
     p.sel_out = sel_ids_out;
     p.sel_cnt_out = sel_count_out;
-    return f8 ? launch_sat<4, 8, true>(L, p, true, as_stream(stream)) : launch_sat<4, 8>(L, p, true, as_stream(stream));
+    return f8 ? launch_sat<4, 16, true>(L, p, true, as_stream(stream)) : launch_sat<4, 8>(L, p, true, as_stream(stream));
 }
 
 ts_status ts_select_merge(const float *cand_scores, const int32_t *cand_ids, int32_t parts,

@@ -23,6 +23,7 @@
 // the tail of the score/select kernel: griddepcontrol.wait sits just before it.
 #pragma once
 
+#include <type_traits>
 
 #include "attn.cuh"
 #include "common.cuh"
@@ -277,7 +278,7 @@ __global__ void __launch_bounds__(W * 32, 512 / (W * 32)) sparse_attn_kernel(Att
 template <int W, int R>
 struct SatSmem {
     static constexpr int kTile = 16 * kRowBytes;                  // 2 KB
-    static constexpr int kStage = 2 * kTile;                      // K + V
+    static constexpr int kStage = 2 * kTile;                      // K + V (FP8: SatSmemF8)
     static constexpr int kRing = 0;
     static constexpr int kWarpPart = kRing + R * kStage;          // [W][8][kSaPart] fp32
     static constexpr int kCtaPart = kWarpPart + W * 8 * kSaPart * 4;
@@ -287,13 +288,28 @@ struct SatSmem {
     static size_t bytes(int sel_stride) { return 1024 + kPages + (size_t)sel_stride * 8; }
 };
 
+// FP8 stages: the K and V sub-page records (2 x 1040 B), so twice the stages fit the bytes
+template <int W, int R>
+struct SatSmemF8 : SatSmem<W, R> {
+    static constexpr int kStage = 2 * kF8Rec;
+    static constexpr int kRing = 0;
+    static constexpr int kWarpPart = kRing + R * kStage;
+    static constexpr int kCtaPart = kWarpPart + W * 8 * kSaPart * 4;
+    static constexpr int kInfo = kCtaPart + 8 * kSaPart * 4;
+    static constexpr int kBars = kInfo + R * 8;
+    static constexpr int kPages = kBars + 2 * R * 8;
+    static size_t bytes(int sel_stride) { return 1024 + kPages + (size_t)sel_stride * 8; }
+};
+template <int W, int R, bool F8>
+using SatSmemT = typename std::conditional<F8, SatSmemF8<W, R>, SatSmem<W, R>>::type;
+
 // F8: FP8 KV (reading R21) — a stage holds the tile's K and V sub-page records (codes +
 // exponents, 1040 B each, 1-D bulk copies), consumed by f8_attend_tile (fp8.cuh).
 template <int W, int R, bool F8 = false>
 __global__ void __launch_bounds__((W + 1) * 32, 4) sparse_attn_tma_kernel(
     const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, AttnParams p,
     int C) {
-    using SM = SatSmem<W, R>;
+    using SM = SatSmemT<W, R, F8>;
     static_assert(R % W == 0, "stage -> consumer warp must be fixed");
     extern __shared__ uint8_t sat_raw[];
     // 1024-byte aligned (TMA swizzle atoms) by pointer arithmetic on the __shared__ array
@@ -465,28 +481,34 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) sparse_attn_tma_kernel(
     const int t0 = (int)((long long)ntile * rank / C), t1 = (int)((long long)ntile * (rank + 1) / C);
     if (dts && threadIdx.x == 0) dts[2] = globaltimer();
 
+    // stage i of this CTA's tiles -> slot i % R, consumed by warp i % W (R % W == 0), which
+    // re-issues the slot with stage i + R right after consuming it: W issuing warps per CTA
+    // (one issuing lane caps a CTA's gather of small tiles at ~20 GB/s: scripts/gatherbench.cu)
+    const uint64_t pol = l2_policy_evict_first();
+    const int ntl = t1 - t0;
+    auto tok0_of = [&](int i) {
+        const int tl = t0 + i, u = tl / tpp;
+        return pages[u].y + 16 * (tl - u * tpp);
+    };
+    auto issue = [&](int i, int kv) {  // part kv (0 = K, 1 = V) of stage i
+        const int st = i % R, tl = t0 + i, u = tl / tpp, sub = tl - u * tpp;
+        const int2 pg = pages[u];
+        const uint32_t dst = sb + SM::kRing + st * SM::kStage;
+        if constexpr (F8) {  // the tile's K / V sub-page record (codes + exponents)
+            const size_t rec = (size_t)(pg.x >> 4) + sub;
+            bulk_load_hint(dst + kv * kF8Rec, static_cast<const uint8_t *>(kv ? p.v_pool : p.k_pool) + rec * kF8Rec,
+                           kF8Rec, full0 + 8 * st, pol);
+        } else {
+            tma_load_2d(dst + kv * SM::kTile, kv ? &tmV : &tmK, 0, pg.x + 16 * sub, full0 + 8 * st, pol);
+        }
+    };
     if (warp == W) {
         // ================================ producer ================================
-        if (lane == 0) {
-            const uint64_t pol = l2_policy_evict_first();
-            for (int i = 0; i < t1 - t0; ++i) {
-                const int st = i % R;
-                mbar_wait(empty0 + 8 * st, ((i / R) & 1) ^ 1);
-                const int tl = t0 + i, u = tl / tpp, sub = tl - u * tpp;
-                const int2 pg = pages[u];
-                info[st] = make_int2(pg.y + 16 * sub, 0);
-                const uint32_t dst = sb + SM::kRing + st * SM::kStage;
-                if constexpr (F8) {  // the tile's K and V sub-page records (codes + exponents)
-                    const size_t rec = (size_t)(pg.x >> 4) + sub;
-                    mbar_arrive_expect_tx(full0 + 8 * st, 2 * kF8Rec);
-                    bulk_load_hint(dst, static_cast<const uint8_t *>(p.k_pool) + rec * kF8Rec, kF8Rec, full0 + 8 * st, pol);
-                    bulk_load_hint(dst + kF8Rec, static_cast<const uint8_t *>(p.v_pool) + rec * kF8Rec, kF8Rec, full0 + 8 * st, pol);
-                } else {
-                    mbar_arrive_expect_tx(full0 + 8 * st, SM::kStage);
-                    tma_load_2d(dst, &tmK, 0, pg.x + 16 * sub, full0 + 8 * st, pol);
-                    tma_load_2d(dst + SM::kTile, &tmV, 0, pg.x + 16 * sub, full0 + 8 * st, pol);
-                }
-            }
+        // the first R stages, two lanes (K, V) per stage in parallel
+        const int i = lane >> 1;
+        if (i < R && i < ntl) {
+            if ((lane & 1) == 0) mbar_arrive_expect_tx(full0 + 8 * i, SM::kStage);
+            issue(i, lane & 1);
         }
     } else if constexpr (F8) {
         // ================================ consumers (FP8) ==========================
@@ -499,13 +521,17 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) sparse_attn_tma_kernel(
         }
         const F8Q fq = f8_q_prep(x0, x1, p.scale * kLog2e);
         F8Acc acc;
-        for (int i = warp; i < t1 - t0; i += W) {
+        for (int i = warp; i < ntl; i += W) {
             const int st = i % R;
             mbar_wait(full0 + 8 * st, (i / R) & 1);
             const uint32_t kb = sb + SM::kRing + st * SM::kStage;
-            f8_attend_tile(acc, fq, kb, kb + kF8Rec, info[st].x, L, gid, t);
+            f8_attend_tile(acc, fq, kb, kb + kF8Rec, tok0_of(i), L, gid, t);
             __syncwarp();
-            if (lane == 0) mbar_arrive(empty0 + 8 * st);
+            if (lane < 2 && i + R < ntl) {  // refill this warp's slot with stage i + R
+                fence_proxy_async();
+                if (lane == 0) mbar_arrive_expect_tx(full0 + 8 * st, SM::kStage);
+                issue(i + R, lane);
+            }
         }
         f8_store_partial(wpart + warp * 8 * kSaPart, kSaPart, acc, gid, t, p.G);
     } else {
@@ -515,10 +541,10 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) sparse_attn_tma_kernel(
         float oacc[4][4];  // O^T: channels (8 gid + 2 db, + 1) x heads (2t, 2t + 1) (attn.cuh)
 #pragma unroll
         for (int j = 0; j < 4; ++j) oacc[j][0] = oacc[j][1] = oacc[j][2] = oacc[j][3] = 0.f;
-        for (int i = warp; i < t1 - t0; i += W) {
+        for (int i = warp; i < ntl; i += W) {
             const int st = i % R;
+            const int tok0 = tok0_of(i);
             mbar_wait(full0 + 8 * st, (i / R) & 1);
-            const int tok0 = info[st].x;
             const uint32_t kb = sb + SM::kRing + st * SM::kStage, vb = kb + SM::kTile;
             float sacc[2][4];
 #pragma unroll
@@ -571,7 +597,11 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) sparse_attn_tma_kernel(
                 }
             ot_pv_tile_bf16(oacc, vr, pr);
             __syncwarp();
-            if (lane == 0) mbar_arrive(empty0 + 8 * st);
+            if (lane < 2 && i + R < ntl) {  // refill this warp's slot with stage i + R
+                fence_proxy_async();
+                if (lane == 0) mbar_arrive_expect_tx(full0 + 8 * st, SM::kStage);
+                issue(i + R, lane);
+            }
         }
         // ---- warp partial: heads 2t, 2t+1 x channels 8 gid + {0..7}; m, l of head gid
         lp += __shfl_xor_sync(0xffffffffu, lp, 1);
