@@ -306,7 +306,7 @@ using SatSmemT = typename std::conditional<F8, SatSmemF8<W, R>, SatSmem<W, R>>::
 // F8: FP8 KV (reading R21) — a stage holds the tile's K and V sub-page records (codes +
 // exponents, 1040 B each, 1-D bulk copies), consumed by f8_attend_tile (fp8.cuh).
 template <int W, int R, bool F8 = false>
-__global__ void __launch_bounds__((W + 1) * 32, 4) sparse_attn_tma_kernel(
+__global__ void __launch_bounds__((W + 1) * 32, W >= 8 ? 2 : 4) sparse_attn_tma_kernel(
     const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, AttnParams p,
     int C) {
     using SM = SatSmemT<W, R, F8>;
