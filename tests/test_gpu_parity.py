@@ -350,6 +350,17 @@ def test_decode_step_integer_ties(ts):
     _step_parity(ts, cfg, case, ref)
 
 
+@pytest.mark.parametrize("ctx,budget", [(4096, 512), (4000, 128), (1000, 160), (250, 48)])
+def test_decode_step_integer_ties_short_rows(ts, ctx, budget):
+    """Rows of <= 256 pages (the one-warp ballot select of the fused step) with real ties
+    (integer q, k; G = 1 as in C2), ragged lengths: lower-id rule exactly as the oracle."""
+    cfg = synth.config("c2", batch=6, num_q_heads=4, num_kv_heads=4, ctx=ctx, budget_tokens=budget)
+    case = synth.make_case(cfg, seed=11, mode="int", ragged=True)
+    ref = oracle.decode_step(case["q"], case["k_pool"], case["v_pool"], case["page_table"],
+                             case["seq_lens"], cfg.budget_tokens, cfg.scale, want_scores=True)
+    _step_parity(ts, cfg, case, ref)
+
+
 @pytest.mark.parametrize("cname", ["c2", "c3", "c4"])
 def test_decode_step_full_size(ts, cname):
     """BASELINE configs at full size, in bench.py's launch configuration."""
