@@ -47,6 +47,21 @@ if [ "${NCU:-1}" = 1 ]; then
     echo "ncu full $t rc=$?"
   }
   n c2 c2 bf16; n c3 c3 bf16; n c5 c5 bf16; n c2-fp8 c2 fp8; n c3-fp8 c3 fp8
+  # summaries + DRAM traffic on the box; the reports stay under /tmp (gpurun_out/ is capped at
+  # 64 MiB), except the C2 one when it is small
+  args=""
+  for t in c2 c3 c5 c2-fp8 c3-fp8; do
+    r=$OUT/ev_prof_${t}_$TAG.ncu-rep
+    [ -f $r ] || continue
+    python scripts/ncu_summary.py $r > $OUT/ev_ncusum_${t}_$TAG.txt 2>&1
+    ncu -i $r --page raw --csv > $OUT/ev_ncuraw_${t}_$TAG.csv 2>/dev/null
+    args="$args $t=$r"
+  done
+  python scripts/traffic_json.py $args -o $OUT/ev_traffic_$TAG.json > /dev/null 2>&1
+  mkdir -p /tmp/ncu_reps; for r in $OUT/ev_prof_*_$TAG.ncu-rep; do
+    case $r in *prof_c2_*) [ $(stat -c %s $r) -lt 25000000 ] && continue;; esac
+    mv $r /tmp/ncu_reps/
+  done
 fi
 if [ "${STAMPS:-1}" = 1 ]; then
   for c in c2 c3 c5; do timeout 120 python scripts/step_stamps.py $c bf16; done > $OUT/ev_stamps_$TAG.txt 2>&1
