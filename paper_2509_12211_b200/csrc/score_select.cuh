@@ -319,12 +319,15 @@ TS_DEV int cta_topk(const uint32_t *keys, int n, int k, uint32_t kmin, uint32_t 
                 TS_TOPK_PROF(3);
                 if (warp == 0) {
                     // rank(c) = #{x : key_x > key_c or (key_x == key_c and idx_x < idx_c)}
-#pragma unroll
+                    // (rolled loops: the select is latency-bound and its code shares the
+                    // instruction cache with the rest of the fused step)
+#pragma unroll 1
                     for (int h = 0; h < 2; ++h) {
                         const int c = lane + 32 * h;
                         if (c < cnt) {
                             const uint32_t kc = cand[2 * c], ic = cand[2 * c + 1];
                             int rk = 0, gt = 0;
+#pragma unroll 4
                             for (int x = 0; x < cnt; ++x) {
                                 const uint2 cx = reinterpret_cast<const uint2 *>(cand)[x];
                                 rk += cx.x > kc || (cx.x == kc && cx.y < ic);
@@ -369,7 +372,7 @@ TS_DEV int cta_topk(const uint32_t *keys, int n, int k, uint32_t kmin, uint32_t 
     const int i0 = tid * per4, i1 = min(n4, i0 + per4);
     if (per4 <= 16) {
         uint64_t gm = 0, em = 0;
-#pragma unroll 4
+#pragma unroll 2
         for (int i = i0; i < i1; ++i) {
             const uint4 v = k4[i];
             const uint32_t e[4] = {v.x, v.y, v.z, v.w};
@@ -399,7 +402,7 @@ TS_DEV int cta_topk(const uint32_t *keys, int n, int k, uint32_t kmin, uint32_t 
         }
     } else {
         int n_gt = 0, n_eq = 0;
-#pragma unroll 4
+#pragma unroll 2
         for (int i = i0; i < i1; ++i) {
             const uint4 v = k4[i];
             n_gt += (v.x > tgt) + (v.y > tgt) + (v.z > tgt) + (v.w > tgt);
