@@ -163,6 +163,40 @@ __global__ void lse_merge_kernel(int parts, int rows, int d, const float *__rest
     pdl_launch_dependents();
     pdl_wait();
     const int r = blockIdx.x;
+    if (parts <= 64) {
+        // warp 0 reads the <= 64 partial lse values in one round (two per lane), reduces max and
+        // sum by shuffles and publishes the normalised weights w_q = exp(lse_q - lse); every
+        // thread then sums its channel over the parts with the loads in flight together
+        __shared__ float w[64];
+        __shared__ float s_tot;
+        if (threadIdx.x < 32) {
+            const int q0 = threadIdx.x, q1 = threadIdx.x + 32;
+            const float a = q0 < parts ? lse_parts[q0 * sl + r] : kNegInf;
+            const float b = q1 < parts ? lse_parts[q1 * sl + r] : kNegInf;
+            float M = fmaxf(a, b);
+#pragma unroll
+            for (int o2 = 16; o2; o2 >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o2));
+            float l = M != kNegInf ? (a != kNegInf ? expf(a - M) : 0.f) + (b != kNegInf ? expf(b - M) : 0.f) : 0.f;
+#pragma unroll
+            for (int o2 = 16; o2; o2 >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o2);
+            const float tot = M != kNegInf ? M + logf(l) : kNegInf;
+            w[q0] = a != kNegInf ? expf(a - tot) : 0.f;
+            w[q1] = b != kNegInf ? expf(b - tot) : 0.f;
+            if (threadIdx.x == 0) s_tot = tot;
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < d; i += blockDim.x) {
+            float acc = 0.f;
+#pragma unroll 8
+            for (int q = 0; q < parts; ++q) {
+                const float wq = w[q];
+                if (wq != 0.f) acc += wq * o_parts[q * so + (size_t)r * d + i];
+            }
+            o[(size_t)r * d + i] = acc;
+        }
+        if (threadIdx.x == 0 && lse) lse[r] = s_tot;
+        return;
+    }
     float M = kNegInf;
     for (int q = 0; q < parts; ++q) M = fmaxf(M, lse_parts[q * sl + r]);
     float l = 0.f;

@@ -481,13 +481,16 @@ def test_meta_append_past_capacity_is_dropped(ts):
     assert torch.equal(meta[0], m0[0])
 
 
-def test_lse_merge_kernel(ts):
+@pytest.mark.parametrize("parts,d", [(5, 64), (1, 64), (8, 128), (64, 64), (70, 64)])
+def test_lse_merge_kernel(ts, parts, d):
+    """<= 64 parts: the one-round weight path; more: the general loop."""
     rng = np.random.default_rng(1)
-    parts, rows, d = 5, 33, 64
+    rows = 33
     op = rng.standard_normal((parts, rows, d))
     lp = rng.standard_normal((parts, rows)) * 3
-    lp[1, :4] = -np.inf
-    lp[:, 7] = -np.inf
+    if parts > 1:
+        lp[1, :4] = -np.inf  # a part without tokens
+    lp[:, 7] = -np.inf  # a row without tokens
     ro, rl = oracle.lse_merge(op, lp)
     go, gl = ts.lse_merge(torch.tensor(op, dtype=torch.float32, device=DEV),
                           torch.tensor(lp, dtype=torch.float32, device=DEV))
