@@ -383,13 +383,38 @@ __global__ void __launch_bounds__((W + 1) * 32, W >= 8 ? 2 : 4) sparse_attn_tma_
         uint32_t *mcand = reinterpret_cast<uint32_t *>(mred + 64);
         int *msel = reinterpret_cast<int *>(mcand + 2 * 64);
         constexpr int NT = (W + 1) * 32;
+        // the candidates are read from L2 once, all of a thread's loads in flight together, and
+        // kept in registers for the placement below (up to kCpt per thread; more: two passes)
+        constexpr int kCpt = 8;
+        const bool inreg = ncand <= kCpt * NT;
+        int rid[kCpt];
+        float rsc[kCpt];
+        if (inreg) {
+#pragma unroll
+            for (int j = 0; j < kCpt; ++j) {
+                const int e = threadIdx.x + j * NT;
+                rid[j] = -1;
+                rsc[j] = kNegInf;
+                if (e < ncand) {
+                    const size_t at = (size_t)(e / p.cand_k) * p.cand_part_stride + (size_t)row * p.cand_k + e % p.cand_k;
+                    rid[j] = __ldcg(p.cand_ids + at);
+                    rsc[j] = __ldcg(p.cand_scores + at);
+                }
+            }
+        }
         for (int i = threadIdx.x; i < nw; i += NT) bits[i] = 0u;
         for (int i = threadIdx.x; i < kSsHistM; i += NT) mhist[i] = 0;
         __syncthreads();
-        for (int e = threadIdx.x; e < ncand; e += NT) {
-            const size_t at = (size_t)(e / p.cand_k) * p.cand_part_stride + (size_t)row * p.cand_k + e % p.cand_k;
-            const int id = __ldcg(p.cand_ids + at);
-            if (__ldcg(p.cand_scores + at) != kNegInf && id >= 0 && id < Pg) atomicOr(&bits[id >> 5], 1u << (id & 31));
+        if (inreg) {
+#pragma unroll
+            for (int j = 0; j < kCpt; ++j)
+                if (rsc[j] != kNegInf && rid[j] >= 0 && rid[j] < Pg) atomicOr(&bits[rid[j] >> 5], 1u << (rid[j] & 31));
+        } else {
+            for (int e = threadIdx.x; e < ncand; e += NT) {
+                const size_t at = (size_t)(e / p.cand_k) * p.cand_part_stride + (size_t)row * p.cand_k + e % p.cand_k;
+                const int id = __ldcg(p.cand_ids + at);
+                if (__ldcg(p.cand_scores + at) != kNegInf && id >= 0 && id < Pg) atomicOr(&bits[id >> 5], 1u << (id & 31));
+            }
         }
         __syncthreads();
         {  // exclusive prefix of the word popcounts (contiguous runs of words per thread)
@@ -407,10 +432,7 @@ __global__ void __launch_bounds__((W + 1) * 32, W >= 8 ? 2 : 4) sparse_attn_tma_
         __syncthreads();
         const int nlive = mred[63];
         uint32_t kmn = 0xffffffffu, kmx = 0u;
-        for (int e = threadIdx.x; e < ncand; e += NT) {
-            const size_t at = (size_t)(e / p.cand_k) * p.cand_part_stride + (size_t)row * p.cand_k + e % p.cand_k;
-            const int id = __ldcg(p.cand_ids + at);
-            const float sv = __ldcg(p.cand_scores + at);
+        auto place = [&](int id, float sv) {
             if (sv != kNegInf && id >= 0 && id < Pg) {
                 const int pos = wpre[id >> 5] + __popc(bits[id >> 5] & ((1u << (id & 31)) - 1u));
                 const uint32_t key = score_key(sv);
@@ -418,6 +440,15 @@ __global__ void __launch_bounds__((W + 1) * 32, W >= 8 ? 2 : 4) sparse_attn_tma_
                 mids[pos] = id;
                 kmn = min(kmn, key);
                 kmx = max(kmx, key);
+            }
+        };
+        if (inreg) {
+#pragma unroll
+            for (int j = 0; j < kCpt; ++j) place(rid[j], rsc[j]);
+        } else {
+            for (int e = threadIdx.x; e < ncand; e += NT) {
+                const size_t at = (size_t)(e / p.cand_k) * p.cand_part_stride + (size_t)row * p.cand_k + e % p.cand_k;
+                place(__ldcg(p.cand_ids + at), __ldcg(p.cand_scores + at));
             }
         }
         for (int i = nlive + threadIdx.x; i < n4; i += NT) mkeys[i] = 0u;
@@ -430,18 +461,26 @@ __global__ void __launch_bounds__((W + 1) * 32, W >= 8 ? 2 : 4) sparse_attn_tma_
             for (int i = threadIdx.x; out && i < p.cand_k; i += NT) out[i] = i < kk ? msel[i] : -1;
             if (p.sel_cnt_out && threadIdx.x == 0) p.sel_cnt_out[row] = kk;
         }
-        if (warp == W) {  // owned pages, compacted in id order
+        if (warp == W) {  // owned pages, compacted in id order (two rounds' page-table loads at once)
             int n = 0;
-            for (int u0 = 0; u0 < kk; u0 += 32) {
-                const int u = u0 + lane;
-                const int j = u < kk ? msel[u] : -1;
-                const bool own = j >= 0 && j % p.stride == p.offset;
-                const unsigned m = __ballot_sync(0xffffffffu, own);
-                if (own) {
-                    const int blk = checked_block(__ldg(p.page_table + (size_t)b * p.max_pages + j / p.stride), p.num_blocks);
-                    pages[n + __popc(m & ((1u << lane) - 1u))] = make_int2((blk * p.Hkv + g) * p.S, j * p.S);
+            for (int u0 = 0; u0 < kk; u0 += 64) {
+                int j[2], blk[2];
+                bool own[2];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int u = u0 + 32 * h + lane;
+                    j[h] = u < kk ? msel[u] : -1;
+                    own[h] = j[h] >= 0 && j[h] % p.stride == p.offset;
+                    blk[h] = own[h] ? __ldg(p.page_table + (size_t)b * p.max_pages + j[h] / p.stride) : 0;
                 }
-                n += __popc(m);
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const unsigned m = __ballot_sync(0xffffffffu, own[h]);
+                    if (own[h])
+                        pages[n + __popc(m & ((1u << lane) - 1u))] =
+                            make_int2((checked_block(blk[h], p.num_blocks) * p.Hkv + g) * p.S, j[h] * p.S);
+                    n += __popc(m);
+                }
             }
             if (lane == 0) s_nown = n;
         }
