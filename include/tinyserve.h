@@ -98,7 +98,8 @@ typedef struct {
     int32_t num_kv_heads;   /* Hkv, Hq % Hkv == 0, group size G = Hq / Hkv                  */
     int32_t head_dim;       /* d                                            */
     int32_t page_size;      /* S tokens per page                             */
-    int32_t max_pages;      /* row stride of page_table and scores (local pages)           */
+    int32_t max_pages;      /* row stride of page_table and scores (local pages);          *
+                             * max_pages * page_size <= 2^26 tokens (else TS_ERR_UNSUPPORTED) */
     int32_t num_blocks;     /* physical blocks in k_pool / v_pool / meta                   */
     int32_t shard_stride;   /* 1 unsharded; G ranks for block-cyclic sequence sharding     */
     int32_t shard_offset;   /* this rank's residue, 0 <= shard_offset < shard_stride       */

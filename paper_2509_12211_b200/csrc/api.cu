@@ -50,6 +50,8 @@ ts_status check_layout(const ts_layout *L) {
     if (L->shard_stride < 1 || L->shard_offset < 0 || L->shard_offset >= L->shard_stride)
         return TS_ERR_SHAPE;
     if (L->head_dim != 64 && L->head_dim != 128) return TS_ERR_UNSUPPORTED;
+    // 64M tokens per row: the kernels' 32-bit tile / page arithmetic (tiles x cluster width < 2^31)
+    if ((long long)L->max_pages * L->page_size > (1LL << 26)) return TS_ERR_UNSUPPORTED;
     if (L->kv_dtype == TS_FP8E4M3 && (L->head_dim != 64 || L->page_size % 16 != 0)) return TS_ERR_UNSUPPORTED;
     return TS_OK;
 }

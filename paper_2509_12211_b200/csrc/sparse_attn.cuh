@@ -517,7 +517,7 @@ __global__ void __launch_bounds__((W + 1) * 32, W >= 8 ? 2 : 4) sparse_attn_tma_
     __syncthreads();
     const int tpp = p.S >> 4;                 // tiles per page
     const int ntile = s_nown * tpp;
-    const int t0 = (int)((long long)ntile * rank / C), t1 = (int)((long long)ntile * (rank + 1) / C);
+    const int t0 = ntile * rank / C, t1 = ntile * (rank + 1) / C;  // < 2^31: check_layout bounds a row
     if (dts && threadIdx.x == 0) dts[2] = globaltimer();
 
     // stage i of this CTA's tiles -> slot i % R, consumed by warp i % W (R % W == 0), which

@@ -345,7 +345,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
     const int S = p.S, tpp = S >> 4, tps = __ffs(tpp) - 1;  // tiles per page (power of 2), log2
     const int kk = min(p.kmax, P);  // the selection size is known before the select
     const int ntile = kk * tpp;
-    const int t0 = (int)((long long)ntile * rank / C), t1 = (int)((long long)ntile * (rank + 1) / C);
+    const int t0 = ntile * rank / C, t1 = ntile * (rank + 1) / C;  // < 2^31: check_layout bounds a row
     const int u0 = t0 / tpp, u1 = (t1 + tpp - 1) / tpp;     // pages of this CTA's tiles
     const int w0 = kk * rank / C, w1 = kk * (rank + 1) / C;  // sel_ids entries this CTA writes
     const int *ptrow = pt_bulk ? pt_s : p.page_table + (size_t)b * p.max_pages;

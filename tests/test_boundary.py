@@ -66,7 +66,8 @@ def test_host_only_entry_points(ts):
 
 @pytest.mark.parametrize("field,value,status", [
     ("page_size", 0, 1), ("head_dim", 0, 1), ("kv_dtype", 7, 1), ("num_q_heads", 15, 2),
-    ("shard_offset", 3, 2), ("head_dim", 96, 4)])
+    ("shard_offset", 3, 2), ("head_dim", 96, 4),
+    ("max_pages", (1 << 22) + 1, 4)])  # > 2^26 tokens per row (32-bit tile arithmetic)
 def test_validation_errors_before_launch(ts, field, value, status):
     lay = ts.Layout(2, 16, 4, 64, 16, 8, 16, 2, 1, ts.TS_BF16)
     setattr(lay, field, value)
