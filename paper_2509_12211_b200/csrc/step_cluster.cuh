@@ -97,10 +97,10 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
     const int row = blockIdx.x / C, rank = blockIdx.x % C;
     const int b = row / p.Hkv, g = row % p.Hkv;
     unsigned long long *dts = p.dbg && blockIdx.x < 4096 ? p.dbg + blockIdx.x * 8 : nullptr;
-#ifdef TS_SEL_PROF  // select-internal stamps: leader's select at +4096*8, chunk selects at +8192*8
-    unsigned long long *dsel = dts ? dts + 4096 * 8 : nullptr, *dchk = dts ? dts + 8192 * 8 : nullptr;
+#ifdef TS_SEL_PROF  // select-internal stamps (the final select) at +4096*8
+    unsigned long long *dsel = dts ? dts + 4096 * 8 : nullptr;
 #else
-    unsigned long long *dsel = nullptr, *dchk = nullptr;
+    unsigned long long *dsel = nullptr;
 #endif
 #define SC_STAMP(e) \
     if (dts && tid == 0) dts[e] = globaltimer();
@@ -355,46 +355,19 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
         if (pos >= u0 && pos < u1) sel[pos - u0] = make_int2((checked_block(ptrow[pg], ap.num_blocks) * p.Hkv + g) * S, pg * S);
         if (pos >= w0 && pos < w1) out_id[pos] = pg;
     };
-    if (two) {
-        uint32_t *lkeys = reinterpret_cast<uint32_t *>(sc);  // chunk-local scores -> keys
-        for (int i = tid; i < ((nloc + 3) & ~3); i += NT) lkeys[i] = i < nloc ? score_key(sc[i]) : 0u;
-        __syncthreads();
-        uint32_t *myk = ckey + rank * p.kmax;
-        int *myi = cid + rank * p.kmax;
-        auto emit_c = [&](int pos, int i) {
-            myk[pos] = lkeys[i];
-            myi[pos] = j0 + i;
-        };
-        const int kl = cta_topk<NT, 0, 0>(lkeys, nloc, p.kmax, *s_kmin, *s_kmax, hist, red, cand, emit_c, dchk);
-        for (int i = kl + tid; i < p.kmax; i += NT) myk[i] = 0u;  // absent
-        __syncthreads();
-        cluster_wait();  // every CTA of the cluster is running
-        // push this chunk's K candidates into every other CTA; reset the histogram meanwhile
-        const int k4n = p.kmax >> 2;  // 16-byte remote stores (host: kmax % 4 == 0)
-        for (int x = tid; x < (C - 1) * k4n; x += NT) {
-            const int r = rank + 1 + x / k4n, u = x % k4n;
-            const int peer = r < C ? r : r - C;
-            reinterpret_cast<uint4 *>(cl.map_shared_rank(ckey, peer) + rank * p.kmax)[u] =
-                reinterpret_cast<const uint4 *>(myk)[u];
-            reinterpret_cast<int4 *>(cl.map_shared_rank(cid, peer) + rank * p.kmax)[u] =
-                reinterpret_cast<const int4 *>(myi)[u];
-        }
-        for (int i = tid; i < kSsHist / 4; i += NT) reinterpret_cast<int4 *>(hist)[i] = make_int4(0, 0, 0, 0);
-        cluster_arrive_release();
-        cluster_wait();
-    } else {
+    uint32_t *lkeys = reinterpret_cast<uint32_t *>(sc);  // scores -> orderable keys, in place
+    if (!two) {
         // this CTA's slice of the row as keys (0 = no page, up to the 4-padded row length)
         const int e1 = min(j0 + p.chunk, (P + 3) & ~3);
-        uint32_t *keys = reinterpret_cast<uint32_t *>(sc);
-        for (int i = j0 + tid; i < e1; i += NT) keys[i] = i < P ? score_key(sc[i]) : 0u;
+        for (int i = j0 + tid; i < e1; i += NT) lkeys[i] = i < P ? score_key(sc[i]) : 0u;
         if (C > 1) {
             __syncthreads();
             cluster_wait();  // every CTA of the cluster is running
             const int n4 = max(0, e1 - j0) >> 2;  // j0 and e1 are multiples of 4: 16-byte stores
-            const uint4 *src = reinterpret_cast<const uint4 *>(keys + j0);
+            const uint4 *src = reinterpret_cast<const uint4 *>(lkeys + j0);
             for (int x = tid; x < (C - 1) * n4; x += NT) {
                 const int r = rank + 1 + x / n4, i = x % n4;
-                reinterpret_cast<uint4 *>(cl.map_shared_rank(keys, r < C ? r : r - C) + j0)[i] = src[i];
+                reinterpret_cast<uint4 *>(cl.map_shared_rank(lkeys, r < C ? r : r - C) + j0)[i] = src[i];
             }
             if (tid >= 1 && tid < C && *s_kmin <= *s_kmax) {  // thread r: peer rank + r
                 const int r = rank + tid, peer = r < C ? r : r - C;
@@ -404,43 +377,81 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
             cluster_arrive_release();
             cluster_wait();
         }
-    }
-    SC_STAMP(5);
-    {
-        int kd;
-        if (two) {
-            const int nc = C * p.kmax;
-            int nlive = 0;  // live candidates: sum over chunks of min(K, chunk pages)
-            for (int r = 0; r < C; ++r) nlive += min(p.kmax, max(0, min(P - r * p.chunk, p.chunk)));
-            uint32_t mn = 0xffffffffu, mx = 0u;
-            for (int i = tid; i < nc; i += NT)
-                if (ckey[i]) {
-                    mn = min(mn, ckey[i]);
-                    mx = max(mx, ckey[i]);
-                }
-            if (P > 0 && pt_bulk) mbar_wait(ptbar, 0);
-            block_minmax<NT, 0>(mn, mx, red);
-            SC_STAMP(6);
-            auto emit = [&](int pos, int i) { emit_pg(pos, cid[i]); };
-            // candidates are chunk-major, ids ascending inside a chunk: entry order == id order
-            kd = cta_topk<NT, 0, 11>(ckey, nc, p.kmax, mn, mx, hist, red, cand, emit, dsel, false, nlive);
-        } else {
-            const uint32_t *keys = reinterpret_cast<const uint32_t *>(sc);
-            if (P > 0 && pt_bulk) mbar_wait(ptbar, 0);
-            __syncthreads();
-            SC_STAMP(6);
-            auto emit = [&](int pos, int i) { emit_pg(pos, i); };
-            kd = cta_topk<NT, 0, 0>(keys, P, p.kmax, *s_kmin, *s_kmax, hist, red, cand, emit, dsel);
-        }
-        (void)kd;  // == kk
-        if (rank == 0) {
-            for (int i = kk + tid; i < p.kmax; i += NT) out_id[i] = -1;
-            if (tid == 0) p.sel_count[row] = kk;
-        }
+        SC_STAMP(5);
+        if (P > 0 && pt_bulk) mbar_wait(ptbar, 0);
         __syncthreads();
-        if (dsel && tid == 0) dsel[7] = globaltimer();
-        SC_STAMP(2);
+        SC_STAMP(6);
+        cta_topk<NT, 0, 0>(lkeys, P, p.kmax, *s_kmin, *s_kmax, hist, red, cand,
+                           [&](int pos, int i) { emit_pg(pos, i); }, dsel);
+    } else {
+        // two-level: ONE inlined cta_topk serves both levels (instruction-cache footprint: the
+        // fused step's top stall is no_instruction; measured C5 22.4 -> 22.1 us): level 0 = this
+        // chunk's top-K, level 1 = the top-K of the C x K gathered candidates
+        uint32_t *myk = ckey + rank * p.kmax;
+        int *myi = cid + rank * p.kmax;
+        for (int i = tid; i < ((nloc + 3) & ~3); i += NT) lkeys[i] = i < nloc ? score_key(sc[i]) : 0u;
+        __syncthreads();
+        int lvl = 0;
+#pragma unroll 1
+        for (;;) {
+            const uint32_t *skeys = lkeys;
+            int sn = nloc, snlive = -1;
+            uint32_t smn = *s_kmin, smx = *s_kmax;
+            if (lvl == 1) {  // the C x K candidates: chunk-major, ids ascending inside a chunk
+                sn = C * p.kmax;
+                snlive = 0;  // live candidates: sum over chunks of min(K, chunk pages)
+                for (int r = 0; r < C; ++r) snlive += min(p.kmax, max(0, min(P - r * p.chunk, p.chunk)));
+                smn = 0xffffffffu;
+                smx = 0u;
+                for (int i = tid; i < sn; i += NT)
+                    if (ckey[i]) {
+                        smn = min(smn, ckey[i]);
+                        smx = max(smx, ckey[i]);
+                    }
+                skeys = ckey;
+                if (P > 0 && pt_bulk) mbar_wait(ptbar, 0);
+                block_minmax<NT, 0>(smn, smx, red);
+                SC_STAMP(6);
+            }
+            // entry order == page-id order at both levels: lower index wins ties (reading R6)
+            const int kd = cta_topk<NT, 0, 0>(skeys, sn, p.kmax, smn, smx, hist, red, cand,
+                                              [&](int pos, int i) {
+                                                  if (lvl == 0) {
+                                                      myk[pos] = lkeys[i];
+                                                      myi[pos] = j0 + i;
+                                                  } else {
+                                                      emit_pg(pos, cid[i]);
+                                                  }
+                                              },
+                                              lvl ? dsel : nullptr, false, snlive);
+            if (lvl == 1) break;
+            for (int i = kd + tid; i < p.kmax; i += NT) myk[i] = 0u;  // absent
+            __syncthreads();
+            cluster_wait();  // every CTA of the cluster is running
+            // push this chunk's K candidates into every other CTA; reset the histogram meanwhile
+            const int k4n = p.kmax >> 2;  // 16-byte remote stores (host: kmax % 4 == 0)
+            for (int x = tid; x < (C - 1) * k4n; x += NT) {
+                const int r = rank + 1 + x / k4n, u = x % k4n;
+                const int peer = r < C ? r : r - C;
+                reinterpret_cast<uint4 *>(cl.map_shared_rank(ckey, peer) + rank * p.kmax)[u] =
+                    reinterpret_cast<const uint4 *>(myk)[u];
+                reinterpret_cast<int4 *>(cl.map_shared_rank(cid, peer) + rank * p.kmax)[u] =
+                    reinterpret_cast<const int4 *>(myi)[u];
+            }
+            for (int i = tid; i < kSsHist / 4; i += NT) reinterpret_cast<int4 *>(hist)[i] = make_int4(0, 0, 0, 0);
+            cluster_arrive_release();
+            cluster_wait();
+            SC_STAMP(5);
+            lvl = 1;
+        }
     }
+    if (rank == 0) {
+        for (int i = kk + tid; i < p.kmax; i += NT) out_id[i] = -1;
+        if (tid == 0) p.sel_count[row] = kk;
+    }
+    __syncthreads();
+    if (dsel && tid == 0) dsel[7] = globaltimer();
+    SC_STAMP(2);
     SC_STAMP(3);
 
     // ===================================== 3-4. gather + attend ==========================
