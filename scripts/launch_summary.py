@@ -1,3 +1,5 @@
+"""Median duration per kernel of an ncu launch list (--metrics gpu__time_duration.sum --csv)
+(development tool).  usage: python scripts/launch_summary.py <launches.csv>"""
 import csv, collections, sys
 rows=[r for r in csv.reader(open(sys.argv[1])) if len(r)>10]
 hdr=rows[0]; ix={h:i for i,h in enumerate(hdr)}

@@ -1,5 +1,6 @@
-"""Timeline of the two-kernel decode step (development tool): per-CTA globaltimer stamps of
-score_select_kernel (K1) and sparse_attn_kernel (K2) in one ts_decode_step."""
+"""Timeline of the one-launch decode step (development tool): per-CTA globaltimer stamps of
+decode_cluster_kernel phases (start, scored, exchanged, selected, listed, consumed, end) in one
+ts_decode_step; dev build only (TS_DEV_LIB=1).  usage: python scripts/step_stamps.py c3 [bf16|fp8]"""
 import ctypes, os, sys
 import numpy as np, torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__))); sys.path.insert(0, ROOT)
