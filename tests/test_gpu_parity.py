@@ -361,6 +361,20 @@ def test_decode_step_integer_ties_short_rows(ts, ctx, budget):
     _step_parity(ts, cfg, case, ref)
 
 
+@pytest.mark.parametrize("ctx,budget,S", [(40000, 512, 16), (140000, 1024, 64)])
+def test_decode_step_integer_ties_two_level(ts, ctx, budget, S):
+    """Rows longer than 2048 pages take the two-level select (chunk top-K, then the top-K of
+    the gathered candidates, one shared select copy): real ties across chunk boundaries must
+    still go to the lower page id."""
+    cfg = synth.config("c3", batch=1, ctx=ctx, budget_tokens=budget, page_size=S)
+    case = synth.make_case(cfg, seed=17, mode="int", ragged=True)
+    ref = oracle.decode_step(case["q"], case["k_pool"], case["v_pool"], case["page_table"],
+                             case["seq_lens"], cfg.budget_tokens, cfg.scale, want_scores=True)
+    s = ref["scores"]
+    assert any(len(np.unique(s[0, g][np.isfinite(s[0, g])])) < np.isfinite(s[0, g]).sum() for g in range(4))
+    _step_parity(ts, cfg, case, ref)
+
+
 @pytest.mark.parametrize("cname", ["c2", "c3", "c4"])
 def test_decode_step_full_size(ts, cname):
     """BASELINE configs at full size, in bench.py's launch configuration."""
