@@ -584,7 +584,9 @@ def main():
     # ---- e2e: public API with host buffers (pinned), H2D of q / new k,v + D2H of o, lse
     e2e = None
     if not args.no_e2e and not seq:
-        e2e = run_e2e_batched(ts, cfg, reps, dev, stream, steps=min(args.steps, 600), warmup=5)
+        # its own sample: >= 240 steps (a 20-step --steps would time one replay of a 24-step
+        # graph, mostly its first-replay cost), <= 600 (bounded run time)
+        e2e = run_e2e_batched(ts, cfg, reps, dev, stream, steps=min(max(args.steps, 240), 600), warmup=5)
         if world > 1:
             tt = torch.tensor([1.0 / e2e["value"]], device=dev)
             torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
