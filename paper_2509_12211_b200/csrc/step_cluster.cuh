@@ -141,6 +141,13 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
 
     // ===================================== 1. score =====================================
     if (warp == W) {
+        // q first: it does not depend on the row length, and the consumers need it together
+        // with the first metadata stage (issued after the R stage copies it arrived last: the
+        // CTA's copies leave the TMA unit one by one)
+        if (lane == R) {
+            mbar_arrive_expect_tx(qbar, p.G * kRowBytes);
+            bulk_load(sb + SM::kQ, p.q + ((size_t)b * p.Hq + g * p.G) * kAttnD, p.G * kRowBytes, qbar);
+        }
         // the first min(R, stages) ring stages are free: one lane each issues its bulk copy
         // in parallel (TMA issue is ~100 cycles); lane 0 then refills stages as they drain
         const uint64_t pol = l2_policy_evict_first();
@@ -154,10 +161,6 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
                            mfull0 + 8 * st, pol);
         };
         if (lane < R && lane < nst) issue(lane);
-        if (lane == R) {
-            mbar_arrive_expect_tx(qbar, p.G * kRowBytes);
-            bulk_load(sb + SM::kQ, p.q + ((size_t)b * p.Hq + g * p.G) * kAttnD, p.G * kRowBytes, qbar);
-        }
         if (lane == R + 1 && P > 0 && pt_bulk) {  // every CTA: it maps its own share of the selection
             const uint32_t ptb = min(((uint32_t)P * 4 + 15) & ~15u, (uint32_t)mp4 * 4);
             mbar_arrive_expect_tx(ptbar, ptb);
