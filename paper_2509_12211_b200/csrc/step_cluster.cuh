@@ -125,9 +125,28 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
     if (C > 1) cluster_arrive_release();
     pdl_wait();  // inputs may come from the previous kernel in the stream
 
+    // The first copies leave before the row length is known (its load is a global round trip):
+    // q (independent of it; the consumers need it with the first stage) and the first R
+    // metadata stages of the chunk's storage, full (pages past P_b are scored -inf and read
+    // only when a row is shorter than its chunk's first R stages; every issued stage is consumed)
+    const int j0 = rank * p.chunk;
+    const int cstore = max(0, min(p.chunk, p.max_pages - j0));  // the chunk's pages in storage
+    const int nspec = min(R, (cstore + kSsStagePages - 1) / kSsStagePages);
+    if (warp == W) {
+        if (lane == R) {
+            mbar_arrive_expect_tx(qbar, p.G * kRowBytes);
+            bulk_load(sb + SM::kQ, p.q + ((size_t)b * p.Hq + g * p.G) * kAttnD, p.G * kRowBytes, qbar);
+        }
+        if (lane < nspec) {
+            const uint32_t bytes = min(kSsStagePages, cstore - lane * kSsStagePages) * 2 * kRowBytes;
+            mbar_arrive_expect_tx(mfull0 + 8 * lane, bytes);
+            bulk_load_hint(sb + lane * kSsStageBytes,
+                           p.meta + ((size_t)row * p.max_pages + j0 + (size_t)lane * kSsStagePages) * 2 * kAttnD,
+                           bytes, mfull0 + 8 * lane, l2_policy_evict_first());
+        }
+    }
     const int L = clamp_len(p.seq_lens[b], p.max_pages, 1, p.S);
     const int P = (L + p.S - 1) / p.S;
-    const int j0 = rank * p.chunk;
     const int nloc = max(0, min(P - j0, p.chunk));
     const int sb0 = two ? 0 : j0;  // index of this CTA's first page in sc[]
     // fused append (ts_decode_step_append, Eq. 1 / SPEC.md:56-59): the row's newest token
@@ -141,26 +160,8 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
 
     // ===================================== 1. score =====================================
     if (warp == W) {
-        // q first: it does not depend on the row length, and the consumers need it together
-        // with the first metadata stage (issued after the R stage copies it arrived last: the
-        // CTA's copies leave the TMA unit one by one)
-        if (lane == R) {
-            mbar_arrive_expect_tx(qbar, p.G * kRowBytes);
-            bulk_load(sb + SM::kQ, p.q + ((size_t)b * p.Hq + g * p.G) * kAttnD, p.G * kRowBytes, qbar);
-        }
-        // the first min(R, stages) ring stages are free: one lane each issues its bulk copy
-        // in parallel (TMA issue is ~100 cycles); lane 0 then refills stages as they drain
-        const uint64_t pol = l2_policy_evict_first();
-        const uint16_t *mrow = p.meta + ((size_t)row * p.max_pages + j0) * 2 * kAttnD;
-        auto issue = [&](int i) {
-            const int st = i % R;
-            const int np = min(kSsStagePages, nloc - i * kSsStagePages);
-            const uint32_t bytes = np * 2 * kRowBytes;
-            mbar_arrive_expect_tx(mfull0 + 8 * st, bytes);
-            bulk_load_hint(sb + st * kSsStageBytes, mrow + (size_t)i * kSsStagePages * 2 * kAttnD, bytes,
-                           mfull0 + 8 * st, pol);
-        };
-        if (lane < R && lane < nst) issue(lane);
+        // (q and the first nspec stages are in flight, above; the consumer warp that owns a
+        // slot refills it as it drains)
         if (lane == R + 1 && P > 0 && pt_bulk) {  // every CTA: it maps its own share of the selection
             const uint32_t ptb = min(((uint32_t)P * 4 + 15) & ~15u, (uint32_t)mp4 * 4);
             mbar_arrive_expect_tx(ptbar, ptb);
@@ -241,7 +242,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
                 kn = make_uint4(d0.x, d0.y, d1.x, d1.y);
             }
         }
-        for (int i = warp; i < nst; i += W) {
+        for (int i = warp; i < max(nst, nspec); i += W) {
             const int st = i % R;
             mbar_wait(mfull0 + 8 * st, (i / R) & 1);
             const uint32_t kb = sb + st * kSsStageBytes;
@@ -315,7 +316,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
             atomicMax(s_kmax, kmx);
         }
     }
-    for (int pg = nst * kSsStagePages + tid; pg < p.chunk; pg += NT)
+    for (int pg = max(nst, nspec) * kSsStagePages + tid; pg < p.chunk; pg += NT)
         if (j0 + pg < p.max_pages) sc[sb0 + pg] = kNegInf;
     __syncthreads();
     SC_STAMP(1);
