@@ -478,10 +478,26 @@ __global__ void __launch_bounds__((W + 1) * 32) score_select_kernel(ScoreSelPara
     if (p.C > 1) cluster_arrive_relaxed();  // "this CTA is running" (before any DSMEM access)
     pdl_wait();  // inputs may come from the previous kernel in the stream (PDL launch)
 
+    // q and the first R metadata stages of the chunk's storage leave before the row length is
+    // known (its load is a global round trip; as in decode_cluster_kernel: full stages, pages
+    // past P_b scored -inf, every issued stage consumed)
+    const int j0 = rank * p.chunk;
+    const int cstore = max(0, min(p.chunk, p.max_pages - j0));
+    const int nspec = min(R, (cstore + kSsStagePages - 1) / kSsStagePages);
+    if (warp == W && lane == 0) {
+        mbar_arrive_expect_tx(qbar, p.G * kRowBytes);
+        bulk_load(sb + SM::kQ, p.q + ((size_t)b * p.Hq + g * p.G) * kAttnD, p.G * kRowBytes, qbar);
+        for (int i = 0; i < nspec; ++i) {  // slots 0 .. R-1 are free
+            const uint32_t bytes = min(kSsStagePages, cstore - i * kSsStagePages) * 2 * kRowBytes;
+            mbar_arrive_expect_tx(full0 + 8 * i, bytes);
+            bulk_load_hint(sb + i * kSsStageBytes,
+                           p.meta + ((size_t)row * p.max_pages + j0 + (size_t)i * kSsStagePages) * 2 * kAttnD,
+                           bytes, full0 + 8 * i, l2_policy_evict_first());
+        }
+    }
     const int sst = p.stride > 1 ? p.stride : 1;  // block-cyclic sharding (ts_select_candidates)
     const int L = clamp_len(p.seq_lens[b], p.max_pages, sst, p.S);
     const int P = sst > 1 ? local_pages(L, p.S, sst, p.offset) : (L + p.S - 1) / p.S;  // local pages
-    const int j0 = rank * p.chunk;
     // page-table row -> smem only when the blocks of the selection are wanted (sel_blk)
     const bool pt_bulk = (p.max_pages & 3) == 0 && p.sel_blk != nullptr;  // row start 16-byte aligned
     const int nloc = max(0, min(P - j0, p.chunk));  // valid pages of this CTA
@@ -491,8 +507,6 @@ __global__ void __launch_bounds__((W + 1) * 32) score_select_kernel(ScoreSelPara
         // ================================ producer ================================
         if (lane == 0) {
             const uint64_t pol = l2_policy_evict_first();
-            mbar_arrive_expect_tx(qbar, p.G * kRowBytes);
-            bulk_load(sb + SM::kQ, p.q + ((size_t)b * p.Hq + g * p.G) * kAttnD, p.G * kRowBytes, qbar);
             if (rank == 0 && P > 0 && pt_bulk) {  // page-table row -> smem (page -> block)
                 const uint32_t ptb = min(((uint32_t)P * 4 + 15) & ~15u, (uint32_t)p.max_pages * 4);
                 mbar_arrive_expect_tx(ptbar, ptb);
@@ -500,7 +514,7 @@ __global__ void __launch_bounds__((W + 1) * 32) score_select_kernel(ScoreSelPara
                           p.page_table + (size_t)b * p.max_pages, ptb, ptbar);
             }
             const uint16_t *mrow = p.meta + ((size_t)row * p.max_pages + j0) * 2 * kAttnD;
-            for (int i = 0; i < nst; ++i) {
+            for (int i = nspec; i < nst; ++i) {
                 const int st = i % R;
                 mbar_wait(empty0 + 8 * st, ((i / R) & 1) ^ 1);
                 const int np = min(kSsStagePages, nloc - i * kSsStagePages);
@@ -531,7 +545,7 @@ __global__ void __launch_bounds__((W + 1) * 32) score_select_kernel(ScoreSelPara
         }
         const bool c0 = 2 * t < p.G, c1 = 2 * t + 1 < p.G;
         uint32_t kmn = 0xffffffffu, kmx = 0u;  // key range of the valid pages (lanes t < 2)
-        for (int i = warp; i < nst; i += W) {
+        for (int i = warp; i < max(nst, nspec); i += W) {
             const int st = i % R;
             mbar_wait(full0 + 8 * st, (i / R) & 1);
             const uint32_t kb = sb + st * kSsStageBytes;
@@ -578,7 +592,7 @@ __global__ void __launch_bounds__((W + 1) * 32) score_select_kernel(ScoreSelPara
         }
     }
     // pages of the chunk past P_b (no stage covered them)
-    for (int pg = nst * kSsStagePages + tid; pg < p.chunk; pg += NT)
+    for (int pg = max(nst, nspec) * kSsStagePages + tid; pg < p.chunk; pg += NT)
         if (j0 + pg < p.max_pages) sc[j0 + pg] = kNegInf;
     __syncthreads();
     SS_STAMP(1);
