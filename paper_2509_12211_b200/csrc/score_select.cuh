@@ -177,10 +177,15 @@ TS_DEV int block_scan(int v, int *red, int *total, int bar = BAR, int tb = 0) {
 // different 16-byte bank groups (no bank conflicts); a bijection on every 64-bin block.
 TS_DEV int hsw(int b) { return b ^ ((b >> 3) & 12); }
 
-template <int NT, int BAR, int HB = 11, typename Emit>
+// pre(x, nc): called by every thread once the first pass has found its boundary bin, with x
+// such that every key > x is selected and nc = their count (a caller may start using them)
+struct NoPre {
+    TS_DEV void operator()(uint32_t, int) const {}
+};
+template <int NT, int BAR, int HB = 11, typename Emit, typename Pre = NoPre>
 TS_DEV int cta_topk(const uint32_t *keys, int n, int k, uint32_t kmin, uint32_t kmax, int *hist,
                     int *red, uint32_t *cand, Emit emit, unsigned long long *dts = nullptr,
-                    bool hist0_built = false, int nvalid = -1, int bar = BAR, int tb = 0) {
+                    bool hist0_built = false, int nvalid = -1, int bar = BAR, int tb = 0, Pre pre = Pre()) {
     // nvalid: number of live (non-zero) keys when keys[] holds zero padding (default n)
     // hist0_built: the first pass histogram over [kmin, kmax] (shift as below) is already
     // in hist (built in parallel by the CTAs of a cluster, score_select / step_cluster)
@@ -292,6 +297,7 @@ TS_DEV int cta_topk(const uint32_t *keys, int n, int k, uint32_t kmin, uint32_t 
             const uint32_t blo = kmin + ((uint32_t)bsel << shift);
             const uint32_t bhi = shift ? min(kmax, blo + ((1u << shift) - 1u)) : blo;
             rem -= above;
+            if (pass == 0) pre(cnt == rem ? blo - 1u : bhi, cnt == rem ? kk : kk - rem);
             if (cnt == rem) {  // the whole bin is taken: keys >= blo
                 tgt = blo - 1u;
                 break;

@@ -359,6 +359,36 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
         if (pos >= u0 && pos < u1) sel[pos - u0] = make_int2((checked_block(ptrow[pg], ap.num_blocks) * p.Hkv + g) * S, pg * S);
         if (pos >= w0 && pos < w1) out_id[pos] = pg;
     };
+    // attention tile i of this CTA (stage i -> warp i % W, slot i % RA): part kv (0 = K, 1 = V)
+    // of its copy; arm_tile sets the slot's expected bytes (one lane per tile)
+    auto issue_tile = [&](int i, int kv) {
+        const int st = i % RA;
+        const int tl = t0 + i, u = tl >> tps, sub = tl & (tpp - 1);
+        const int2 pg = sel[u - u0];
+        if constexpr (F8) {  // the tile's K / V sub-page record (codes + exponents)
+            bulk_load_hint(sb + st * kF8Stage + kv * kF8Rec,
+                           static_cast<const uint8_t *>(kv ? ap.v_pool : ap.k_pool) + (size_t)((pg.x >> 4) + sub) * kF8Rec,
+                           kF8Rec, afull0 + 8 * st, l2_policy_evict_first());
+        } else {
+            tma_load_2d(sb + st * 2 * 16 * kRowBytes + kv * 16 * kRowBytes, kv ? &tmV : &tmK, 0, pg.x + 16 * sub,
+                        afull0 + 8 * st, l2_policy_evict_first());
+        }
+    };
+    auto arm_tile = [&](int i) { mbar_arrive_expect_tx(afull0 + 8 * (i % RA), F8 ? kF8Stage : 2 * 16 * kRowBytes); };
+    // C == 1: the first attention tiles leave DURING the select.  As soon as its first radix
+    // pass has found the boundary bin, every key above the bin is known to be selected: those
+    // pages go first in the attention order (ascending), their first RA tiles are issued at
+    // once, and the rest of the select (boundary ranking, compaction) overlaps the copies; the
+    // remaining selected pages follow in ascending order.  sel_ids stays ascending.
+    int s_pre = 0;  // attention tiles [0, s_pre) already issued
+    uint64_t pre_gm = 0;  // this thread's run of keys: which are "above the bin"
+    int pre_cb = 0, pre_nc = 0;
+    uint32_t pre_x = 0xffffffffu;
+    bool pre_on = false;
+    const int pn4 = (P + 3) >> 2, pper4 = (pn4 + NT - 1) / NT, pi0 = tid * pper4;  // cta_topk's compaction runs
+    auto emit_att = [&](int q, int i) {
+        sel[q] = make_int2((checked_block(ptrow[i], ap.num_blocks) * p.Hkv + g) * S, i * S);
+    };
     uint32_t *lkeys = reinterpret_cast<uint32_t *>(sc);  // scores -> orderable keys, in place
     if (!two) {
         // this CTA's slice of the row as keys (0 = no page, up to the 4-padded row length)
@@ -385,8 +415,57 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
         if (P > 0 && pt_bulk) mbar_wait(ptbar, 0);
         __syncthreads();
         SC_STAMP(6);
-        cta_topk<NT, 0, 0>(lkeys, P, p.kmax, *s_kmin, *s_kmax, hist, red, cand,
-                           [&](int pos, int i) { emit_pg(pos, i); }, dsel);
+        if (C > 1) {
+            cta_topk<NT, 0, 0>(lkeys, P, p.kmax, *s_kmin, *s_kmax, hist, red, cand,
+                               [&](int pos, int i) { emit_pg(pos, i); }, dsel);
+        } else {
+            auto pre = [&](uint32_t x, int nc) {  // every key > x is selected; nc of them
+                // block-uniform; not for FP8 KV (measured 0.5 % slower there: its consumer,
+                // not the first copies' latency, bounds the attention)
+                if (F8 || pper4 > 16 || nc <= 0) return;
+                const uint4 *k4 = reinterpret_cast<const uint4 *>(lkeys);
+                const int pi1 = min(pn4, pi0 + pper4);
+                uint64_t gm = 0;
+                for (int i = pi0; i < pi1; ++i) {
+                    const uint4 v = k4[i];
+                    gm |= (uint64_t)((uint32_t)(v.x > x) | ((uint32_t)(v.y > x) << 1) | ((uint32_t)(v.z > x) << 2) |
+                                     ((uint32_t)(v.w > x) << 3)) << (4 * (i - pi0));
+                }
+                int tot;
+                const int before = block_scan<NT, 0>(__popcll(gm), red, &tot);
+                int q = before;
+                for (uint64_t sm = gm; sm; sm &= sm - 1) emit_att(q++, 4 * pi0 + __ffsll((long long)sm) - 1);
+                pre_gm = gm;
+                pre_cb = before;
+                pre_nc = nc;
+                pre_x = x;
+                pre_on = true;
+                __syncthreads();  // the first nc attention entries are in place
+                s_pre = min(nc * tpp, RA);
+                if (warp < W) {
+                    if constexpr (APP)
+                        fence_proxy_async_all();  // the appended row (generic stores) may be gathered
+                    else
+                        fence_proxy_async();  // the ring was last accessed by the generic proxy
+                    const int e = lane >> 1, i = warp + W * e;
+                    if (e < RA / W && i < s_pre) {
+                        if ((lane & 1) == 0) arm_tile(i);
+                        issue_tile(i, lane & 1);
+                    }
+                }
+            };
+            cta_topk<NT, 0, 0>(lkeys, P, p.kmax, *s_kmin, *s_kmax, hist, red, cand,
+                               [&](int pos, int i) {
+                                   out_id[pos] = i;
+                                   if (!pre_on) {
+                                       emit_att(pos, i);
+                                   } else if (lkeys[i] <= pre_x) {  // after the nc keys above the bin
+                                       const int below = __popcll(pre_gm & ((1ull << (i - 4 * pi0)) - 1ull));
+                                       emit_att(pre_nc + pos - (pre_cb + below), i);
+                                   }
+                               },
+                               dsel, false, -1, 0, 0, pre);
+        }
     } else {
         // two-level: ONE inlined cta_topk serves both levels (instruction-cache footprint: the
         // fused step's top stall is no_instruction; measured C5 22.4 -> 22.1 us): level 0 = this
@@ -476,22 +555,12 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
         }
         const F8Q fq = f8_q_prep(x0, x1, sl2);
         fence_proxy_async();  // the ring was last accessed by the generic proxy (scoring)
-        const uint64_t pol = l2_policy_evict_first();
         const int ntl = t1 - t0;
-        // lane 2e + kv issues the K (kv 0) or V (kv 1) sub-page record of the warp's e-th stage
-        auto issue_f8 = [&](int i, int kv) {
-            const int st = i % RA;
-            const int tl = t0 + i, u = tl >> tps, sub = tl & (tpp - 1);
-            const int rec = (sel[u - u0].x >> 4) + sub;  // the tile's sub-page record
-            bulk_load_hint(sb + st * kF8Stage + kv * kF8Rec,
-                           static_cast<const uint8_t *>(kv ? ap.v_pool : ap.k_pool) + (size_t)rec * kF8Rec,
-                           kF8Rec, afull0 + 8 * st, pol);
-        };
-        {
+        {  // lane 2e + kv issues the K (kv 0) or V (kv 1) record of the warp's e-th stage
             const int e = lane >> 1, i = warp + W * e;
-            if (e < RA / W && i < ntl) {
-                if ((lane & 1) == 0) mbar_arrive_expect_tx(afull0 + 8 * (i % RA), kF8Stage);
-                issue_f8(i, lane & 1);
+            if (e < RA / W && i < ntl && i >= s_pre) {
+                if ((lane & 1) == 0) arm_tile(i);
+                issue_tile(i, lane & 1);
             }
         }
         F8Acc acc;
@@ -505,8 +574,8 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
             __syncwarp();
             if (lane < 2 && i + RA < ntl) {  // refill this warp's slot with stage i + RA
                 fence_proxy_async();
-                if (lane == 0) mbar_arrive_expect_tx(afull0 + 8 * st, kF8Stage);
-                issue_f8(i + RA, lane);
+                if (lane == 0) arm_tile(i + RA);
+                issue_tile(i + RA, lane);
             }
         }
         f8_store_partial(wpart + warp * 8 * kSaPart, kSaPart, acc, gid, t, p.G);
@@ -529,21 +598,12 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
             fence_proxy_async_all();
         else
             fence_proxy_async();
-        const uint64_t pol = l2_policy_evict_first();
         const int ntl = t1 - t0;
-        // lane 2e + kv issues the K (kv 0) or V (kv 1) tile of this warp's e-th stage
-        auto issue_kv = [&](int i, int kv) {
-            const int st = i % RA;
-            const int tl = t0 + i, u = tl >> tps, sub = tl & (tpp - 1);
-            const int2 pg = sel[u - u0];
-            const uint32_t dst = sb + st * 2 * 16 * kRowBytes + kv * 16 * kRowBytes;
-            tma_load_2d(dst, kv ? &tmV : &tmK, 0, pg.x + 16 * sub, afull0 + 8 * st, pol);
-        };
-        {
+        {  // lane 2e + kv issues the K (kv 0) or V (kv 1) tile of this warp's e-th stage
             const int e = lane >> 1, i = warp + W * e;
-            if (e < RA / W && i < ntl) {
-                if ((lane & 1) == 0) mbar_arrive_expect_tx(afull0 + 8 * (i % RA), 2 * 16 * kRowBytes);
-                issue_kv(i, lane & 1);
+            if (e < RA / W && i < ntl && i >= s_pre) {
+                if ((lane & 1) == 0) arm_tile(i);
+                issue_tile(i, lane & 1);
             }
         }
         float m = kNegInf, lp = 0.f;
@@ -612,8 +672,8 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
             __syncwarp();
             if (lane < 2 && i + RA < ntl) {  // refill this warp's slot with stage i + RA
                 fence_proxy_async();
-                if (lane == 0) mbar_arrive_expect_tx(afull0 + 8 * st, 2 * 16 * kRowBytes);
-                issue_kv(i + RA, lane);
+                if (lane == 0) arm_tile(i + RA);
+                issue_tile(i + RA, lane);
             }
         }
         lp += __shfl_xor_sync(0xffffffffu, lp, 1);
