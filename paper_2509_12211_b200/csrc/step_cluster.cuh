@@ -375,7 +375,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
         }
     };
     auto arm_tile = [&](int i) { mbar_arrive_expect_tx(afull0 + 8 * (i % RA), F8 ? kF8Stage : 2 * 16 * kRowBytes); };
-    // C == 1: the first attention tiles leave DURING the select.  As soon as its first radix
+    // One-level rows: the first attention tiles leave DURING the select.  As soon as its first radix
     // pass has found the boundary bin, every key above the bin is known to be selected: those
     // pages go first in the attention order (ascending), their first RA tiles are issued at
     // once, and the rest of the select (boundary ranking, compaction) overlaps the copies; the
@@ -386,8 +386,8 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
     uint32_t pre_x = 0xffffffffu;
     bool pre_on = false;
     const int pn4 = (P + 3) >> 2, pper4 = (pn4 + NT - 1) / NT, pi0 = tid * pper4;  // cta_topk's compaction runs
-    auto emit_att = [&](int q, int i) {
-        sel[q] = make_int2((checked_block(ptrow[i], ap.num_blocks) * p.Hkv + g) * S, i * S);
+    auto emit_att = [&](int q, int i) {  // attention-order entry q (this CTA keeps its share)
+        if (q >= u0 && q < u1) sel[q - u0] = make_int2((checked_block(ptrow[i], ap.num_blocks) * p.Hkv + g) * S, i * S);
     };
     uint32_t *lkeys = reinterpret_cast<uint32_t *>(sc);  // scores -> orderable keys, in place
     if (!two) {
@@ -415,10 +415,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
         if (P > 0 && pt_bulk) mbar_wait(ptbar, 0);
         __syncthreads();
         SC_STAMP(6);
-        if (C > 1) {
-            cta_topk<NT, 0, 0>(lkeys, P, p.kmax, *s_kmin, *s_kmax, hist, red, cand,
-                               [&](int pos, int i) { emit_pg(pos, i); }, dsel);
-        } else {
+        {
             auto pre = [&](uint32_t x, int nc) {  // every key > x is selected; nc of them
                 // block-uniform; not for FP8 KV (measured 0.5 % slower there: its consumer,
                 // not the first copies' latency, bounds the attention)
@@ -441,7 +438,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
                 pre_x = x;
                 pre_on = true;
                 __syncthreads();  // the first nc attention entries are in place
-                s_pre = min(nc * tpp, RA);
+                s_pre = max(0, min(nc * tpp - t0, min(RA, t1 - t0)));  // this CTA's share of them
                 if (warp < W) {
                     if constexpr (APP)
                         fence_proxy_async_all();  // the appended row (generic stores) may be gathered
@@ -456,7 +453,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 4) decode_cluster_kernel(
             };
             cta_topk<NT, 0, 0>(lkeys, P, p.kmax, *s_kmin, *s_kmax, hist, red, cand,
                                [&](int pos, int i) {
-                                   out_id[pos] = i;
+                                   if (pos >= w0 && pos < w1) out_id[pos] = i;
                                    if (!pre_on) {
                                        emit_att(pos, i);
                                    } else if (lkeys[i] <= pre_x) {  // after the nc keys above the bin
